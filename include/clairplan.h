@@ -1,0 +1,144 @@
+/* clairplan — B200-native NoPFS clairvoyant plan build, C ABI (the drop-in boundary).
+ *
+ * The reference (clairsim, /root/reference/proj) exposes this path as C++ free functions in
+ * namespace clairsim with host std::vector results.  Each entry point below names the
+ * reference interface it replaces (path:line, relative to /root/reference/proj).  The
+ * C++ shim paper_2101_08734_b200/csrc/compat/clairsim_compat.cpp re-exports the exact
+ * clairsim:: signatures on top of these calls; INTEGRATION.md shows the bindings.
+ *
+ * Conventions
+ *  - Every call returns an int status: CLAIRPLAN_OK (0) or one of the codes below; the
+ *    message for the calling thread is clairplan_last_error().  Validation failures use
+ *    the reference's exact std::invalid_argument texts (access.cpp:41-50, :53).
+ *  - Plain pointers and sizes only; "host" buffers are caller-owned CPU memory, "device"
+ *    buffers live on the handle's CUDA device and stay owned by the handle.
+ *  - Handles are independent (own CUDA stream + workspace): concurrent calls on different
+ *    handles from different host threads are safe, as the reference's sweep pool requires
+ *    (simulator.cpp:471-480).  One handle must not be used by two threads at once.
+ *  - There is no CPU fallback: without a usable sm_100 device every compute call returns
+ *    CLAIRPLAN_ENODEV.
+ */
+#ifndef CLAIRPLAN_H
+#define CLAIRPLAN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CLAIRPLAN_OK 0
+#define CLAIRPLAN_ENOMEM 12    /* device or host allocation failed */
+#define CLAIRPLAN_ENODEV 19    /* no CUDA device / not sm_100 */
+#define CLAIRPLAN_EINVAL 22    /* invalid argument (reference message text) */
+#define CLAIRPLAN_ERANGE 34    /* caller buffer too small */
+#define CLAIRPLAN_EOVERFLOW 75 /* result does not fit the requested (reference u32) layout */
+#define CLAIRPLAN_ECUDA 1001   /* CUDA runtime error */
+#define CLAIRPLAN_ENCCL 1002   /* NCCL error (multi-GPU) */
+
+typedef struct clairplan_plan* clairplan_t;
+
+/* Everything nopfs_assign_caches + build_access_streams read (policies.cpp:144-166,
+ * access.cpp:59-78): Seed, PartitionSpec, SystemConfig::storage[1..J].capacity_mb and
+ * DatasetModel::sizes_mb. */
+typedef struct {
+    uint64_t seed;              /* Seed::value                        access.hpp:14-16 */
+    uint32_t samples;           /* F = DatasetModel::samples           perfmodel.hpp:60 */
+    uint32_t num_workers;       /* PartitionSpec::num_workers          access.hpp:20 */
+    uint32_t global_batch;      /* PartitionSpec::global_batch (B)     access.hpp:21 */
+    uint32_t epochs;            /* PartitionSpec::epochs               access.hpp:22 */
+    int32_t drop_last;          /* PartitionSpec::drop_last            access.hpp:23 */
+    uint32_t num_classes;       /* J = SystemConfig::cache_class_count perfmodel.hpp:55 */
+    const double* capacities_mb; /* host [J]: storage[1..J].capacity_mb */
+    const double* sizes_mb;     /* [F] DatasetModel::sizes_mb, host or device */
+    int32_t sizes_on_device;    /* 1: sizes_mb is a device pointer on `device` */
+    int32_t device;             /* CUDA ordinal */
+    uint32_t worker_begin;      /* worker range planned by this handle: [begin, end); */
+    uint32_t worker_end;        /*   0,0 = all workers (single-GPU plan) */
+} clairplan_config;
+
+/* Per-build counters. */
+typedef struct {
+    uint64_t accesses;        /* A: stream entries of the handle's workers */
+    uint64_t pairs;           /* D: distinct (worker, sample) pairs of those workers */
+    uint64_t holders;         /* assigned pairs = holder records */
+    uint64_t rejections;      /* Lemire rejections resolved (rng.hpp:54-60) */
+    double device_ms;         /* device time of the last clairplan_build (CUDA events) */
+} clairplan_stats;
+
+int clairplan_version(void);
+const char* clairplan_last_error(void);
+
+/* PartitionSpec::validate (access.cpp:41-50) with the same messages. */
+int clairplan_validate(const clairplan_config* cfg);
+
+/* Allocates the handle, its stream and workspace; copies capacities and sizes. */
+int clairplan_create(const clairplan_config* cfg, clairplan_t* out);
+int clairplan_destroy(clairplan_t plan);
+
+/* The whole hot path, device-resident: epoch permutations -> per-worker streams ->
+ * (count, first-access) per (worker, sample) -> tier assignment -> prefetch orders ->
+ * holder CSR.  Replaces build_access_streams (access.cpp:59-78) + access_frequencies for
+ * every worker + nopfs_assign_caches + build_index (policies.cpp:446-456).  Synchronous. */
+int clairplan_build(clairplan_t plan);
+int clairplan_stats_get(clairplan_t plan, clairplan_stats* out);
+
+/* ---- device views (valid until the next build/destroy) ---------------------------- */
+/* Worker-major streams: worker w's AccessStream::entries (access.hpp:32-43) is
+ * entries[stream_offset(w) .. stream_offset(w+1)). */
+int clairplan_device_streams(clairplan_t plan, const uint32_t** entries, uint64_t* total);
+uint64_t clairplan_stream_offset(clairplan_t plan, uint32_t worker);
+/* CacheAssignment::class_lists[w][j-1] (policies.hpp:56-57), prefetch-ordered:
+ * entries[off[w*J + j-1] .. off[w*J + j-1] + len[w*J + j-1]) — host arrays filled here. */
+int clairplan_class_list_bounds(clairplan_t plan, uint64_t* off, uint64_t* len);
+int clairplan_device_class_lists(clairplan_t plan, const uint32_t** entries);
+/* CacheAssignment::holder_offsets/holders (policies.hpp:58-61) with u64 offsets:
+ * offsets[F+1], holders = {worker, storage_class (1-based), position} x count. */
+int clairplan_device_holders(clairplan_t plan, const uint64_t** offsets,
+                             const uint32_t** holders, uint64_t* count);
+
+/* ---- host export ------------------------------------------------------------------- */
+int clairplan_export_stream(clairplan_t plan, uint32_t worker, uint32_t* out, uint64_t cap,
+                            uint64_t* len);
+int clairplan_export_streams(clairplan_t plan, uint32_t* out, uint64_t cap);
+/* all class lists, (w, j)-major, with the N*J bounds from clairplan_class_list_bounds */
+int clairplan_export_class_lists(clairplan_t plan, uint32_t* out, uint64_t cap);
+int clairplan_export_holders(clairplan_t plan, uint64_t* offsets, uint32_t* holders,
+                             uint64_t cap);
+/* FrequencyTable::counts of worker w over all epochs (access.cpp:80-88), dense [F]. */
+int clairplan_export_counts(clairplan_t plan, uint32_t worker, uint32_t* counts);
+
+/* ---- stand-alone entry points of the same path --------------------------------------- */
+/* epoch_permutation (access.hpp:58, access.cpp:52-57) into a host buffer [samples]. */
+int clairplan_epoch_permutation(uint64_t seed, uint32_t epoch, uint32_t samples,
+                                uint32_t* out, int device);
+/* access_frequencies (access.hpp:66-67): entries/epoch_offsets are one host AccessStream. */
+int clairplan_access_frequencies(const uint32_t* entries, const uint64_t* epoch_offsets,
+                                 uint32_t epoch_count, uint32_t samples, uint32_t epoch_begin,
+                                 uint32_t epoch_end, uint32_t* counts, int device);
+/* worker_access_counts / all_access_counts (access.hpp:71-77); all: counts is [N][F]. */
+int clairplan_worker_access_counts(const clairplan_config* cfg, uint32_t worker,
+                                   uint32_t* counts);
+int clairplan_all_access_counts(const clairplan_config* cfg, uint32_t* counts);
+/* nopfs_assign_caches (policies.hpp:88-90) on caller-supplied streams and dense
+ * frequency tables (N x F).  Creates a handle whose class lists / holders are readable
+ * through the calls above.  entries: concatenated streams, offsets[N+1]. */
+int clairplan_assign_from_streams(uint32_t num_workers, uint32_t samples,
+                                  const uint32_t* entries, const uint64_t* offsets,
+                                  const uint32_t* counts, uint32_t num_classes,
+                                  const double* capacities_mb, const double* sizes_mb,
+                                  int device, clairplan_t* out);
+
+/* Host-side input generator: DatasetModel::generate (perfmodel.cpp:68-99), bit-identical
+ * with the reference built with the same glibc (no FMA contraction).  Not timed. */
+int clairplan_generate_sizes(uint64_t samples, double mean_mb, double sigma_mb, int has_total,
+                             double total_mb, uint64_t seed, int sigma_relative, double* out);
+
+/* Number of kernel launches issued by the last clairplan_build on this handle. */
+uint64_t clairplan_launch_count(clairplan_t plan);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CLAIRPLAN_H */

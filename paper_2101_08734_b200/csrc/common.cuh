@@ -1,0 +1,178 @@
+// Shared device/host helpers for the clairplan kernels (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace clairplan {
+
+constexpr uint32_t kNone = 0xFFFFFFFFu;
+constexpr int kThreads = 256;
+
+// ---- counter PRNG (rng.hpp:16-47) ------------------------------------------------------
+constexpr uint64_t kGolden = 0x9e3779b97f4a7c15ULL;
+constexpr uint64_t kPermTag = 0x7065726dULL;  // rng.hpp:29
+constexpr uint64_t kSizeTag = 0x73697a65ULL;  // rng.hpp:30
+constexpr int kEpochShift = 34;               // access.cpp:10
+
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z ^= z >> 30;
+    z *= 0xbf58476d1ce4e5b9ULL;
+    z ^= z >> 27;
+    z *= 0x94d049bb133111ebULL;
+    z ^= z >> 31;
+    return z;
+}
+
+__host__ __device__ __forceinline__ uint64_t derive_key(uint64_t seed, uint64_t tag) {
+    return mix64(seed ^ mix64(tag));
+}
+
+__host__ __device__ __forceinline__ uint64_t umulhi64(uint64_t a, uint64_t b) {
+#ifdef __CUDA_ARCH__
+    return __umul64hi(a, b);
+#else
+    return (uint64_t)(((unsigned __int128)a * b) >> 64);
+#endif
+}
+
+// CounterRng::bounded (rng.hpp:50-63) evaluated at an explicit stream position: the draw
+// uses position pos+1 (pre-increment), rejections consume further positions. Returns the
+// value; *extra = number of rejected draws.
+__host__ __device__ __forceinline__ uint64_t bounded_at(uint64_t key, uint64_t pos, uint64_t n,
+                                                        uint32_t* extra) {
+    uint64_t x = mix64(key + (pos + 1) * kGolden);
+    uint64_t lo = x * n;
+    uint32_t rej = 0;
+    if (lo < n) {
+        const uint64_t t = (0 - n) % n;
+        while (lo < t) {
+            ++rej;
+            x = mix64(key + (pos + 1 + rej) * kGolden);
+            lo = x * n;
+        }
+    }
+    *extra = rej;
+    return umulhi64(x, n);
+}
+
+// ---- Fisher-Yates step draw with the per-epoch rejection table --------------------------
+// Step i (i = F-1 .. 1) of epoch e draws at position (e << 34) + (F - 1 - i) + shift(i)
+// (+1 pre-increment inside bounded_at).  shift(i) = extra draws consumed by steps > i,
+// recorded in a tiny table of (step, cumulative extra) sorted by step descending.
+struct RejTable {
+    const uint32_t* step;  // [cap] per epoch
+    const uint32_t* cum;
+    const uint32_t* count; // per epoch
+    uint32_t cap;
+    uint32_t e_base;       // tables are indexed by (epoch - e_base)
+};
+
+__host__ __device__ __forceinline__ uint32_t rej_shift(const uint32_t* step, const uint32_t* cum,
+                                                       uint32_t n, uint32_t i) {
+    uint32_t s = 0;
+    for (uint32_t t = 0; t < n; ++t) {
+        if (step[t] > i) s = cum[t];
+        else break;
+    }
+    return s;
+}
+
+__host__ __device__ __forceinline__ uint32_t fy_draw(uint64_t key, uint32_t e, uint32_t F,
+                                                     uint32_t i, uint32_t shift,
+                                                     uint32_t* extra) {
+    const uint64_t pos = ((uint64_t)e << kEpochShift) + (uint64_t)(F - 1 - i) + shift;
+    return (uint32_t)bounded_at(key, pos, (uint64_t)i + 1, extra);
+}
+
+// ---- partition geometry (access.cpp:14-39, config.cpp:37-44) ----------------------------
+struct Part {
+    uint32_t F, N, B, E;
+    uint32_t drop_last;
+    uint64_t full, tail, P;          // T = full batches, tail batch size, covered positions
+    uint64_t base, extra;            // batch_slice of a full batch
+    uint64_t tbase, textra;          // batch_slice of the tail batch
+    uint32_t wbegin, wend;           // worker range of this handle
+    uint64_t off0;                   // stream_offset(wbegin)
+
+    __host__ __device__ uint64_t len(uint32_t w) const { return base + (w < extra ? 1 : 0); }
+    __host__ __device__ uint64_t tlen(uint32_t w) const {
+        return tail ? tbase + (w < textra ? 1 : 0) : 0;
+    }
+    __host__ __device__ uint64_t epoch_len(uint32_t w) const { return full * len(w) + tlen(w); }
+    // sum_{w' < w} epoch_len(w')
+    __host__ __device__ uint64_t prefix_len(uint32_t w) const {
+        const uint64_t mw = w < extra ? w : extra;
+        uint64_t s = full * ((uint64_t)w * base + mw);
+        if (tail) s += (uint64_t)w * tbase + (w < textra ? w : textra);
+        return s;
+    }
+    __host__ __device__ uint64_t stream_offset(uint32_t w) const {
+        return (uint64_t)E * prefix_len(w) - off0;
+    }
+    // perm position p (< P) of epoch e -> worker and position within that worker's stream
+    __host__ __device__ void locate(uint64_t p, uint32_t e, uint32_t& w, uint64_t& spos) const {
+        const uint64_t h = p / B;
+        const uint64_t o = p - h * B;
+        uint64_t b = base, x = extra, off;
+        if (h >= full) { b = tbase; x = textra; }
+        const uint64_t big = x * (b + 1);
+        if (o < big) {
+            w = (uint32_t)(o / (b + 1));
+            off = o - (uint64_t)w * (b + 1);
+        } else {
+            const uint64_t o2 = o - big;
+            const uint64_t q = o2 / b;
+            w = (uint32_t)(x + q);
+            off = o2 - q * b;
+        }
+        spos = (uint64_t)e * epoch_len(w) + (h < full ? h * len(w) : full * len(w)) + off;
+    }
+    __host__ __device__ uint32_t worker_of(uint64_t p) const {
+        const uint64_t h = p / B;
+        const uint64_t o = p - h * B;
+        uint64_t b = base, x = extra;
+        if (h >= full) { b = tbase; x = textra; }
+        const uint64_t big = x * (b + 1);
+        if (o < big) return (uint32_t)(o / (b + 1));
+        return (uint32_t)(x + (o - big) / b);
+    }
+};
+
+inline Part make_part(uint32_t F, uint32_t N, uint32_t B, uint32_t E, bool drop_last,
+                      uint32_t wbegin, uint32_t wend) {
+    Part p{};
+    p.F = F; p.N = N; p.B = B; p.E = E; p.drop_last = drop_last ? 1 : 0;
+    p.full = F / B;
+    p.tail = drop_last ? 0 : F % B;
+    p.P = p.full * B + p.tail;
+    p.base = B / N; p.extra = B % N;
+    p.tbase = p.tail / N; p.textra = p.tail % N;
+    p.wbegin = wbegin; p.wend = wend;
+    p.off0 = 0;
+    p.off0 = p.stream_offset(wbegin);
+    return p;
+}
+
+// ---- small device utilities --------------------------------------------------------------
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+inline unsigned grid_for(uint64_t n, unsigned per_block, unsigned cap = 148u * 64u) {
+    uint64_t g = (n + per_block - 1) / per_block;
+    if (g < 1) g = 1;
+    if (g > cap) g = cap;
+    return (unsigned)g;
+}
+
+}  // namespace clairplan

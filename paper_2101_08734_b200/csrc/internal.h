@@ -1,0 +1,108 @@
+// Internal declarations shared by the clairplan translation units (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace clairplan {
+
+// Bump allocator over one device buffer; all users run on one stream, so memory released
+// by mark/release may be reused by later kernels of the same stream.
+struct Workspace {
+    char* base = nullptr;
+    size_t cap = 0, used = 0, peak = 0;
+    bool overflow = false;
+    template <typename T>
+    T* scratch(uint64_t n) {
+        const size_t bytes = ((size_t)n * sizeof(T) + 255) & ~(size_t)255;
+        if (used + bytes > cap) {
+            overflow = true;
+            return nullptr;
+        }
+        T* p = reinterpret_cast<T*>(base + used);
+        used += bytes;
+        if (used > peak) peak = used;
+        return p;
+    }
+    size_t mark() const { return used; }
+    void release(size_t m) { used = m; }
+};
+
+// Tiles of `tile` elements over segments (never straddling one).
+struct TileMap {
+    uint32_t tile = 0, nseg = 0;
+    uint64_t max_tiles = 0;        // upper bound; tile_seg[t] == kNone past the real count
+    uint64_t* tile_base = nullptr; // [nseg+1] first tile of each segment
+    uint32_t* tile_seg = nullptr;  // [max_tiles]
+};
+
+void exclusive_scan(cudaStream_t s, const uint32_t* in, uint64_t n, uint64_t* out, Workspace& ws);
+void exclusive_scan(cudaStream_t s, const uint64_t* in, uint64_t n, uint64_t* out, Workspace& ws);
+
+void build_tilemap(cudaStream_t s, const uint64_t* seg_len, uint32_t nseg, uint64_t total_len,
+                   uint32_t tile, TileMap& tm, Workspace& ws);
+void radix_pass(cudaStream_t s, const TileMap& tm, const uint64_t* seg_begin,
+                const uint64_t* seg_len, const uint32_t* keys, const uint32_t* vals,
+                uint32_t shift, uint32_t* okeys, uint32_t* ovals, uint32_t* dest,
+                uint64_t** scanned_out, Workspace& ws);
+void radix_regions(cudaStream_t s, const TileMap& tm, const uint64_t* seg_begin,
+                   const uint64_t* seg_len, const uint64_t* scanned, uint32_t ndig,
+                   uint64_t* rstart, uint64_t* rlen);
+constexpr uint32_t kRadixTile = 2048;
+
+void launch_fy_link(cudaStream_t s, uint64_t key, uint32_t F, uint32_t e0, uint32_t ne,
+                    uint32_t* head, uint32_t* next, const RejTable& rt, uint32_t* rej_flag,
+                    bool detect_only, uint32_t i_limit);
+void launch_fy_group(cudaStream_t s, uint32_t F, uint32_t ne, const uint32_t* head,
+                     uint32_t* next, uint32_t* q, uint32_t* scratch, uint32_t scratch_cap,
+                     uint32_t* scratch_used, uint32_t* err);
+void launch_fy_emit(cudaStream_t s, uint64_t key, const Part& part, uint32_t e0, uint32_t ne,
+                    const uint32_t* succ, const uint32_t* q, const RejTable& rt, uint32_t* inv,
+                    uint32_t* stream, uint32_t* perm_out);
+
+int sample_pass_config(const Part& part, uint32_t* hs, uint32_t* nw_words, uint32_t* warps,
+                       size_t* smem);
+void launch_sample_pass(cudaStream_t s, const Part& part, uint32_t* info, uint32_t* pair_count,
+                        uint32_t hs, uint32_t nw_words, uint32_t warps, size_t smem);
+
+void launch_seg_count(cudaStream_t s, const Part& part, const uint32_t* stream,
+                      const uint32_t* info, uint32_t* segcnt);
+void launch_seg_write(cudaStream_t s, const Part& part, const uint32_t* stream,
+                      const uint32_t* info, const uint64_t* seg_off, uint32_t* cand_k,
+                      uint32_t* cand_info);
+void launch_worker_segments(cudaStream_t s, const uint64_t* seg_off, uint32_t nloc, uint32_t E,
+                            uint64_t* wbegin, uint64_t* wlen);
+
+void first_fit_pass(cudaStream_t s, const uint64_t* seg_begin, const uint64_t* seg_len,
+                    uint32_t nseg, uint64_t total, const double* sz, double C, uint8_t* taken,
+                    Workspace& ws);
+
+void launch_gather_sizes(cudaStream_t s, const uint32_t* order, const uint32_t* cand_k,
+                         const double* sizes, uint64_t n, double* out);
+void launch_count_keys(cudaStream_t s, const uint32_t* cand_info, uint64_t n, uint32_t maxc,
+                       uint32_t* keys);
+void launch_apply_pass(cudaStream_t s, const uint8_t* taken, uint64_t n,
+                       const uint32_t* seq_to_sorted, const uint32_t* order, uint8_t cls,
+                       uint8_t* cand_cls);
+void launch_reject_keys(cudaStream_t s, const uint8_t* taken, uint64_t n,
+                        const uint32_t* seq_to_sorted, uint32_t* keys, uint32_t* vals);
+void launch_gather_seq_sizes(cudaStream_t s, const uint32_t* idx, const double* sorted_size,
+                             const uint64_t* seg_begin, const uint64_t* seg_len, uint32_t nseg,
+                             double* out);
+void launch_class_keys(cudaStream_t s, const uint8_t* cand_cls, uint64_t n, uint32_t J,
+                       uint32_t* keys);
+void launch_holder_scatter(cudaStream_t s, const uint32_t* cand_k, const uint32_t* cand_info,
+                           const uint8_t* cand_cls, const uint32_t* dest, const uint64_t* wbegin,
+                           const uint64_t* wlen, const uint64_t* class_start, uint32_t J,
+                           uint32_t nloc, uint32_t worker0, const uint64_t* pair_off,
+                           uint32_t* holders);
+void launch_holder_count(cudaStream_t s, const uint64_t* pair_off, uint32_t F, const uint32_t* tmp,
+                         uint32_t* cnt);
+void launch_holder_compact(cudaStream_t s, const uint64_t* pair_off, uint32_t F,
+                           const uint32_t* tmp, const uint64_t* hoff, uint32_t* holders);
+void launch_dense_counts(cudaStream_t s, const uint32_t* cand_k, const uint32_t* cand_info,
+                         uint64_t b, uint64_t L, uint32_t* counts);
+
+}  // namespace clairplan

@@ -1,0 +1,183 @@
+// K1-K3: bit-exact parallel Fisher-Yates (rng.cpp:15-24, access.cpp:52-57) fused with the
+// partition into per-worker streams (access.cpp:14-39, 59-78).
+//
+// The sequential shuffle "for i = F-1 .. 1: swap(a[i], a[j_i])" is resolved without
+// executing the swaps in order.  Group the steps by target: writers of y are the steps
+// i >= y with j_i = y, ascending w_1 < ... < w_m.
+//   q(y)   = smallest writer of y other than y itself (the last write into y before step y)
+//   succ(i)= next larger writer of the same target (the last write into j_i before step i)
+//   V(x)   = value at position x just before step x = V(q(x)) if q(x) exists, else x
+//   out[i] = V(succ(i)) if succ(i) exists, else j_i;      out[0] = V(0)
+// Every j_i depends only on (key, epoch, i) once the rare Lemire rejections are known
+// (RejTable), so the draws are embarrassingly parallel:
+//   fy_link  : draw j_i, push i onto target j_i's list (atomicExch linked list)
+//   fy_group : per target, sort its (short) writer list -> q[y], succ[] (in place of next)
+//   fy_emit  : chase V, write the permutation value straight into the worker stream slot
+//              and the inverse permutation inv[e][value] = position (for the histograms).
+#include "internal.h"
+
+namespace clairplan {
+
+__global__ void __launch_bounds__(kThreads) fy_link_kernel(uint64_t key, uint32_t F, uint32_t e0,
+                                                            uint32_t* __restrict__ head,
+                                                            uint32_t* __restrict__ next,
+                                                            RejTable rt,
+                                                            uint32_t* __restrict__ rej_flag,
+                                                            int detect_only, uint32_t i_limit) {
+    const uint32_t slot = blockIdx.y;
+    const uint32_t e = e0 + slot;
+    uint32_t* hd = head + (size_t)slot * F;
+    uint32_t* nx = next + (size_t)slot * F;
+    const uint32_t er = e - rt.e_base;
+    const uint32_t n = rt.count[er];
+    const uint32_t* st = rt.step + (size_t)er * rt.cap;
+    const uint32_t* cu = rt.cum + (size_t)er * rt.cap;
+    const uint32_t lim = i_limit < F ? i_limit : F;
+    for (uint32_t i = 1 + blockIdx.x * blockDim.x + threadIdx.x; i < lim;
+         i += gridDim.x * blockDim.x) {
+        const uint32_t shift = n ? rej_shift(st, cu, n, i) : 0;
+        uint32_t extra;
+        const uint32_t j = fy_draw(key, e, F, i, shift, &extra);
+        if (extra) {
+            bool known = false;
+            for (uint32_t t = 0; t < n; ++t) known |= (st[t] == i);
+            if (!known) atomicMax(&rej_flag[er], i + 1);
+        }
+        if (!detect_only) nx[i] = atomicExch(&hd[j], i);
+    }
+}
+
+// Lists longer than kLocal go through a global scratch area (never seen in practice: the
+// expected list length at target y is ~ln(F/y)).
+constexpr int kLocal = 48;
+
+__global__ void __launch_bounds__(kThreads) fy_group_kernel(uint32_t F,
+                                                             const uint32_t* __restrict__ head,
+                                                             uint32_t* __restrict__ next,
+                                                             uint32_t* __restrict__ q,
+                                                             uint32_t* __restrict__ scratch,
+                                                             uint32_t scratch_cap,
+                                                             uint32_t* __restrict__ scratch_used,
+                                                             uint32_t* __restrict__ err) {
+    const uint32_t slot = blockIdx.y;
+    const uint32_t* hd = head + (size_t)slot * F;
+    uint32_t* nx = next + (size_t)slot * F;
+    uint32_t* qq = q + (size_t)slot * F;
+    for (uint32_t y = blockIdx.x * blockDim.x + threadIdx.x; y < F; y += gridDim.x * blockDim.x) {
+        uint32_t buf[kLocal];
+        uint32_t n = 0;
+        uint32_t cur = hd[y];
+        while (cur != kNone && n < (uint32_t)kLocal) {
+            // insertion into the sorted prefix
+            int t = (int)n - 1;
+            while (t >= 0 && buf[t] > cur) {
+                buf[t + 1] = buf[t];
+                --t;
+            }
+            buf[t + 1] = cur;
+            ++n;
+            cur = nx[cur];
+        }
+        uint32_t* list = buf;
+        if (cur != kNone) {  // overflow: move the whole list to global scratch
+            uint32_t m = n;
+            for (uint32_t c = cur; c != kNone; c = nx[c]) ++m;
+            const uint32_t base = atomicAdd(scratch_used, m);
+            if (base + m > scratch_cap) {
+                atomicOr(err, 1u);
+                continue;
+            }
+            list = scratch + base;
+            for (uint32_t t = 0; t < n; ++t) list[t] = buf[t];
+            for (uint32_t c = cur; c != kNone; c = nx[c]) {
+                int t = (int)n - 1;
+                while (t >= 0 && list[t] > c) {
+                    list[t + 1] = list[t];
+                    --t;
+                }
+                list[t + 1] = c;
+                ++n;
+            }
+        }
+        uint32_t qv = kNone;
+        if (n > 0) qv = (list[0] == y) ? (n > 1 ? list[1] : kNone) : list[0];
+        qq[y] = qv;
+        for (uint32_t t = 0; t + 1 < n; ++t) nx[list[t]] = list[t + 1];
+        if (n > 0) nx[list[n - 1]] = kNone;
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) fy_emit_kernel(uint64_t key, Part part, uint32_t e0,
+                                                            const uint32_t* __restrict__ succ,
+                                                            const uint32_t* __restrict__ q,
+                                                            RejTable rt,
+                                                            uint32_t* __restrict__ inv,
+                                                            uint32_t* __restrict__ stream,
+                                                            uint32_t* __restrict__ perm_out) {
+    const uint32_t slot = blockIdx.y;
+    const uint32_t e = e0 + slot;
+    const uint32_t F = part.F;
+    const uint32_t* sc = succ + (size_t)slot * F;
+    const uint32_t* qq = q + (size_t)slot * F;
+    const uint32_t er = e - rt.e_base;
+    const uint32_t n = rt.count[er];
+    const uint32_t* st = rt.step + (size_t)er * rt.cap;
+    const uint32_t* cu = rt.cum + (size_t)er * rt.cap;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < F; i += gridDim.x * blockDim.x) {
+        uint32_t v;
+        uint32_t x = kNone;
+        if (i == 0) {
+            x = 0;
+        } else {
+            const uint32_t s = sc[i];
+            if (s == kNone) {
+                uint32_t extra;
+                v = fy_draw(key, e, F, i, n ? rej_shift(st, cu, n, i) : 0, &extra);
+            } else {
+                x = s;
+            }
+        }
+        if (x != kNone) {
+            uint32_t nq = qq[x];
+            while (nq != kNone) {
+                x = nq;
+                nq = qq[x];
+            }
+            v = x;
+        }
+        if (perm_out) perm_out[(size_t)slot * F + i] = v;
+        if (inv) inv[(size_t)e * F + v] = i;
+        if (stream && i < part.P) {
+            uint32_t w;
+            uint64_t spos;
+            part.locate(i, e, w, spos);
+            if (w >= part.wbegin && w < part.wend) stream[part.stream_offset(w) + spos] = v;
+        }
+    }
+}
+
+// ---- host launchers ------------------------------------------------------------------
+void launch_fy_link(cudaStream_t s, uint64_t key, uint32_t F, uint32_t e0, uint32_t ne,
+                    uint32_t* head, uint32_t* next, const RejTable& rt, uint32_t* rej_flag,
+                    bool detect_only, uint32_t i_limit) {
+    dim3 grid(grid_for(F, kThreads * 4, 148u * 16u), ne);
+    fy_link_kernel<<<grid, kThreads, 0, s>>>(key, F, e0, head, next, rt, rej_flag,
+                                             detect_only ? 1 : 0, i_limit);
+}
+
+void launch_fy_group(cudaStream_t s, uint32_t F, uint32_t ne, const uint32_t* head,
+                     uint32_t* next, uint32_t* q, uint32_t* scratch, uint32_t scratch_cap,
+                     uint32_t* scratch_used, uint32_t* err) {
+    dim3 grid(grid_for(F, kThreads * 4, 148u * 16u), ne);
+    fy_group_kernel<<<grid, kThreads, 0, s>>>(F, head, next, q, scratch, scratch_cap,
+                                              scratch_used, err);
+}
+
+void launch_fy_emit(cudaStream_t s, uint64_t key, const Part& part, uint32_t e0, uint32_t ne,
+                    const uint32_t* succ, const uint32_t* q, const RejTable& rt, uint32_t* inv,
+                    uint32_t* stream, uint32_t* perm_out) {
+    dim3 grid(grid_for(part.F, kThreads * 4, 148u * 16u), ne);
+    fy_emit_kernel<<<grid, kThreads, 0, s>>>(key, part, e0, succ, q, rt, inv, stream, perm_out);
+}
+
+}  // namespace clairplan

@@ -1,0 +1,575 @@
+// clairplan C ABI (include/clairplan.h): host orchestration of the device plan build.
+//
+// Pipeline of clairplan_build (one CUDA stream per handle, 2 host syncs):
+//   K1-K3 fy_link / fy_group / fy_emit   per batch of epochs: permutation -> streams + inv
+//   K4a   sample_pass                    per sample: (w,k) counts, first epoch, holder rank
+//         scan(pair_count)               -> pair offsets (= holder_offsets when all assigned)
+//   K4b   seg_count, scan, seg_write     -> candidates per worker in first-access order
+//   K5    radix pass on (E - count)      -> tier order (count desc, first asc)
+//   K6    first_fit_pass per class       -> class of every candidate
+//   K7    radix pass on class digit      -> prefetch-ordered class lists
+//   K8    holder_scatter (+ compaction)  -> holder CSR
+#include "plan_impl.h"
+
+namespace clairplan {
+thread_local std::string g_err;
+}  // namespace clairplan
+
+namespace clairplan {
+
+uint32_t epochs_per_batch(uint32_t F, uint32_t E) {
+    const uint64_t per = (uint64_t)F * 12;
+    uint64_t eb = (96ull << 20) / (per ? per : 1);
+    if (eb < 1) eb = 1;
+    if (eb > E) eb = E;
+    if (eb > 64) eb = 64;
+    return (uint32_t)eb;
+}
+
+RejTable rej_table(clairplan_plan* p) {
+    RejTable rt;
+    rt.step = p->rej_step.get<uint32_t>();
+    rt.cum = p->rej_cum.get<uint32_t>();
+    rt.count = p->rej_count.get<uint32_t>();
+    rt.cap = kRejCap;
+    rt.e_base = p->rej_ebase;
+    return rt;
+}
+
+// Enqueues the permutations of epochs [0, E): stream + inverse (or plain permutations).
+int enqueue_perms(clairplan_plan* p, uint32_t* stream_out, uint32_t* inv_out, uint32_t* perm_out,
+                  uint32_t e_first, uint32_t e_count) {
+    const uint32_t F = p->part.F;
+    const uint32_t EB = perm_out ? 1 : epochs_per_batch(F, e_count);
+    bool ok = true;
+    uint32_t* head = need<uint32_t>(p->head, (uint64_t)EB * F, ok);
+    uint32_t* next = need<uint32_t>(p->next, (uint64_t)EB * F, ok);
+    uint32_t* q = need<uint32_t>(p->q, (uint64_t)EB * F, ok);
+    const uint32_t scap = 1u << 20;
+    uint32_t* scratch = need<uint32_t>(p->scratch, scap, ok);
+    uint32_t* counters = need<uint32_t>(p->counters, 4, ok);
+    if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed (permutation workspace)");
+    const RejTable rt = rej_table(p);
+    for (uint32_t e0 = e_first; e0 < e_first + e_count; e0 += EB) {
+        const uint32_t ne = std::min(EB, e_first + e_count - e0);
+        CK(cudaMemsetAsync(head, 0xFF, (size_t)ne * F * sizeof(uint32_t), p->stream));
+        CK(cudaMemsetAsync(counters, 0, sizeof(uint32_t), p->stream));
+        launch_fy_link(p->stream, p->key, F, e0, ne, head, next, rt, p->rej_flag.get<uint32_t>(),
+                       false, F);
+        launch_fy_group(p->stream, F, ne, head, next, q, scratch, scap, counters, counters + 1);
+        launch_fy_emit(p->stream, p->key, p->part, e0, ne, next, q, rt, inv_out, stream_out,
+                       perm_out);
+        p->launches += 3;
+    }
+    CK(cudaGetLastError());
+    return 0;
+}
+
+// Resolves Lemire rejections (rng.hpp:54-60) of the flagged epochs into the per-epoch
+// shift tables.  Rare: ~F^2/2^66 rejections per epoch.
+int resolve_rejections(clairplan_plan* p, const std::vector<uint32_t>& flags, bool* any) {
+    *any = false;
+    const uint32_t F = p->part.F;
+    for (uint32_t er = 0; er < flags.size(); ++er) {
+        const uint32_t e = er + p->rej_ebase;
+        uint32_t flag = flags[er];
+        while (flag) {
+            *any = true;
+            const uint32_t i = flag - 1;
+            uint32_t* st = &p->rej_step_h[(size_t)er * kRejCap];
+            uint32_t* cu = &p->rej_cum_h[(size_t)er * kRejCap];
+            uint32_t& n = p->rej_count_h[er];
+            if (n >= kRejCap) return fail(CLAIRPLAN_EOVERFLOW, "too many Lemire rejections in one epoch");
+            const uint32_t shift = rej_shift(st, cu, n, i);
+            uint32_t extra = 0;
+            fy_draw(p->key, e, F, i, shift, &extra);
+            st[n] = i;
+            cu[n] = shift + extra;
+            ++n;
+            ++p->rejections;
+            CK(cudaMemcpyAsync(p->rej_step.get<uint32_t>() + (size_t)er * kRejCap, st,
+                               kRejCap * sizeof(uint32_t), cudaMemcpyHostToDevice, p->stream));
+            CK(cudaMemcpyAsync(p->rej_cum.get<uint32_t>() + (size_t)er * kRejCap, cu,
+                               kRejCap * sizeof(uint32_t), cudaMemcpyHostToDevice, p->stream));
+            CK(cudaMemcpyAsync(p->rej_count.get<uint32_t>() + er, &n, sizeof(uint32_t),
+                               cudaMemcpyHostToDevice, p->stream));
+            CK(cudaMemsetAsync(p->rej_flag.get<uint32_t>() + er, 0, sizeof(uint32_t), p->stream));
+            launch_fy_link(p->stream, p->key, F, e, 1, nullptr, nullptr, rej_table(p),
+                           p->rej_flag.get<uint32_t>(), true, i);
+            ++p->launches;
+            CK(cudaMemcpyAsync(&flag, p->rej_flag.get<uint32_t>() + er, sizeof(uint32_t),
+                               cudaMemcpyDeviceToHost, p->stream));
+            CK(cudaStreamSynchronize(p->stream));
+        }
+    }
+    return 0;
+}
+
+int alloc_rej(clairplan_plan* p, uint32_t E) {
+    bool ok = true;
+    need<uint32_t>(p->rej_flag, E, ok);
+    need<uint32_t>(p->rej_step, (uint64_t)E * kRejCap, ok);
+    need<uint32_t>(p->rej_cum, (uint64_t)E * kRejCap, ok);
+    need<uint32_t>(p->rej_count, E, ok);
+    if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed (rejection tables)");
+    if (p->rej_count_h.size() != E) {
+        p->rej_step_h.assign((size_t)E * kRejCap, 0);
+        p->rej_cum_h.assign((size_t)E * kRejCap, 0);
+        p->rej_count_h.assign(E, 0);
+        CK(cudaMemsetAsync(p->rej_count.get<uint32_t>(), 0, E * sizeof(uint32_t), p->stream));
+    }
+    CK(cudaMemsetAsync(p->rej_flag.get<uint32_t>(), 0, E * sizeof(uint32_t), p->stream));
+    return 0;
+}
+
+int ensure_ws(clairplan_plan* p, uint64_t n_elems, uint32_t nseg) {
+    // radix tables: 256 x (n/2048 + nseg + 1) x (4 + 8) B, first-fit chunk arrays, scans
+    const uint64_t tiles = n_elems / kRadixTile + nseg + 2;
+    const uint64_t bytes = 256ull * tiles * 12 * 2 + (n_elems / 1024 + nseg + 2) * 96 +
+                           (uint64_t)nseg * 64 + (64ull << 20);
+    if (!p->wsbuf.ensure(bytes)) return fail(CLAIRPLAN_ENOMEM, "device allocation failed (workspace)");
+    p->ws.base = p->wsbuf.get<char>();
+    p->ws.cap = p->wsbuf.bytes;
+    p->ws.used = 0;
+    p->ws.overflow = false;
+    return 0;
+}
+
+// K5-K8 on candidates (cand_k, cand_info: count<<16|rank) grouped per worker (wbeg/wlen).
+int assign_tiers(clairplan_plan* p) {
+    const uint32_t J = p->cfg.num_classes, nloc = p->nloc, F = p->part.F;
+    const uint64_t D = p->D;
+    cudaStream_t s = p->stream;
+    bool ok = true;
+    uint8_t* cand_cls = need<uint8_t>(p->cand_cls, D, ok);
+    uint32_t* order = need<uint32_t>(p->order, D, ok);
+    double* ssize = need<double>(p->sorted_size, D, ok);
+    uint32_t* keys = need<uint32_t>(p->keys, D, ok);
+    uint32_t* vals = need<uint32_t>(p->vals, D, ok);
+    uint32_t* okeys = need<uint32_t>(p->okeys, D, ok);
+    uint32_t* ovals = need<uint32_t>(p->ovals, D, ok);
+    uint8_t* taken = need<uint8_t>(p->taken, D, ok);
+    double* seqsz = need<double>(p->seqsz, D, ok);
+    uint32_t* dest = need<uint32_t>(p->dest, D, ok);
+    uint32_t* centries = need<uint32_t>(p->class_entries, D, ok);
+    uint64_t* cstart = need<uint64_t>(p->class_start, (uint64_t)nloc * (J + 1), ok);
+    uint64_t* clen = need<uint64_t>(p->class_len, (uint64_t)nloc * (J + 1), ok);
+    uint32_t* htmp = need<uint32_t>(p->holders_tmp, 3 * D, ok);
+    if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed (tier assignment)");
+    if (int rc = ensure_ws(p, D, nloc)) return rc;
+    Workspace& ws = p->ws;
+    const uint64_t* wbeg = p->wbeg.get<uint64_t>();
+    const uint64_t* wlen = p->wlen.get<uint64_t>();
+    const uint32_t* cand_k = p->cand_k.get<uint32_t>();
+    const uint32_t* cand_info = p->cand_info.get<uint32_t>();
+
+    TileMap tm;
+    build_tilemap(s, wlen, nloc, D, kRadixTile, tm, ws);
+    // K5: tier order
+    const uint32_t maxc = p->generic ? p->maxcount : p->part.E;
+    if (p->generic) launch_generic_count_keys(s, cand_info, D, maxc, keys);
+    else launch_count_keys(s, cand_info, D, maxc, keys);
+    {
+        const uint32_t* kin = keys;
+        const uint32_t* vin = nullptr;
+        uint32_t passes = 0;
+        for (uint32_t shift = 0; shift == 0 || ((uint64_t)maxc >> shift) != 0; shift += 8) {
+            uint32_t* ko = (passes & 1) ? keys : okeys;
+            uint32_t* vo = (passes & 1) ? vals : ovals;
+            const size_t m = ws.mark();
+            radix_pass(s, tm, wbeg, wlen, kin, vin, shift, ko, vo, nullptr, nullptr, ws);
+            ws.release(m);
+            kin = ko;
+            vin = vo;
+            ++passes;
+            p->launches += 5;
+        }
+        CK(cudaMemcpyAsync(order, vin, D * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+    }
+    launch_gather_sizes(s, order, cand_k, p->sizes.get<double>(), D, ssize);
+    CK(cudaMemsetAsync(cand_cls, 0, D, s));
+    p->launches += 2;
+
+    // K6: first fit, class by class
+    uint64_t* sb = ws.scratch<uint64_t>(nloc);
+    uint64_t* sl = ws.scratch<uint64_t>(nloc);
+    CK(cudaMemcpyAsync(sb, wbeg, nloc * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(sl, wlen, nloc * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+    const uint32_t* seq_idx = nullptr;  // pass 1: identity over the tier order
+    const double* seq_sz = ssize;
+    uint32_t* idx_buf[2] = {vals, ovals};
+    for (uint32_t j = 1; j <= J; ++j) {
+        if (j > 1) {
+            // rejects of the previous pass, still in tier order
+            launch_reject_keys(s, taken, D, seq_idx, keys, j % 2 ? idx_buf[0] : idx_buf[1]);
+            const size_t m = ws.mark();
+            TileMap tj;
+            build_tilemap(s, sl, nloc, D, kRadixTile, tj, ws);
+            uint64_t* sc = nullptr;
+            uint32_t* nidx = j % 2 ? idx_buf[1] : idx_buf[0];
+            radix_pass(s, tj, sb, sl, keys, j % 2 ? idx_buf[0] : idx_buf[1], 0, okeys, nidx,
+                       nullptr, &sc, ws);
+            uint64_t* nb = ws.scratch<uint64_t>(2 * (uint64_t)nloc);
+            radix_regions(s, tj, sb, sl, sc, 1, nb, nb + nloc);
+            CK(cudaMemcpyAsync(sb, nb, nloc * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+            CK(cudaMemcpyAsync(sl, nb + nloc, nloc * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+            ws.release(m);
+            launch_gather_seq_sizes(s, nidx, ssize, sb, sl, nloc, seqsz);
+            seq_idx = nidx;
+            seq_sz = seqsz;
+            p->launches += 10;
+        }
+        CK(cudaMemsetAsync(taken, 0, D, s));
+        const size_t m = ws.mark();
+        first_fit_pass(s, sb, sl, nloc, D, seq_sz, p->caps[j - 1], taken, ws);
+        ws.release(m);
+        launch_apply_pass(s, taken, D, seq_idx, order, (uint8_t)j, cand_cls);
+        p->launches += 10;
+    }
+
+    // K7: class lists = stable partition of first-access order by class
+    launch_class_keys(s, cand_cls, D, J, keys);
+    uint64_t* sc = nullptr;
+    radix_pass(s, tm, wbeg, wlen, keys, cand_k, 0, okeys, centries, dest, &sc, ws);
+    radix_regions(s, tm, wbeg, wlen, sc, J + 1, cstart, clen);
+    p->launches += 7;
+    p->class_start_h.resize((size_t)nloc * (J + 1));
+    p->class_len_h.resize((size_t)nloc * (J + 1));
+    CK(cudaMemcpyAsync(p->class_start_h.data(), cstart, p->class_start_h.size() * 8,
+                       cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(p->class_len_h.data(), clen, p->class_len_h.size() * 8,
+                       cudaMemcpyDeviceToHost, s));
+
+    if (p->generic) return generic_holders(p);
+    // K8: holders at their pair slots
+    launch_holder_scatter(s, cand_k, cand_info, cand_cls, dest, wbeg, wlen, cstart, J, nloc,
+                          p->part.wbegin, p->pair_off.get<uint64_t>(), htmp);
+    ++p->launches;
+    CK(cudaStreamSynchronize(s));
+    if (ws.overflow) return fail(CLAIRPLAN_ENOMEM, "internal workspace overflow");
+    uint64_t H = 0;
+    for (uint32_t w = 0; w < nloc; ++w)
+        for (uint32_t d = 0; d < J; ++d) H += p->class_len_h[(size_t)w * (J + 1) + d];
+    p->H = H;
+    if (H == D) {
+        p->holder_off_dev = p->pair_off.get<uint64_t>();
+        p->holders_dev = htmp;
+    } else {
+        uint32_t* hc = need<uint32_t>(p->hcount, F, ok);
+        uint64_t* ho = need<uint64_t>(p->hoff, (uint64_t)F + 1, ok);
+        uint32_t* hl = need<uint32_t>(p->holders, 3 * std::max<uint64_t>(H, 1), ok);
+        if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed (holders)");
+        launch_holder_count(s, p->pair_off.get<uint64_t>(), F, htmp, hc);
+        exclusive_scan(s, hc, F, ho, ws);
+        launch_holder_compact(s, p->pair_off.get<uint64_t>(), F, htmp, ho, hl);
+        p->launches += 5;
+        p->holder_off_dev = ho;
+        p->holders_dev = hl;
+    }
+    return 0;
+}
+
+int build_seed_path(clairplan_plan* p) {
+    cudaStream_t s = p->stream;
+    const Part& part = p->part;
+    const uint32_t F = part.F, E = part.E, nloc = p->nloc;
+    bool ok = true;
+    uint32_t* stream_buf = need<uint32_t>(p->stream_buf, p->A, ok);
+    uint32_t* info = need<uint32_t>(p->info, (uint64_t)E * F, ok);
+    uint32_t* pcount = need<uint32_t>(p->pair_count, F, ok);
+    uint64_t* poff = need<uint64_t>(p->pair_off, (uint64_t)F + 1, ok);
+    uint32_t* segcnt = need<uint32_t>(p->segcnt, (uint64_t)nloc * E, ok);
+    uint64_t* segoff = need<uint64_t>(p->seg_off, (uint64_t)nloc * E + 1, ok);
+    uint64_t* wbeg = need<uint64_t>(p->wbeg, nloc, ok);
+    uint64_t* wlen = need<uint64_t>(p->wlen, nloc, ok);
+    if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed (streams / histograms)");
+    if (int rc = ensure_ws(p, std::max<uint64_t>((uint64_t)nloc * E, F), nloc)) return rc;
+    if (int rc = alloc_rej(p, E)) return rc;
+    uint32_t hs, nw, warps;
+    size_t smem;
+    if (sample_pass_config(part, &hs, &nw, &warps, &smem))
+        return fail(CLAIRPLAN_EINVAL, "epochs/workers too large for the device histogram");
+
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        p->launches = 0;
+        CK(cudaEventRecord(p->ev0, s));
+        // K1-K3
+        if (int rc = enqueue_perms(p, stream_buf, info, nullptr, 0, E)) return rc;
+        // K4a
+        launch_sample_pass(s, part, info, pcount, hs, nw, warps, smem);
+        exclusive_scan(s, pcount, F, poff, p->ws);
+        // K4b
+        launch_seg_count(s, part, stream_buf, info, segcnt);
+        exclusive_scan(s, segcnt, (uint64_t)nloc * E, segoff, p->ws);
+        p->launches += 8;
+        std::vector<uint32_t> flags(E);
+        uint64_t D = 0;
+        CK(cudaMemcpyAsync(&D, segoff + (uint64_t)nloc * E, sizeof(uint64_t),
+                           cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(flags.data(), p->rej_flag.get<uint32_t>(), E * sizeof(uint32_t),
+                           cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        bool any = false;
+        if (int rc = resolve_rejections(p, flags, &any)) return rc;
+        if (any) continue;  // rebuild with the completed rejection tables
+        p->D = D;
+        if (D >= 0xFFFFFFFFull)
+            return fail(CLAIRPLAN_EOVERFLOW, "more than 2^32-1 (worker, sample) pairs in one handle; "
+                                             "shard the workers over several handles");
+        uint32_t* ck = need<uint32_t>(p->cand_k, D, ok);
+        uint32_t* ci = need<uint32_t>(p->cand_info, D, ok);
+        if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed (candidates)");
+        launch_seg_write(s, part, stream_buf, info, segoff, ck, ci);
+        launch_worker_segments(s, segoff, nloc, E, wbeg, wlen);
+        p->launches += 2;
+        if (p->cfg.num_classes > 0) {
+            if (int rc = assign_tiers(p)) return rc;
+        } else {
+            p->H = 0;
+            uint64_t* ho = need<uint64_t>(p->hoff, (uint64_t)F + 1, ok);
+            if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed");
+            CK(cudaMemsetAsync(ho, 0, ((uint64_t)F + 1) * 8, s));
+            p->holder_off_dev = ho;
+            p->holders_dev = nullptr;
+            p->class_start_h.assign(nloc, 0);
+            p->class_len_h.assign(nloc, 0);
+        }
+        CK(cudaEventRecord(p->ev1, s));
+        CK(cudaEventSynchronize(p->ev1));
+        CK(cudaGetLastError());
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
+        p->device_ms = ms;
+        p->built = true;
+        return 0;
+    }
+    return fail(CLAIRPLAN_ECUDA, "rejection tables did not converge");
+}
+
+}  // namespace clairplan
+
+// ---------------------------------------------------------------------------------------
+extern "C" {
+
+int clairplan_version(void) { return 1; }
+
+const char* clairplan_last_error(void) { return g_err.c_str(); }
+
+int clairplan_validate(const clairplan_config* c) {
+    if (!c) return fail(CLAIRPLAN_EINVAL, "null config");
+    return validate_partition(c->samples, c->num_workers, c->global_batch, c->epochs);
+}
+
+int clairplan_create(const clairplan_config* c, clairplan_t* out) {
+    if (!c || !out) return fail(CLAIRPLAN_EINVAL, "null argument");
+    *out = nullptr;
+    if (int rc = validate_partition(c->samples, c->num_workers, c->global_batch, c->epochs))
+        return rc;
+    if (c->epochs > 65535) return fail(CLAIRPLAN_EINVAL, "device plan supports at most 65535 epochs");
+    if (c->num_classes > 254) return fail(CLAIRPLAN_EINVAL, "device plan supports at most 254 cache classes");
+    if (c->num_classes && !c->capacities_mb) return fail(CLAIRPLAN_EINVAL, "capacities_mb is null");
+    if (!c->sizes_mb) return fail(CLAIRPLAN_EINVAL, "sizes_mb is null");
+    uint32_t wb = c->worker_begin, we = c->worker_end;
+    if (wb == 0 && we == 0) we = c->num_workers;
+    if (wb >= we || we > c->num_workers) return fail(CLAIRPLAN_EINVAL, "invalid worker range");
+    if (int rc = check_device(c->device)) return rc;
+    auto* p = new clairplan_plan();
+    p->device = c->device;
+    p->cfg = *c;
+    p->cfg.worker_begin = wb;
+    p->cfg.worker_end = we;
+    p->caps.assign(c->capacities_mb, c->capacities_mb + c->num_classes);
+    p->cfg.capacities_mb = nullptr;
+    p->cfg.sizes_mb = nullptr;
+    p->part = make_part(c->samples, c->num_workers, c->global_batch, c->epochs, c->drop_last != 0,
+                        wb, we);
+    p->nloc = we - wb;
+    p->key = derive_key(c->seed, kPermTag);
+    Part tmp = p->part;
+    p->A = (uint64_t)tmp.E * (tmp.prefix_len(we) - tmp.prefix_len(wb));
+    if (p->A >= 0xFFFFFFFFull) {
+        delete p;
+        return fail(CLAIRPLAN_EOVERFLOW, "more than 2^32-1 stream entries in one handle; shard the "
+                                         "workers over several handles");
+    }
+    if (cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreate(&p->ev0) != cudaSuccess || cudaEventCreate(&p->ev1) != cudaSuccess) {
+        delete p;
+        return fail(CLAIRPLAN_ECUDA, "stream/event creation failed");
+    }
+    if (!p->sizes.ensure((size_t)c->samples * sizeof(double))) {
+        delete p;
+        return fail(CLAIRPLAN_ENOMEM, "device allocation failed (sizes)");
+    }
+    cudaError_t e = cudaMemcpy(p->sizes.get<double>(), c->sizes_mb, (size_t)c->samples * 8,
+                               c->sizes_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        delete p;
+        return fail(CLAIRPLAN_ECUDA, std::string("sizes upload: ") + cudaGetErrorString(e));
+    }
+    *out = p;
+    return 0;
+}
+
+int clairplan_destroy(clairplan_t p) {
+    if (!p) return 0;
+    cudaSetDevice(p->device);
+    delete p;
+    return 0;
+}
+
+int clairplan_build(clairplan_t p) {
+    if (!p) return fail(CLAIRPLAN_EINVAL, "null plan");
+    if (p->generic) return fail(CLAIRPLAN_EINVAL, "plan was created from explicit streams");
+    CK(cudaSetDevice(p->device));
+    p->built = false;
+    return build_seed_path(p);
+}
+
+int clairplan_stats_get(clairplan_t p, clairplan_stats* s) {
+    if (!p || !s) return fail(CLAIRPLAN_EINVAL, "null argument");
+    s->accesses = p->A;
+    s->pairs = p->D;
+    s->holders = p->H;
+    s->rejections = p->rejections;
+    s->device_ms = p->device_ms;
+    return 0;
+}
+
+uint64_t clairplan_launch_count(clairplan_t p) { return p ? p->launches : 0; }
+
+int clairplan_device_streams(clairplan_t p, const uint32_t** entries, uint64_t* total) {
+    if (!p || !p->built) return fail(CLAIRPLAN_EINVAL, "plan not built");
+    *entries = p->stream_buf.get<uint32_t>();
+    *total = p->A;
+    return 0;
+}
+
+uint64_t clairplan_stream_offset(clairplan_t p, uint32_t w) {
+    if (!p) return 0;
+    if (w < p->part.wbegin) w = p->part.wbegin;
+    if (w > p->part.wend) w = p->part.wend;
+    return p->part.stream_offset(w);
+}
+
+int clairplan_class_list_bounds(clairplan_t p, uint64_t* off, uint64_t* len) {
+    if (!p || !p->built) return fail(CLAIRPLAN_EINVAL, "plan not built");
+    const uint32_t J = p->cfg.num_classes;
+    for (uint32_t w = 0; w < p->nloc; ++w)
+        for (uint32_t j = 0; j < J; ++j) {
+            off[(size_t)w * J + j] = p->class_start_h[(size_t)w * (J + 1) + j];
+            len[(size_t)w * J + j] = p->class_len_h[(size_t)w * (J + 1) + j];
+        }
+    return 0;
+}
+
+int clairplan_device_class_lists(clairplan_t p, const uint32_t** entries) {
+    if (!p || !p->built) return fail(CLAIRPLAN_EINVAL, "plan not built");
+    *entries = p->class_entries.get<uint32_t>();
+    return 0;
+}
+
+int clairplan_device_holders(clairplan_t p, const uint64_t** offsets, const uint32_t** holders,
+                             uint64_t* count) {
+    if (!p || !p->built) return fail(CLAIRPLAN_EINVAL, "plan not built");
+    *offsets = p->holder_off_dev;
+    *holders = p->holders_dev;
+    *count = p->H;
+    return 0;
+}
+
+int clairplan_export_stream(clairplan_t p, uint32_t w, uint32_t* out, uint64_t cap, uint64_t* len) {
+    if (!p || !p->built) return fail(CLAIRPLAN_EINVAL, "plan not built");
+    if (w < p->part.wbegin || w >= p->part.wend) return fail(CLAIRPLAN_EINVAL, "worker not in plan");
+    const uint64_t a = p->part.stream_offset(w), b = p->part.stream_offset(w + 1);
+    *len = b - a;
+    if (cap < b - a) return fail(CLAIRPLAN_ERANGE, "output buffer too small");
+    CK(cudaSetDevice(p->device));
+    CK(cudaMemcpy(out, p->stream_buf.get<uint32_t>() + a, (b - a) * 4, cudaMemcpyDeviceToHost));
+    return 0;
+}
+
+int clairplan_export_streams(clairplan_t p, uint32_t* out, uint64_t cap) {
+    if (!p || !p->built) return fail(CLAIRPLAN_EINVAL, "plan not built");
+    if (cap < p->A) return fail(CLAIRPLAN_ERANGE, "output buffer too small");
+    CK(cudaSetDevice(p->device));
+    CK(cudaMemcpy(out, p->stream_buf.get<uint32_t>(), p->A * 4, cudaMemcpyDeviceToHost));
+    return 0;
+}
+
+int clairplan_export_class_lists(clairplan_t p, uint32_t* out, uint64_t cap) {
+    if (!p || !p->built) return fail(CLAIRPLAN_EINVAL, "plan not built");
+    const uint32_t J = p->cfg.num_classes;
+    uint64_t need_n = 0;
+    for (uint32_t w = 0; w < p->nloc; ++w)
+        for (uint32_t j = 0; j < J; ++j) need_n += p->class_len_h[(size_t)w * (J + 1) + j];
+    if (cap < need_n) return fail(CLAIRPLAN_ERANGE, "output buffer too small");
+    CK(cudaSetDevice(p->device));
+    uint64_t o = 0;
+    for (uint32_t w = 0; w < p->nloc; ++w) {
+        // classes 1..J of a worker are adjacent in the class-partitioned array
+        const uint64_t a = p->class_start_h[(size_t)w * (J + 1)];
+        uint64_t n = 0;
+        for (uint32_t j = 0; j < J; ++j) n += p->class_len_h[(size_t)w * (J + 1) + j];
+        if (n) CK(cudaMemcpy(out + o, p->class_entries.get<uint32_t>() + a, n * 4, cudaMemcpyDeviceToHost));
+        o += n;
+    }
+    return 0;
+}
+
+int clairplan_export_holders(clairplan_t p, uint64_t* offsets, uint32_t* holders, uint64_t cap) {
+    if (!p || !p->built) return fail(CLAIRPLAN_EINVAL, "plan not built");
+    if (cap < p->H) return fail(CLAIRPLAN_ERANGE, "output buffer too small");
+    CK(cudaSetDevice(p->device));
+    CK(cudaMemcpy(offsets, p->holder_off_dev, ((uint64_t)p->part.F + 1) * 8, cudaMemcpyDeviceToHost));
+    if (p->H) CK(cudaMemcpy(holders, p->holders_dev, p->H * 12, cudaMemcpyDeviceToHost));
+    return 0;
+}
+
+int clairplan_export_counts(clairplan_t p, uint32_t w, uint32_t* counts) {
+    if (!p || !p->built) return fail(CLAIRPLAN_EINVAL, "plan not built");
+    if (w < p->part.wbegin || w >= p->part.wend) return fail(CLAIRPLAN_EINVAL, "worker not in plan");
+    CK(cudaSetDevice(p->device));
+    const uint32_t wl = w - p->part.wbegin;
+    uint64_t b = 0, L = 0;
+    CK(cudaMemcpy(&b, p->wbeg.get<uint64_t>() + wl, 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&L, p->wlen.get<uint64_t>() + wl, 8, cudaMemcpyDeviceToHost));
+    DevBuf tmp;
+    if (!tmp.ensure((size_t)p->part.F * 4)) return fail(CLAIRPLAN_ENOMEM, "device allocation failed");
+    CK(cudaMemsetAsync(tmp.p, 0, (size_t)p->part.F * 4, p->stream));
+    launch_dense_counts(p->stream, p->cand_k.get<uint32_t>(), p->cand_info.get<uint32_t>(), b, L,
+                        tmp.get<uint32_t>());
+    CK(cudaStreamSynchronize(p->stream));
+    CK(cudaMemcpy(counts, tmp.p, (size_t)p->part.F * 4, cudaMemcpyDeviceToHost));
+    return 0;
+}
+
+int clairplan_epoch_permutation(uint64_t seed, uint32_t epoch, uint32_t samples, uint32_t* out,
+                                int device) {
+    if (samples < 1) return fail(CLAIRPLAN_EINVAL, "permutation needs samples >= 1");  // access.cpp:53
+    if (int rc = check_device(device)) return rc;
+    clairplan_plan p;
+    p.device = device;
+    CK(cudaStreamCreateWithFlags(&p.stream, cudaStreamNonBlocking));
+    p.part = make_part(samples, 1, 1, 1, true, 0, 1);
+    p.key = derive_key(seed, kPermTag);
+    p.rej_ebase = epoch;
+    if (int rc = alloc_rej(&p, 1)) return rc;
+    DevBuf perm;
+    if (!perm.ensure((size_t)samples * 4)) return fail(CLAIRPLAN_ENOMEM, "device allocation failed");
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        if (int rc = enqueue_perms(&p, nullptr, nullptr, perm.get<uint32_t>(), epoch, 1)) return rc;
+        std::vector<uint32_t> flags(1, 0);
+        CK(cudaMemcpyAsync(&flags[0], p.rej_flag.get<uint32_t>(), 4,
+                           cudaMemcpyDeviceToHost, p.stream));
+        CK(cudaStreamSynchronize(p.stream));
+        bool any = false;
+        if (int rc = resolve_rejections(&p, flags, &any)) return rc;
+        if (any) continue;
+        CK(cudaMemcpy(out, perm.p, (size_t)samples * 4, cudaMemcpyDeviceToHost));
+        return 0;
+    }
+    return fail(CLAIRPLAN_ECUDA, "rejection tables did not converge");
+}
+
+}  // extern "C"

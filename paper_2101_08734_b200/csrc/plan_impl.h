@@ -1,0 +1,141 @@
+// Private host-side declarations of the clairplan handle (plan.cu, generic.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/clairplan.h"
+#include "internal.h"
+
+namespace clairplan {
+
+extern thread_local std::string g_err;
+
+inline int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CK(call)                                                                      \
+    do {                                                                              \
+        cudaError_t e_ = (call);                                                      \
+        if (e_ != cudaSuccess)                                                        \
+            return fail(CLAIRPLAN_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    template <typename T>
+    T* get() const { return static_cast<T*>(p); }
+    // grow-only; returns false on allocation failure
+    bool ensure(size_t need) {
+        if (need <= bytes) return true;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        size_t b = need + (need >> 3) + 256;
+        if (cudaMalloc(&p, b) != cudaSuccess) {
+            cudaGetLastError();
+            p = nullptr;
+            return false;
+        }
+        bytes = b;
+        return true;
+    }
+};
+
+constexpr uint32_t kRejCap = 16;
+
+inline int check_device(int device) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        return fail(CLAIRPLAN_ENODEV, "no CUDA device available (clairplan has no CPU fallback)");
+    }
+    if (device < 0 || device >= n) return fail(CLAIRPLAN_ENODEV, "CUDA device ordinal out of range");
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+        return fail(CLAIRPLAN_ENODEV, "clairplan kernels are built for sm_100a (B200) only");
+    CK(cudaSetDevice(device));
+    return 0;
+}
+
+inline int validate_partition(uint64_t F, uint32_t N, uint32_t B, uint32_t E) {
+    // access.cpp:41-50, same messages
+    if (F < 1) return fail(CLAIRPLAN_EINVAL, "dataset must have at least one sample");
+    if (N < 1) return fail(CLAIRPLAN_EINVAL, "num_workers must be >= 1");
+    if (E < 1) return fail(CLAIRPLAN_EINVAL, "epochs must be >= 1");
+    if (B < N) return fail(CLAIRPLAN_EINVAL, "global batch must be >= num_workers");
+    if (B > F)
+        return fail(CLAIRPLAN_EINVAL, "global batch " + std::to_string(B) +
+                                          " exceeds dataset size " + std::to_string(F));
+    return 0;
+}
+
+}  // namespace clairplan
+
+using namespace clairplan;
+
+struct clairplan_plan {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    clairplan_config cfg{};
+    std::vector<double> caps;
+    Part part{};
+    uint32_t nloc = 0;
+    uint64_t key = 0;
+    uint64_t A = 0, D = 0, H = 0, rejections = 0;
+    double device_ms = 0;
+    bool built = false;
+    bool generic = false;
+    uint64_t launches = 0;
+    uint32_t rej_ebase = 0;  // rejection tables are indexed by epoch - rej_ebase
+
+    DevBuf sizes, stream_buf, info, pair_count, pair_off, segcnt, seg_off, wbeg, wlen;
+    DevBuf cand_k, cand_info, cand_cls, order, sorted_size;
+    DevBuf keys, vals, okeys, ovals, taken, seqsz, dest;
+    DevBuf class_entries, class_start, class_len, holders, holders_tmp, hcount, hoff;
+    DevBuf head, next, q, scratch, counters, rej_flag, rej_step, rej_cum, rej_count;
+    DevBuf wsbuf;
+    DevBuf cand_w, dfirst, dcounts;  // explicit-stream (generic) path
+    uint32_t maxcount = 0;           // generic path: largest frequency value
+    Workspace ws;
+
+    std::vector<uint64_t> class_start_h, class_len_h;  // [(w, d)] d in 0..J
+    std::vector<uint32_t> rej_step_h, rej_cum_h, rej_count_h;
+    const uint64_t* holder_off_dev = nullptr;
+    const uint32_t* holders_dev = nullptr;
+
+    ~clairplan_plan() {
+        if (stream) cudaStreamDestroy(stream);
+        if (ev0) cudaEventDestroy(ev0);
+        if (ev1) cudaEventDestroy(ev1);
+    }
+};
+
+
+namespace clairplan {
+template <typename T>
+inline T* need(DevBuf& b, uint64_t n, bool& ok) {
+    if (!b.ensure(std::max<uint64_t>(n, 1) * sizeof(T))) ok = false;
+    return b.get<T>();
+}
+
+
+int assign_tiers(clairplan_plan* p);
+int generic_holders(clairplan_plan* p);
+void launch_generic_count_keys(cudaStream_t s, const uint32_t* cnt, uint64_t n, uint32_t maxc,
+                               uint32_t* keys);
+int ensure_ws(clairplan_plan* p, uint64_t n_elems, uint32_t nseg);
+}  // namespace clairplan

@@ -1,0 +1,197 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference / the oracle.
+
+Bit-exact for everything: permutations, streams, tier assignments, prefetch orders, holder
+CSR (integer/index work plus an order-sensitive double chain reproduced exactly)."""
+import os
+
+import numpy as np
+import pytest
+
+from _oracle import Plan as OPlan
+from _oracle import plans_equal
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+@pytest.fixture(scope="module")
+def cp():
+    from paper_2101_08734_b200 import clairplan
+    return clairplan
+
+
+def device_plan(cp, seed, F, N, B, E, dl, caps, sizes):
+    p = cp.Plan(seed, F, cp.PartitionSpec(N, B, E, dl), caps, sizes).build()
+    offs, hold = p.holders()
+    out = OPlan(N, len(caps), [p.stream(w) for w in range(N)], p.class_lists(), offs, hold)
+    out.stats = p.stats()
+    out.launches = p.launch_count()
+    p.close()
+    return out
+
+
+def load_perm(name):
+    with open(os.path.join(HERE, "golden", name)) as f:
+        return np.array(f.read().split(), np.uint32)
+
+
+def test_perm_golden(cp):
+    assert np.array_equal(cp.epoch_permutation(42, 0, 8), load_perm("perm_seed42_epoch0_f8.txt"))
+    assert np.array_equal(cp.epoch_permutation(42, 1, 8), load_perm("perm_seed42_epoch1_f8.txt"))
+    assert np.array_equal(cp.epoch_permutation(42, 0, 16), load_perm("perm_seed42_epoch0_f16.txt"))
+    assert list(cp.epoch_permutation(123, 0, 1)) == [0]
+    with pytest.raises(ValueError, match="permutation needs samples >= 1"):
+        cp.epoch_permutation(1, 0, 0)
+
+
+def test_perm_random_small(cp, port):
+    rng = np.random.default_rng(2)
+    for _ in range(150):
+        F = int(rng.integers(1, 5000))
+        seed = int(rng.integers(0, 2**63))
+        e = int(rng.integers(0, 1000))
+        assert np.array_equal(cp.epoch_permutation(seed, e, F), port.epoch_permutation(seed, e, F)), \
+            (seed, e, F)
+
+
+@pytest.mark.parametrize("F,epoch", [(1_281_167, 0), (1_281_167, 89), (262_144, 7),
+                                     (14_197_122, 3)])
+def test_perm_large(cp, ref, F, epoch):
+    assert np.array_equal(cp.epoch_permutation(42, epoch, F), ref.epoch_permutation(42, epoch, F))
+
+
+CASES = [
+    (42, 2000, 4, 128, 10, True, [20.0, 900.0], (0.1077, 0.1)),
+    (7, 1500, 3, 7, 5, False, [5.0, 30.0], (0.1, 0.3)),
+    (9, 1000, 16, 16, 6, True, [1e6, 1e6], (1.0, 0.0)),
+    (1, 777, 5, 13, 4, False, [3.0], (0.5, 0.5)),
+    (3, 600, 2, 9, 3, True, [2.0, 3.0, 40.0], (0.2, 0.1)),
+    (11, 500, 4, 4, 20, True, [], (0.1, 0.1)),
+    (5, 24, 2, 4, 2, False, [16.0, 8.0], (1.0, 0.0)),      # test_policies.cpp:328-350 shape
+    (7, 100, 4, 20, 3, False, [10.0, 1e6], (1.0, 0.0)),    # test_policies.cpp:69-102 shape
+    (11, 60, 2, 10, 4, False, [7.5, 13.0], (1.0, 0.4)),    # test_policies.cpp:104-125 shape
+    (2, 30, 3, 6, 4, False, [5.0, 5.0], (1.0, 0.0)),
+    (77, 7, 1, 3, 2, False, [100.0], (1.0, 0.0)),
+    (13, 5000, 7, 300, 33, True, [25.0, 120.0], (0.1077, 0.2)),
+    (21, 4096, 64, 64, 40, False, [3.0, 9.0], (0.1, 0.05)),
+    (8, 3000, 5, 5, 300, True, [40.0, 400.0], (0.1, 0.1)),   # E > 255: two radix digits
+]
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_plan_small_matches_reference(cp, ref, case):
+    seed, F, N, B, E, dl, caps, (mu, sd) = case
+    sizes = ref.generate_sizes(F, mu, sd, None, 1)
+    a = ref.plan(seed, F, N, B, E, dl, caps, sizes)
+    b = device_plan(cp, seed, F, N, B, E, dl, caps, sizes)
+    assert plans_equal(a, b) is None
+
+
+def test_plan_random_configs(cp, ref):
+    rng = np.random.default_rng(9)
+    for _ in range(25):
+        F = int(rng.integers(10, 4000))
+        N = int(rng.integers(1, 40))
+        B = int(rng.integers(N, min(F, 8 * N + 30) + 1))
+        E = int(rng.integers(1, 50))
+        dl = bool(rng.integers(0, 2))
+        J = int(rng.integers(0, 4))
+        caps = [float(x) for x in rng.uniform(0.5, 200.0, J)]
+        sizes = rng.uniform(0.001, 2.0, F) if rng.integers(0, 2) else np.full(F, 0.37)
+        seed = int(rng.integers(0, 2**62))
+        a = ref.plan(seed, F, N, B, E, dl, caps, sizes)
+        b = device_plan(cp, seed, F, N, B, E, dl, caps, sizes)
+        assert plans_equal(a, b) is None, (seed, F, N, B, E, dl, caps)
+
+
+def config_sizes(ref, which):
+    if which in (1, 2):
+        return ref.generate_sizes(1_281_167, 0.1077, 0.1, 135_000.0, 1)
+    if which == 3:
+        return ref.generate_sizes(262_144, 16.0, 0.0, None, 1)
+    raise ValueError(which)
+
+
+def test_config1_imagenet1k_e10_n4(cp, ref):
+    sizes = config_sizes(ref, 1)
+    a = ref.plan(42, 1_281_167, 4, 128, 10, True, [120_000.0, 900_000.0], sizes)
+    b = device_plan(cp, 42, 1_281_167, 4, 128, 10, True, [120_000.0, 900_000.0], sizes)
+    assert plans_equal(a, b) is None
+    assert b.stats["accesses"] == 12_811_520 and b.stats["pairs"] == 4_836_013
+
+
+def test_config3_cosmoflow_e100_n1024(cp, ref):
+    sizes = config_sizes(ref, 3)
+    a = ref.plan(42, 262_144, 1024, 16 * 1024, 100, True, [120_000.0, 900_000.0], sizes)
+    b = device_plan(cp, 42, 262_144, 1024, 16 * 1024, 100, True, [120_000.0, 900_000.0], sizes)
+    assert plans_equal(a, b) is None
+    assert b.stats["pairs"] == 24_985_949
+
+
+def test_config2_imagenet1k_e90_n256(cp, ref):
+    sizes = config_sizes(ref, 2)
+    a = ref.plan(42, 1_281_167, 256, 32 * 256, 90, True, [120_000.0, 900_000.0], sizes,
+                 mode=1, threads=os.cpu_count() or 4)
+    b = device_plan(cp, 42, 1_281_167, 256, 32 * 256, 90, True, [120_000.0, 900_000.0], sizes)
+    assert plans_equal(a, b) is None
+    assert b.stats["accesses"] == 115_015_680 and b.stats["pairs"] == 97_174_801
+
+
+def test_generic_assign_matches_reference(cp, ref):
+    # test_policies.cpp:54-67
+    st = cp.AccessStream(0, np.array([0, 1, 0, 0, 1, 0, 0], np.uint32))
+    a = cp.nopfs_assign_caches([cp.FrequencyTable(0, np.array([5, 2], np.uint32))], [1.0, 10.0],
+                               [1.0, 1.0], [st])
+    assert list(a.class_lists[0][0]) == [0] and list(a.class_lists[0][1]) == [1]
+    rng = np.random.default_rng(5)
+    for _ in range(20):
+        N, F = int(rng.integers(1, 5)), int(rng.integers(5, 60))
+        streams = [rng.integers(0, F, int(rng.integers(0, 80))).astype(np.uint32) for _ in range(N)]
+        counts = rng.integers(0, 4, (N, F)).astype(np.uint32)
+        sizes = rng.uniform(0.1, 2.0, F)
+        caps = [float(rng.uniform(1, 10)), float(rng.uniform(1, 30))]
+        r = ref.assign_from_streams(streams, counts, caps, sizes)
+        g = cp.nopfs_assign_caches([cp.FrequencyTable(w, counts[w]) for w in range(N)], caps, sizes,
+                                   [cp.AccessStream(w, streams[w]) for w in range(N)])
+        got = OPlan(N, 2, streams, g.class_lists, g.holder_offsets, g.holders)
+        assert plans_equal(r, got, check_streams=False) is None
+
+
+def test_counts_entry_points(cp, ref):
+    F, N, B, E = 30, 3, 6, 4
+    part = cp.PartitionSpec(N, B, E, False)
+    # test_access.cpp:107-131: conservation and worker_access_counts == access_frequencies
+    streams = cp.build_access_streams(2, F, part)
+    rp = ref.plan(2, F, N, B, E, False, [], np.ones(F), keep=True)
+    for w in range(N):
+        assert np.array_equal(streams[w].entries, rp.streams[w])
+        assert np.array_equal(streams[w].epoch_offsets, rp.epoch_offsets[w])
+        assert np.array_equal(streams[w].batch_offsets, rp.batch_offsets[w])
+        for eb, ee in ((0, E), (1, 3), (2, 2), (0, E + 3)):
+            f = cp.access_frequencies(streams[w], F, eb, ee)
+            assert np.array_equal(f.counts, ref.access_frequencies(rp, w, eb, ee, F))
+        assert np.array_equal(cp.worker_access_counts(2, F, part, w),
+                              ref.worker_access_counts(2, F, N, B, E, False, w))
+    ref.free(rp)
+    allc = cp.all_access_counts(2, F, part)
+    assert np.array_equal(allc, ref.all_access_counts(2, F, N, B, E, False))
+    assert np.all(allc.sum(axis=0) == E)
+    # acceptance.cpp:102-107 shape (Lemma-1 suite input): B = N, no drop
+    for N in (2, 4, 16):
+        p = cp.PartitionSpec(N, N, 10, False)
+        assert np.array_equal(cp.all_access_counts(3, 1000, p),
+                              ref.all_access_counts(3, 1000, N, N, 10, False))
+
+
+def test_rebuild_is_deterministic(cp, ref):
+    sizes = ref.generate_sizes(3000, 0.1, 0.1, None, 1)
+    p = cp.Plan(5, 3000, cp.PartitionSpec(6, 60, 12, True), [30.0, 100.0], sizes)
+    p.build()
+    s1, c1, h1 = p.streams_flat(), p.class_lists(), p.holders()
+    p.build()
+    s2, c2, h2 = p.streams_flat(), p.class_lists(), p.holders()
+    assert np.array_equal(s1, s2)
+    assert all(np.array_equal(x, y) for a, b in zip(c1, c2) for x, y in zip(a, b))
+    assert np.array_equal(h1[0], h2[0]) and np.array_equal(h1[1], h2[1])
+    p.close()
