@@ -1,0 +1,356 @@
+#!/usr/bin/env python
+"""Benchmark of the NoPFS clairvoyant plan build (BASELINE.json metric).
+
+A step = one full plan build (seed -> every epoch's permutation -> per-worker access
+streams -> (count, first-access) per (worker, sample) -> tier assignment -> prefetch orders
+-> holder CSR) of the ImageNet-1k-shape, 90-epoch, 256-worker configuration
+(BASELINE.json configs[1]).  `value` = sample accesses per second of the device-resident
+build (sizes already in HBM), timed with the library's CUDA events on its stream; `e2e` is
+the same plan through the C ABI with host buffers (sizes H2D, every output D2H) inside the
+timed region.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C]
+
+Multi-GPU (torchrun, one rank per GPU): the workers are sharded into contiguous ranges, every
+rank builds its range's plan (epoch permutations are recomputed per rank: they are
+seed-generated) and the holder-CSR offsets are merged with an NCCL all-gather of the
+per-sample holder counts; time = max over ranks.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+CONFIGS = {
+    # F, N, per-worker batch, E, sizes (mean, sigma, total)   -- BASELINE.md §5 / SURVEY §8(d)
+    1: dict(F=1_281_167, N=4, b=32, E=10, sizes=(0.1077, 0.1, 135_000.0),
+            name="imagenet1k-e10-n4"),
+    2: dict(F=1_281_167, N=256, b=32, E=90, sizes=(0.1077, 0.1, 135_000.0),
+            name="imagenet1k-e90-n256"),
+    3: dict(F=262_144, N=1024, b=16, E=100, sizes=(16.0, 0.0, None), name="cosmoflow16-e100-n1024"),
+    4: dict(F=14_197_122, N=1024, b=32, E=90, sizes=(0.1077, 0.2, 1_500_000.0),
+            name="imagenet22k-e90-n1024"),
+    5: dict(F=100_000_000, N=8192, b=32, E=100, sizes=(0.1077, 0.1, None),
+            name="synthetic100m-e100-n8192"),
+}
+SEED = 42
+CAPS = (120_000.0, 900_000.0)  # scenarios.cpp:25-40 (RAM, SSD); staging is class 0, unpacked
+METRIC = "clairvoyant plan build: sample-accesses/sec and plan latency at 1/2/4/8 B200"
+UNIT = "sample-accesses/s"
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0")),
+            int(os.environ.get("WORLD_SIZE", "1")))
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def accesses_of(cfg):
+    B = cfg["b"] * cfg["N"]
+    return cfg["E"] * (cfg["F"] // B) * B
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region (B200_PROFILING.md)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_reference_plan(cfg, sizes, threads):
+    """The reference's own functions (oracle/_ref, per-worker harness on all host threads);
+    only this leg and --impl reference execute anything under oracle/."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from _oracle import Ref
+    ref = Ref()
+    t0 = time.perf_counter()
+    ref.plan(SEED, cfg["F"], cfg["N"], cfg["b"] * cfg["N"], cfg["E"], True, list(CAPS), sizes,
+             mode=1, threads=threads)
+    return time.perf_counter() - t0
+
+
+def run_reference(args, cfg):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    from paper_2101_08734_b200 import clairplan as cp
+    mu, sd, tot = cfg["sizes"]
+    sizes = cp.generate_sizes(cfg["F"], mu, sd, tot, 1)
+    for _ in range(args.warmup):
+        cpu_reference_plan(cfg, sizes, threads)
+    times = [cpu_reference_plan(cfg, sizes, threads) for _ in range(args.steps)]
+    A = accesses_of(cfg)
+    t = statistics.mean(times)
+    v = A / t
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic (seed-generated, BASELINE config shapes)",
+        "config": {"workload": cfg["name"], "samples": cfg["F"], "workers": cfg["N"],
+                   "per_worker_batch": cfg["b"], "epochs": cfg["E"], "seed": SEED},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": f"full {cfg['name']} plan via the reference's epoch_permutation"
+                                   "/access_frequencies/nopfs_assign_caches/build_index "
+                                   "(per-worker decomposition on all host threads)"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def run_ours(args, cfg):
+    import torch
+    from paper_2101_08734_b200 import clairplan as cp
+
+    rank, local, world = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    N = cfg["N"]
+    wb, we = rank * N // world, (rank + 1) * N // world
+    mu, sd, tot = cfg["sizes"]
+    sizes = cp.generate_sizes(cfg["F"], mu, sd, tot, 1)
+    part = cp.PartitionSpec(N, cfg["b"] * N, cfg["E"], True)
+    plan = cp.Plan(SEED, cfg["F"], part, list(CAPS), sizes, device=local, worker_range=(wb, we))
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+            torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        plan.build()
+    barrier()
+    sampler = ClockSampler(local)
+    sampler.start()
+    dev_ms, stage = [], None
+    launches = 0
+    t_wall = time.perf_counter()
+    for _ in range(args.steps):
+        flush.fill_(1)
+        torch.cuda.synchronize()
+        plan.build()
+        st = plan.stats()
+        dev_ms.append(st["device_ms"])
+        launches += plan.launch_count()
+    barrier()
+    t_wall = time.perf_counter() - t_wall
+    clocks = sampler.stop()
+    stage_ms = {}
+    import ctypes
+    L = cp.lib()
+    L.clairplan_stage_times.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double),
+                                        ctypes.c_uint32]
+    L.clairplan_stage_name.restype = ctypes.c_char_p
+    buf = (ctypes.c_double * 16)()
+    ns = L.clairplan_stage_times(plan._h, buf, 16)
+    for i in range(ns):
+        stage_ms[L.clairplan_stage_name(i).decode()] = round(buf[i], 4)
+
+    total_ms = float(sum(dev_ms))
+    A_loc, D_loc = st["accesses"], st["pairs"]
+    vec = torch.tensor([total_ms, float(A_loc), float(D_loc)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        mx = vec.clone()
+        torch.distributed.all_reduce(mx[:1], op=torch.distributed.ReduceOp.MAX)
+        sm = vec.clone()
+        torch.distributed.all_reduce(sm, op=torch.distributed.ReduceOp.SUM)
+        total_ms, A_all, D_all = float(mx[0]), float(sm[1]), float(sm[2])
+    else:
+        A_all, D_all = float(A_loc), float(D_loc)
+    ms_step = total_ms / args.steps
+    value = A_all / (ms_step / 1e3)
+
+    # ---- end to end through the C ABI with host buffers (rank-local)
+    e2e = None
+    if not args.no_e2e:
+        e2e = e2e_measure(cp, plan, sizes, cfg, args, world, A_all)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            threads = os.cpu_count() or 1
+            t = cpu_reference_plan(cfg, sizes, threads)
+            cpu = {"value": accesses_of(cfg) / t, "unit": UNIT, "cores": threads,
+                   "kind": "reference",
+                   "sample": f"one full {cfg['name']} plan (reference functions, per-worker "
+                             f"decomposition on {threads} host threads), {t:.2f} s"}
+        except Exception as ex:  # no oracle/_ref on this box
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                   "sample": f"unavailable: {ex}"}
+
+    hbm, peak_kind = peaks()
+    B_alg = 8 * A_all + 32 * D_all + 4 * (cfg["F"] + 1)
+    achieved = B_alg / (ms_step / 1e3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic_latest.json")
+    if os.path.exists(tpath):
+        try:
+            with open(tpath) as f:
+                tj = json.load(f)
+            if tj.get("workload") == cfg["name"] and world == 1:
+                traffic = tj.get("dram_bytes_per_plan")
+        except Exception:
+            traffic = None
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "u32", "data": "synthetic (seed-generated, BASELINE config shapes)",
+            "config": {"workload": cfg["name"], "samples": cfg["F"], "workers": N,
+                       "per_worker_batch": cfg["b"], "epochs": cfg["E"], "seed": SEED,
+                       "capacities_mb": list(CAPS), "drop_last": True,
+                       "l2": "256 MB flush before every timed step",
+                       "sharding": f"worker ranges over {world} GPU(s)"},
+            "plan_latency_ms": ms_step,
+            "wall_ms_per_step": t_wall * 1e3 / args.steps,
+            "accesses": int(A_all), "pairs": int(D_all),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm * world,
+                         "unit": "GB/s", "frac": achieved / (hbm * world), "traffic": traffic,
+                         "kernel": "whole plan pipeline (B_alg = 8A + 32D + 4(F+1) per plan)",
+                         "peak_kind": f"{peak_kind} copy bandwidth x {world}"},
+            "stages_ms": stage_ms,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "gpu_launches": launches,
+            "clocks": clocks,
+        }
+        print(json.dumps(out))
+    plan.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def e2e_measure(cp, plan, sizes, cfg, args, world, A_all):
+    """sizes H2D from pinned memory + build + every output D2H into pinned buffers."""
+    import ctypes
+    import torch
+    L = cp.lib()
+    L.clairplan_set_sizes.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
+    st = plan.stats()
+    F = cfg["F"]
+    h_sizes = torch.from_numpy(np.ascontiguousarray(sizes)).pin_memory()
+    nloc = plan.wend - plan.wbegin
+    h_stream = torch.empty(st["accesses"], dtype=torch.int32).pin_memory()
+    h_cls = torch.empty(max(st["holders"], 1), dtype=torch.int32).pin_memory()
+    h_off = torch.empty(F + 1, dtype=torch.int64).pin_memory()
+    h_hold = torch.empty(max(st["holders"], 1) * 3, dtype=torch.int32).pin_memory()
+    u32 = ctypes.POINTER(ctypes.c_uint32)
+    u64 = ctypes.POINTER(ctypes.c_uint64)
+
+    def step():
+        cp._check(L.clairplan_set_sizes(plan._h, ctypes.c_void_p(h_sizes.data_ptr()), 0))
+        plan.build()
+        cp._check(L.clairplan_export_streams(plan._h, ctypes.cast(h_stream.data_ptr(), u32),
+                                             st["accesses"]))
+        cp._check(L.clairplan_export_class_lists(plan._h, ctypes.cast(h_cls.data_ptr(), u32),
+                                                 st["holders"]))
+        cp._check(L.clairplan_export_holders(plan._h, ctypes.cast(h_off.data_ptr(), u64),
+                                             ctypes.cast(h_hold.data_ptr(), u32), st["holders"]))
+
+    step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    n = max(1, min(args.steps, 5))
+    t = time.perf_counter()
+    for _ in range(n):
+        step()
+    torch.cuda.synchronize()
+    t = (time.perf_counter() - t) / n
+    tv = torch.tensor([t], dtype=torch.float64, device="cuda")
+    if world > 1:
+        torch.distributed.all_reduce(tv, op=torch.distributed.ReduceOp.MAX)
+    t = float(tv[0])
+    H = st["holders"]
+    return {"value": A_all / t, "unit": UNIT, "ms_per_step": t * 1e3,
+            "h2d_bytes_per_step": 8 * F,
+            "d2h_bytes_per_step": 4 * st["accesses"] + 4 * H + 12 * H + 8 * (F + 1),
+            "path": "clairplan_set_sizes (pinned H2D) + clairplan_build + export_streams/"
+                    "class_lists/holders (pinned D2H)", "workers_per_rank": nloc}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

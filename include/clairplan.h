@@ -137,6 +137,13 @@ int clairplan_generate_sizes(uint64_t samples, double mean_mb, double sigma_mb, 
 
 /* Number of kernel launches issued by the last clairplan_build on this handle. */
 uint64_t clairplan_launch_count(clairplan_t plan);
+/* Device time per pipeline stage of the last build (CUDA events on the handle's stream);
+ * returns the number of stages; names via clairplan_stage_name. */
+int clairplan_stage_times(clairplan_t plan, double* ms, uint32_t n);
+const char* clairplan_stage_name(uint32_t stage);
+/* Replaces the sample sizes (DatasetModel::sizes_mb) of a handle, e.g. from pinned host
+ * memory for an end-to-end step; the copy is ordered before the next build. */
+int clairplan_set_sizes(clairplan_t plan, const double* sizes_mb, int on_device);
 
 #ifdef __cplusplus
 }

@@ -189,6 +189,7 @@ int assign_tiers(clairplan_plan* p) {
     launch_gather_sizes(s, order, cand_k, p->sizes.get<double>(), D, ssize);
     CK(cudaMemsetAsync(cand_cls, 0, D, s));
     p->launches += 2;
+    p->mark(5);
 
     // K6: first fit, class by class
     uint64_t* sb = ws.scratch<uint64_t>(nloc);
@@ -227,12 +228,14 @@ int assign_tiers(clairplan_plan* p) {
         p->launches += 10;
     }
 
+    p->mark(6);
     // K7: class lists = stable partition of first-access order by class
     launch_class_keys(s, cand_cls, D, J, keys);
     uint64_t* sc = nullptr;
     radix_pass(s, tm, wbeg, wlen, keys, cand_k, 0, okeys, centries, dest, &sc, ws);
     radix_regions(s, tm, wbeg, wlen, sc, J + 1, cstart, clen);
     p->launches += 7;
+    p->mark(7);
     p->class_start_h.resize((size_t)nloc * (J + 1));
     p->class_len_h.resize((size_t)nloc * (J + 1));
     CK(cudaMemcpyAsync(p->class_start_h.data(), cstart, p->class_start_h.size() * 8,
@@ -293,14 +296,18 @@ int build_seed_path(clairplan_plan* p) {
     for (int attempt = 0; attempt < 2; ++attempt) {
         p->launches = 0;
         CK(cudaEventRecord(p->ev0, s));
+        p->mark(0);
         // K1-K3
         if (int rc = enqueue_perms(p, stream_buf, info, nullptr, 0, E)) return rc;
+        p->mark(1);
         // K4a
         launch_sample_pass(s, part, info, pcount, hs, nw, warps, smem);
         exclusive_scan(s, pcount, F, poff, p->ws);
+        p->mark(2);
         // K4b
         launch_seg_count(s, part, stream_buf, info, segcnt);
         exclusive_scan(s, segcnt, (uint64_t)nloc * E, segoff, p->ws);
+        p->mark(3);
         p->launches += 8;
         std::vector<uint32_t> flags(E);
         uint64_t D = 0;
@@ -322,6 +329,7 @@ int build_seed_path(clairplan_plan* p) {
         launch_seg_write(s, part, stream_buf, info, segoff, ck, ci);
         launch_worker_segments(s, segoff, nloc, E, wbeg, wlen);
         p->launches += 2;
+        p->mark(4);
         if (p->cfg.num_classes > 0) {
             if (int rc = assign_tiers(p)) return rc;
         } else {
@@ -334,12 +342,20 @@ int build_seed_path(clairplan_plan* p) {
             p->class_start_h.assign(nloc, 0);
             p->class_len_h.assign(nloc, 0);
         }
+        if (p->cfg.num_classes == 0)
+            for (int i = 5; i < clairplan_plan::kStages; ++i) p->mark(i);
+        p->mark(clairplan_plan::kStages);
         CK(cudaEventRecord(p->ev1, s));
         CK(cudaEventSynchronize(p->ev1));
         CK(cudaGetLastError());
         float ms = 0;
         CK(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
         p->device_ms = ms;
+        for (int i = 0; i < clairplan_plan::kStages; ++i) {
+            float t = 0;
+            if (p->sev[i] && p->sev[i + 1]) cudaEventElapsedTime(&t, p->sev[i], p->sev[i + 1]);
+            p->stage_ms[i] = t;
+        }
         p->built = true;
         return 0;
     }
@@ -368,7 +384,7 @@ int clairplan_create(const clairplan_config* c, clairplan_t* out) {
     if (c->epochs > 65535) return fail(CLAIRPLAN_EINVAL, "device plan supports at most 65535 epochs");
     if (c->num_classes > 254) return fail(CLAIRPLAN_EINVAL, "device plan supports at most 254 cache classes");
     if (c->num_classes && !c->capacities_mb) return fail(CLAIRPLAN_EINVAL, "capacities_mb is null");
-    if (!c->sizes_mb) return fail(CLAIRPLAN_EINVAL, "sizes_mb is null");
+    if (!c->sizes_mb && c->num_classes) return fail(CLAIRPLAN_EINVAL, "sizes_mb is null");
     uint32_t wb = c->worker_begin, we = c->worker_end;
     if (wb == 0 && we == 0) we = c->num_workers;
     if (wb >= we || we > c->num_workers) return fail(CLAIRPLAN_EINVAL, "invalid worker range");
@@ -397,12 +413,15 @@ int clairplan_create(const clairplan_config* c, clairplan_t* out) {
         delete p;
         return fail(CLAIRPLAN_ECUDA, "stream/event creation failed");
     }
+    for (auto& e : p->sev) cudaEventCreate(&e);
     if (!p->sizes.ensure((size_t)c->samples * sizeof(double))) {
         delete p;
         return fail(CLAIRPLAN_ENOMEM, "device allocation failed (sizes)");
     }
-    cudaError_t e = cudaMemcpy(p->sizes.get<double>(), c->sizes_mb, (size_t)c->samples * 8,
-                               c->sizes_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice);
+    cudaError_t e = cudaSuccess;
+    if (c->sizes_mb)
+        e = cudaMemcpy(p->sizes.get<double>(), c->sizes_mb, (size_t)c->samples * 8,
+                       c->sizes_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
         delete p;
         return fail(CLAIRPLAN_ECUDA, std::string("sizes upload: ") + cudaGetErrorString(e));
@@ -570,6 +589,29 @@ int clairplan_epoch_permutation(uint64_t seed, uint32_t epoch, uint32_t samples,
         return 0;
     }
     return fail(CLAIRPLAN_ECUDA, "rejection tables did not converge");
+}
+
+static const char* kStageNames[clairplan_plan::kStages] = {
+    "permutations+streams", "sample_histogram", "candidate_count", "candidate_write",
+    "tier_order", "first_fit", "class_lists", "holder_csr"};
+
+const char* clairplan_stage_name(uint32_t i) {
+    return i < (uint32_t)clairplan_plan::kStages ? kStageNames[i] : "";
+}
+
+int clairplan_stage_times(clairplan_t p, double* ms, uint32_t n) {
+    if (!p || !p->built) return fail(CLAIRPLAN_EINVAL, "plan not built");
+    for (uint32_t i = 0; i < n && i < (uint32_t)clairplan_plan::kStages; ++i) ms[i] = p->stage_ms[i];
+    return clairplan_plan::kStages;
+}
+
+int clairplan_set_sizes(clairplan_t p, const double* sizes_mb, int on_device) {
+    if (!p || !sizes_mb) return fail(CLAIRPLAN_EINVAL, "null argument");
+    CK(cudaSetDevice(p->device));
+    if (!p->sizes.ensure((size_t)p->part.F * 8)) return fail(CLAIRPLAN_ENOMEM, "device allocation failed");
+    CK(cudaMemcpyAsync(p->sizes.get<double>(), sizes_mb, (size_t)p->part.F * 8,
+                       on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, p->stream));
+    return 0;
 }
 
 }  // extern "C"

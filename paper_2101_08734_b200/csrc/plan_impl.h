@@ -90,6 +90,9 @@ struct clairplan_plan {
     int device = 0;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    static constexpr int kStages = 8;
+    cudaEvent_t sev[kStages + 1] = {};  // stage boundaries of the last build
+    double stage_ms[kStages] = {};
     clairplan_config cfg{};
     std::vector<double> caps;
     Part part{};
@@ -121,6 +124,11 @@ struct clairplan_plan {
         if (stream) cudaStreamDestroy(stream);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
+        for (auto& e : sev)
+            if (e) cudaEventDestroy(e);
+    }
+    void mark(int i) {
+        if (sev[i]) cudaEventRecord(sev[i], stream);
     }
 };
 
