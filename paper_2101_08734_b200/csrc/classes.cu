@@ -31,7 +31,7 @@ __global__ void apply_pass_kernel(const uint8_t* __restrict__ taken, uint64_t n,
          i += (uint64_t)gridDim.x * blockDim.x) {
         if (!taken[i]) continue;
         const uint32_t si = seq_to_sorted ? seq_to_sorted[i] : (uint32_t)i;
-        cand_cls[order[si]] = cls;
+        cand_cls[order ? order[si] : si] = cls;
     }
 }
 
@@ -130,6 +130,32 @@ __global__ void dense_counts_kernel(const uint32_t* __restrict__ cand_k,
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < L;
          i += (uint64_t)gridDim.x * blockDim.x)
         counts[cand_k[b + i]] = cand_info[b + i] >> 16;
+}
+
+__global__ void count_nonzero_kernel(const uint8_t* __restrict__ a, uint64_t n,
+                                     unsigned long long* __restrict__ out) {
+    uint32_t c = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        c += a[i] != 0;
+    c = warp_sum(c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, (unsigned long long)c);
+}
+
+void launch_count_nonzero(cudaStream_t s, const uint8_t* a, uint64_t n, unsigned long long* out) {
+    cudaMemsetAsync(out, 0, sizeof(unsigned long long), s);
+    count_nonzero_kernel<<<grid_for(n, kThreads * 8, 148u * 8u), kThreads, 0, s>>>(a, n, out);
+}
+
+__global__ void stream_hist_kernel(const uint32_t* __restrict__ st, uint64_t n,
+                                   uint32_t* __restrict__ counts) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        atomicAdd(&counts[st[i]], 1u);
+}
+
+void launch_stream_hist(cudaStream_t s, const uint32_t* st, uint64_t n, uint32_t* counts) {
+    stream_hist_kernel<<<grid_for(n, kThreads), kThreads, 0, s>>>(st, n, counts);
 }
 
 void launch_gather_sizes(cudaStream_t s, const uint32_t* order, const uint32_t* cand_k,

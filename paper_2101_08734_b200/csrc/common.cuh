@@ -84,6 +84,27 @@ __host__ __device__ __forceinline__ uint32_t fy_draw(uint64_t key, uint32_t e, u
     return (uint32_t)bounded_at(key, pos, (uint64_t)i + 1, extra);
 }
 
+// ---- fast unsigned division by a runtime constant (32-bit dividends) ---------------------
+// Round-up multiply-shift: q = (umulhi(n, m) + n) >> l with l = ceil(log2 d),
+// m = floor(2^32 (2^l - d) / d) + 1; exact for every 32-bit n and d >= 1.
+struct FastDiv {
+    uint32_t d = 1, m = 1, l = 0;
+    FastDiv() = default;
+    explicit FastDiv(uint32_t dv) : d(dv) {
+        l = 0;
+        while ((1ull << l) < dv) ++l;
+        m = (uint32_t)(((1ull << 32) * ((1ull << l) - dv)) / dv + 1);
+    }
+    __host__ __device__ __forceinline__ uint32_t div(uint32_t n) const {
+#ifdef __CUDA_ARCH__
+        const uint32_t t = __umulhi(n, m);
+#else
+        const uint32_t t = (uint32_t)(((uint64_t)n * m) >> 32);
+#endif
+        return (uint32_t)(((uint64_t)t + n) >> l);
+    }
+};
+
 // ---- partition geometry (access.cpp:14-39, config.cpp:37-44) ----------------------------
 struct Part {
     uint32_t F, N, B, E;
@@ -93,6 +114,7 @@ struct Part {
     uint64_t tbase, textra;          // batch_slice of the tail batch
     uint32_t wbegin, wend;           // worker range of this handle
     uint64_t off0;                   // stream_offset(wbegin)
+    FastDiv dB, dFull1, dFull0, dTail1, dTail0;  // B, base+1, base, tbase+1, tbase
 
     __host__ __device__ uint64_t len(uint32_t w) const { return base + (w < extra ? 1 : 0); }
     __host__ __device__ uint64_t tlen(uint32_t w) const {
@@ -109,32 +131,35 @@ struct Part {
     __host__ __device__ uint64_t stream_offset(uint32_t w) const {
         return (uint64_t)E * prefix_len(w) - off0;
     }
-    // perm position p (< P) of epoch e -> worker and position within that worker's stream
-    __host__ __device__ void locate(uint64_t p, uint32_t e, uint32_t& w, uint64_t& spos) const {
-        const uint64_t h = p / B;
-        const uint64_t o = p - h * B;
-        uint64_t b = base, x = extra, off;
-        if (h >= full) { b = tbase; x = textra; }
-        const uint64_t big = x * (b + 1);
+    // perm position p (< P < 2^32) of epoch e -> worker and position within its stream
+    __host__ __device__ __forceinline__ void slice_of(uint32_t p, uint32_t& w, uint32_t& h,
+                                                      uint32_t& off) const {
+        h = dB.div(p);
+        const uint32_t o = p - h * B;
+        const bool tl = h >= full;
+        const uint32_t x = (uint32_t)(tl ? textra : extra);
+        const uint32_t b1 = (uint32_t)(tl ? tbase : base) + 1;
+        const uint32_t big = x * b1;
         if (o < big) {
-            w = (uint32_t)(o / (b + 1));
-            off = o - (uint64_t)w * (b + 1);
+            w = tl ? dTail1.div(o) : dFull1.div(o);
+            off = o - w * b1;
         } else {
-            const uint64_t o2 = o - big;
-            const uint64_t q = o2 / b;
-            w = (uint32_t)(x + q);
-            off = o2 - q * b;
+            const uint32_t o2 = o - big;
+            const uint32_t q = tl ? dTail0.div(o2) : dFull0.div(o2);
+            w = x + q;
+            off = o2 - q * (b1 - 1);
         }
-        spos = (uint64_t)e * epoch_len(w) + (h < full ? h * len(w) : full * len(w)) + off;
     }
-    __host__ __device__ uint32_t worker_of(uint64_t p) const {
-        const uint64_t h = p / B;
-        const uint64_t o = p - h * B;
-        uint64_t b = base, x = extra;
-        if (h >= full) { b = tbase; x = textra; }
-        const uint64_t big = x * (b + 1);
-        if (o < big) return (uint32_t)(o / (b + 1));
-        return (uint32_t)(x + (o - big) / b);
+    __host__ __device__ __forceinline__ void locate(uint64_t p, uint32_t e, uint32_t& w,
+                                                    uint64_t& spos) const {
+        uint32_t h, off;
+        slice_of((uint32_t)p, w, h, off);
+        spos = (uint64_t)e * epoch_len(w) + (h < full ? (uint64_t)h * len(w) : full * len(w)) + off;
+    }
+    __host__ __device__ __forceinline__ uint32_t worker_of(uint64_t p) const {
+        uint32_t w, h, off;
+        slice_of((uint32_t)p, w, h, off);
+        return w;
     }
 };
 
@@ -148,6 +173,11 @@ inline Part make_part(uint32_t F, uint32_t N, uint32_t B, uint32_t E, bool drop_
     p.base = B / N; p.extra = B % N;
     p.tbase = p.tail / N; p.textra = p.tail % N;
     p.wbegin = wbegin; p.wend = wend;
+    p.dB = FastDiv(B);
+    p.dFull1 = FastDiv((uint32_t)p.base + 1);
+    p.dFull0 = FastDiv(p.base ? (uint32_t)p.base : 1u);
+    p.dTail1 = FastDiv((uint32_t)p.tbase + 1);
+    p.dTail0 = FastDiv(p.tbase ? (uint32_t)p.tbase : 1u);
     p.off0 = 0;
     p.off0 = p.stream_offset(wbegin);
     return p;

@@ -1,0 +1,622 @@
+// Seed-path kernels of the plan build after the permutations (K4-K8), v2.
+//
+// Data layout (one handle = a worker range [wb, we), nloc workers):
+//   inv   [E][F] u32   position of sample k in epoch e's permutation (K3 output)
+//   info  [E][F] u16   access count of (w,k) at the epoch of its first access, else 0
+//   stream         u32 worker-major access streams; segment (w,e) = worker w's epoch e,
+//                      contiguous, length Le(w); split into 32-entry blocks
+//                      blk(w,e,t) = ((w-wb)*E + e)*MB + t/32, MB = ceil(max Le / 32)
+//   candidates     per worker in first-access order ("first order", c)   -- dest[c]
+//   sorted         per worker in tier order (count desc, first asc)      -- sorted_size[s]
+//   block records  blkmask/blkbase (first-access bits, first-order index of the first one),
+//                  np class bit-planes and per-class prefix counts
+//
+// K4a sample_lanes   lane = sample: per-lane worker bitmap in shared memory (conflict-free
+//                    [word][lane] layout) gives first accesses and the distinct count; the
+//                    few repeated workers go to a short per-lane list for their counts.
+// K4b seg_hist       per (w,e) segment: histogram of first accesses by count
+// K4c seg_write      per segment: first-order index, tier-order index (stable counting sort
+//                    by count desc = policies.cpp:157-160), sizes gathered in tier order,
+//                    block first-masks
+// K7  blk_codes      class bit-planes + per-class counts per block (after first fit)
+//     class_write    prefetch-ordered class lists (policies.cpp:31-36,162)
+// K8  holder_lanes   lane = sample again: holders written in worker order at the pair slot
+//                    (build_index, policies.cpp:124-142) from the L2-resident block records
+#include "internal.h"
+
+namespace clairplan {
+
+constexpr uint32_t kOv = 16;  // repeated-worker list per lane
+constexpr int kU = 8;         // epochs loaded per batch (memory-level parallelism)
+
+__device__ __forceinline__ uint32_t ld_inv(const uint32_t* p) { return __ldcg(p); }
+
+// ---------------------------------------------------------------------------- K4a
+// Lane = sample.  One pass over the E inverse entries (8 coalesced loads in flight per lane)
+// marks the sample's workers in a per-lane bitmap (shared memory, [word][lane] layout: no bank
+// conflicts), records the worker of each first access, and keeps repeated workers (bitmap b2)
+// with their counts in a short list; the second pass works from shared memory only and writes
+//   info[e][k] = count of (w,k) at its first epoch, else 0          (u16)
+//   rank[e][k] = rank of w among k's workers (worker order), else 0xFFFF  (u16)
+__global__ void __launch_bounds__(128) sample_lanes_kernel(Part part, const uint32_t* __restrict__ inv,
+                                                           uint16_t* __restrict__ info,
+                                                           uint16_t* __restrict__ rank16,
+                                                           uint32_t* __restrict__ pair_count,
+                                                           uint32_t W, uint32_t* __restrict__ hard,
+                                                           uint32_t* __restrict__ nhard) {
+    extern __shared__ uint32_t sm[];
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t E = part.E, F = part.F;
+    const uint32_t per_warp = 32 * (3 * W + kOv) + 16 * E;  // words
+    uint32_t* bm = sm + warp * per_warp;  // [W][32] workers seen
+    uint32_t* b2 = bm + 32 * W;           // [W][32] workers seen twice or more
+    uint32_t* pre = b2 + 32 * W;          // [W][32] popcount prefix of bm
+    uint32_t* ov = pre + 32 * W;          // [kOv][32] (w << 16 | count) of repeated workers
+    uint16_t* wls = reinterpret_cast<uint16_t*>(ov + 32 * kOv);  // [E][32] worker of a first access
+    for (uint32_t t = 0; t < W; ++t) {
+        bm[t * 32 + lane] = 0;
+        b2[t * 32 + lane] = 0;
+    }
+    const uint64_t ngroups = (F + 31) / 32;
+    const uint64_t gw = (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    for (uint64_t g = gw; g < ngroups; g += nw) {
+        const uint32_t k = (uint32_t)(g * 32 + lane);
+        const bool live = k < F;
+        uint32_t nov = 0;
+        bool overflow = false;
+        for (uint32_t e0 = 0; e0 < E; e0 += kU) {
+            uint32_t pv[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u)
+                pv[u] = (live && e0 + u < E) ? ld_inv(inv + (size_t)(e0 + u) * F + k) : kNone;
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const uint32_t e = e0 + u;
+                if (e >= E) break;
+                uint16_t wrec = 0xFFFFu;
+                const uint32_t p = pv[u];
+                if (p < part.P) {
+                    const uint32_t w = part.worker_of(p);
+                    if (w >= part.wbegin && w < part.wend) {
+                        const uint32_t wl = w - part.wbegin;
+                        uint32_t* word = &bm[(wl >> 5) * 32 + lane];
+                        const uint32_t bit = 1u << (wl & 31);
+                        const uint32_t v = *word;
+                        if (!(v & bit)) {
+                            *word = v | bit;
+                            wrec = (uint16_t)wl;
+                        } else {
+                            b2[(wl >> 5) * 32 + lane] |= bit;
+                            uint32_t i = 0;
+                            for (; i < nov; ++i) {
+                                const uint32_t o = ov[i * 32 + lane];
+                                if ((o >> 16) == wl) {
+                                    ov[i * 32 + lane] = o + 1;
+                                    break;
+                                }
+                            }
+                            if (i == nov) {
+                                if (nov < kOv) ov[(nov++) * 32 + lane] = (wl << 16) | 2u;
+                                else overflow = true;
+                            }
+                        }
+                    }
+                }
+                wls[e * 32 + lane] = wrec;
+            }
+        }
+        uint32_t d = 0;
+        for (uint32_t t = 0; t < W; ++t) {
+            pre[t * 32 + lane] = d;
+            d += __popc(bm[t * 32 + lane]);
+        }
+        if (live) pair_count[k] = d;
+        if (overflow) hard[atomicAdd(nhard, 1u)] = k;
+        if (live && !overflow) {
+            for (uint32_t e = 0; e < E; ++e) {
+                const uint32_t wl = wls[e * 32 + lane];
+                uint16_t c = 0, r = 0xFFFFu;
+                if (wl != 0xFFFFu) {
+                    const uint32_t sh = wl & 31, wd = (wl >> 5) * 32 + lane;
+                    c = 1;
+                    if ((b2[wd] >> sh) & 1u)
+                        for (uint32_t i = 0; i < nov; ++i) {
+                            const uint32_t o = ov[i * 32 + lane];
+                            if ((o >> 16) == wl) c = (uint16_t)(o & 0xFFFFu);
+                        }
+                    r = (uint16_t)(pre[wd] + __popc(bm[wd] & ((1u << sh) - 1u)));
+                }
+                info[(size_t)e * F + k] = c;
+                rank16[(size_t)e * F + k] = r;
+            }
+        }
+        for (uint32_t t = 0; t < W; ++t) {
+            bm[t * 32 + lane] = 0;
+            b2[t * 32 + lane] = 0;
+        }
+    }
+}
+
+// Exact fallback for samples whose repeated-worker list overflowed (and for handles with
+// more than kMaxLaneWorkers workers): one warp per sample, __match_any_sync per 32-epoch
+// round + a per-warp shared-memory hash keyed by worker.
+__global__ void __launch_bounds__(128) sample_hash_kernel(Part part, const uint32_t* __restrict__ inv,
+                                                          uint16_t* __restrict__ info,
+                                                          uint16_t* __restrict__ rank16,
+                                                          uint32_t* __restrict__ pair_count,
+                                                          const uint32_t* __restrict__ list,
+                                                          const uint32_t* __restrict__ nlist,
+                                                          uint32_t hs) {
+    extern __shared__ uint32_t sm[];
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t* keys = sm + warp * 2 * hs;
+    uint32_t* vals = keys + hs;
+    const uint32_t mask = hs - 1;
+    const uint32_t E = part.E, F = part.F;
+    const uint32_t n = list ? *nlist : F;
+    for (uint32_t t = lane; t < hs; t += 32) keys[t] = kNone;
+    __syncwarp();
+    for (uint32_t idx = blockIdx.x * (blockDim.x >> 5) + warp; idx < n;
+         idx += gridDim.x * (blockDim.x >> 5)) {
+        const uint32_t k = list ? list[idx] : idx;
+        uint32_t distinct = 0;
+        for (uint32_t r = 0; r * 32 < E; ++r) {
+            const uint32_t e = r * 32 + lane;
+            uint32_t w = kNone;
+            if (e < E) {
+                const uint32_t p = inv[(size_t)e * F + k];
+                if (p < part.P) {
+                    const uint32_t ww = part.worker_of(p);
+                    if (ww >= part.wbegin && ww < part.wend) w = ww - part.wbegin;
+                }
+            }
+            const uint32_t m = __match_any_sync(0xffffffffu, w);
+            const bool leader = (__ffs(m) - 1) == (int)lane;
+            bool fresh = false;
+            if (w != kNone && leader) {
+                uint32_t slot = (w * 0x9E3779B1u >> 7) & mask;
+                while (true) {
+                    const uint32_t old = atomicCAS(&keys[slot], kNone, w);
+                    if (old == kNone) {
+                        vals[slot] = (e << 16) | __popc(m);
+                        fresh = true;
+                        break;
+                    }
+                    if (old == w) {
+                        vals[slot] += __popc(m);
+                        break;
+                    }
+                    slot = (slot + 1) & mask;
+                }
+            }
+            distinct += __popc(__ballot_sync(0xffffffffu, fresh));
+            __syncwarp();
+        }
+        for (uint32_t r = 0; r * 32 < E; ++r) {
+            const uint32_t e = r * 32 + lane;
+            if (e >= E) continue;
+            const uint32_t p = inv[(size_t)e * F + k];
+            uint16_t out = 0, rk = 0xFFFFu;
+            if (p < part.P) {
+                const uint32_t ww = part.worker_of(p);
+                if (ww >= part.wbegin && ww < part.wend) {
+                    const uint32_t w = ww - part.wbegin;
+                    uint32_t slot = (w * 0x9E3779B1u >> 7) & mask;
+                    while (keys[slot] != w) slot = (slot + 1) & mask;
+                    const uint32_t v = vals[slot];
+                    if ((v >> 16) == e) {
+                        out = (uint16_t)(v & 0xFFFFu);
+                        uint32_t less = 0;  // rank = distinct workers below w (rare path)
+                        for (uint32_t t = 0; t <= mask; ++t) less += keys[t] < w;
+                        rk = (uint16_t)less;
+                    }
+                }
+            }
+            info[(size_t)e * F + k] = out;
+            rank16[(size_t)e * F + k] = rk;
+        }
+        __syncwarp();
+        for (uint32_t t = lane; t < hs; t += 32) keys[t] = kNone;
+        if (lane == 0) pair_count[k] = distinct;
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------- K4b
+// seghist[(wl*E + (E - c))*E + e] = first accesses with count c in segment (w, e)
+__global__ void __launch_bounds__(kThreads) seg_hist_kernel(Part part, const uint32_t* __restrict__ stream,
+                                                             const uint16_t* __restrict__ info,
+                                                             uint32_t* __restrict__ seghist,
+                                                             uint32_t* __restrict__ segcnt) {
+    extern __shared__ uint32_t hist[];  // [E]
+    __shared__ uint32_t wsum[kThreads / 32];
+    const uint32_t E = part.E, nloc = part.wend - part.wbegin;
+    const uint64_t nseg = (uint64_t)nloc * E;
+    for (uint64_t b = blockIdx.x; b < nseg; b += gridDim.x) {
+        const uint32_t e = (uint32_t)(b / nloc), wl = (uint32_t)(b % nloc);
+        const uint32_t w = part.wbegin + wl;
+        for (uint32_t i = threadIdx.x; i < E; i += blockDim.x) hist[i] = 0;
+        __syncthreads();
+        const uint64_t Le = part.epoch_len(w);
+        const uint64_t g0 = part.stream_offset(w) + (uint64_t)e * Le;
+        const uint16_t* row = info + (size_t)e * part.F;
+        uint32_t tot = 0;
+        for (uint64_t t = threadIdx.x; t < Le; t += blockDim.x) {
+            const uint32_t c = row[stream[g0 + t]];
+            if (c) {
+                atomicAdd(&hist[E - c], 1u);
+                ++tot;
+            }
+        }
+        tot = warp_sum(tot);
+        if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = tot;
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < E; i += blockDim.x)
+            seghist[((uint64_t)wl * E + i) * E + e] = hist[i];
+        if (threadIdx.x == 0) {
+            uint32_t s = 0;
+            for (int i = 0; i < kThreads / 32; ++i) s += wsum[i];
+            segcnt[(uint64_t)wl * E + e] = s;
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------- K4c
+__global__ void __launch_bounds__(kThreads) seg_write_kernel2(
+    Part part, const uint32_t* __restrict__ stream, const uint16_t* __restrict__ info,
+    const double* __restrict__ sizes, const uint64_t* __restrict__ seg_off,
+    const uint64_t* __restrict__ sorted_base, uint32_t MB, uint32_t* __restrict__ dest,
+    double* __restrict__ sorted_size, uint32_t* __restrict__ blkmask,
+    uint32_t* __restrict__ blkbase) {
+    extern __shared__ uint32_t sm2[];
+    const uint32_t E = part.E, nloc = part.wend - part.wbegin;
+    uint32_t* run = sm2;              // [E]
+    uint32_t* wcnt = sm2 + E;         // [8][E]
+    __shared__ uint32_t wtot[kThreads / 32];
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t nseg = (uint64_t)nloc * E;
+    for (uint32_t i = threadIdx.x; i < 9 * E; i += blockDim.x) sm2[i] = 0;
+    __syncthreads();
+    for (uint64_t b = blockIdx.x; b < nseg; b += gridDim.x) {
+        const uint32_t e = (uint32_t)(b / nloc), wl = (uint32_t)(b % nloc);
+        const uint32_t w = part.wbegin + wl;
+        const uint64_t Le = part.epoch_len(w);
+        const uint64_t g0 = part.stream_offset(w) + (uint64_t)e * Le;
+        const uint16_t* row = info + (size_t)e * part.F;
+        const uint64_t fbase = seg_off[(uint64_t)wl * E + e];
+        const uint64_t* sbase = sorted_base + (uint64_t)wl * E * E + e;  // + (E-c)*E
+        uint64_t frun = 0;
+        for (uint64_t t0 = 0; t0 < Le; t0 += blockDim.x) {
+            const uint64_t t = t0 + threadIdx.x;
+            uint32_t k = 0, c = 0;
+            if (t < Le) {
+                k = stream[g0 + t];
+                c = row[k];
+            }
+            const bool first = c != 0;
+            const uint32_t bal = __ballot_sync(0xffffffffu, first);
+            if (lane == 0) wtot[warp] = __popc(bal);
+            const uint32_t key = first ? (E - c) : (0x80000000u | lane);
+            const uint32_t m = __match_any_sync(0xffffffffu, key);
+            const uint32_t rnk = __popc(m & lanemask_lt());
+            if (first && rnk == 0) wcnt[warp * E + key] = __popc(m);
+            __syncthreads();
+            uint32_t fbelow = 0, ftot = 0;
+#pragma unroll
+            for (int i = 0; i < kThreads / 32; ++i) {
+                fbelow += (i < (int)warp) ? wtot[i] : 0;
+                ftot += wtot[i];
+            }
+            if (lane == 0 && t < Le) {
+                const uint64_t blk = ((uint64_t)wl * E + e) * MB + (t >> 5);
+                blkmask[blk] = bal;
+                blkbase[blk] = (uint32_t)(fbase + frun + fbelow);
+            }
+            if (first) {
+                uint32_t below = 0;
+                for (uint32_t i = 0; i < warp; ++i) below += wcnt[i * E + key];
+                const uint64_t fpos = fbase + frun + fbelow + __popc(bal & lanemask_lt());
+                const uint64_t spos = sbase[(uint64_t)key * E] + run[key] + below + rnk;
+                dest[fpos] = (uint32_t)spos;
+                sorted_size[spos] = sizes[k];
+            }
+            __syncthreads();
+            for (uint32_t i = threadIdx.x; i < E; i += blockDim.x) {
+                uint32_t s = 0;
+#pragma unroll
+                for (int x = 0; x < kThreads / 32; ++x) {
+                    s += wcnt[x * E + i];
+                    wcnt[x * E + i] = 0;
+                }
+                run[i] += s;
+            }
+            frun += ftot;
+            __syncthreads();
+        }
+        for (uint32_t i = threadIdx.x; i < E; i += blockDim.x) run[i] = 0;
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------- K7
+// Block record rec[blk][Rp], Rp = R rounded up to 4 words, R = np + J: np class bit-planes
+// (bit p of the class of every first access of the block; class 0 = not cached / not a first
+// access) followed by the J per-class prefix counts (class-j first accesses in all earlier
+// blocks of the handle).  Four blocks per warp iteration keep the dependent gathers
+// (mask -> first-order index -> tier position -> class) overlapped.
+constexpr int kBU = 4;
+
+__global__ void __launch_bounds__(kThreads) blk_codes_kernel(
+    Part part, uint32_t MB, const uint32_t* __restrict__ blkmask,
+    const uint32_t* __restrict__ blkbase, const uint32_t* __restrict__ dest,
+    const uint8_t* __restrict__ cls_sorted, uint32_t np, uint32_t J, uint32_t Rp,
+    uint32_t* __restrict__ rec, uint32_t* __restrict__ ccount, uint64_t nblk, FastDiv dMB,
+    FastDiv dE) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t b0 = ((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5) * kBU; b0 < nblk;
+         b0 += nwarps * kBU) {
+        uint32_t m[kBU], c[kBU], d[kBU], cls[kBU];
+#pragma unroll
+        for (int u = 0; u < kBU; ++u) {
+            const uint64_t blk = b0 + u;
+            m[u] = 0;
+            if (blk < nblk) {
+                const uint32_t seg = dMB.div((uint32_t)blk);
+                const uint32_t wl = dE.div(seg);
+                const uint64_t t = (uint64_t)((uint32_t)blk - seg * MB) * 32;
+                if (t < part.epoch_len(part.wbegin + wl)) {
+                    m[u] = blkmask[blk];
+                    c[u] = blkbase[blk];
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kBU; ++u)
+            d[u] = ((m[u] >> lane) & 1u) ? dest[c[u] + __popc(m[u] & lanemask_lt())] : kNone;
+#pragma unroll
+        for (int u = 0; u < kBU; ++u) cls[u] = d[u] != kNone ? cls_sorted[d[u]] : 0u;
+#pragma unroll
+        for (int u = 0; u < kBU; ++u) {
+            const uint64_t blk = b0 + u;
+            if (blk >= nblk) break;
+            for (uint32_t p = 0; p < np; ++p) {
+                const uint32_t pl = __ballot_sync(0xffffffffu, (cls[u] >> p) & 1u);
+                if (lane == 0) rec[blk * Rp + p] = pl;
+            }
+            for (uint32_t j = 1; j <= J; ++j) {
+                const uint32_t bj = __ballot_sync(0xffffffffu, cls[u] == j);
+                if (lane == 0) ccount[(uint64_t)(j - 1) * nblk + blk] = __popc(bj);
+            }
+        }
+    }
+}
+
+__global__ void rec_fill_kernel(const uint64_t* __restrict__ cpre, uint64_t nblk, uint32_t np,
+                                uint32_t J, uint32_t Rp, uint32_t* __restrict__ rec) {
+    for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < nblk * J;
+         x += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t blk = x / J;
+        const uint32_t j = (uint32_t)(x % J);
+        rec[blk * Rp + np + j] = (uint32_t)cpre[(uint64_t)j * (nblk + 1) + blk];
+    }
+}
+
+// class base of every (worker, class): prefix count at the worker's first block
+__global__ void class_base_kernel(const uint64_t* __restrict__ cpre, uint64_t nblk, uint32_t nloc,
+                                  uint32_t E, uint32_t MB, uint32_t J, uint32_t* __restrict__ cbase) {
+    for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < nloc * J; x += gridDim.x * blockDim.x) {
+        const uint32_t wl = x / J, j = x % J;
+        cbase[x] = (uint32_t)cpre[(uint64_t)j * (nblk + 1) + (uint64_t)wl * E * MB];
+    }
+}
+
+// class_list[cstart[wl*J + j-1] + pos] = sample, pos = position in the worker's class list.
+// The block record is spread over lanes 0..Rp-1 and read through shuffles.
+__global__ void __launch_bounds__(kThreads) class_write_kernel(
+    Part part, uint32_t MB, const uint32_t* __restrict__ stream, const uint32_t* __restrict__ rec,
+    uint32_t np, uint32_t J, uint32_t Rp, const uint32_t* __restrict__ cbase,
+    const uint64_t* __restrict__ cstart, uint32_t* __restrict__ class_list, uint64_t nblk,
+    FastDiv dMB, FastDiv dE) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t E = part.E;
+    for (uint64_t blk = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; blk < nblk;
+         blk += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+        const uint32_t seg = dMB.div((uint32_t)blk);
+        const uint32_t wl = dE.div(seg), e = seg - wl * E;
+        const uint32_t w = part.wbegin + wl;
+        const uint64_t Le = part.epoch_len(w);
+        const uint64_t t0 = (uint64_t)((uint32_t)blk - seg * MB) * 32;
+        if (t0 >= Le) continue;
+        const uint32_t mine = lane < Rp ? rec[blk * Rp + lane] : 0;
+        const uint64_t t = t0 + lane;
+        uint32_t cls = 0;
+        for (uint32_t p = 0; p < np; ++p)
+            cls |= ((__shfl_sync(0xffffffffu, mine, p) >> lane) & 1u) << p;
+        if (t >= Le) cls = 0;
+        uint32_t cm = 0xffffffffu;
+        for (uint32_t p = 0; p < np; ++p) {
+            const uint32_t pl = __shfl_sync(0xffffffffu, mine, p);
+            cm &= ((cls >> p) & 1u) ? pl : ~pl;
+        }
+        const uint32_t pre = __shfl_sync(0xffffffffu, mine, (np + (cls ? cls - 1 : 0)) & 31);
+        if (cls) {
+            const uint32_t pos = pre - cbase[wl * J + cls - 1] + __popc(cm & lanemask_lt());
+            const uint64_t g = part.stream_offset(w) + (uint64_t)e * Le + t;
+            class_list[cstart[(uint64_t)wl * J + cls - 1] + pos] = stream[g];
+        }
+    }
+}
+
+// per (worker, class) list lengths from the class prefix counts
+__global__ void class_lens_kernel(uint32_t nloc, uint32_t E, uint32_t MB, uint32_t J,
+                                  const uint64_t* __restrict__ cpre, uint64_t nblk,
+                                  uint64_t* __restrict__ clen) {
+    for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < nloc * J; x += gridDim.x * blockDim.x) {
+        const uint32_t wl = x / J, j = x % J;
+        const uint64_t a = (uint64_t)wl * E * MB, b = (uint64_t)(wl + 1) * E * MB;
+        clen[x] = cpre[(uint64_t)j * (nblk + 1) + b] - cpre[(uint64_t)j * (nblk + 1) + a];
+    }
+}
+
+// ---------------------------------------------------------------------------- K8
+// One CTA takes 32 samples: their inverse-permutation and rank rows are loaded with coalesced
+// 128-B rows into padded shared tiles; then one warp per sample, lanes = epochs: every first
+// access (rank != 0xFFFF) looks up its class and class-list position in the block record and
+// writes its holder record at pair_off[k] + rank — the 32 stores of a warp land in one
+// sample's contiguous holder range (build_index order: workers ascending).
+__device__ __forceinline__ uint32_t pick(const uint4& a, uint32_t i) {
+    return i == 0 ? a.x : i == 1 ? a.y : i == 2 ? a.z : a.w;
+}
+
+__global__ void __launch_bounds__(kThreads) holder_tile_kernel(
+    Part part, const uint32_t* __restrict__ inv, const uint16_t* __restrict__ rank16, uint32_t MB,
+    const uint32_t* __restrict__ rec, uint32_t np, uint32_t J, uint32_t Rp,
+    const uint32_t* __restrict__ cbase, const uint64_t* __restrict__ pair_off,
+    uint32_t* __restrict__ holders) {
+    extern __shared__ uint32_t sm[];
+    const uint32_t E = part.E, F = part.F;
+    uint32_t* tinv = sm;                                            // [E][33]
+    uint16_t* trk = reinterpret_cast<uint16_t*>(sm + (size_t)E * 33);  // [E][33]
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+    for (uint64_t k0 = (uint64_t)blockIdx.x * 32; k0 < F; k0 += (uint64_t)gridDim.x * 32) {
+        __syncthreads();
+        for (uint32_t idx = threadIdx.x; idx < E * 32; idx += blockDim.x) {
+            const uint32_t e = idx >> 5, l = idx & 31;
+            const bool ok = k0 + l < F;
+            tinv[e * 33 + l] = ok ? ld_inv(inv + (size_t)e * F + k0 + l) : kNone;
+            trk[e * 33 + l] = ok ? rank16[(size_t)e * F + k0 + l] : (uint16_t)0xFFFFu;
+        }
+        __syncthreads();
+        for (uint32_t s = warp; s < 32; s += nwarps) {
+            if (k0 + s >= F) break;
+            const uint64_t slot0 = pair_off[k0 + s];
+            for (uint32_t e = lane; e < E; e += 32) {
+                const uint32_t rk = trk[e * 33 + s];
+                if (rk == 0xFFFFu) continue;
+                const uint32_t p = tinv[e * 33 + s];
+                uint32_t w;
+                uint64_t spos;
+                part.locate(p, e, w, spos);
+                const uint32_t wl = w - part.wbegin;
+                const uint64_t tseg = spos - (uint64_t)e * part.epoch_len(w);
+                const uint64_t blk = ((uint64_t)wl * E + e) * MB + (tseg >> 5);
+                const uint32_t bit = (uint32_t)(tseg & 31);
+                const uint4* r4 = reinterpret_cast<const uint4*>(rec + blk * Rp);
+                const uint4 a = r4[0];
+                uint32_t cls = 0;
+                for (uint32_t q = 0; q < np; ++q) cls |= ((pick(a, q) >> bit) & 1u) << q;
+                uint32_t pos = 0;
+                if (cls) {
+                    uint32_t cm = 0xffffffffu;
+                    for (uint32_t q = 0; q < np; ++q) {
+                        const uint32_t pl = pick(a, q);
+                        cm &= ((cls >> q) & 1u) ? pl : ~pl;
+                    }
+                    const uint32_t wi = np + cls - 1;
+                    const uint32_t prew = wi < 4 ? pick(a, wi) : pick(r4[wi >> 2], wi & 3);
+                    pos = prew - cbase[wl * J + cls - 1] + __popc(cm & ((1u << bit) - 1u));
+                }
+                uint32_t* h = holders + 3 * (slot0 + rk);
+                h[0] = w;
+                h[1] = cls;
+                h[2] = pos;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------- launchers
+constexpr uint32_t kMaxLaneWorkers = 2048;
+
+bool lane_path_ok(const Part& part) {
+    return (part.wend - part.wbegin) <= kMaxLaneWorkers && part.E <= 1024;
+}
+
+void launch_blk_codes(cudaStream_t s, const Part& part, uint32_t MB, const uint32_t* blkmask,
+                      const uint32_t* blkbase, const uint32_t* dest, const uint8_t* cls_sorted,
+                      uint32_t np, uint32_t J, uint32_t Rp, uint32_t* rec, uint32_t* ccount,
+                      uint64_t nblk) {
+    blk_codes_kernel<<<grid_for(nblk * 32 / kBU + 32, kThreads, 148u * 64u), kThreads, 0, s>>>(
+        part, MB, blkmask, blkbase, dest, cls_sorted, np, J, Rp, rec, ccount, nblk, FastDiv(MB),
+        FastDiv(part.E));
+}
+
+void launch_rec_fill(cudaStream_t s, const uint64_t* cpre, uint64_t nblk, uint32_t np, uint32_t J,
+                     uint32_t Rp, uint32_t* rec, uint32_t nloc, uint32_t E, uint32_t MB,
+                     uint32_t* cbase) {
+    rec_fill_kernel<<<grid_for(nblk * J, kThreads), kThreads, 0, s>>>(cpre, nblk, np, J, Rp, rec);
+    class_base_kernel<<<grid_for((uint64_t)nloc * J, kThreads), kThreads, 0, s>>>(cpre, nblk, nloc, E,
+                                                                                 MB, J, cbase);
+}
+
+void launch_class_write(cudaStream_t s, const Part& part, uint32_t MB, const uint32_t* stream,
+                        const uint32_t* rec, uint32_t np, uint32_t J, uint32_t Rp,
+                        const uint32_t* cbase, const uint64_t* cstart, uint32_t* class_list,
+                        uint64_t nblk) {
+    class_write_kernel<<<grid_for(nblk * 32, kThreads, 148u * 64u), kThreads, 0, s>>>(
+        part, MB, stream, rec, np, J, Rp, cbase, cstart, class_list, nblk, FastDiv(MB),
+        FastDiv(part.E));
+}
+
+void launch_class_lens(cudaStream_t s, uint32_t nloc, uint32_t E, uint32_t MB, uint32_t J,
+                       const uint64_t* cpre, uint64_t nblk, uint64_t* clen) {
+    class_lens_kernel<<<grid_for((uint64_t)nloc * J, kThreads), kThreads, 0, s>>>(nloc, E, MB, J, cpre,
+                                                                                 nblk, clen);
+}
+
+void launch_holder_tile(cudaStream_t s, const Part& part, const uint32_t* inv, const uint16_t* rank16,
+                        uint32_t MB, const uint32_t* rec, uint32_t np, uint32_t J, uint32_t Rp,
+                        const uint32_t* cbase, const uint64_t* pair_off, uint32_t* holders) {
+    const size_t smem = (size_t)part.E * 33 * 4 + (size_t)part.E * 33 * 2 + 16;
+    cudaFuncSetAttribute(holder_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const uint64_t tiles = ((uint64_t)part.F + 31) / 32;
+    holder_tile_kernel<<<grid_for(tiles, 1, 148u * 16u), kThreads, smem, s>>>(
+        part, inv, rank16, MB, rec, np, J, Rp, cbase, pair_off, holders);
+}
+
+void launch_sample_lanes(cudaStream_t s, const Part& part, const uint32_t* inv, uint16_t* info,
+                         uint16_t* rank16, uint32_t* pair_count, uint32_t* hard, uint32_t* nhard) {
+    const uint32_t nloc = part.wend - part.wbegin;
+    const uint32_t W = (nloc + 31) / 32;
+    const size_t smem = (size_t)4 * (32 * (3 * W + kOv) + 16 * part.E) * 4;
+    cudaFuncSetAttribute(sample_lanes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const uint64_t groups = ((uint64_t)part.F + 31) / 32;
+    sample_lanes_kernel<<<grid_for(groups, 4, 148u * 8u), 128, smem, s>>>(part, inv, info, rank16,
+                                                                         pair_count, W, hard, nhard);
+}
+
+void launch_sample_hash(cudaStream_t s, const Part& part, const uint32_t* inv, uint16_t* info,
+                        uint16_t* rank16, uint32_t* pair_count, const uint32_t* list,
+                        const uint32_t* nlist, uint64_t max_items) {
+    const uint32_t nloc = part.wend - part.wbegin;
+    const uint32_t d = part.E < nloc ? part.E : nloc;
+    uint32_t hs = 32;
+    while (hs < 2 * d) hs <<= 1;
+    const size_t smem = (size_t)4 * 2 * hs * 4;
+    cudaFuncSetAttribute(sample_hash_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    sample_hash_kernel<<<grid_for(max_items, 4, 148u * 16u), 128, smem, s>>>(part, inv, info, rank16,
+                                                                            pair_count, list, nlist, hs);
+}
+
+void launch_seg_hist(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info,
+                     uint32_t* seghist, uint32_t* segcnt) {
+    const uint64_t nseg = (uint64_t)(part.wend - part.wbegin) * part.E;
+    seg_hist_kernel<<<grid_for(nseg, 1, 148u * 32u), kThreads, part.E * 4, s>>>(part, stream, info,
+                                                                                seghist, segcnt);
+}
+
+void launch_seg_write2(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info,
+                       const double* sizes, const uint64_t* seg_off, const uint64_t* sorted_base,
+                       uint32_t MB, uint32_t* dest, double* sorted_size, uint32_t* blkmask,
+                       uint32_t* blkbase) {
+    const uint64_t nseg = (uint64_t)(part.wend - part.wbegin) * part.E;
+    const size_t smem = (size_t)9 * part.E * 4;
+    cudaFuncSetAttribute(seg_write_kernel2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    seg_write_kernel2<<<grid_for(nseg, 1, 148u * 32u), kThreads, smem, s>>>(
+        part, stream, info, sizes, seg_off, sorted_base, MB, dest, sorted_size, blkmask, blkbase);
+}
+
+}  // namespace clairplan

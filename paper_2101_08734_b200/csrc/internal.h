@@ -105,4 +105,37 @@ void launch_holder_compact(cudaStream_t s, const uint64_t* pair_off, uint32_t F,
 void launch_dense_counts(cudaStream_t s, const uint32_t* cand_k, const uint32_t* cand_info,
                          uint64_t b, uint64_t L, uint32_t* counts);
 
+void launch_count_nonzero(cudaStream_t s, const uint8_t* a, uint64_t n, unsigned long long* out);
+void launch_stream_hist(cudaStream_t s, const uint32_t* st, uint64_t n, uint32_t* counts);
+
+// v2 seed path (fastpath.cu)
+bool lane_path_ok(const Part& part);
+void launch_sample_lanes(cudaStream_t s, const Part& part, const uint32_t* inv, uint16_t* info,
+                         uint16_t* rank16, uint32_t* pair_count, uint32_t* hard, uint32_t* nhard);
+void launch_sample_hash(cudaStream_t s, const Part& part, const uint32_t* inv, uint16_t* info,
+                        uint16_t* rank16, uint32_t* pair_count, const uint32_t* list,
+                        const uint32_t* nlist, uint64_t max_items);
+void launch_seg_hist(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info,
+                     uint32_t* seghist, uint32_t* segcnt);
+void launch_seg_write2(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info,
+                       const double* sizes, const uint64_t* seg_off, const uint64_t* sorted_base,
+                       uint32_t MB, uint32_t* dest, double* sorted_size, uint32_t* blkmask,
+                       uint32_t* blkbase);
+void launch_blk_codes(cudaStream_t s, const Part& part, uint32_t MB, const uint32_t* blkmask,
+                      const uint32_t* blkbase, const uint32_t* dest, const uint8_t* cls_sorted,
+                      uint32_t np, uint32_t J, uint32_t Rp, uint32_t* rec, uint32_t* ccount,
+                      uint64_t nblk);
+void launch_rec_fill(cudaStream_t s, const uint64_t* cpre, uint64_t nblk, uint32_t np, uint32_t J,
+                     uint32_t Rp, uint32_t* rec, uint32_t nloc, uint32_t E, uint32_t MB,
+                     uint32_t* cbase);
+void launch_class_write(cudaStream_t s, const Part& part, uint32_t MB, const uint32_t* stream,
+                        const uint32_t* rec, uint32_t np, uint32_t J, uint32_t Rp,
+                        const uint32_t* cbase, const uint64_t* cstart, uint32_t* class_list,
+                        uint64_t nblk);
+void launch_class_lens(cudaStream_t s, uint32_t nloc, uint32_t E, uint32_t MB, uint32_t J,
+                       const uint64_t* cpre, uint64_t nblk, uint64_t* clen);
+void launch_holder_tile(cudaStream_t s, const Part& part, const uint32_t* inv, const uint16_t* rank16,
+                        uint32_t MB, const uint32_t* rec, uint32_t np, uint32_t J, uint32_t Rp,
+                        const uint32_t* cbase, const uint64_t* pair_off, uint32_t* holders);
+
 }  // namespace clairplan

@@ -33,17 +33,32 @@ __global__ void __launch_bounds__(kThreads) fy_link_kernel(uint64_t key, uint32_
     const uint32_t* st = rt.step + (size_t)er * rt.cap;
     const uint32_t* cu = rt.cum + (size_t)er * rt.cap;
     const uint32_t lim = i_limit < F ? i_limit : F;
-    for (uint32_t i = 1 + blockIdx.x * blockDim.x + threadIdx.x; i < lim;
-         i += gridDim.x * blockDim.x) {
-        const uint32_t shift = n ? rej_shift(st, cu, n, i) : 0;
-        uint32_t extra;
-        const uint32_t j = fy_draw(key, e, F, i, shift, &extra);
-        if (extra) {
-            bool known = false;
-            for (uint32_t t = 0; t < n; ++t) known |= (st[t] == i);
-            if (!known) atomicMax(&rej_flag[er], i + 1);
+    constexpr int U = 4;  // independent draws + exchanges in flight per thread
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t i0 = 1 + blockIdx.x * blockDim.x + threadIdx.x; i0 < lim; i0 += U * stride) {
+        uint32_t j[U], old[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t i = i0 + u * stride;
+            j[u] = kNone;
+            if (i < lim) {
+                const uint32_t shift = n ? rej_shift(st, cu, n, i) : 0;
+                uint32_t extra;
+                j[u] = fy_draw(key, e, F, i, shift, &extra);
+                if (extra) {
+                    bool known = false;
+                    for (uint32_t t = 0; t < n; ++t) known |= (st[t] == i);
+                    if (!known) atomicMax(&rej_flag[er], i + 1);
+                }
+            }
         }
-        if (!detect_only) nx[i] = atomicExch(&hd[j], i);
+        if (detect_only) continue;
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (j[u] != kNone) old[u] = atomicExch(&hd[j[u]], i0 + u * stride);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (j[u] != kNone) nx[i0 + u * stride] = old[u];
     }
 }
 
@@ -64,6 +79,26 @@ __global__ void __launch_bounds__(kThreads) fy_group_kernel(uint32_t F,
     uint32_t* nx = next + (size_t)slot * F;
     uint32_t* qq = q + (size_t)slot * F;
     for (uint32_t y = blockIdx.x * blockDim.x + threadIdx.x; y < F; y += gridDim.x * blockDim.x) {
+        const uint32_t a0 = hd[y];
+        if (a0 == kNone) {
+            qq[y] = kNone;
+            continue;
+        }
+        const uint32_t a1 = nx[a0];
+        if (a1 == kNone) {  // one writer; its succ is already kNone
+            qq[y] = (a0 == y) ? kNone : a0;
+            continue;
+        }
+        const uint32_t a2 = nx[a1];
+        if (a2 == kNone) {  // two writers: list a0 -> a1, needs ascending order
+            const uint32_t lo = a0 < a1 ? a0 : a1, hi = a0 < a1 ? a1 : a0;
+            qq[y] = (lo == y) ? hi : lo;
+            if (a0 > a1) {
+                nx[a1] = a0;
+                nx[a0] = kNone;
+            }
+            continue;
+        }
         uint32_t buf[kLocal];
         uint32_t n = 0;
         uint32_t cur = hd[y];

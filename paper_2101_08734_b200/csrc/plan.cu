@@ -9,17 +9,20 @@
 //   K6    first_fit_pass per class       -> class of every candidate
 //   K7    radix pass on class digit      -> prefetch-ordered class lists
 //   K8    holder_scatter (+ compaction)  -> holder CSR
+#include <stdlib.h>
+
 #include "plan_impl.h"
 
 namespace clairplan {
 thread_local std::string g_err;
+
 }  // namespace clairplan
 
 namespace clairplan {
 
 uint32_t epochs_per_batch(uint32_t F, uint32_t E) {
     const uint64_t per = (uint64_t)F * 12;
-    uint64_t eb = (96ull << 20) / (per ? per : 1);
+    uint64_t eb = (48ull << 20) / (per ? per : 1);
     if (eb < 1) eb = 1;
     if (eb > E) eb = E;
     if (eb > 64) eb = 64;
@@ -365,6 +368,241 @@ int build_seed_path(clairplan_plan* p) {
 }  // namespace clairplan
 
 // ---------------------------------------------------------------------------------------
+namespace clairplan {
+
+// ---- v2 seed path --------------------------------------------------------------------
+bool v2_ok(const clairplan_plan* p) {
+    const Part& part = p->part;
+    return lane_path_ok(part) && part.E <= 1024 && p->cfg.num_classes <= 12 &&
+           (uint64_t)p->nloc * part.E * part.E <= (1ull << 28);
+}
+
+// First fit of the tier-ordered sizes, class by class (pack_first_fit, policies.cpp:40-55);
+// cls[s] = class of tier-ordered element s (0 = not cached).
+int first_fit_classes(clairplan_plan* p, const double* ssize, uint8_t* cls) {
+    const uint32_t J = p->cfg.num_classes, nloc = p->nloc;
+    const uint64_t D = p->D;
+    cudaStream_t s = p->stream;
+    Workspace& ws = p->ws;
+    bool ok = true;
+    uint8_t* taken = need<uint8_t>(p->taken, D, ok);
+    unsigned long long* cnt = need<unsigned long long>(p->counters, 4, ok);
+    if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed (first fit)");
+    CK(cudaMemsetAsync(cls, 0, D, s));
+    uint64_t* sb = ws.scratch<uint64_t>(nloc);
+    uint64_t* sl = ws.scratch<uint64_t>(nloc);
+    CK(cudaMemcpyAsync(sb, p->wbeg.get<uint64_t>(), nloc * 8, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(sl, p->wlen.get<uint64_t>(), nloc * 8, cudaMemcpyDeviceToDevice, s));
+    const uint32_t* seq_idx = nullptr;
+    const double* seq_sz = ssize;
+    uint64_t remaining = D;
+    for (uint32_t j = 1; j <= J; ++j) {
+        if (remaining == 0) break;
+        if (j > 1) {
+            uint32_t* keys = need<uint32_t>(p->keys, D, ok);
+            uint32_t* okeys = need<uint32_t>(p->okeys, D, ok);
+            uint32_t* ib0 = need<uint32_t>(p->vals, D, ok);
+            uint32_t* ib1 = need<uint32_t>(p->ovals, D, ok);
+            double* seqsz = need<double>(p->seqsz, D, ok);
+            if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed (first fit)");
+            uint32_t* in_idx = (j % 2) ? ib0 : ib1;
+            uint32_t* out_idx = (j % 2) ? ib1 : ib0;
+            launch_reject_keys(s, taken, D, seq_idx, keys, in_idx);
+            const size_t m = ws.mark();
+            TileMap tj;
+            build_tilemap(s, sl, nloc, D, kRadixTile, tj, ws);
+            uint64_t* sc = nullptr;
+            radix_pass(s, tj, sb, sl, keys, in_idx, 0, okeys, out_idx, nullptr, &sc, ws);
+            uint64_t* nb = ws.scratch<uint64_t>(2 * (uint64_t)nloc);
+            radix_regions(s, tj, sb, sl, sc, 1, nb, nb + nloc);
+            CK(cudaMemcpyAsync(sb, nb, nloc * 8, cudaMemcpyDeviceToDevice, s));
+            CK(cudaMemcpyAsync(sl, nb + nloc, nloc * 8, cudaMemcpyDeviceToDevice, s));
+            ws.release(m);
+            launch_gather_seq_sizes(s, out_idx, ssize, sb, sl, nloc, seqsz);
+            seq_idx = out_idx;
+            seq_sz = seqsz;
+            p->launches += 10;
+        }
+        CK(cudaMemsetAsync(taken, 0, D, s));
+        const size_t m = ws.mark();
+        first_fit_pass(s, sb, sl, nloc, D, seq_sz, p->caps[j - 1], taken, ws);
+        ws.release(m);
+        launch_apply_pass(s, taken, D, seq_idx, nullptr, (uint8_t)j, cls);
+        p->launches += 9;
+        if (j < J) {
+            unsigned long long t = 0;
+            launch_count_nonzero(s, taken, D, cnt);
+            CK(cudaMemcpyAsync(&t, cnt, 8, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            remaining -= t;
+            ++p->launches;
+        }
+    }
+    return 0;
+}
+
+int build_seed_path_v2(clairplan_plan* p) {
+    cudaStream_t s = p->stream;
+    const Part& part = p->part;
+    const uint32_t F = part.F, E = part.E, nloc = p->nloc, J = p->cfg.num_classes;
+    const uint32_t MB = (uint32_t)((part.epoch_len(part.wbegin) + 31) / 32);
+    const uint64_t nblk = (uint64_t)nloc * E * MB;
+    uint32_t np = 0;
+    while ((1u << np) <= J) ++np;  // bits to hold classes 0..J
+    const uint64_t EF = (uint64_t)E * F, NEE = (uint64_t)nloc * E * E;
+    bool ok = true;
+    uint32_t* stream_buf = need<uint32_t>(p->stream_buf, p->A, ok);
+    uint32_t* inv = need<uint32_t>(p->inv, EF, ok);
+    uint16_t* info = need<uint16_t>(p->info16, EF, ok);
+    uint16_t* rank16 = need<uint16_t>(p->rank16, EF, ok);
+    uint32_t* pcount = need<uint32_t>(p->pair_count, F, ok);
+    uint64_t* poff = need<uint64_t>(p->pair_off, (uint64_t)F + 1, ok);
+    uint32_t* seghist = need<uint32_t>(p->seghist, NEE, ok);
+    uint64_t* sbase = need<uint64_t>(p->sorted_base, NEE + 1, ok);
+    uint32_t* segcnt = need<uint32_t>(p->segcnt, (uint64_t)nloc * E, ok);
+    uint64_t* segoff = need<uint64_t>(p->seg_off, (uint64_t)nloc * E + 1, ok);
+    uint64_t* wbeg = need<uint64_t>(p->wbeg, nloc, ok);
+    uint64_t* wlen = need<uint64_t>(p->wlen, nloc, ok);
+    uint32_t* bmask = need<uint32_t>(p->blkmask, nblk, ok);
+    uint32_t* bbase = need<uint32_t>(p->blkbase, nblk, ok);
+    uint32_t* hard = need<uint32_t>(p->hard, (uint64_t)F + 1, ok);
+    if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed (streams / histograms)");
+    if (int rc = ensure_ws(p, std::max<uint64_t>(p->A, std::max<uint64_t>(NEE, F)), nloc)) return rc;
+    if (int rc = alloc_rej(p, E)) return rc;
+    uint32_t* nhard = hard + F;
+
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        p->launches = 0;
+        p->ws.used = 0;
+        CK(cudaEventRecord(p->ev0, s));
+        p->mark(0);
+        // K1-K3: permutations -> streams + inverse permutations
+        if (int rc = enqueue_perms(p, stream_buf, inv, nullptr, 0, E)) return rc;
+        p->mark(1);
+        // K4a: per-sample (worker, count, first epoch)
+        CK(cudaMemsetAsync(nhard, 0, 4, s));
+        launch_sample_lanes(s, part, inv, info, rank16, pcount, hard, nhard);
+        launch_sample_hash(s, part, inv, info, rank16, pcount, hard, nhard, 148u * 16u * 4u);
+        exclusive_scan(s, pcount, F, poff, p->ws);
+        p->mark(2);
+        // K4b: per-segment count histograms -> first-order and tier-order bases
+        launch_seg_hist(s, part, stream_buf, info, seghist, segcnt);
+        exclusive_scan(s, seghist, NEE, sbase, p->ws);
+        exclusive_scan(s, segcnt, (uint64_t)nloc * E, segoff, p->ws);
+        p->mark(3);
+        p->launches += 10;
+        std::vector<uint32_t> flags(E);
+        uint64_t D = 0;
+        CK(cudaMemcpyAsync(&D, segoff + (uint64_t)nloc * E, 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(flags.data(), p->rej_flag.get<uint32_t>(), E * 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        bool any = false;
+        if (int rc = resolve_rejections(p, flags, &any)) return rc;
+        if (any) continue;
+        p->D = D;
+        if (D >= 0xFFFFFFFFull)
+            return fail(CLAIRPLAN_EOVERFLOW, "more than 2^32-1 (worker, sample) pairs in one handle; "
+                                             "shard the workers over several handles");
+        uint32_t* dest = need<uint32_t>(p->dest, D, ok);
+        double* ssize = need<double>(p->sorted_size, D, ok);
+        uint8_t* cls = need<uint8_t>(p->cand_cls, D, ok);
+        uint32_t* htmp = need<uint32_t>(p->holders_tmp, 3 * D, ok);
+        uint32_t* centries = need<uint32_t>(p->class_entries, D, ok);
+        const uint32_t Rp = ((np + J) + 3) & ~3u;
+        uint32_t* rec = need<uint32_t>(p->planes, (uint64_t)std::max<uint32_t>(Rp, 4) * nblk, ok);
+        uint32_t* cbase = need<uint32_t>(p->cbase, (uint64_t)nloc * std::max<uint32_t>(J, 1), ok);
+        uint32_t* ccount = need<uint32_t>(p->ccount, std::max<uint32_t>(J, 1) * nblk, ok);
+        uint64_t* cpre = need<uint64_t>(p->cpre, std::max<uint32_t>(J, 1) * (nblk + 1), ok);
+        uint64_t* clen = need<uint64_t>(p->class_len, (uint64_t)nloc * std::max<uint32_t>(J, 1), ok);
+        uint64_t* cstart = need<uint64_t>(p->class_start, (uint64_t)nloc * std::max<uint32_t>(J, 1) + 1, ok);
+        if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed (candidates)");
+        // K4c: candidates in first order / tier order
+        launch_seg_write2(s, part, stream_buf, info, p->sizes.get<double>(), segoff, sbase, MB, dest,
+                          ssize, bmask, bbase);
+        launch_worker_segments(s, segoff, nloc, E, wbeg, wlen);
+        p->launches += 2;
+        p->mark(4);
+        p->mark(5);
+        if (J > 0) {
+            // K6: first fit class by class
+            if (int rc = first_fit_classes(p, ssize, cls)) return rc;
+            p->mark(6);
+            // K7: block class records, class lists
+            launch_blk_codes(s, part, MB, bmask, bbase, dest, cls, np, J, Rp, rec, ccount, nblk);
+            for (uint32_t j = 0; j < J; ++j)
+                exclusive_scan(s, ccount + (uint64_t)j * nblk, nblk, cpre + (uint64_t)j * (nblk + 1), p->ws);
+            launch_rec_fill(s, cpre, nblk, np, J, Rp, rec, nloc, E, MB, cbase);
+            launch_class_lens(s, nloc, E, MB, J, cpre, nblk, clen);
+            exclusive_scan(s, clen, (uint64_t)nloc * J, cstart, p->ws);
+            launch_class_write(s, part, MB, stream_buf, rec, np, J, Rp, cbase, cstart, centries, nblk);
+            p->launches += 4 + 3 * J + 3;
+            std::vector<uint64_t> hlen((size_t)nloc * J), hst((size_t)nloc * J);
+            CK(cudaMemcpyAsync(hlen.data(), clen, hlen.size() * 8, cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(hst.data(), cstart, hst.size() * 8, cudaMemcpyDeviceToHost, s));
+            p->mark(7);
+            // K8: holder CSR, sample-major
+            launch_holder_tile(s, part, inv, rank16, MB, rec, np, J, Rp, cbase, poff, htmp);
+            ++p->launches;
+            CK(cudaStreamSynchronize(s));
+            p->class_start_h.assign((size_t)nloc * (J + 1), 0);
+            p->class_len_h.assign((size_t)nloc * (J + 1), 0);
+            uint64_t H = 0;
+            for (uint32_t w = 0; w < nloc; ++w)
+                for (uint32_t j = 0; j < J; ++j) {
+                    p->class_start_h[(size_t)w * (J + 1) + j] = hst[(size_t)w * J + j];
+                    p->class_len_h[(size_t)w * (J + 1) + j] = hlen[(size_t)w * J + j];
+                    H += hlen[(size_t)w * J + j];
+                }
+            p->H = H;
+            if (H == D) {
+                p->holder_off_dev = poff;
+                p->holders_dev = htmp;
+            } else {
+                uint32_t* hc = need<uint32_t>(p->hcount, F, ok);
+                uint64_t* ho = need<uint64_t>(p->hoff, (uint64_t)F + 1, ok);
+                uint32_t* hl = need<uint32_t>(p->holders, 3 * std::max<uint64_t>(H, 1), ok);
+                if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed (holders)");
+                launch_holder_count(s, poff, F, htmp, hc);
+                exclusive_scan(s, hc, F, ho, p->ws);
+                launch_holder_compact(s, poff, F, htmp, ho, hl);
+                p->launches += 5;
+                p->holder_off_dev = ho;
+                p->holders_dev = hl;
+            }
+        } else {
+            p->H = 0;
+            uint64_t* ho = need<uint64_t>(p->hoff, (uint64_t)F + 1, ok);
+            if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed");
+            CK(cudaMemsetAsync(ho, 0, ((uint64_t)F + 1) * 8, s));
+            p->holder_off_dev = ho;
+            p->holders_dev = nullptr;
+            p->class_start_h.assign(nloc, 0);
+            p->class_len_h.assign(nloc, 0);
+            p->mark(6);
+            p->mark(7);
+        }
+        p->mark(clairplan_plan::kStages);
+        CK(cudaEventRecord(p->ev1, s));
+        CK(cudaEventSynchronize(p->ev1));
+        CK(cudaGetLastError());
+        if (p->ws.overflow) return fail(CLAIRPLAN_ENOMEM, "internal workspace overflow");
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
+        p->device_ms = ms;
+        for (int i = 0; i < clairplan_plan::kStages; ++i) {
+            float t = 0;
+            if (p->sev[i] && p->sev[i + 1]) cudaEventElapsedTime(&t, p->sev[i], p->sev[i + 1]);
+            p->stage_ms[i] = t;
+        }
+        p->v2 = true;
+        p->built = true;
+        return 0;
+    }
+    return fail(CLAIRPLAN_ECUDA, "rejection tables did not converge");
+}
+
+}  // namespace clairplan
+
 extern "C" {
 
 int clairplan_version(void) { return 1; }
@@ -442,6 +680,9 @@ int clairplan_build(clairplan_t p) {
     if (p->generic) return fail(CLAIRPLAN_EINVAL, "plan was created from explicit streams");
     CK(cudaSetDevice(p->device));
     p->built = false;
+    p->v2 = false;
+    const char* force = getenv("CLAIRPLAN_FORCE_V1");
+    if (v2_ok(p) && !(force && force[0] == '1')) return build_seed_path_v2(p);
     return build_seed_path(p);
 }
 
@@ -548,17 +789,15 @@ int clairplan_export_holders(clairplan_t p, uint64_t* offsets, uint32_t* holders
 int clairplan_export_counts(clairplan_t p, uint32_t w, uint32_t* counts) {
     if (!p || !p->built) return fail(CLAIRPLAN_EINVAL, "plan not built");
     if (w < p->part.wbegin || w >= p->part.wend) return fail(CLAIRPLAN_EINVAL, "worker not in plan");
+    if (p->generic) return fail(CLAIRPLAN_EINVAL, "counts of an explicit-stream plan are the caller's");
     CK(cudaSetDevice(p->device));
-    const uint32_t wl = w - p->part.wbegin;
-    uint64_t b = 0, L = 0;
-    CK(cudaMemcpy(&b, p->wbeg.get<uint64_t>() + wl, 8, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(&L, p->wlen.get<uint64_t>() + wl, 8, cudaMemcpyDeviceToHost));
+    const uint64_t a = p->part.stream_offset(w), b = p->part.stream_offset(w + 1);
     DevBuf tmp;
     if (!tmp.ensure((size_t)p->part.F * 4)) return fail(CLAIRPLAN_ENOMEM, "device allocation failed");
     CK(cudaMemsetAsync(tmp.p, 0, (size_t)p->part.F * 4, p->stream));
-    launch_dense_counts(p->stream, p->cand_k.get<uint32_t>(), p->cand_info.get<uint32_t>(), b, L,
-                        tmp.get<uint32_t>());
+    if (b > a) launch_stream_hist(p->stream, p->stream_buf.get<uint32_t>() + a, b - a, tmp.get<uint32_t>());
     CK(cudaStreamSynchronize(p->stream));
+    CK(cudaGetLastError());
     CK(cudaMemcpy(counts, tmp.p, (size_t)p->part.F * 4, cudaMemcpyDeviceToHost));
     return 0;
 }

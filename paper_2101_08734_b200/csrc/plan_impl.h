@@ -112,6 +112,8 @@ struct clairplan_plan {
     DevBuf head, next, q, scratch, counters, rej_flag, rej_step, rej_cum, rej_count;
     DevBuf wsbuf;
     DevBuf cand_w, dfirst, dcounts;  // explicit-stream (generic) path
+    DevBuf inv, info16, rank16, cbase, seghist, sorted_base, blkmask, blkbase, planes, ccount, cpre, hard;
+    bool v2 = false;                 // fast seed path in use for the last build
     uint32_t maxcount = 0;           // generic path: largest frequency value
     Workspace ws;
 
