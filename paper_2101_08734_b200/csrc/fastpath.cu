@@ -26,45 +26,37 @@
 
 namespace clairplan {
 
-constexpr uint32_t kOv = 16;  // repeated-worker list per lane
 constexpr int kU = 8;         // epochs loaded per batch (memory-level parallelism)
 
 __device__ __forceinline__ uint32_t ld_inv(const uint32_t* p) { return __ldcg(p); }
 
 // ---------------------------------------------------------------------------- K4a
-// Lane = sample.  One pass over the E inverse entries (8 coalesced loads in flight per lane)
-// marks the sample's workers in a per-lane bitmap (shared memory, [word][lane] layout: no bank
-// conflicts), records the worker of each first access, and keeps repeated workers (bitmap b2)
-// with their counts in a short list; the second pass works from shared memory only and writes
+// Lane = sample, everything per lane in shared memory with a [row][lane] layout (no bank
+// conflicts).  Pass 1 streams the E inverse entries (kU coalesced loads in flight) and records
+// the worker of every access (bit 15 = first access of that worker) while marking a per-lane
+// worker bitmap; after its popcount prefix, pass 2 counts accesses per rank, pass 3 writes
 //   info[e][k] = count of (w,k) at its first epoch, else 0          (u16)
 //   rank[e][k] = rank of w among k's workers (worker order), else 0xFFFF  (u16)
 __global__ void __launch_bounds__(128) sample_lanes_kernel(Part part, const uint32_t* __restrict__ inv,
                                                            uint16_t* __restrict__ info,
                                                            uint16_t* __restrict__ rank16,
                                                            uint32_t* __restrict__ pair_count,
-                                                           uint32_t W, uint32_t* __restrict__ hard,
-                                                           uint32_t* __restrict__ nhard) {
+                                                           uint32_t W) {
     extern __shared__ uint32_t sm[];
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t E = part.E, F = part.F;
-    const uint32_t per_warp = 32 * (3 * W + kOv) + 16 * E;  // words
-    uint32_t* bm = sm + warp * per_warp;  // [W][32] workers seen
-    uint32_t* b2 = bm + 32 * W;           // [W][32] workers seen twice or more
-    uint32_t* pre = b2 + 32 * W;          // [W][32] popcount prefix of bm
-    uint32_t* ov = pre + 32 * W;          // [kOv][32] (w << 16 | count) of repeated workers
-    uint16_t* wls = reinterpret_cast<uint16_t*>(ov + 32 * kOv);  // [E][32] worker of a first access
-    for (uint32_t t = 0; t < W; ++t) {
-        bm[t * 32 + lane] = 0;
-        b2[t * 32 + lane] = 0;
-    }
+    const uint32_t per_warp = 64 * W + 32 * E;  // words: bm, pre, wls (u16), cnt (u16)
+    uint32_t* bm = sm + warp * per_warp;  // [W][32]
+    uint32_t* pre = bm + 32 * W;          // [W][32]
+    uint16_t* wls = reinterpret_cast<uint16_t*>(pre + 32 * W);  // [E][32]
+    uint16_t* cnt = wls + 32 * E;                                // [E][32] by rank
+    for (uint32_t t = 0; t < W; ++t) bm[t * 32 + lane] = 0;
     const uint64_t ngroups = (F + 31) / 32;
     const uint64_t gw = (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp;
     const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x >> 5);
     for (uint64_t g = gw; g < ngroups; g += nw) {
         const uint32_t k = (uint32_t)(g * 32 + lane);
         const bool live = k < F;
-        uint32_t nov = 0;
-        bool overflow = false;
         for (uint32_t e0 = 0; e0 < E; e0 += kU) {
             uint32_t pv[kU];
 #pragma unroll
@@ -74,7 +66,7 @@ __global__ void __launch_bounds__(128) sample_lanes_kernel(Part part, const uint
             for (int u = 0; u < kU; ++u) {
                 const uint32_t e = e0 + u;
                 if (e >= E) break;
-                uint16_t wrec = 0xFFFFu;
+                uint32_t rec = 0xFFFFu;
                 const uint32_t p = pv[u];
                 if (p < part.P) {
                     const uint32_t w = part.worker_of(p);
@@ -83,27 +75,11 @@ __global__ void __launch_bounds__(128) sample_lanes_kernel(Part part, const uint
                         uint32_t* word = &bm[(wl >> 5) * 32 + lane];
                         const uint32_t bit = 1u << (wl & 31);
                         const uint32_t v = *word;
-                        if (!(v & bit)) {
-                            *word = v | bit;
-                            wrec = (uint16_t)wl;
-                        } else {
-                            b2[(wl >> 5) * 32 + lane] |= bit;
-                            uint32_t i = 0;
-                            for (; i < nov; ++i) {
-                                const uint32_t o = ov[i * 32 + lane];
-                                if ((o >> 16) == wl) {
-                                    ov[i * 32 + lane] = o + 1;
-                                    break;
-                                }
-                            }
-                            if (i == nov) {
-                                if (nov < kOv) ov[(nov++) * 32 + lane] = (wl << 16) | 2u;
-                                else overflow = true;
-                            }
-                        }
+                        *word = v | bit;
+                        rec = wl | ((v & bit) ? 0u : 0x8000u);
                     }
                 }
-                wls[e * 32 + lane] = wrec;
+                wls[e * 32 + lane] = (uint16_t)rec;
             }
         }
         uint32_t d = 0;
@@ -112,29 +88,29 @@ __global__ void __launch_bounds__(128) sample_lanes_kernel(Part part, const uint
             d += __popc(bm[t * 32 + lane]);
         }
         if (live) pair_count[k] = d;
-        if (overflow) hard[atomicAdd(nhard, 1u)] = k;
-        if (live && !overflow) {
+        for (uint32_t r = 0; r < d; ++r) cnt[r * 32 + lane] = 0;
+        for (uint32_t e = 0; e < E; ++e) {
+            const uint32_t rec = wls[e * 32 + lane];
+            if (rec == 0xFFFFu) continue;
+            const uint32_t wl = rec & 0x7FFFu, wd = (wl >> 5) * 32 + lane;
+            const uint32_t r = pre[wd] + __popc(bm[wd] & ((1u << (wl & 31)) - 1u));
+            cnt[r * 32 + lane] += 1;
+        }
+        if (live) {
             for (uint32_t e = 0; e < E; ++e) {
-                const uint32_t wl = wls[e * 32 + lane];
-                uint16_t c = 0, r = 0xFFFFu;
-                if (wl != 0xFFFFu) {
-                    const uint32_t sh = wl & 31, wd = (wl >> 5) * 32 + lane;
-                    c = 1;
-                    if ((b2[wd] >> sh) & 1u)
-                        for (uint32_t i = 0; i < nov; ++i) {
-                            const uint32_t o = ov[i * 32 + lane];
-                            if ((o >> 16) == wl) c = (uint16_t)(o & 0xFFFFu);
-                        }
-                    r = (uint16_t)(pre[wd] + __popc(bm[wd] & ((1u << sh) - 1u)));
+                const uint32_t rec = wls[e * 32 + lane];
+                uint16_t c = 0, rk = 0xFFFFu;
+                if (rec != 0xFFFFu && (rec & 0x8000u)) {
+                    const uint32_t wl = rec & 0x7FFFu, wd = (wl >> 5) * 32 + lane;
+                    const uint32_t r = pre[wd] + __popc(bm[wd] & ((1u << (wl & 31)) - 1u));
+                    c = cnt[r * 32 + lane];
+                    rk = (uint16_t)r;
                 }
                 info[(size_t)e * F + k] = c;
-                rank16[(size_t)e * F + k] = r;
+                rank16[(size_t)e * F + k] = rk;
             }
         }
-        for (uint32_t t = 0; t < W; ++t) {
-            bm[t * 32 + lane] = 0;
-            b2[t * 32 + lane] = 0;
-        }
+        for (uint32_t t = 0; t < W; ++t) bm[t * 32 + lane] = 0;
     }
 }
 
@@ -147,15 +123,18 @@ __global__ void __launch_bounds__(128) sample_hash_kernel(Part part, const uint3
                                                           uint32_t* __restrict__ pair_count,
                                                           const uint32_t* __restrict__ list,
                                                           const uint32_t* __restrict__ nlist,
-                                                          uint32_t hs) {
+                                                          uint32_t hs, uint32_t W) {
     extern __shared__ uint32_t sm[];
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t* keys = sm + warp * 2 * hs;
+    uint32_t* keys = sm + warp * (2 * hs + 2 * W);
     uint32_t* vals = keys + hs;
+    uint32_t* bm = vals + hs;   // [W] workers of the current sample
+    uint32_t* pre = bm + W;     // [W] popcount prefix
     const uint32_t mask = hs - 1;
     const uint32_t E = part.E, F = part.F;
     const uint32_t n = list ? *nlist : F;
     for (uint32_t t = lane; t < hs; t += 32) keys[t] = kNone;
+    for (uint32_t t = lane; t < W; t += 32) bm[t] = 0;
     __syncwarp();
     for (uint32_t idx = blockIdx.x * (blockDim.x >> 5) + warp; idx < n;
          idx += gridDim.x * (blockDim.x >> 5)) {
@@ -189,10 +168,27 @@ __global__ void __launch_bounds__(128) sample_hash_kernel(Part part, const uint3
                     }
                     slot = (slot + 1) & mask;
                 }
+                if (fresh) atomicOr(&bm[w >> 5], 1u << (w & 31));
             }
             distinct += __popc(__ballot_sync(0xffffffffu, fresh));
             __syncwarp();
         }
+        {   // prefix popcounts of the worker bitmap (lane-strided words, warp scan)
+            uint32_t carry = 0;
+            for (uint32_t t0 = 0; t0 < W; t0 += 32) {
+                const uint32_t t = t0 + lane;
+                const uint32_t c = t < W ? __popc(bm[t]) : 0;
+                uint32_t incl = c;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                    if ((int)lane >= o) incl += y;
+                }
+                if (t < W) pre[t] = carry + incl - c;
+                carry += __shfl_sync(0xffffffffu, incl, 31);
+            }
+        }
+        __syncwarp();
         for (uint32_t r = 0; r * 32 < E; ++r) {
             const uint32_t e = r * 32 + lane;
             if (e >= E) continue;
@@ -207,9 +203,7 @@ __global__ void __launch_bounds__(128) sample_hash_kernel(Part part, const uint3
                     const uint32_t v = vals[slot];
                     if ((v >> 16) == e) {
                         out = (uint16_t)(v & 0xFFFFu);
-                        uint32_t less = 0;  // rank = distinct workers below w (rare path)
-                        for (uint32_t t = 0; t <= mask; ++t) less += keys[t] < w;
-                        rk = (uint16_t)less;
+                        rk = (uint16_t)(pre[w >> 5] + __popc(bm[w >> 5] & ((1u << (w & 31)) - 1u)));
                     }
                 }
             }
@@ -218,6 +212,7 @@ __global__ void __launch_bounds__(128) sample_hash_kernel(Part part, const uint3
         }
         __syncwarp();
         for (uint32_t t = lane; t < hs; t += 32) keys[t] = kNone;
+        for (uint32_t t = lane; t < W; t += 32) bm[t] = 0;
         if (lane == 0) pair_count[k] = distinct;
         __syncwarp();
     }
@@ -532,6 +527,7 @@ __global__ void __launch_bounds__(kThreads) holder_tile_kernel(
 constexpr uint32_t kMaxLaneWorkers = 2048;
 
 bool lane_path_ok(const Part& part) {
+    // per-lane shared rows: 2 x W bitmap words + E x (worker, count) u16 pairs, 4 warps / CTA
     return (part.wend - part.wbegin) <= kMaxLaneWorkers && part.E <= 1024;
 }
 
@@ -578,14 +574,14 @@ void launch_holder_tile(cudaStream_t s, const Part& part, const uint32_t* inv, c
 }
 
 void launch_sample_lanes(cudaStream_t s, const Part& part, const uint32_t* inv, uint16_t* info,
-                         uint16_t* rank16, uint32_t* pair_count, uint32_t* hard, uint32_t* nhard) {
+                         uint16_t* rank16, uint32_t* pair_count) {
     const uint32_t nloc = part.wend - part.wbegin;
     const uint32_t W = (nloc + 31) / 32;
-    const size_t smem = (size_t)4 * (32 * (3 * W + kOv) + 16 * part.E) * 4;
+    const size_t smem = (size_t)4 * (64 * W + 32 * part.E) * 4;
     cudaFuncSetAttribute(sample_lanes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const uint64_t groups = ((uint64_t)part.F + 31) / 32;
     sample_lanes_kernel<<<grid_for(groups, 4, 148u * 8u), 128, smem, s>>>(part, inv, info, rank16,
-                                                                         pair_count, W, hard, nhard);
+                                                                         pair_count, W);
 }
 
 void launch_sample_hash(cudaStream_t s, const Part& part, const uint32_t* inv, uint16_t* info,
@@ -595,10 +591,11 @@ void launch_sample_hash(cudaStream_t s, const Part& part, const uint32_t* inv, u
     const uint32_t d = part.E < nloc ? part.E : nloc;
     uint32_t hs = 32;
     while (hs < 2 * d) hs <<= 1;
-    const size_t smem = (size_t)4 * 2 * hs * 4;
+    const uint32_t W = (nloc + 31) / 32;
+    const size_t smem = (size_t)4 * (2 * hs + 2 * W) * 4;
     cudaFuncSetAttribute(sample_hash_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    sample_hash_kernel<<<grid_for(max_items, 4, 148u * 16u), 128, smem, s>>>(part, inv, info, rank16,
-                                                                            pair_count, list, nlist, hs);
+    sample_hash_kernel<<<grid_for(max_items, 4, 148u * 16u), 128, smem, s>>>(
+        part, inv, info, rank16, pair_count, list, nlist, hs, W);
 }
 
 void launch_seg_hist(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info,

@@ -111,7 +111,7 @@ void launch_stream_hist(cudaStream_t s, const uint32_t* st, uint64_t n, uint32_t
 // v2 seed path (fastpath.cu)
 bool lane_path_ok(const Part& part);
 void launch_sample_lanes(cudaStream_t s, const Part& part, const uint32_t* inv, uint16_t* info,
-                         uint16_t* rank16, uint32_t* pair_count, uint32_t* hard, uint32_t* nhard);
+                         uint16_t* rank16, uint32_t* pair_count);
 void launch_sample_hash(cudaStream_t s, const Part& part, const uint32_t* inv, uint16_t* info,
                         uint16_t* rank16, uint32_t* pair_count, const uint32_t* list,
                         const uint32_t* nlist, uint64_t max_items);

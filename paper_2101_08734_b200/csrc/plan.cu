@@ -373,7 +373,7 @@ namespace clairplan {
 // ---- v2 seed path --------------------------------------------------------------------
 bool v2_ok(const clairplan_plan* p) {
     const Part& part = p->part;
-    return lane_path_ok(part) && part.E <= 1024 && p->cfg.num_classes <= 12 &&
+    return (p->nloc <= 65535) && part.E <= 1024 && p->cfg.num_classes <= 12 &&
            (uint64_t)p->nloc * part.E * part.E <= (1ull << 28);
 }
 
@@ -469,7 +469,8 @@ int build_seed_path_v2(clairplan_plan* p) {
     if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed (streams / histograms)");
     if (int rc = ensure_ws(p, std::max<uint64_t>(p->A, std::max<uint64_t>(NEE, F)), nloc)) return rc;
     if (int rc = alloc_rej(p, E)) return rc;
-    uint32_t* nhard = hard + F;
+    (void)hard;
+    const bool lanes = lane_path_ok(part);
 
     for (int attempt = 0; attempt < 2; ++attempt) {
         p->launches = 0;
@@ -480,9 +481,11 @@ int build_seed_path_v2(clairplan_plan* p) {
         if (int rc = enqueue_perms(p, stream_buf, inv, nullptr, 0, E)) return rc;
         p->mark(1);
         // K4a: per-sample (worker, count, first epoch)
-        CK(cudaMemsetAsync(nhard, 0, 4, s));
-        launch_sample_lanes(s, part, inv, info, rank16, pcount, hard, nhard);
-        launch_sample_hash(s, part, inv, info, rank16, pcount, hard, nhard, 148u * 16u * 4u);
+        if (lanes) {
+            launch_sample_lanes(s, part, inv, info, rank16, pcount);
+        } else {
+            launch_sample_hash(s, part, inv, info, rank16, pcount, nullptr, nullptr, F);
+        }
         exclusive_scan(s, pcount, F, poff, p->ws);
         p->mark(2);
         // K4b: per-segment count histograms -> first-order and tier-order bases

@@ -88,6 +88,28 @@ def test_plan_small_matches_reference(cp, ref, case):
     assert plans_equal(a, b) is None
 
 
+@pytest.mark.parametrize("case", [
+    (4, 2000, 64, 64, 200, False, [30.0, 60.0], (0.1, 0.1)),   # >32 repeated workers: hash fallback
+    (6, 6000, 3000, 3000, 3, True, [2.0, 5.0], (0.1, 0.1)),    # >2048 workers: v1 pipeline
+])
+def test_plan_fallback_paths(cp, ref, case):
+    seed, F, N, B, E, dl, caps, (mu, sd) = case
+    sizes = ref.generate_sizes(F, mu, sd, None, 1)
+    a = ref.plan(seed, F, N, B, E, dl, caps, sizes)
+    b = device_plan(cp, seed, F, N, B, E, dl, caps, sizes)
+    assert plans_equal(a, b) is None
+
+
+@pytest.mark.parametrize("case", CASES[:6])
+def test_plan_v1_pipeline_matches_reference(cp, ref, case, monkeypatch):
+    monkeypatch.setenv("CLAIRPLAN_FORCE_V1", "1")
+    seed, F, N, B, E, dl, caps, (mu, sd) = case
+    sizes = ref.generate_sizes(F, mu, sd, None, 1)
+    a = ref.plan(seed, F, N, B, E, dl, caps, sizes)
+    b = device_plan(cp, seed, F, N, B, E, dl, caps, sizes)
+    assert plans_equal(a, b) is None
+
+
 def test_plan_random_configs(cp, ref):
     rng = np.random.default_rng(9)
     for _ in range(25):
