@@ -481,8 +481,8 @@ __global__ void __launch_bounds__(kThreads) holder_tile_kernel(
         for (uint32_t idx = threadIdx.x; idx < E * 32; idx += blockDim.x) {
             const uint32_t e = idx >> 5, l = idx & 31;
             const bool ok = k0 + l < F;
-            tinv[e * 33 + l] = ok ? ld_inv(inv + (size_t)e * F + k0 + l) : kNone;
-            trk[e * 33 + l] = ok ? rank16[(size_t)e * F + k0 + l] : (uint16_t)0xFFFFu;
+            tinv[e * 33 + l] = ok ? __ldcs(inv + (size_t)e * F + k0 + l) : kNone;
+            trk[e * 33 + l] = ok ? __ldcs(rank16 + (size_t)e * F + k0 + l) : (uint16_t)0xFFFFu;
         }
         __syncthreads();
         for (uint32_t s = warp; s < 32; s += nwarps) {

@@ -32,23 +32,43 @@ struct Mono {
 
 __device__ __forceinline__ Mono mono_id() { return Mono{0, 0, 0u, 1u}; }
 
+// s / u = m * 2^(es - (k - 52)) with m the 53-bit significand: integer shifts only.
 __device__ __forceinline__ Mono mono_elem(double s, int k) {
-    const double t = ldexp(s, 52 - k);  // exact power-of-two scaling, t <= 2^52
-    const double D = floor(t);
-    const double fr = t - D;
-    const long long Di = (long long)D;
-    const uint32_t dpar = (uint32_t)(Di & 1);
-    Mono m;
-    if (fr == 0.5) {  // tie: the result R - D - 1/2 rounds to the even neighbour
-        m.d0 = Di + (0u ^ dpar);
-        m.d1 = Di + (1u ^ dpar);
+    const uint64_t bits = (uint64_t)__double_as_longlong(s);
+    const int bexp = (int)((bits >> 52) & 0x7FF);
+    uint64_t m = bits & ((1ull << 52) - 1);
+    int es;
+    if (bexp) {
+        m |= 1ull << 52;
+        es = bexp - 1075;  // s = m * 2^es
     } else {
-        const long long d = Di + (fr > 0.5 ? 1 : 0);
-        m.d0 = m.d1 = d;
+        es = -1074;        // subnormal
     }
-    m.p0 = (uint32_t)((0 ^ m.d0) & 1);
-    m.p1 = (uint32_t)((1 ^ m.d1) & 1);
-    return m;
+    const int sh = (k - 52) - es;  // t = m >> sh (s <= 2^k guarantees t <= 2^52)
+    long long Di;
+    bool up = false, tie = false;
+    if (sh <= 0) {
+        Di = (long long)(m << (-sh));  // exact integer multiple of u
+    } else if (sh >= 64) {
+        Di = 0;                        // s < u/2^11: rounds away entirely
+    } else {
+        Di = (long long)(m >> sh);
+        const uint64_t rem = m & ((1ull << sh) - 1);
+        const uint64_t half = 1ull << (sh - 1);
+        up = rem > half;
+        tie = rem == half;
+    }
+    const uint32_t dpar = (uint32_t)(Di & 1);
+    Mono r;
+    if (tie) {  // the result R - D - 1/2 rounds to the even neighbour
+        r.d0 = Di + (0u ^ dpar);
+        r.d1 = Di + (1u ^ dpar);
+    } else {
+        r.d0 = r.d1 = Di + (up ? 1 : 0);
+    }
+    r.p0 = (uint32_t)((0 ^ r.d0) & 1);
+    r.p1 = (uint32_t)((1 ^ r.d1) & 1);
+    return r;
 }
 
 // a then b

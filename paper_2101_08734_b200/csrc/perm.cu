@@ -66,6 +66,57 @@ __global__ void __launch_bounds__(kThreads) fy_link_kernel(uint64_t key, uint32_
 // expected list length at target y is ~ln(F/y)).
 constexpr int kLocal = 48;
 
+
+// Sorts one target's writer list (>= 3 writers, rare) and links it in place.
+__device__ void fy_group_long(uint32_t y, uint32_t a0, uint32_t* nx, uint32_t* qq,
+                              uint32_t* scratch, uint32_t scratch_cap, uint32_t* scratch_used,
+                              uint32_t* err) {
+    uint32_t buf[kLocal];
+    uint32_t n = 0;
+    uint32_t cur = a0;
+    while (cur != kNone && n < (uint32_t)kLocal) {
+        int t = (int)n - 1;
+        while (t >= 0 && buf[t] > cur) {
+            buf[t + 1] = buf[t];
+            --t;
+        }
+        buf[t + 1] = cur;
+        ++n;
+        cur = nx[cur];
+    }
+    uint32_t* list = buf;
+    if (cur != kNone) {  // overflow: move the whole list to global scratch
+        uint32_t m = n;
+        for (uint32_t c = cur; c != kNone; c = nx[c]) ++m;
+        const uint32_t base = atomicAdd(scratch_used, m);
+        if (base + m > scratch_cap) {
+            atomicOr(err, 1u);
+            return;
+        }
+        list = scratch + base;
+        for (uint32_t t = 0; t < n; ++t) list[t] = buf[t];
+        for (uint32_t c = cur; c != kNone; c = nx[c]) {
+            int t = (int)n - 1;
+            while (t >= 0 && list[t] > c) {
+                list[t + 1] = list[t];
+                --t;
+            }
+            list[t + 1] = c;
+            ++n;
+        }
+    }
+    qq[y] = (list[0] == y) ? list[1] : list[0];
+    for (uint32_t t = 0; t + 1 < n; ++t) nx[list[t]] = list[t + 1];
+    nx[list[n - 1]] = kNone;
+}
+
+// Per target y: q[y] and the ascending writer chain (succ) in place of the exchange list.
+// Lists of up to kReg writers stay in registers: each writer's successor is the smallest
+// larger writer (O(n^2) compares, no local memory), written only where the exchange order
+// differs.  Each thread walks kGU targets at once so their dependent list loads overlap.
+constexpr int kGU = 2;
+constexpr int kReg = 8;
+
 __global__ void __launch_bounds__(kThreads) fy_group_kernel(uint32_t F,
                                                              const uint32_t* __restrict__ head,
                                                              uint32_t* __restrict__ next,
@@ -78,67 +129,46 @@ __global__ void __launch_bounds__(kThreads) fy_group_kernel(uint32_t F,
     const uint32_t* hd = head + (size_t)slot * F;
     uint32_t* nx = next + (size_t)slot * F;
     uint32_t* qq = q + (size_t)slot * F;
-    for (uint32_t y = blockIdx.x * blockDim.x + threadIdx.x; y < F; y += gridDim.x * blockDim.x) {
-        const uint32_t a0 = hd[y];
-        if (a0 == kNone) {
-            qq[y] = kNone;
-            continue;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t y0 = blockIdx.x * blockDim.x + threadIdx.x; y0 < F; y0 += kGU * stride) {
+        uint32_t a[kGU][kReg + 1];
+#pragma unroll
+        for (int u = 0; u < kGU; ++u) {
+            const uint32_t y = y0 + u * stride;
+            a[u][0] = y < F ? hd[y] : kNone;
         }
-        const uint32_t a1 = nx[a0];
-        if (a1 == kNone) {  // one writer; its succ is already kNone
-            qq[y] = (a0 == y) ? kNone : a0;
-            continue;
-        }
-        const uint32_t a2 = nx[a1];
-        if (a2 == kNone) {  // two writers: list a0 -> a1, needs ascending order
-            const uint32_t lo = a0 < a1 ? a0 : a1, hi = a0 < a1 ? a1 : a0;
-            qq[y] = (lo == y) ? hi : lo;
-            if (a0 > a1) {
-                nx[a1] = a0;
-                nx[a0] = kNone;
-            }
-            continue;
-        }
-        uint32_t buf[kLocal];
-        uint32_t n = 0;
-        uint32_t cur = hd[y];
-        while (cur != kNone && n < (uint32_t)kLocal) {
-            // insertion into the sorted prefix
-            int t = (int)n - 1;
-            while (t >= 0 && buf[t] > cur) {
-                buf[t + 1] = buf[t];
-                --t;
-            }
-            buf[t + 1] = cur;
-            ++n;
-            cur = nx[cur];
-        }
-        uint32_t* list = buf;
-        if (cur != kNone) {  // overflow: move the whole list to global scratch
-            uint32_t m = n;
-            for (uint32_t c = cur; c != kNone; c = nx[c]) ++m;
-            const uint32_t base = atomicAdd(scratch_used, m);
-            if (base + m > scratch_cap) {
-                atomicOr(err, 1u);
+#pragma unroll
+        for (int t = 1; t <= kReg; ++t)
+#pragma unroll
+            for (int u = 0; u < kGU; ++u) a[u][t] = a[u][t - 1] != kNone ? nx[a[u][t - 1]] : kNone;
+#pragma unroll
+        for (int u = 0; u < kGU; ++u) {
+            const uint32_t y = y0 + u * stride;
+            if (y >= F) break;
+            if (a[u][kReg] != kNone) {  // more than kReg writers (small y only)
+                fy_group_long(y, a[u][0], nx, qq, scratch, scratch_cap, scratch_used, err);
                 continue;
             }
-            list = scratch + base;
-            for (uint32_t t = 0; t < n; ++t) list[t] = buf[t];
-            for (uint32_t c = cur; c != kNone; c = nx[c]) {
-                int t = (int)n - 1;
-                while (t >= 0 && list[t] > c) {
-                    list[t + 1] = list[t];
-                    --t;
+            uint32_t qv = kNone;
+#pragma unroll
+            for (int t = 0; t < kReg; ++t) {
+                const uint32_t x = a[u][t];
+                if (x != kNone && x != y && x < qv) qv = x;
+            }
+            qq[y] = qv;
+#pragma unroll
+            for (int t = 0; t < kReg; ++t) {
+                const uint32_t x = a[u][t];
+                if (x == kNone) continue;
+                uint32_t sc = kNone;
+#pragma unroll
+                for (int r = 0; r < kReg; ++r) {
+                    const uint32_t z = a[u][r];
+                    if (z != kNone && z > x && z < sc) sc = z;
                 }
-                list[t + 1] = c;
-                ++n;
+                if (sc != a[u][t + 1]) nx[x] = sc;
             }
         }
-        uint32_t qv = kNone;
-        if (n > 0) qv = (list[0] == y) ? (n > 1 ? list[1] : kNone) : list[0];
-        qq[y] = qv;
-        for (uint32_t t = 0; t + 1 < n; ++t) nx[list[t]] = list[t + 1];
-        if (n > 0) nx[list[n - 1]] = kNone;
     }
 }
 

@@ -22,7 +22,9 @@ namespace clairplan {
 
 uint32_t epochs_per_batch(uint32_t F, uint32_t E) {
     const uint64_t per = (uint64_t)F * 12;
-    uint64_t eb = (48ull << 20) / (per ? per : 1);
+    uint64_t budget = 768ull << 20;
+    if (const char* env = getenv("CLAIRPLAN_PERM_BUDGET_MB")) budget = strtoull(env, nullptr, 10) << 20;
+    uint64_t eb = budget / (per ? per : 1);
     if (eb < 1) eb = 1;
     if (eb > E) eb = E;
     if (eb > 64) eb = 64;
@@ -767,7 +769,12 @@ int clairplan_export_class_lists(clairplan_t p, uint32_t* out, uint64_t cap) {
     for (uint32_t w = 0; w < p->nloc; ++w)
         for (uint32_t j = 0; j < J; ++j) need_n += p->class_len_h[(size_t)w * (J + 1) + j];
     if (cap < need_n) return fail(CLAIRPLAN_ERANGE, "output buffer too small");
+    if (need_n == 0) return 0;
     CK(cudaSetDevice(p->device));
+    if (p->v2) {  // class lists are stored back to back in (worker, class) order
+        CK(cudaMemcpy(out, p->class_entries.get<uint32_t>(), need_n * 4, cudaMemcpyDeviceToHost));
+        return 0;
+    }
     uint64_t o = 0;
     for (uint32_t w = 0; w < p->nloc; ++w) {
         // classes 1..J of a worker are adjacent in the class-partitioned array
