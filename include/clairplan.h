@@ -130,6 +130,13 @@ int clairplan_assign_from_streams(uint32_t num_workers, uint32_t samples,
                                   const double* capacities_mb, const double* sizes_mb,
                                   int device, clairplan_t* out);
 
+/* CacheAssignment::build_index (policies.cpp:124-142) for caller-edited class lists:
+ * entries = class lists concatenated in (worker, class) order, list_off[N*J + 1];
+ * offsets_out[samples+1] (u64) and holders_out[3 x total] in build_index order. */
+int clairplan_build_index(uint32_t num_workers, uint32_t num_classes, uint64_t samples,
+                          const uint32_t* entries, const uint64_t* list_off,
+                          uint64_t* offsets_out, uint32_t* holders_out, int device);
+
 /* Host-side input generator: DatasetModel::generate (perfmodel.cpp:68-99), bit-identical
  * with the reference built with the same glibc (no FMA contraction).  Not timed. */
 int clairplan_generate_sizes(uint64_t samples, double mean_mb, double sigma_mb, int has_total,

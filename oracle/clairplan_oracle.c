@@ -74,6 +74,22 @@ int orc_epoch_permutation(uint64_t seed, uint32_t epoch, uint32_t F, uint32_t* a
     return 0;
 }
 
+/* Same shuffle with the Lemire rejection loop removed (test-only counterfactual: shows that a
+ * rejection KAT really exercises rng.hpp:54-60). */
+int orc_epoch_permutation_norej(uint64_t seed, uint32_t epoch, uint32_t F, uint32_t* a) {
+    const uint64_t key = orc_derive_key(seed, kPermTag);
+    uint64_t pos = (uint64_t)epoch << 34;
+    for (uint32_t i = 0; i < F; ++i) a[i] = i;
+    for (uint32_t i = F - 1; i > 0; --i) {
+        const uint64_t x = next_draw(key, &pos);
+        const uint32_t j = (uint32_t)(((unsigned __int128)x * ((uint64_t)i + 1)) >> 64);
+        const uint32_t t = a[i];
+        a[i] = a[j];
+        a[j] = t;
+    }
+    return 0;
+}
+
 /* access.cpp:33-39 */
 void orc_batch_slice(uint64_t batch_size, uint32_t workers, uint32_t worker, uint64_t* begin,
                      uint64_t* end) {

@@ -22,6 +22,7 @@ uint64_t orc_derive_key(uint64_t seed, uint64_t tag);
 /* bounded draw at stream state (key, *pos): advances *pos like CounterRng::bounded */
 uint64_t orc_bounded(uint64_t key, uint64_t* pos, uint64_t n);
 int orc_epoch_permutation(uint64_t seed, uint32_t epoch, uint32_t F, uint32_t* out);
+int orc_epoch_permutation_norej(uint64_t seed, uint32_t epoch, uint32_t F, uint32_t* out);
 void orc_batch_slice(uint64_t batch_size, uint32_t workers, uint32_t worker, uint64_t* begin,
                      uint64_t* end);
 int orc_generate_sizes(uint64_t F, double mean, double sigma, int has_total, double total,

@@ -100,6 +100,8 @@ def lib():
     L.clairplan_assign_from_streams.argtypes = [C.c_uint32, C.c_uint32, u32p, u64p, u32p,
                                                 C.c_uint32, f64p, f64p, C.c_int,
                                                 C.POINTER(C.c_void_p)]
+    L.clairplan_build_index.argtypes = [C.c_uint32, C.c_uint32, C.c_uint64, u32p, u64p, u64p,
+                                        u32p, C.c_int]
     L.clairplan_generate_sizes.argtypes = [C.c_uint64, C.c_double, C.c_double, C.c_int,
                                            C.c_double, C.c_uint64, C.c_int, f64p]
     _lib = L
@@ -166,21 +168,22 @@ class CacheAssignment:
             return self.holders[:0]
         return self.holders[int(self.holder_offsets[sample]):int(self.holder_offsets[sample + 1])]
 
-    def build_index(self, samples: int) -> None:
-        """policies.cpp:124-142 — host bookkeeping of an edited assignment (not the hot path;
-        the device build produces the CSR directly)."""
-        cnt = np.zeros(samples + 1, np.uint64)
-        for lists in self.class_lists:
-            for lst in lists:
-                np.add.at(cnt, np.asarray(lst, np.int64) + 1, 1)
-        self.holder_offsets = np.cumsum(cnt).astype(np.uint64)
-        cur = self.holder_offsets[:-1].copy()
-        self.holders = np.zeros((int(self.holder_offsets[-1]), 3), np.uint32)
-        for w, lists in enumerate(self.class_lists):
-            for j, lst in enumerate(lists):
-                for pos, k in enumerate(lst):
-                    self.holders[int(cur[k])] = (w, j + 1, pos)
-                    cur[k] += 1
+    def build_index(self, samples: int, device: int = 0) -> None:
+        """policies.cpp:124-142 — rebuilds the CSR on the GPU from (edited) class lists."""
+        N = len(self.class_lists)
+        J = len(self.class_lists[0]) if N else 0
+        lens = [len(l) for lists in self.class_lists for l in lists]
+        off = np.zeros(N * J + 1, np.uint64)
+        off[1:] = np.cumsum(lens) if lens else []
+        flat = np.ascontiguousarray(np.concatenate([np.asarray(l, np.uint32) for lists in
+                                                    self.class_lists for l in lists])
+                                    if lens else np.empty(0, np.uint32), np.uint32)
+        offs = np.empty(samples + 1, np.uint64)
+        hold = np.empty(max(len(flat), 1) * 3, np.uint32)
+        _check(lib().clairplan_build_index(N, J, samples, _p(flat, u32p) if len(flat) else None,
+                                           _p(off, u64p), _p(offs, u64p), _p(hold, u32p), device))
+        self.holder_offsets = offs
+        self.holders = hold[:len(flat) * 3].reshape(len(flat), 3)
 
 
 # ----------------------------------------------------------------- the device plan

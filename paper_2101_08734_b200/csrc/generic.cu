@@ -197,6 +197,111 @@ int generic_holders(clairplan_plan* p) {
     return 0;
 }
 
+
+// ---- build_index (policies.cpp:124-142) on caller class lists ---------------------------
+// entries: all class lists concatenated in (worker, class) order; list_off[N*J + 1].
+__global__ void index_records_kernel(const uint64_t* __restrict__ list_off, uint32_t nlists,
+                                     uint32_t J, uint64_t n, uint32_t* __restrict__ wj,
+                                     uint32_t* __restrict__ pos) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t lo = 0, hi = nlists;  // last list with list_off[x] <= i
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) / 2;
+            if (list_off[mid] <= i) lo = mid;
+            else hi = mid;
+        }
+        wj[i] = lo;
+        pos[i] = (uint32_t)(i - list_off[lo]);
+    }
+}
+
+__global__ void index_emit_kernel(const uint32_t* __restrict__ sorted_idx, uint64_t n,
+                                  const uint32_t* __restrict__ wj, const uint32_t* __restrict__ pos,
+                                  uint32_t J, uint32_t* __restrict__ holders) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t x = sorted_idx[i];
+        holders[3 * i + 0] = wj[x] / J;
+        holders[3 * i + 1] = wj[x] % J + 1;
+        holders[3 * i + 2] = pos[x];
+    }
+}
+
+}  // namespace clairplan
+using namespace clairplan;
+extern "C" int clairplan_build_index(uint32_t N, uint32_t J, uint64_t samples,
+                                     const uint32_t* entries, const uint64_t* list_off,
+                                     uint64_t* offsets_out, uint32_t* holders_out, int device) {
+    if (!list_off || !offsets_out) return fail(CLAIRPLAN_EINVAL, "null argument");
+    if (samples >= 0xFFFFFFFFull) return fail(CLAIRPLAN_EOVERFLOW, "too many samples");
+    const uint32_t nl = N * J;
+    const uint64_t n = nl ? list_off[nl] : 0;
+    for (uint64_t i = 0; i < n; ++i)
+        if (entries[i] >= samples) return fail(CLAIRPLAN_EINVAL, "class list entry out of range");
+    if (int rc = check_device(device)) return rc;
+    const uint32_t F = (uint32_t)samples;
+    cudaStream_t s;
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    DevBuf dent, doff, dwj, dpos, keys, okeys, vals, ovals, hc, ho, hold, wsb;
+    const uint64_t m = n ? n : 1;
+    if (!dent.ensure(m * 4) || !doff.ensure(((uint64_t)nl + 1) * 8) || !dwj.ensure(m * 4) ||
+        !dpos.ensure(m * 4) || !keys.ensure(m * 4) || !okeys.ensure(m * 4) || !vals.ensure(m * 4) ||
+        !ovals.ensure(m * 4) || !hc.ensure(((uint64_t)F + 1) * 4) || !ho.ensure(((uint64_t)F + 1) * 8) ||
+        !hold.ensure(m * 12)) {
+        cudaStreamDestroy(s);
+        return fail(CLAIRPLAN_ENOMEM, "device allocation failed");
+    }
+    const uint64_t ws_bytes = 256ull * (n / kRadixTile + 3) * 12 * 2 + (64ull << 20);
+    if (!wsb.ensure(ws_bytes)) {
+        cudaStreamDestroy(s);
+        return fail(CLAIRPLAN_ENOMEM, "device allocation failed");
+    }
+    Workspace ws;
+    ws.base = wsb.get<char>();
+    ws.cap = wsb.bytes;
+    CK(cudaMemsetAsync(hc.p, 0, ((uint64_t)F + 1) * 4, s));
+    if (n) {
+        CK(cudaMemcpyAsync(dent.p, entries, n * 4, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(doff.p, list_off, ((uint64_t)nl + 1) * 8, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(keys.p, entries, n * 4, cudaMemcpyHostToDevice, s));
+        histogram_kernel<<<grid_for(n, kThreads), kThreads, 0, s>>>(dent.get<uint32_t>(), n, F,
+                                                                   hc.get<uint32_t>());
+        index_records_kernel<<<grid_for(n, kThreads), kThreads, 0, s>>>(
+            doff.get<uint64_t>(), nl, J, n, dwj.get<uint32_t>(), dpos.get<uint32_t>());
+    }
+    exclusive_scan(s, hc.get<uint32_t>(), F, ho.get<uint64_t>(), ws);
+    if (n) {
+        uint64_t* seg = ws.scratch<uint64_t>(2);
+        const uint64_t hseg[2] = {0, n};
+        CK(cudaMemcpyAsync(seg, hseg, 16, cudaMemcpyHostToDevice, s));
+        TileMap tm;
+        build_tilemap(s, seg + 1, 1, n, kRadixTile, tm, ws);
+        const uint32_t* kin = keys.get<uint32_t>();
+        const uint32_t* vin = nullptr;
+        uint32_t pass = 0;
+        for (uint32_t shift = 0; shift == 0 || ((uint64_t)(F - 1) >> shift) != 0; shift += 8, ++pass) {
+            uint32_t* ko = (pass & 1) ? keys.get<uint32_t>() : okeys.get<uint32_t>();
+            uint32_t* vo = (pass & 1) ? vals.get<uint32_t>() : ovals.get<uint32_t>();
+            const size_t mk = ws.mark();
+            radix_pass(s, tm, seg, seg + 1, kin, vin, shift, ko, vo, nullptr, nullptr, ws);
+            ws.release(mk);
+            kin = ko;
+            vin = vo;
+        }
+        index_emit_kernel<<<grid_for(n, kThreads), kThreads, 0, s>>>(vin, n, dwj.get<uint32_t>(),
+                                                                    dpos.get<uint32_t>(), J,
+                                                                    hold.get<uint32_t>());
+    }
+    CK(cudaMemcpyAsync(offsets_out, ho.p, ((uint64_t)F + 1) * 8, cudaMemcpyDeviceToHost, s));
+    if (n) CK(cudaMemcpyAsync(holders_out, hold.p, n * 12, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    CK(cudaGetLastError());
+    cudaStreamDestroy(s);
+    if (ws.overflow) return fail(CLAIRPLAN_ENOMEM, "internal workspace overflow");
+    return 0;
+}
+namespace clairplan {
 }  // namespace clairplan
 
 using namespace clairplan;

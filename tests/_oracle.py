@@ -60,6 +60,7 @@ class Port:
         L.orc_bounded.restype = C.c_uint64
         L.orc_bounded.argtypes = [C.c_uint64, u64p, C.c_uint64]
         L.orc_epoch_permutation.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, u32p]
+        L.orc_epoch_permutation_norej.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, u32p]
         L.orc_generate_sizes.argtypes = [C.c_uint64, C.c_double, C.c_double, C.c_int,
                                          C.c_double, C.c_uint64, C.c_int, f64p]
         L.orc_plan_build.restype = C.c_void_p
@@ -83,6 +84,11 @@ class Port:
         rc = self.L.orc_epoch_permutation(seed, epoch, F, _ptr(out, u32p))
         if rc:
             raise ValueError(self.L.orc_last_error().decode())
+        return out
+
+    def epoch_permutation_norej(self, seed, epoch, F):
+        out = np.empty(F, np.uint32)
+        self.L.orc_epoch_permutation_norej(seed, epoch, F, _ptr(out, u32p))
         return out
 
     def generate_sizes(self, F, mean, sigma, total=None, seed=1, sigma_relative=False):

@@ -27,6 +27,18 @@ def main():
     }
     with open(os.path.join(HERE, "rng_kat.json"), "w") as f:
         json.dump(rng, f, indent=1)
+    # Lemire-rejection KAT (rng.hpp:54-60): epochs found by tools/find_rejection on a B200
+    # (F = 16,777,259, seed 42); the permutation digests come from the reference itself.
+    import hashlib
+    F, seed = 16_777_259, 42
+    kat = {"samples": F, "seed": seed, "epochs": []}
+    for epoch, step in ((66486, 11002896), (108120, 8809816), (118368, 4995318)):
+        p = r.epoch_permutation(seed, epoch, F)
+        kat["epochs"].append({"epoch": epoch, "rejecting_step": step,
+                              "sha256": hashlib.sha256(p.tobytes()).hexdigest(),
+                              "head": [int(x) for x in p[:8]]})
+    with open(os.path.join(HERE, "rejection_kat.json"), "w") as f:
+        json.dump(kat, f, indent=1)
     print("golden vectors written to", HERE)
 
 

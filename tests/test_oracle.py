@@ -137,3 +137,21 @@ def test_port_generic_assign_matches_reference(port, ref):
         a = ref.assign_from_streams(streams, counts, caps, sizes)
         b = port.assign_from_streams(streams, counts, caps, sizes)
         assert plans_equal(a, b, check_streams=False) is None
+
+
+def _kat():
+    with open(os.path.join(GOLDEN, "rejection_kat.json")) as f:
+        return json.load(f)
+
+
+def test_rejection_kat_oracle(port):
+    """Lemire rejection (rng.hpp:54-60) KAT: the C restatement reproduces the reference's
+    permutation digest, and ignoring the rejection would change it."""
+    import hashlib
+    kat = _kat()
+    e = kat["epochs"][0]
+    p = port.epoch_permutation(kat["seed"], e["epoch"], kat["samples"])
+    assert hashlib.sha256(p.tobytes()).hexdigest() == e["sha256"]
+    assert [int(x) for x in p[:8]] == e["head"]
+    naive = port.epoch_permutation_norej(kat["seed"], e["epoch"], kat["samples"])
+    assert hashlib.sha256(naive.tobytes()).hexdigest() != e["sha256"]
