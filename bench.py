@@ -11,10 +11,11 @@ timed region.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C]
 
-Multi-GPU (torchrun, one rank per GPU): the workers are sharded into contiguous ranges, every
-rank builds its range's plan (epoch permutations are recomputed per rank: they are
-seed-generated) and the holder-CSR offsets are merged with an NCCL all-gather of the
-per-sample holder counts; time = max over ranks.
+Multi-GPU (torchrun, one rank per GPU, paper_2101_08734_b200/distributed.py): every rank
+draws the permutations of its epoch range, the rows are all-gathered over NVLink (NCCL), every
+rank builds the plan of its contiguous worker range and the holder-CSR offsets are merged with
+an NCCL all-gather of the per-sample holder counts; time = max over ranks (strong scaling: the
+same configuration at every N).
 """
 import argparse
 import json
@@ -173,7 +174,18 @@ def run_ours(args, cfg):
     mu, sd, tot = cfg["sizes"]
     sizes = cp.generate_sizes(cfg["F"], mu, sd, tot, 1)
     part = cp.PartitionSpec(N, cfg["b"] * N, cfg["E"], True)
-    plan = cp.Plan(SEED, cfg["F"], part, list(CAPS), sizes, device=local, worker_range=(wb, we))
+    if world > 1:
+        from paper_2101_08734_b200.distributed import DistributedPlan
+        dplan = DistributedPlan(SEED, cfg["F"], part, list(CAPS), sizes)
+        plan = dplan.plan
+
+        def build():
+            dplan.build()
+    else:
+        plan = cp.Plan(SEED, cfg["F"], part, list(CAPS), sizes, device=local, worker_range=(wb, we))
+
+        def build():
+            plan.build()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
 
     def barrier():
@@ -183,7 +195,7 @@ def run_ours(args, cfg):
             torch.cuda.synchronize()
 
     for _ in range(args.warmup):
-        plan.build()
+        build()
     barrier()
     sampler = ClockSampler(local)
     sampler.start()
@@ -193,9 +205,19 @@ def run_ours(args, cfg):
     for _ in range(args.steps):
         flush.fill_(1)
         torch.cuda.synchronize()
-        plan.build()
+        if world > 1:
+            # the sharded build spans the library stream and NCCL on torch's stream; every
+            # library call synchronises its own stream, so events on torch's stream bracket it
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev0.record()
+            build()
+            ev1.record()
+            ev1.synchronize()
+            dev_ms.append(ev0.elapsed_time(ev1))
+        else:
+            build()
+            dev_ms.append(plan.stats()["device_ms"])
         st = plan.stats()
-        dev_ms.append(st["device_ms"])
         launches += plan.launch_count()
     barrier()
     t_wall = time.perf_counter() - t_wall
@@ -228,7 +250,7 @@ def run_ours(args, cfg):
     # ---- end to end through the C ABI with host buffers (rank-local)
     e2e = None
     if not args.no_e2e:
-        e2e = e2e_measure(cp, plan, sizes, cfg, args, world, A_all)
+        e2e = e2e_measure(cp, plan, build, sizes, cfg, args, world, A_all)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -266,7 +288,10 @@ def run_ours(args, cfg):
                        "per_worker_batch": cfg["b"], "epochs": cfg["E"], "seed": SEED,
                        "capacities_mb": list(CAPS), "drop_last": True,
                        "l2": "256 MB flush before every timed step",
-                       "sharding": f"worker ranges over {world} GPU(s)"},
+                       "sharding": ("single GPU" if world == 1 else
+                                    f"epochs sharded over {world} GPUs for the permutations, "
+                                    "NCCL all-gather of the rows, worker ranges for the rest, "
+                                    "holder offsets merged by NCCL all-gather")}, 
             "plan_latency_ms": ms_step,
             "wall_ms_per_step": t_wall * 1e3 / args.steps,
             "accesses": int(A_all), "pairs": int(D_all),
@@ -286,7 +311,7 @@ def run_ours(args, cfg):
         torch.distributed.destroy_process_group()
 
 
-def e2e_measure(cp, plan, sizes, cfg, args, world, A_all):
+def e2e_measure(cp, plan, build, sizes, cfg, args, world, A_all):
     """sizes H2D from pinned memory + build + every output D2H into pinned buffers."""
     import ctypes
     import torch
@@ -305,7 +330,7 @@ def e2e_measure(cp, plan, sizes, cfg, args, world, A_all):
 
     def step():
         cp._check(L.clairplan_set_sizes(plan._h, ctypes.c_void_p(h_sizes.data_ptr()), 0))
-        plan.build()
+        build()
         cp._check(L.clairplan_export_streams(plan._h, ctypes.cast(h_stream.data_ptr(), u32),
                                              st["accesses"]))
         cp._check(L.clairplan_export_class_lists(plan._h, ctypes.cast(h_cls.data_ptr(), u32),

@@ -137,6 +137,18 @@ int clairplan_build_index(uint32_t num_workers, uint32_t num_classes, uint64_t s
                           const uint32_t* entries, const uint64_t* list_off,
                           uint64_t* offsets_out, uint32_t* holders_out, int device);
 
+/* ---- multi-GPU building blocks (one process per GPU, NCCL between the calls) ---------- */
+/* Permutation rows of epochs [epoch_begin, epoch_begin+count) into a device buffer
+ * d_out[count][F] (epoch_permutation for each epoch, rejections resolved). */
+int clairplan_generate_perms(clairplan_t plan, uint32_t epoch_begin, uint32_t epoch_count,
+                             uint32_t* d_out);
+/* clairplan_build for the handle's worker range from all E permutation rows d_perms[E][F]
+ * (e.g. epoch-sharded rows all-gathered over NVLink). */
+int clairplan_build_from_perms(clairplan_t plan, const uint32_t* d_perms);
+/* Per-sample number of holder records of the handle's workers, d_out[F] (device): the
+ * input of the cross-GPU holder-offset merge (all-gather + exclusive scan over ranks). */
+int clairplan_holder_counts(clairplan_t plan, uint32_t* d_out);
+
 /* Host-side input generator: DatasetModel::generate (perfmodel.cpp:68-99), bit-identical
  * with the reference built with the same glibc (no FMA contraction).  Not timed. */
 int clairplan_generate_sizes(uint64_t samples, double mean_mb, double sigma_mb, int has_total,

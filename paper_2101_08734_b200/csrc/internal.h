@@ -62,6 +62,9 @@ void launch_fy_emit(cudaStream_t s, uint64_t key, const Part& part, uint32_t e0,
                     const uint32_t* succ, const uint32_t* q, const RejTable& rt, uint32_t* inv,
                     uint32_t* stream, uint32_t* perm_out);
 
+void launch_perm_scatter(cudaStream_t s, const Part& part, const uint32_t* perms, uint32_t* inv,
+                         uint32_t* stream);
+
 int sample_pass_config(const Part& part, uint32_t* hs, uint32_t* nw_words, uint32_t* warps,
                        size_t* smem);
 void launch_sample_pass(cudaStream_t s, const Part& part, uint32_t* info, uint32_t* pair_count,

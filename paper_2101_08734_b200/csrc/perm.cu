@@ -221,6 +221,32 @@ __global__ void __launch_bounds__(kThreads) fy_emit_kernel(uint64_t key, Part pa
     }
 }
 
+// Streams + inverse permutations from externally supplied permutation rows (multi-GPU: rows
+// computed on other GPUs and all-gathered over NVLink).  perms[e][p] = value at position p.
+__global__ void __launch_bounds__(kThreads) perm_scatter_kernel(Part part, const uint32_t* __restrict__ perms,
+                                                                 uint32_t* __restrict__ inv,
+                                                                 uint32_t* __restrict__ stream) {
+    const uint32_t e = blockIdx.y;
+    const uint32_t F = part.F;
+    const uint32_t* row = perms + (size_t)e * F;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < F; i += gridDim.x * blockDim.x) {
+        const uint32_t v = __ldcs(row + i);
+        inv[(size_t)e * F + v] = i;
+        if (i < part.P) {
+            uint32_t w;
+            uint64_t spos;
+            part.locate(i, e, w, spos);
+            if (w >= part.wbegin && w < part.wend) stream[part.stream_offset(w) + spos] = v;
+        }
+    }
+}
+
+void launch_perm_scatter(cudaStream_t s, const Part& part, const uint32_t* perms, uint32_t* inv,
+                         uint32_t* stream) {
+    dim3 grid(grid_for(part.F, kThreads * 4, 148u * 16u), part.E);
+    perm_scatter_kernel<<<grid, kThreads, 0, s>>>(part, perms, inv, stream);
+}
+
 // ---- host launchers ------------------------------------------------------------------
 void launch_fy_link(cudaStream_t s, uint64_t key, uint32_t F, uint32_t e0, uint32_t ne,
                     uint32_t* head, uint32_t* next, const RejTable& rt, uint32_t* rej_flag,

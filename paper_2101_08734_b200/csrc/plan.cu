@@ -45,7 +45,7 @@ RejTable rej_table(clairplan_plan* p) {
 int enqueue_perms(clairplan_plan* p, uint32_t* stream_out, uint32_t* inv_out, uint32_t* perm_out,
                   uint32_t e_first, uint32_t e_count) {
     const uint32_t F = p->part.F;
-    const uint32_t EB = perm_out ? 1 : epochs_per_batch(F, e_count);
+    const uint32_t EB = epochs_per_batch(F, e_count);
     bool ok = true;
     uint32_t* head = need<uint32_t>(p->head, (uint64_t)EB * F, ok);
     uint32_t* next = need<uint32_t>(p->next, (uint64_t)EB * F, ok);
@@ -63,7 +63,7 @@ int enqueue_perms(clairplan_plan* p, uint32_t* stream_out, uint32_t* inv_out, ui
                        false, F);
         launch_fy_group(p->stream, F, ne, head, next, q, scratch, scap, counters, counters + 1);
         launch_fy_emit(p->stream, p->key, p->part, e0, ne, next, q, rt, inv_out, stream_out,
-                       perm_out);
+                       perm_out ? perm_out + (size_t)(e0 - e_first) * F : nullptr);
         p->launches += 3;
     }
     CK(cudaGetLastError());
@@ -443,7 +443,7 @@ int first_fit_classes(clairplan_plan* p, const double* ssize, uint8_t* cls) {
     return 0;
 }
 
-int build_seed_path_v2(clairplan_plan* p) {
+int build_seed_path_v2(clairplan_plan* p, const uint32_t* ext_perms) {
     cudaStream_t s = p->stream;
     const Part& part = p->part;
     const uint32_t F = part.F, E = part.E, nloc = p->nloc, J = p->cfg.num_classes;
@@ -480,7 +480,12 @@ int build_seed_path_v2(clairplan_plan* p) {
         CK(cudaEventRecord(p->ev0, s));
         p->mark(0);
         // K1-K3: permutations -> streams + inverse permutations
-        if (int rc = enqueue_perms(p, stream_buf, inv, nullptr, 0, E)) return rc;
+        if (ext_perms) {
+            launch_perm_scatter(s, part, ext_perms, inv, stream_buf);
+            ++p->launches;
+        } else if (int rc = enqueue_perms(p, stream_buf, inv, nullptr, 0, E)) {
+            return rc;
+        }
         p->mark(1);
         // K4a: per-sample (worker, count, first epoch)
         if (lanes) {
@@ -687,7 +692,7 @@ int clairplan_build(clairplan_t p) {
     p->built = false;
     p->v2 = false;
     const char* force = getenv("CLAIRPLAN_FORCE_V1");
-    if (v2_ok(p) && !(force && force[0] == '1')) return build_seed_path_v2(p);
+    if (v2_ok(p) && !(force && force[0] == '1')) return build_seed_path_v2(p, nullptr);
     return build_seed_path(p);
 }
 
@@ -860,6 +865,48 @@ int clairplan_set_sizes(clairplan_t p, const double* sizes_mb, int on_device) {
     if (!p->sizes.ensure((size_t)p->part.F * 8)) return fail(CLAIRPLAN_ENOMEM, "device allocation failed");
     CK(cudaMemcpyAsync(p->sizes.get<double>(), sizes_mb, (size_t)p->part.F * 8,
                        on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, p->stream));
+    return 0;
+}
+
+// ---- multi-GPU building blocks ---------------------------------------------------------
+int clairplan_generate_perms(clairplan_t p, uint32_t epoch_begin, uint32_t epoch_count,
+                             uint32_t* d_out) {
+    if (!p || p->generic) return fail(CLAIRPLAN_EINVAL, "invalid plan");
+    if (epoch_count == 0) return 0;
+    if (epoch_begin + epoch_count > p->part.E) return fail(CLAIRPLAN_EINVAL, "epoch range outside plan");
+    CK(cudaSetDevice(p->device));
+    if (int rc = alloc_rej(p, p->part.E)) return rc;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        p->launches = 0;
+        if (int rc = enqueue_perms(p, nullptr, nullptr, d_out, epoch_begin, epoch_count)) return rc;
+        std::vector<uint32_t> flags(p->part.E);
+        CK(cudaMemcpyAsync(flags.data(), p->rej_flag.get<uint32_t>(), flags.size() * 4,
+                           cudaMemcpyDeviceToHost, p->stream));
+        CK(cudaStreamSynchronize(p->stream));
+        bool any = false;
+        if (int rc = resolve_rejections(p, flags, &any)) return rc;
+        if (!any) return 0;
+    }
+    return fail(CLAIRPLAN_ECUDA, "rejection tables did not converge");
+}
+
+int clairplan_build_from_perms(clairplan_t p, const uint32_t* d_perms) {
+    if (!p || p->generic || !d_perms) return fail(CLAIRPLAN_EINVAL, "invalid argument");
+    CK(cudaSetDevice(p->device));
+    if (!v2_ok(p)) return fail(CLAIRPLAN_EINVAL, "configuration not supported by the sharded path");
+    p->built = false;
+    p->v2 = false;
+    return build_seed_path_v2(p, d_perms);
+}
+
+int clairplan_holder_counts(clairplan_t p, uint32_t* d_out) {
+    if (!p || !p->built || p->generic) return fail(CLAIRPLAN_EINVAL, "plan not built");
+    CK(cudaSetDevice(p->device));
+    const uint32_t F = p->part.F;
+    const uint32_t* src = (p->H == p->D) ? p->pair_count.get<uint32_t>() : p->hcount.get<uint32_t>();
+    if (p->cfg.num_classes == 0) CK(cudaMemsetAsync(d_out, 0, (size_t)F * 4, p->stream));
+    else CK(cudaMemcpyAsync(d_out, src, (size_t)F * 4, cudaMemcpyDeviceToDevice, p->stream));
+    CK(cudaStreamSynchronize(p->stream));
     return 0;
 }
 

@@ -1,0 +1,119 @@
+"""Multi-GPU plan build: one process per GPU, torch.distributed (NCCL) for the exchanges.
+
+Decomposition ("Multi-GPU"):
+  1. epoch sharding  — rank r draws the permutations of its epoch range
+                       (clairplan_generate_perms); epochs are independent by construction
+                       (access.cpp:52-57: epoch e owns stream positions [e<<34, (e+1)<<34)).
+  2. all-gather      — the permutation rows of every epoch are all-gathered over NVLink
+                       (ncclAllGather through torch.distributed).
+  3. worker sharding — rank r builds streams, (count, first-access) tables, tier assignment,
+                       prefetch orders and holder records for its contiguous worker range
+                       (clairplan_build_from_perms); nopfs_assign_caches has no cross-worker
+                       dependency (policies.cpp:151-163).
+  4. holder merge    — per-sample holder counts are all-gathered; the global CSR offset of
+                       sample k is the exclusive scan of the per-sample totals and rank r's
+                       records of k start after those of ranks < r (worker ranges ascend, so
+                       this is build_index's worker order, policies.cpp:124-142).
+
+The output stays sharded: rank r owns its workers' streams / class lists and its holder
+records with their global CSR positions.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+
+def epoch_ranges(E: int, world: int):
+    """Balanced contiguous epoch ranges, one per rank; padded row count for the gather."""
+    base, extra = divmod(E, world)
+    ranges, b = [], 0
+    for r in range(world):
+        n = base + (1 if r < extra else 0)
+        ranges.append((b, n))
+        b += n
+    return ranges, base + (1 if extra else 0)
+
+
+def worker_range(N: int, rank: int, world: int):
+    return rank * N // world, (rank + 1) * N // world
+
+
+def holder_offsets_from_counts(counts):
+    """counts: [world, F] per-rank per-sample holder counts (torch or numpy, integer).
+    Returns (global_offsets[F+1], rank_starts[world, F]): the global CSR offsets and, for
+    every rank, where its records of sample k start in the global holder array."""
+    import torch
+    c = torch.as_tensor(counts).to(torch.int64)
+    tot = c.sum(dim=0)
+    glob = torch.zeros(c.shape[1] + 1, dtype=torch.int64, device=c.device)
+    glob[1:] = torch.cumsum(tot, dim=0)
+    before = torch.cumsum(c, dim=0) - c  # exclusive over ranks
+    return glob, glob[:-1].unsqueeze(0) + before
+
+
+def gather_rows(local, ranges, pad, group=None):
+    """All-gather per-rank permutation rows (uneven epoch ranges, padded) -> [E, F]."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    F = local.shape[1]
+    buf = torch.zeros((pad, F), dtype=local.dtype, device=local.device)
+    buf[: local.shape[0]] = local
+    out = torch.empty((world * pad, F), dtype=local.dtype, device=local.device)
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(out, buf, group=group)
+    else:  # gloo (CPU tests of the host logic)
+        dist.all_gather(list(out.chunk(world)), buf, group=group)
+    rows = [out[r * pad: r * pad + n] for r, (_, n) in enumerate(ranges)]
+    return torch.cat(rows, dim=0).contiguous()
+
+
+class DistributedPlan:
+    """Sharded plan of one rank (call the same sequence on every rank)."""
+
+    def __init__(self, seed, samples, part, capacities_mb, sizes_mb, group=None):
+        import torch
+        import torch.distributed as dist
+        from . import clairplan as cp
+        self.cp, self.torch, self.dist = cp, torch, dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.device = torch.cuda.current_device()
+        self.samples, self.part = samples, part
+        self.wrange = worker_range(part.num_workers, self.rank, self.world)
+        self.plan = cp.Plan(seed, samples, part, capacities_mb, sizes_mb, device=self.device,
+                            worker_range=self.wrange)
+        self.ranges, self.pad = epoch_ranges(part.epochs, self.world)
+        L = cp.lib()
+        L.clairplan_generate_perms.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p]
+        L.clairplan_build_from_perms.argtypes = [C.c_void_p, C.c_void_p]
+        L.clairplan_holder_counts.argtypes = [C.c_void_p, C.c_void_p]
+        self.L = L
+        self.local_rows = torch.empty((max(self.pad, 1), samples), dtype=torch.int32, device="cuda")
+        self.counts = torch.empty(samples, dtype=torch.int32, device="cuda")
+        self.global_offsets = None
+        self.rank_starts = None
+
+    def build(self):
+        torch, cp = self.torch, self.cp
+        e0, n = self.ranges[self.rank]
+        cp._check(self.L.clairplan_generate_perms(self.plan._h, e0, n,
+                                                  C.c_void_p(self.local_rows.data_ptr())))
+        perms = gather_rows(self.local_rows[:n], self.ranges, self.pad, self.group)
+        cp._check(self.L.clairplan_build_from_perms(self.plan._h, C.c_void_p(perms.data_ptr())))
+        del perms
+        cp._check(self.L.clairplan_holder_counts(self.plan._h, C.c_void_p(self.counts.data_ptr())))
+        allc = torch.empty((self.world, self.samples), dtype=torch.int32, device="cuda")
+        self.dist.all_gather_into_tensor(allc, self.counts, group=self.group)
+        self.global_offsets, starts = holder_offsets_from_counts(allc)
+        self.rank_starts = starts[self.rank]
+        return self
+
+    def stats(self):
+        return self.plan.stats()
+
+    def close(self):
+        self.plan.close()

@@ -251,3 +251,36 @@ def test_rejection_kat_device(cp):
     for e in kat["epochs"]:
         p = cp.epoch_permutation(kat["seed"], e["epoch"], kat["samples"])
         assert hashlib.sha256(p.tobytes()).hexdigest() == e["sha256"], e["epoch"]
+
+
+def test_build_from_perms_matches_build(cp, ref):
+    """The sharded path on one GPU: permutation rows generated in two epoch ranges, then the
+    worker-range build from those rows == the plain build of the same worker range."""
+    import ctypes as C
+    import torch
+    F, N, B, E = 5000, 12, 120, 9
+    sizes = ref.generate_sizes(F, 0.1, 0.1, None, 1)
+    part = cp.PartitionSpec(N, B, E, True)
+    L = cp.lib()
+    L.clairplan_generate_perms.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p]
+    L.clairplan_build_from_perms.argtypes = [C.c_void_p, C.c_void_p]
+    L.clairplan_holder_counts.argtypes = [C.c_void_p, C.c_void_p]
+    for wr in ((0, 12), (3, 8)):
+        a = cp.Plan(7, F, part, [8.0, 30.0], sizes, worker_range=wr).build()
+        b = cp.Plan(7, F, part, [8.0, 30.0], sizes, worker_range=wr)
+        rows = torch.empty((E, F), dtype=torch.int32, device="cuda")
+        cp._check(L.clairplan_generate_perms(b._h, 0, 4, C.c_void_p(rows.data_ptr())))
+        cp._check(L.clairplan_generate_perms(b._h, 4, E - 4, C.c_void_p(rows[4].data_ptr())))
+        for e in (0, 5, 8):
+            assert np.array_equal(rows[e].cpu().numpy().astype(np.uint32), ref.epoch_permutation(7, e, F))
+        cp._check(L.clairplan_build_from_perms(b._h, C.c_void_p(rows.data_ptr())))
+        assert np.array_equal(a.streams_flat(), b.streams_flat())
+        for x, y in zip(a.class_lists(), b.class_lists()):
+            assert all(np.array_equal(u, v) for u, v in zip(x, y))
+        ha, hb = a.holders(), b.holders()
+        assert np.array_equal(ha[0], hb[0]) and np.array_equal(ha[1], hb[1])
+        cnt = torch.empty(F, dtype=torch.int32, device="cuda")
+        cp._check(L.clairplan_holder_counts(b._h, C.c_void_p(cnt.data_ptr())))
+        assert np.array_equal(np.diff(ha[0].astype(np.int64)), cnt.cpu().numpy())
+        a.close()
+        b.close()
