@@ -251,7 +251,8 @@ __device__ __forceinline__ bool apply_mono(double& r, int k, long long d0, long 
 __global__ void ff_resolve_kernel(TileMap tm, const uint64_t* __restrict__ seg_begin,
                                   const uint64_t* __restrict__ seg_len,
                                   const double* __restrict__ sz, double C, FFChunks ch,
-                                  uint8_t* __restrict__ taken) {
+                                  uint8_t* __restrict__ taken,
+                                  unsigned long long* __restrict__ taken_count) {
     const uint32_t lane = threadIdx.x & 31;
     for (uint32_t seg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; seg < tm.nseg;
          seg += (gridDim.x * blockDim.x) >> 5) {
@@ -260,6 +261,7 @@ __global__ void ff_resolve_kernel(TileMap tm, const uint64_t* __restrict__ seg_b
         const double* base = sz + seg_begin[seg];
         uint8_t* flags = taken + seg_begin[seg];
         double r = C;
+        unsigned long long ntaken = 0;
         for (uint64_t t = tb; t < te; ++t) {
             const uint64_t off = (t - tb) * (uint64_t)tm.tile;
             if (r < ch.mn[t]) {
@@ -269,6 +271,7 @@ __global__ void ff_resolve_kernel(TileMap tm, const uint64_t* __restrict__ seg_b
             const int k = ch.k[t];
             if (k != kNoBinade && apply_mono(r, k, ch.d0[t], ch.d1[t])) {
                 if (lane == 0) ch.status[t] = 1;
+                ntaken += L - off < tm.tile ? L - off : tm.tile;
                 continue;
             }
             if (lane == 0) ch.status[t] = 2;
@@ -308,8 +311,10 @@ __global__ void ff_resolve_kernel(TileMap tm, const uint64_t* __restrict__ seg_b
                     }
                 }
                 if (valid) flags[i] = flag;
+                ntaken += __popc(__ballot_sync(0xffffffffu, valid && flag));
             }
         }
+        if (lane == 0 && taken_count && ntaken) atomicAdd(taken_count, ntaken);
     }
 }
 
@@ -335,7 +340,7 @@ __global__ void __launch_bounds__(kThreads) ff_expand_kernel(TileMap tm,
 // capacity C (same capacity for every worker, SystemConfig is shared).
 void first_fit_pass(cudaStream_t s, const uint64_t* seg_begin, const uint64_t* seg_len,
                     uint32_t nseg, uint64_t total, const double* sz, double C, uint8_t* taken,
-                    Workspace& ws) {
+                    Workspace& ws, unsigned long long* taken_count) {
     TileMap tm;
     build_tilemap(s, seg_len, nseg, total, kChunk, tm, ws);
     FFChunks ch;
@@ -349,12 +354,13 @@ void first_fit_pass(cudaStream_t s, const uint64_t* seg_begin, const uint64_t* s
     ch.d1 = ws.scratch<long long>(m);
     ch.pbits = ws.scratch<uint8_t>(m);
     ch.status = ws.scratch<uint8_t>(m);
-    const unsigned g = grid_for(m, 1, 148u * 8u);
+    const unsigned g = grid_for(m, 1, 148u * 64u);
     ff_stats_kernel<<<g, kThreads, 0, s>>>(tm, seg_begin, seg_len, sz, ch);
     ff_prefix_kernel<<<grid_for((uint64_t)nseg * 32, kThreads), kThreads, 0, s>>>(tm, C, ch);
     ff_agg_kernel<<<g, kThreads, 0, s>>>(tm, seg_begin, seg_len, sz, C, ch);
     ff_resolve_kernel<<<grid_for((uint64_t)nseg * 32, 128), 128, 0, s>>>(tm, seg_begin, seg_len,
-                                                                         sz, C, ch, taken);
+                                                                         sz, C, ch, taken,
+                                                                         taken_count);
     ff_expand_kernel<<<g, kThreads, 0, s>>>(tm, seg_begin, seg_len, ch, taken);
 }
 

@@ -80,7 +80,7 @@ void launch_worker_segments(cudaStream_t s, const uint64_t* seg_off, uint32_t nl
 
 void first_fit_pass(cudaStream_t s, const uint64_t* seg_begin, const uint64_t* seg_len,
                     uint32_t nseg, uint64_t total, const double* sz, double C, uint8_t* taken,
-                    Workspace& ws);
+                    Workspace& ws, unsigned long long* taken_count = nullptr);
 
 void launch_gather_sizes(cudaStream_t s, const uint32_t* order, const uint32_t* cand_k,
                          const double* sizes, uint64_t n, double* out);

@@ -387,7 +387,6 @@ int first_fit_classes(clairplan_plan* p, const double* ssize, uint8_t* cls) {
     cudaStream_t s = p->stream;
     Workspace& ws = p->ws;
     bool ok = true;
-    uint8_t* taken = need<uint8_t>(p->taken, D, ok);
     unsigned long long* cnt = need<unsigned long long>(p->counters, 4, ok);
     if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed (first fit)");
     CK(cudaMemsetAsync(cls, 0, D, s));
@@ -397,10 +396,13 @@ int first_fit_classes(clairplan_plan* p, const double* ssize, uint8_t* cls) {
     CK(cudaMemcpyAsync(sl, p->wlen.get<uint64_t>(), nloc * 8, cudaMemcpyDeviceToDevice, s));
     const uint32_t* seq_idx = nullptr;
     const double* seq_sz = ssize;
+    const uint8_t* prev_taken = cls;  // class 1 writes its flags straight into cls (0/1)
     uint64_t remaining = D;
     for (uint32_t j = 1; j <= J; ++j) {
         if (remaining == 0) break;
+        uint8_t* taken = cls;
         if (j > 1) {
+            taken = need<uint8_t>(p->taken, D, ok);
             uint32_t* keys = need<uint32_t>(p->keys, D, ok);
             uint32_t* okeys = need<uint32_t>(p->okeys, D, ok);
             uint32_t* ib0 = need<uint32_t>(p->vals, D, ok);
@@ -409,7 +411,7 @@ int first_fit_classes(clairplan_plan* p, const double* ssize, uint8_t* cls) {
             if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed (first fit)");
             uint32_t* in_idx = (j % 2) ? ib0 : ib1;
             uint32_t* out_idx = (j % 2) ? ib1 : ib0;
-            launch_reject_keys(s, taken, D, seq_idx, keys, in_idx);
+            launch_reject_keys(s, prev_taken, D, seq_idx, keys, in_idx);
             const size_t m = ws.mark();
             TileMap tj;
             build_tilemap(s, sl, nloc, D, kRadixTile, tj, ws);
@@ -423,21 +425,24 @@ int first_fit_classes(clairplan_plan* p, const double* ssize, uint8_t* cls) {
             launch_gather_seq_sizes(s, out_idx, ssize, sb, sl, nloc, seqsz);
             seq_idx = out_idx;
             seq_sz = seqsz;
+            CK(cudaMemsetAsync(taken, 0, D, s));
             p->launches += 10;
         }
-        CK(cudaMemsetAsync(taken, 0, D, s));
+        CK(cudaMemsetAsync(cnt, 0, 8, s));
         const size_t m = ws.mark();
-        first_fit_pass(s, sb, sl, nloc, D, seq_sz, p->caps[j - 1], taken, ws);
+        first_fit_pass(s, sb, sl, nloc, D, seq_sz, p->caps[j - 1], taken, ws, cnt);
         ws.release(m);
-        launch_apply_pass(s, taken, D, seq_idx, nullptr, (uint8_t)j, cls);
-        p->launches += 9;
+        p->launches += 6;
+        if (j > 1) {
+            launch_apply_pass(s, taken, D, seq_idx, nullptr, (uint8_t)j, cls);
+            ++p->launches;
+        }
+        prev_taken = taken;
         if (j < J) {
             unsigned long long t = 0;
-            launch_count_nonzero(s, taken, D, cnt);
             CK(cudaMemcpyAsync(&t, cnt, 8, cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
             remaining -= t;
-            ++p->launches;
         }
     }
     return 0;
