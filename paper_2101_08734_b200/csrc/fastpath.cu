@@ -343,47 +343,53 @@ __global__ void __launch_bounds__(kThreads) seg_write_kernel2(
 // (mask -> first-order index -> tier position -> class) overlapped.
 constexpr int kBU = 4;
 
+// One warp per (worker, epoch) segment, kBU blocks per iteration: no per-block division and
+// the dependent gathers (mask -> first-order index -> tier position -> class) of kBU blocks
+// overlap.
 __global__ void __launch_bounds__(kThreads) blk_codes_kernel(
     Part part, uint32_t MB, const uint32_t* __restrict__ blkmask,
     const uint32_t* __restrict__ blkbase, const uint32_t* __restrict__ dest,
     const uint8_t* __restrict__ cls_sorted, uint32_t np, uint32_t J, uint32_t Rp,
-    uint32_t* __restrict__ rec, uint32_t* __restrict__ ccount, uint64_t nblk, FastDiv dMB,
-    FastDiv dE) {
+    uint32_t* __restrict__ rec, uint32_t* __restrict__ ccount, uint64_t nblk) {
     const uint32_t lane = threadIdx.x & 31;
-    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    for (uint64_t b0 = ((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5) * kBU; b0 < nblk;
-         b0 += nwarps * kBU) {
-        uint32_t m[kBU], c[kBU], d[kBU], cls[kBU];
+    const uint32_t E = part.E, nloc = part.wend - part.wbegin;
+    const uint64_t nseg = (uint64_t)nloc * E;
+    for (uint64_t seg = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; seg < nseg;
+         seg += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+        const uint32_t wl = (uint32_t)(seg / E);
+        const uint32_t nb = (uint32_t)((part.epoch_len(part.wbegin + wl) + 31) >> 5);
+        const uint64_t blk0 = seg * MB;
+        for (uint32_t b0 = 0; b0 < MB; b0 += kBU) {
+            uint32_t m[kBU], c[kBU], d[kBU], cls[kBU];
 #pragma unroll
-        for (int u = 0; u < kBU; ++u) {
-            const uint64_t blk = b0 + u;
-            m[u] = 0;
-            if (blk < nblk) {
-                const uint32_t seg = dMB.div((uint32_t)blk);
-                const uint32_t wl = dE.div(seg);
-                const uint64_t t = (uint64_t)((uint32_t)blk - seg * MB) * 32;
-                if (t < part.epoch_len(part.wbegin + wl)) {
-                    m[u] = blkmask[blk];
-                    c[u] = blkbase[blk];
+            for (int u = 0; u < kBU; ++u) {
+                const uint32_t bi = b0 + u;
+                m[u] = 0;
+                if (bi < nb) {
+                    m[u] = blkmask[blk0 + bi];
+                    c[u] = blkbase[blk0 + bi];
                 }
             }
-        }
 #pragma unroll
-        for (int u = 0; u < kBU; ++u)
-            d[u] = ((m[u] >> lane) & 1u) ? dest[c[u] + __popc(m[u] & lanemask_lt())] : kNone;
+            for (int u = 0; u < kBU; ++u)
+                d[u] = ((m[u] >> lane) & 1u) ? dest[c[u] + __popc(m[u] & lanemask_lt())] : kNone;
 #pragma unroll
-        for (int u = 0; u < kBU; ++u) cls[u] = d[u] != kNone ? cls_sorted[d[u]] : 0u;
+            for (int u = 0; u < kBU; ++u) cls[u] = d[u] != kNone ? cls_sorted[d[u]] : 0u;
 #pragma unroll
-        for (int u = 0; u < kBU; ++u) {
-            const uint64_t blk = b0 + u;
-            if (blk >= nblk) break;
-            for (uint32_t p = 0; p < np; ++p) {
-                const uint32_t pl = __ballot_sync(0xffffffffu, (cls[u] >> p) & 1u);
-                if (lane == 0) rec[blk * Rp + p] = pl;
-            }
-            for (uint32_t j = 1; j <= J; ++j) {
-                const uint32_t bj = __ballot_sync(0xffffffffu, cls[u] == j);
-                if (lane == 0) ccount[(uint64_t)(j - 1) * nblk + blk] = __popc(bj);
+            for (int u = 0; u < kBU; ++u) {
+                const uint32_t bi = b0 + u;
+                if (bi >= MB) break;
+                const uint64_t blk = blk0 + bi;
+                uint32_t word = 0;  // lane p < np holds plane p, lane np + j holds count of class j+1
+                for (uint32_t p = 0; p < np; ++p) {
+                    const uint32_t pl = __ballot_sync(0xffffffffu, (cls[u] >> p) & 1u);
+                    if (lane == p) word = pl;
+                }
+                for (uint32_t j = 1; j <= J; ++j) {
+                    const uint32_t bj = __ballot_sync(0xffffffffu, cls[u] == j);
+                    if (lane == j - 1) ccount[(uint64_t)(j - 1) * nblk + blk] = __popc(bj);
+                }
+                if (lane < np) rec[blk * Rp + lane] = word;
             }
         }
     }
@@ -409,38 +415,54 @@ __global__ void class_base_kernel(const uint64_t* __restrict__ cpre, uint64_t nb
 }
 
 // class_list[cstart[wl*J + j-1] + pos] = sample, pos = position in the worker's class list.
-// The block record is spread over lanes 0..Rp-1 and read through shuffles.
+// One warp per (worker, epoch) segment, kBU blocks per iteration; the block record is spread
+// over lanes 0..Rp-1 and read through shuffles, the stream words are loaded up front.
 __global__ void __launch_bounds__(kThreads) class_write_kernel(
     Part part, uint32_t MB, const uint32_t* __restrict__ stream, const uint32_t* __restrict__ rec,
     uint32_t np, uint32_t J, uint32_t Rp, const uint32_t* __restrict__ cbase,
-    const uint64_t* __restrict__ cstart, uint32_t* __restrict__ class_list, uint64_t nblk,
-    FastDiv dMB, FastDiv dE) {
+    const uint64_t* __restrict__ cstart, uint32_t* __restrict__ class_list, uint64_t nblk) {
     const uint32_t lane = threadIdx.x & 31;
-    const uint32_t E = part.E;
-    for (uint64_t blk = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; blk < nblk;
-         blk += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
-        const uint32_t seg = dMB.div((uint32_t)blk);
-        const uint32_t wl = dE.div(seg), e = seg - wl * E;
+    const uint32_t E = part.E, nloc = part.wend - part.wbegin;
+    const uint64_t nseg = (uint64_t)nloc * E;
+    for (uint64_t seg = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; seg < nseg;
+         seg += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+        const uint32_t wl = (uint32_t)(seg / E), e = (uint32_t)(seg - (uint64_t)wl * E);
         const uint32_t w = part.wbegin + wl;
         const uint64_t Le = part.epoch_len(w);
-        const uint64_t t0 = (uint64_t)((uint32_t)blk - seg * MB) * 32;
-        if (t0 >= Le) continue;
-        const uint32_t mine = lane < Rp ? rec[blk * Rp + lane] : 0;
-        const uint64_t t = t0 + lane;
-        uint32_t cls = 0;
-        for (uint32_t p = 0; p < np; ++p)
-            cls |= ((__shfl_sync(0xffffffffu, mine, p) >> lane) & 1u) << p;
-        if (t >= Le) cls = 0;
-        uint32_t cm = 0xffffffffu;
-        for (uint32_t p = 0; p < np; ++p) {
-            const uint32_t pl = __shfl_sync(0xffffffffu, mine, p);
-            cm &= ((cls >> p) & 1u) ? pl : ~pl;
-        }
-        const uint32_t pre = __shfl_sync(0xffffffffu, mine, (np + (cls ? cls - 1 : 0)) & 31);
-        if (cls) {
-            const uint32_t pos = pre - cbase[wl * J + cls - 1] + __popc(cm & lanemask_lt());
-            const uint64_t g = part.stream_offset(w) + (uint64_t)e * Le + t;
-            class_list[cstart[(uint64_t)wl * J + cls - 1] + pos] = stream[g];
+        const uint64_t g0 = part.stream_offset(w) + (uint64_t)e * Le;
+        const uint64_t blk0 = seg * MB;
+        // class bases / list starts of this worker: lanes j < J
+        const uint32_t cb = lane < J ? cbase[wl * J + lane] : 0;
+        const uint64_t cs = lane < J ? cstart[(uint64_t)wl * J + lane] : 0;
+        const uint32_t nb = (uint32_t)((Le + 31) >> 5);
+        for (uint32_t b0 = 0; b0 < nb; b0 += kBU) {
+            uint32_t mine[kBU], kv[kBU];
+#pragma unroll
+            for (int u = 0; u < kBU; ++u) {
+                const uint32_t bi = b0 + u;
+                const uint64_t t = (uint64_t)bi * 32 + lane;
+                mine[u] = (bi < nb && lane < Rp) ? rec[(blk0 + bi) * Rp + lane] : 0;
+                kv[u] = (bi < nb && t < Le) ? stream[g0 + t] : 0;
+            }
+#pragma unroll
+            for (int u = 0; u < kBU; ++u) {
+                const uint32_t bi = b0 + u;
+                if (bi >= nb) break;
+                const uint64_t t = (uint64_t)bi * 32 + lane;
+                uint32_t cls = 0, cm = 0xffffffffu;
+                for (uint32_t p = 0; p < np; ++p)
+                    cls |= ((__shfl_sync(0xffffffffu, mine[u], p) >> lane) & 1u) << p;
+                if (t >= Le) cls = 0;
+                for (uint32_t p = 0; p < np; ++p) {
+                    const uint32_t pl = __shfl_sync(0xffffffffu, mine[u], p);
+                    cm &= ((cls >> p) & 1u) ? pl : ~pl;
+                }
+                const uint32_t ci = cls ? cls - 1 : 0;
+                const uint32_t pre = __shfl_sync(0xffffffffu, mine[u], (np + ci) & 31);
+                const uint32_t base = __shfl_sync(0xffffffffu, cb, ci & 31);
+                const uint64_t start = __shfl_sync(0xffffffffu, cs, ci & 31);
+                if (cls) class_list[start + (pre - base) + __popc(cm & lanemask_lt())] = kv[u];
+            }
         }
     }
 }
@@ -535,9 +557,9 @@ void launch_blk_codes(cudaStream_t s, const Part& part, uint32_t MB, const uint3
                       const uint32_t* blkbase, const uint32_t* dest, const uint8_t* cls_sorted,
                       uint32_t np, uint32_t J, uint32_t Rp, uint32_t* rec, uint32_t* ccount,
                       uint64_t nblk) {
-    blk_codes_kernel<<<grid_for(nblk * 32 / kBU + 32, kThreads, 148u * 64u), kThreads, 0, s>>>(
-        part, MB, blkmask, blkbase, dest, cls_sorted, np, J, Rp, rec, ccount, nblk, FastDiv(MB),
-        FastDiv(part.E));
+    const uint64_t nseg = (uint64_t)(part.wend - part.wbegin) * part.E;
+    blk_codes_kernel<<<grid_for(nseg * 32, kThreads, 148u * 64u), kThreads, 0, s>>>(
+        part, MB, blkmask, blkbase, dest, cls_sorted, np, J, Rp, rec, ccount, nblk);
 }
 
 void launch_rec_fill(cudaStream_t s, const uint64_t* cpre, uint64_t nblk, uint32_t np, uint32_t J,
@@ -552,9 +574,9 @@ void launch_class_write(cudaStream_t s, const Part& part, uint32_t MB, const uin
                         const uint32_t* rec, uint32_t np, uint32_t J, uint32_t Rp,
                         const uint32_t* cbase, const uint64_t* cstart, uint32_t* class_list,
                         uint64_t nblk) {
-    class_write_kernel<<<grid_for(nblk * 32, kThreads, 148u * 64u), kThreads, 0, s>>>(
-        part, MB, stream, rec, np, J, Rp, cbase, cstart, class_list, nblk, FastDiv(MB),
-        FastDiv(part.E));
+    const uint64_t nseg = (uint64_t)(part.wend - part.wbegin) * part.E;
+    class_write_kernel<<<grid_for(nseg * 32, kThreads, 148u * 64u), kThreads, 0, s>>>(
+        part, MB, stream, rec, np, J, Rp, cbase, cstart, class_list, nblk);
 }
 
 void launch_class_lens(cudaStream_t s, uint32_t nloc, uint32_t E, uint32_t MB, uint32_t J,
