@@ -219,42 +219,56 @@ __global__ void __launch_bounds__(128) sample_hash_kernel(Part part, const uint3
 }
 
 // ---------------------------------------------------------------------------- K4b
+// One warp per (worker, epoch) segment; kSU 32-entry steps are loaded ahead (stream words,
+// then their info words — the join with the sample pass, L2-resident per epoch because the
+// segments are ordered epoch-major).  No block barriers: per-count counters live in the
+// warp's shared slice, one leader per count value per step (__match_any_sync).
+constexpr int kSU = 4;
+
 // seghist[(wl*E + (E - c))*E + e] = first accesses with count c in segment (w, e)
 __global__ void __launch_bounds__(kThreads) seg_hist_kernel(Part part, const uint32_t* __restrict__ stream,
                                                              const uint16_t* __restrict__ info,
                                                              uint32_t* __restrict__ seghist,
                                                              uint32_t* __restrict__ segcnt) {
-    extern __shared__ uint32_t hist[];  // [E]
-    __shared__ uint32_t wsum[kThreads / 32];
+    extern __shared__ uint32_t shist[];  // [warps][E]
     const uint32_t E = part.E, nloc = part.wend - part.wbegin;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t* hist = shist + warp * E;
     const uint64_t nseg = (uint64_t)nloc * E;
-    for (uint64_t b = blockIdx.x; b < nseg; b += gridDim.x) {
-        const uint32_t e = (uint32_t)(b / nloc), wl = (uint32_t)(b % nloc);
+    for (uint64_t b = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; b < nseg;
+         b += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+        const uint32_t e = (uint32_t)(b / nloc), wl = (uint32_t)(b - (uint64_t)e * nloc);
         const uint32_t w = part.wbegin + wl;
-        for (uint32_t i = threadIdx.x; i < E; i += blockDim.x) hist[i] = 0;
-        __syncthreads();
+        for (uint32_t i = lane; i < E; i += 32) hist[i] = 0;
+        __syncwarp();
         const uint64_t Le = part.epoch_len(w);
         const uint64_t g0 = part.stream_offset(w) + (uint64_t)e * Le;
         const uint16_t* row = info + (size_t)e * part.F;
         uint32_t tot = 0;
-        for (uint64_t t = threadIdx.x; t < Le; t += blockDim.x) {
-            const uint32_t c = row[stream[g0 + t]];
-            if (c) {
-                atomicAdd(&hist[E - c], 1u);
-                ++tot;
+        for (uint64_t t0 = 0; t0 < Le; t0 += 32 * kSU) {
+            uint32_t k[kSU], c[kSU];
+#pragma unroll
+            for (int u = 0; u < kSU; ++u) {
+                const uint64_t t = t0 + 32 * u + lane;
+                k[u] = t < Le ? stream[g0 + t] : kNone;
             }
+#pragma unroll
+            for (int u = 0; u < kSU; ++u) c[u] = k[u] != kNone ? row[k[u]] : 0u;
+#pragma unroll
+            for (int u = 0; u < kSU; ++u) {
+                const bool first = c[u] != 0;
+                const uint32_t key = first ? E - c[u] : (0x80000000u | lane);
+                const uint32_t m = __match_any_sync(0xffffffffu, key);
+                if (first && __popc(m & lanemask_lt()) == 0) hist[key] += __popc(m);
+                tot += first;
+            }
+            __syncwarp();
         }
         tot = warp_sum(tot);
-        if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = tot;
-        __syncthreads();
-        for (uint32_t i = threadIdx.x; i < E; i += blockDim.x)
-            seghist[((uint64_t)wl * E + i) * E + e] = hist[i];
-        if (threadIdx.x == 0) {
-            uint32_t s = 0;
-            for (int i = 0; i < kThreads / 32; ++i) s += wsum[i];
-            segcnt[(uint64_t)wl * E + e] = s;
-        }
-        __syncthreads();
+        __syncwarp();
+        for (uint32_t i = lane; i < E; i += 32) seghist[((uint64_t)wl * E + i) * E + e] = hist[i];
+        if (lane == 0) segcnt[(uint64_t)wl * E + e] = tot;
+        __syncwarp();
     }
 }
 
@@ -265,73 +279,63 @@ __global__ void __launch_bounds__(kThreads) seg_write_kernel2(
     const uint64_t* __restrict__ sorted_base, uint32_t MB, uint32_t* __restrict__ dest,
     double* __restrict__ sorted_size, uint32_t* __restrict__ blkmask,
     uint32_t* __restrict__ blkbase) {
-    extern __shared__ uint32_t sm2[];
+    extern __shared__ uint32_t srun[];  // [warps][E] running count per count value
     const uint32_t E = part.E, nloc = part.wend - part.wbegin;
-    uint32_t* run = sm2;              // [E]
-    uint32_t* wcnt = sm2 + E;         // [8][E]
-    __shared__ uint32_t wtot[kThreads / 32];
-    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t* run = srun + warp * E;
     const uint64_t nseg = (uint64_t)nloc * E;
-    for (uint32_t i = threadIdx.x; i < 9 * E; i += blockDim.x) sm2[i] = 0;
-    __syncthreads();
-    for (uint64_t b = blockIdx.x; b < nseg; b += gridDim.x) {
-        const uint32_t e = (uint32_t)(b / nloc), wl = (uint32_t)(b % nloc);
+    for (uint64_t b = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; b < nseg;
+         b += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+        const uint32_t e = (uint32_t)(b / nloc), wl = (uint32_t)(b - (uint64_t)e * nloc);
         const uint32_t w = part.wbegin + wl;
+        for (uint32_t i = lane; i < E; i += 32) run[i] = 0;
+        __syncwarp();
         const uint64_t Le = part.epoch_len(w);
         const uint64_t g0 = part.stream_offset(w) + (uint64_t)e * Le;
         const uint16_t* row = info + (size_t)e * part.F;
         const uint64_t fbase = seg_off[(uint64_t)wl * E + e];
         const uint64_t* sbase = sorted_base + (uint64_t)wl * E * E + e;  // + (E-c)*E
+        const uint64_t blk0 = ((uint64_t)wl * E + e) * MB;
         uint64_t frun = 0;
-        for (uint64_t t0 = 0; t0 < Le; t0 += blockDim.x) {
-            const uint64_t t = t0 + threadIdx.x;
-            uint32_t k = 0, c = 0;
-            if (t < Le) {
-                k = stream[g0 + t];
-                c = row[k];
-            }
-            const bool first = c != 0;
-            const uint32_t bal = __ballot_sync(0xffffffffu, first);
-            if (lane == 0) wtot[warp] = __popc(bal);
-            const uint32_t key = first ? (E - c) : (0x80000000u | lane);
-            const uint32_t m = __match_any_sync(0xffffffffu, key);
-            const uint32_t rnk = __popc(m & lanemask_lt());
-            if (first && rnk == 0) wcnt[warp * E + key] = __popc(m);
-            __syncthreads();
-            uint32_t fbelow = 0, ftot = 0;
+        for (uint64_t t0 = 0; t0 < Le; t0 += 32 * kSU) {
+            uint32_t k[kSU], c[kSU];
 #pragma unroll
-            for (int i = 0; i < kThreads / 32; ++i) {
-                fbelow += (i < (int)warp) ? wtot[i] : 0;
-                ftot += wtot[i];
+            for (int u = 0; u < kSU; ++u) {
+                const uint64_t t = t0 + 32 * u + lane;
+                k[u] = t < Le ? stream[g0 + t] : kNone;
             }
-            if (lane == 0 && t < Le) {
-                const uint64_t blk = ((uint64_t)wl * E + e) * MB + (t >> 5);
-                blkmask[blk] = bal;
-                blkbase[blk] = (uint32_t)(fbase + frun + fbelow);
-            }
-            if (first) {
-                uint32_t below = 0;
-                for (uint32_t i = 0; i < warp; ++i) below += wcnt[i * E + key];
-                const uint64_t fpos = fbase + frun + fbelow + __popc(bal & lanemask_lt());
-                const uint64_t spos = sbase[(uint64_t)key * E] + run[key] + below + rnk;
-                dest[fpos] = (uint32_t)spos;
-                sorted_size[spos] = sizes[k];
-            }
-            __syncthreads();
-            for (uint32_t i = threadIdx.x; i < E; i += blockDim.x) {
-                uint32_t s = 0;
 #pragma unroll
-                for (int x = 0; x < kThreads / 32; ++x) {
-                    s += wcnt[x * E + i];
-                    wcnt[x * E + i] = 0;
+            for (int u = 0; u < kSU; ++u) c[u] = k[u] != kNone ? row[k[u]] : 0u;
+#pragma unroll
+            for (int u = 0; u < kSU; ++u) {
+                const uint64_t tb = t0 + 32 * u;
+                if (tb >= Le) break;
+                const bool first = c[u] != 0;
+                const uint32_t bal = __ballot_sync(0xffffffffu, first);
+                if (lane == 0) {
+                    blkmask[blk0 + (tb >> 5)] = bal;
+                    blkbase[blk0 + (tb >> 5)] = (uint32_t)(fbase + frun);
                 }
-                run[i] += s;
+                const uint32_t key = first ? E - c[u] : (0x80000000u | lane);
+                const uint32_t m = __match_any_sync(0xffffffffu, key);
+                const uint32_t leader = __ffs(m) - 1;
+                uint32_t r0 = 0;
+                if (first && lane == leader) {
+                    r0 = run[key];
+                    run[key] = r0 + __popc(m);
+                }
+                r0 = __shfl_sync(0xffffffffu, r0, leader);
+                if (first) {
+                    const uint64_t fpos = fbase + frun + __popc(bal & lanemask_lt());
+                    const uint64_t spos = sbase[(uint64_t)key * E] + r0 + __popc(m & lanemask_lt());
+                    dest[fpos] = (uint32_t)spos;
+                    sorted_size[spos] = sizes[k[u]];
+                }
+                frun += __popc(bal);
             }
-            frun += ftot;
-            __syncthreads();
+            __syncwarp();
         }
-        for (uint32_t i = threadIdx.x; i < E; i += blockDim.x) run[i] = 0;
-        __syncthreads();
+        __syncwarp();
     }
 }
 
@@ -623,8 +627,10 @@ void launch_sample_hash(cudaStream_t s, const Part& part, const uint32_t* inv, u
 void launch_seg_hist(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info,
                      uint32_t* seghist, uint32_t* segcnt) {
     const uint64_t nseg = (uint64_t)(part.wend - part.wbegin) * part.E;
-    seg_hist_kernel<<<grid_for(nseg, 1, 148u * 32u), kThreads, part.E * 4, s>>>(part, stream, info,
-                                                                                seghist, segcnt);
+    const size_t smem = (size_t)(kThreads / 32) * part.E * 4;
+    cudaFuncSetAttribute(seg_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    seg_hist_kernel<<<grid_for(nseg * 32, kThreads, 148u * 64u), kThreads, smem, s>>>(
+        part, stream, info, seghist, segcnt);
 }
 
 void launch_seg_write2(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info,
@@ -632,9 +638,9 @@ void launch_seg_write2(cudaStream_t s, const Part& part, const uint32_t* stream,
                        uint32_t MB, uint32_t* dest, double* sorted_size, uint32_t* blkmask,
                        uint32_t* blkbase) {
     const uint64_t nseg = (uint64_t)(part.wend - part.wbegin) * part.E;
-    const size_t smem = (size_t)9 * part.E * 4;
+    const size_t smem = (size_t)(kThreads / 32) * part.E * 4;
     cudaFuncSetAttribute(seg_write_kernel2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    seg_write_kernel2<<<grid_for(nseg, 1, 148u * 32u), kThreads, smem, s>>>(
+    seg_write_kernel2<<<grid_for(nseg * 32, kThreads, 148u * 64u), kThreads, smem, s>>>(
         part, stream, info, sizes, seg_off, sorted_base, MB, dest, sorted_size, blkmask, blkbase);
 }
 
