@@ -68,7 +68,7 @@ constexpr int kLocal = 48;
 
 
 // Sorts one target's writer list (>= 3 writers, rare) and links it in place.
-__device__ void fy_group_long(uint32_t y, uint32_t a0, uint32_t* nx, uint32_t* qq,
+__device__ __noinline__ void fy_group_long(uint32_t y, uint32_t a0, uint32_t* nx, uint32_t* qq,
                               uint32_t* scratch, uint32_t scratch_cap, uint32_t* scratch_used,
                               uint32_t* err) {
     uint32_t buf[kLocal];
@@ -145,8 +145,26 @@ __global__ void __launch_bounds__(kThreads) fy_group_kernel(uint32_t F,
         for (int u = 0; u < kGU; ++u) {
             const uint32_t y = y0 + u * stride;
             if (y >= F) break;
+            const uint32_t a0 = a[u][0], a1 = a[u][1];
+            if (a0 == kNone) {
+                qq[y] = kNone;
+                continue;
+            }
+            if (a1 == kNone) {  // one writer; its succ is already kNone
+                qq[y] = (a0 == y) ? kNone : a0;
+                continue;
+            }
+            if (a[u][2] == kNone) {  // two writers: list a0 -> a1, needs ascending order
+                const uint32_t lo = min(a0, a1), hi = max(a0, a1);
+                qq[y] = (lo == y) ? hi : lo;
+                if (a0 > a1) {
+                    nx[a1] = a0;
+                    nx[a0] = kNone;
+                }
+                continue;
+            }
             if (a[u][kReg] != kNone) {  // more than kReg writers (small y only)
-                fy_group_long(y, a[u][0], nx, qq, scratch, scratch_cap, scratch_used, err);
+                fy_group_long(y, a0, nx, qq, scratch, scratch_cap, scratch_used, err);
                 continue;
             }
             uint32_t qv = kNone;
