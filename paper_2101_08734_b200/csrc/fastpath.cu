@@ -28,7 +28,7 @@ namespace clairplan {
 
 constexpr int kU = 8;         // epochs loaded per batch (memory-level parallelism)
 
-__device__ __forceinline__ uint32_t ld_inv(const uint32_t* p) { return __ldcg(p); }
+__device__ __forceinline__ uint32_t ld_inv(const uint32_t* p) { return __ldcs(p); }
 
 // ---------------------------------------------------------------------------- K4a
 // Lane = sample, everything per lane in shared memory with a [row][lane] layout (no bank
@@ -106,8 +106,8 @@ __global__ void __launch_bounds__(128) sample_lanes_kernel(Part part, const uint
                     c = cnt[r * 32 + lane];
                     rk = (uint16_t)r;
                 }
-                info[(size_t)e * F + k] = c;
-                rank16[(size_t)e * F + k] = rk;
+                __stcs(info + (size_t)e * F + k, c);
+                __stcs(rank16 + (size_t)e * F + k, rk);
             }
         }
         for (uint32_t t = 0; t < W; ++t) bm[t * 32 + lane] = 0;
@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(kThreads) seg_hist_kernel(Part part, const uin
 #pragma unroll
             for (int u = 0; u < kSU; ++u) {
                 const uint64_t t = t0 + 32 * u + lane;
-                k[u] = t < Le ? stream[g0 + t] : kNone;
+                k[u] = t < Le ? __ldcs(stream + g0 + t) : kNone;
             }
 #pragma unroll
             for (int u = 0; u < kSU; ++u) c[u] = k[u] != kNone ? row[k[u]] : 0u;
@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(kThreads) seg_write_kernel2(
 #pragma unroll
             for (int u = 0; u < kSU; ++u) {
                 const uint64_t t = t0 + 32 * u + lane;
-                k[u] = t < Le ? stream[g0 + t] : kNone;
+                k[u] = t < Le ? __ldcs(stream + g0 + t) : kNone;
             }
 #pragma unroll
             for (int u = 0; u < kSU; ++u) c[u] = k[u] != kNone ? row[k[u]] : 0u;
@@ -328,8 +328,8 @@ __global__ void __launch_bounds__(kThreads) seg_write_kernel2(
                 if (first) {
                     const uint64_t fpos = fbase + frun + __popc(bal & lanemask_lt());
                     const uint64_t spos = sbase[(uint64_t)key * E] + r0 + __popc(m & lanemask_lt());
-                    dest[fpos] = (uint32_t)spos;
-                    sorted_size[spos] = sizes[k[u]];
+                    __stcs(dest + fpos, (uint32_t)spos);
+                    __stcs(sorted_size + spos, sizes[k[u]]);
                 }
                 frun += __popc(bal);
             }
@@ -446,7 +446,7 @@ __global__ void __launch_bounds__(kThreads) class_write_kernel(
                 const uint32_t bi = b0 + u;
                 const uint64_t t = (uint64_t)bi * 32 + lane;
                 mine[u] = (bi < nb && lane < Rp) ? rec[(blk0 + bi) * Rp + lane] : 0;
-                kv[u] = (bi < nb && t < Le) ? stream[g0 + t] : 0;
+                kv[u] = (bi < nb && t < Le) ? __ldcs(stream + g0 + t) : 0;
             }
 #pragma unroll
             for (int u = 0; u < kBU; ++u) {
@@ -465,7 +465,7 @@ __global__ void __launch_bounds__(kThreads) class_write_kernel(
                 const uint32_t pre = __shfl_sync(0xffffffffu, mine[u], (np + ci) & 31);
                 const uint32_t base = __shfl_sync(0xffffffffu, cb, ci & 31);
                 const uint64_t start = __shfl_sync(0xffffffffu, cs, ci & 31);
-                if (cls) class_list[start + (pre - base) + __popc(cm & lanemask_lt())] = kv[u];
+                if (cls) __stcs(class_list + start + (pre - base) + __popc(cm & lanemask_lt()), kv[u]);
             }
         }
     }
@@ -541,9 +541,9 @@ __global__ void __launch_bounds__(kThreads) holder_tile_kernel(
                     pos = prew - cbase[wl * J + cls - 1] + __popc(cm & ((1u << bit) - 1u));
                 }
                 uint32_t* h = holders + 3 * (slot0 + rk);
-                h[0] = w;
-                h[1] = cls;
-                h[2] = pos;
+                __stcs(h, w);
+                __stcs(h + 1, cls);
+                __stcs(h + 2, pos);
             }
         }
     }

@@ -111,13 +111,48 @@ __device__ __noinline__ void fy_group_long(uint32_t y, uint32_t a0, uint32_t* nx
 }
 
 // Per target y: q[y] and the ascending writer chain (succ) in place of the exchange list.
-// Lists of up to kReg writers stay in registers: each writer's successor is the smallest
-// larger writer (O(n^2) compares, no local memory), written only where the exchange order
-// differs.  Each thread walks kGU targets at once so their dependent list loads overlap.
-constexpr int kGU = 2;
+// Each thread walks kGU targets at once (their dependent list loads overlap) and resolves the
+// common 0/1/2-writer lists in registers; >= 3 writers go through a register network of up to
+// kReg writers, longer lists (small y only) through local memory / global scratch.
+constexpr int kGU = 4;
 constexpr int kReg = 8;
 
-__global__ void __launch_bounds__(kThreads) fy_group_kernel(uint32_t F,
+__device__ __noinline__ void fy_group_mid(uint32_t y, uint32_t a0, uint32_t a1, uint32_t a2,
+                                          uint32_t* nx, uint32_t* qq, uint32_t* scratch,
+                                          uint32_t scratch_cap, uint32_t* scratch_used,
+                                          uint32_t* err) {
+    uint32_t a[kReg + 1];
+    a[0] = a0;
+    a[1] = a1;
+    a[2] = a2;
+#pragma unroll
+    for (int t = 3; t <= kReg; ++t) a[t] = a[t - 1] != kNone ? nx[a[t - 1]] : kNone;
+    if (a[kReg] != kNone) {
+        fy_group_long(y, a0, nx, qq, scratch, scratch_cap, scratch_used, err);
+        return;
+    }
+    uint32_t qv = kNone;
+#pragma unroll
+    for (int t = 0; t < kReg; ++t) {
+        const uint32_t x = a[t];
+        if (x != kNone && x != y && x < qv) qv = x;
+    }
+    qq[y] = qv;
+#pragma unroll
+    for (int t = 0; t < kReg; ++t) {
+        const uint32_t x = a[t];
+        if (x == kNone) continue;
+        uint32_t sc = kNone;
+#pragma unroll
+        for (int r = 0; r < kReg; ++r) {
+            const uint32_t z = a[r];
+            if (z != kNone && z > x && z < sc) sc = z;
+        }
+        if (sc != a[t + 1]) nx[x] = sc;
+    }
+}
+
+__global__ void __launch_bounds__(kThreads, 6) fy_group_kernel(uint32_t F,
                                                              const uint32_t* __restrict__ head,
                                                              uint32_t* __restrict__ next,
                                                              uint32_t* __restrict__ q,
@@ -131,60 +166,33 @@ __global__ void __launch_bounds__(kThreads) fy_group_kernel(uint32_t F,
     uint32_t* qq = q + (size_t)slot * F;
     const uint32_t stride = gridDim.x * blockDim.x;
     for (uint32_t y0 = blockIdx.x * blockDim.x + threadIdx.x; y0 < F; y0 += kGU * stride) {
-        uint32_t a[kGU][kReg + 1];
+        uint32_t a0[kGU], a1[kGU], a2[kGU];
 #pragma unroll
         for (int u = 0; u < kGU; ++u) {
             const uint32_t y = y0 + u * stride;
-            a[u][0] = y < F ? hd[y] : kNone;
+            a0[u] = y < F ? hd[y] : kNone;
         }
 #pragma unroll
-        for (int t = 1; t <= kReg; ++t)
+        for (int u = 0; u < kGU; ++u) a1[u] = a0[u] != kNone ? nx[a0[u]] : kNone;
 #pragma unroll
-            for (int u = 0; u < kGU; ++u) a[u][t] = a[u][t - 1] != kNone ? nx[a[u][t - 1]] : kNone;
+        for (int u = 0; u < kGU; ++u) a2[u] = a1[u] != kNone ? nx[a1[u]] : kNone;
 #pragma unroll
         for (int u = 0; u < kGU; ++u) {
             const uint32_t y = y0 + u * stride;
             if (y >= F) break;
-            const uint32_t a0 = a[u][0], a1 = a[u][1];
-            if (a0 == kNone) {
+            if (a0[u] == kNone) {
                 qq[y] = kNone;
-                continue;
-            }
-            if (a1 == kNone) {  // one writer; its succ is already kNone
-                qq[y] = (a0 == y) ? kNone : a0;
-                continue;
-            }
-            if (a[u][2] == kNone) {  // two writers: list a0 -> a1, needs ascending order
-                const uint32_t lo = min(a0, a1), hi = max(a0, a1);
+            } else if (a1[u] == kNone) {  // one writer; its succ is already kNone
+                qq[y] = (a0[u] == y) ? kNone : a0[u];
+            } else if (a2[u] == kNone) {  // two writers: list a0 -> a1, needs ascending order
+                const uint32_t lo = min(a0[u], a1[u]), hi = max(a0[u], a1[u]);
                 qq[y] = (lo == y) ? hi : lo;
-                if (a0 > a1) {
-                    nx[a1] = a0;
-                    nx[a0] = kNone;
+                if (a0[u] > a1[u]) {
+                    nx[a1[u]] = a0[u];
+                    nx[a0[u]] = kNone;
                 }
-                continue;
-            }
-            if (a[u][kReg] != kNone) {  // more than kReg writers (small y only)
-                fy_group_long(y, a0, nx, qq, scratch, scratch_cap, scratch_used, err);
-                continue;
-            }
-            uint32_t qv = kNone;
-#pragma unroll
-            for (int t = 0; t < kReg; ++t) {
-                const uint32_t x = a[u][t];
-                if (x != kNone && x != y && x < qv) qv = x;
-            }
-            qq[y] = qv;
-#pragma unroll
-            for (int t = 0; t < kReg; ++t) {
-                const uint32_t x = a[u][t];
-                if (x == kNone) continue;
-                uint32_t sc = kNone;
-#pragma unroll
-                for (int r = 0; r < kReg; ++r) {
-                    const uint32_t z = a[u][r];
-                    if (z != kNone && z > x && z < sc) sc = z;
-                }
-                if (sc != a[u][t + 1]) nx[x] = sc;
+            } else {
+                fy_group_mid(y, a0[u], a1[u], a2[u], nx, qq, scratch, scratch_cap, scratch_used, err);
             }
         }
     }
