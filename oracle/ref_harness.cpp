@@ -156,9 +156,15 @@ int ref_generate_sizes(uint64_t F, double mean, double sigma, int has_total, dou
 }
 
 // Full reference plan. mode 0 = verbatim, mode 1 = per-worker decomposition on `threads`.
+void* ref_plan_build_subset(uint64_t seed, uint32_t F, uint32_t N, uint32_t B, uint32_t E,
+                            int drop_last, uint32_t J, const double* caps, const double* sizes,
+                            int threads, const uint32_t* subset, uint32_t nsubset);
+
 void* ref_plan_build(uint64_t seed, uint32_t F, uint32_t N, uint32_t B, uint32_t E,
                      int drop_last, uint32_t J, const double* caps, const double* sizes,
                      int mode, int threads) {
+    if (mode == 1) return ref_plan_build_subset(seed, F, N, B, E, drop_last, J, caps, sizes,
+                                                threads, nullptr, 0);
     try {
         auto p = std::make_unique<RefPlan>();
         p->F = F;
@@ -171,44 +177,66 @@ void* ref_plan_build(uint64_t seed, uint32_t F, uint32_t N, uint32_t B, uint32_t
             for (const auto& st : p->streams)
                 p->freqs.push_back(access_frequencies(st, F, 0, st.epoch_count()));
             p->assign = nopfs_assign_caches(p->freqs, cfg, dataset, p->streams);
-        } else {
-            part.validate(F);
-            std::vector<std::vector<uint32_t>> perms(E);
-            parallel_for(E, threads, [&](uint64_t e) {
-                perms[e] = epoch_permutation(Seed{seed}, static_cast<uint32_t>(e), F);
-            });
-            const uint64_t full = F / B;
-            const uint64_t tail = part.drop_last ? 0 : F % B;
-            const uint64_t nb = full + (tail > 0 ? 1 : 0);
-            p->streams.resize(N);
-            parallel_for(N, threads, [&](uint64_t w) {
-                auto& st = p->streams[w];
-                st.worker_id = static_cast<uint32_t>(w);
-                st.epoch_offsets.push_back(0);
-                st.batch_offsets.push_back(0);
-                for (uint32_t e = 0; e < E; ++e) {
-                    for (uint64_t h = 0; h < nb; ++h) {
-                        const uint64_t bs = h < full ? B : tail;
-                        const auto [sb, se] = batch_slice(bs, N, static_cast<uint32_t>(w));
-                        st.entries.insert(st.entries.end(), perms[e].begin() + h * B + sb,
-                                          perms[e].begin() + h * B + se);
-                        st.batch_offsets.push_back(st.entries.size());
-                    }
-                    st.epoch_offsets.push_back(st.entries.size());
-                }
-            });
-            perms.clear();
-            perms.shrink_to_fit();
-            p->assign.class_lists.assign(N, std::vector<std::vector<uint32_t>>(J));
-            const SystemConfig cfg1 = make_cfg(1, J, caps);
-            parallel_for(N, threads, [&](uint64_t w) {
-                const auto& st = p->streams[w];
-                const auto freq = access_frequencies(st, F, 0, st.epoch_count());
-                auto one = nopfs_assign_caches({freq}, cfg1, dataset, {st});
-                if (J > 0) p->assign.class_lists[w] = std::move(one.class_lists[0]);
-            });
-            p->assign.build_index(F);
         }
+        flatten_holders(*p);
+        return p.release();
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+
+// Per-worker decomposition restricted to a worker subset (the others' class lists stay empty,
+// so build_index yields the holder CSR restricted to the subset: a subsequence of the full
+// CSR because holders are worker-ordered).  subset == nullptr: all workers.
+void* ref_plan_build_subset(uint64_t seed, uint32_t F, uint32_t N, uint32_t B, uint32_t E,
+                            int drop_last, uint32_t J, const double* caps, const double* sizes,
+                            int threads, const uint32_t* subset, uint32_t nsubset) {
+    try {
+        auto p = std::make_unique<RefPlan>();
+        p->F = F;
+        PartitionSpec part{N, B, E, drop_last != 0};
+        const DatasetModel dataset = DatasetModel::from_sizes(std::vector<double>(sizes, sizes + F));
+        part.validate(F);
+        std::vector<std::vector<uint32_t>> perms(E);
+        parallel_for(E, threads, [&](uint64_t e) {
+            perms[e] = epoch_permutation(Seed{seed}, static_cast<uint32_t>(e), F);
+        });
+        const uint64_t full = F / B;
+        const uint64_t tail = part.drop_last ? 0 : F % B;
+        const uint64_t nb = full + (tail > 0 ? 1 : 0);
+        p->streams.resize(N);
+        parallel_for(N, threads, [&](uint64_t w) {
+            auto& st = p->streams[w];
+            st.worker_id = static_cast<uint32_t>(w);
+            st.epoch_offsets.push_back(0);
+            st.batch_offsets.push_back(0);
+            for (uint32_t e = 0; e < E; ++e) {
+                for (uint64_t h = 0; h < nb; ++h) {
+                    const uint64_t bs = h < full ? B : tail;
+                    const auto [sb, se] = batch_slice(bs, N, static_cast<uint32_t>(w));
+                    st.entries.insert(st.entries.end(), perms[e].begin() + h * B + sb,
+                                      perms[e].begin() + h * B + se);
+                    st.batch_offsets.push_back(st.entries.size());
+                }
+                st.epoch_offsets.push_back(st.entries.size());
+            }
+        });
+        perms.clear();
+        perms.shrink_to_fit();
+        p->assign.class_lists.assign(N, std::vector<std::vector<uint32_t>>(J));
+        const SystemConfig cfg1 = make_cfg(1, J, caps);
+        std::vector<uint32_t> todo;
+        if (subset) todo.assign(subset, subset + nsubset);
+        else for (uint32_t w = 0; w < N; ++w) todo.push_back(w);
+        parallel_for(todo.size(), threads, [&](uint64_t i) {
+            const uint32_t w = todo[i];
+            const auto& st = p->streams[w];
+            const auto freq = access_frequencies(st, F, 0, st.epoch_count());
+            auto one = nopfs_assign_caches({freq}, cfg1, dataset, {st});
+            if (J > 0) p->assign.class_lists[w] = std::move(one.class_lists[0]);
+        });
+        p->assign.build_index(F);
         flatten_holders(*p);
         return p.release();
     } catch (const std::exception& e) {

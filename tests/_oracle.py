@@ -162,6 +162,10 @@ class Ref:
         L.ref_plan_build.restype = C.c_void_p
         L.ref_plan_build.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
                                      C.c_int, C.c_uint32, f64p, f64p, C.c_int, C.c_int]
+        L.ref_plan_build_subset.restype = C.c_void_p
+        L.ref_plan_build_subset.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
+                                            C.c_uint32, C.c_int, C.c_uint32, f64p, f64p, C.c_int,
+                                            u32p, C.c_uint32]
         L.ref_assign_from_streams.restype = C.c_void_p
         L.ref_assign_from_streams.argtypes = [C.c_uint32, C.c_uint32, u32p, u64p, u32p,
                                               C.c_uint32, f64p, f64p]
@@ -255,6 +259,17 @@ class Ref:
         if not h:
             raise ValueError(self.err())
         return self._collect(h, N, len(caps), F, keep)
+
+    def plan_subset(self, seed, F, N, B, E, drop_last, caps, sizes, workers, threads):
+        caps = np.ascontiguousarray(caps, np.float64)
+        sizes = np.ascontiguousarray(sizes, np.float64)
+        ws = np.ascontiguousarray(workers, np.uint32)
+        h = self.L.ref_plan_build_subset(seed, F, N, B, E, int(drop_last), len(caps),
+                                         _ptr(caps, f64p), _ptr(sizes, f64p), threads,
+                                         _ptr(ws, u32p), len(ws))
+        if not h:
+            raise ValueError(self.err())
+        return self._collect(h, N, len(caps), F)
 
     def access_frequencies(self, plan, w, eb, ee, F):
         out = np.empty(F, np.uint32)

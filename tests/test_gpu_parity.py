@@ -284,3 +284,37 @@ def test_build_from_perms_matches_build(cp, ref):
         assert np.array_equal(np.diff(ha[0].astype(np.int64)), cnt.cpu().numpy())
         a.close()
         b.close()
+
+
+def test_config4_imagenet22k_against_reference_worker_subset(cp, ref):
+    """Config 4 (ImageNet-22k shape, 90 epochs, 1024 workers): every stream bit-exact with the
+    reference; class lists and holder CSR bit-exact for a worker subset (the reference's own
+    per-worker functions; the CSR restricted to a worker subset is a subsequence of the full
+    CSR because build_index orders holders by worker)."""
+    F, N, b, E = 14_197_122, 1024, 32, 90
+    caps = [120_000.0, 900_000.0]
+    sizes = ref.generate_sizes(F, 0.1077, 0.2, 1_500_000.0, 1)
+    subset = np.array([0, 1, 2, 255, 511, 512, 777, 1022, 1023], np.uint32)
+    a = ref.plan_subset(42, F, N, b * N, E, True, caps, sizes, subset, os.cpu_count() or 8)
+    p = cp.Plan(42, F, cp.PartitionSpec(N, b * N, E, True), caps, sizes).build()
+    st = p.stats()
+    assert st["accesses"] == 1_276_968_960
+    flat = p.streams_flat()
+    o = 0
+    for w in range(N):
+        n = len(a.streams[w])
+        assert np.array_equal(flat[o:o + n], a.streams[w]), w
+        o += n
+    del flat
+    cl = p.class_lists()
+    for w in subset:
+        for j in range(2):
+            assert np.array_equal(cl[w][j], a.class_lists[w][j]), (w, j)
+    offs, hold = p.holders()
+    p.close()
+    keep = np.isin(hold[:, 0], subset)
+    owner = np.repeat(np.arange(F, dtype=np.int64), np.diff(offs.astype(np.int64)))
+    sub_offs = np.zeros(F + 1, np.int64)
+    sub_offs[1:] = np.cumsum(np.bincount(owner[keep], minlength=F))
+    assert np.array_equal(sub_offs, a.holder_offsets.astype(np.int64))
+    assert np.array_equal(hold[keep], a.holders)
