@@ -364,4 +364,104 @@ void first_fit_pass(cudaStream_t s, const uint64_t* seg_begin, const uint64_t* s
     ff_expand_kernel<<<g, kThreads, 0, s>>>(tm, seg_begin, seg_len, ch, taken);
 }
 
+
+// ---- rejects of a pass, in order, for the next class (stable compaction) ----------------
+__global__ void __launch_bounds__(kThreads) rej_count_kernel(TileMap tm,
+                                                              const uint64_t* __restrict__ seg_begin,
+                                                              const uint64_t* __restrict__ seg_len,
+                                                              const uint8_t* __restrict__ taken,
+                                                              uint32_t* __restrict__ cnt) {
+    __shared__ uint32_t ws[kThreads / 32];
+    for (uint64_t t = blockIdx.x; t < tm.max_tiles; t += gridDim.x) {
+        const uint32_t seg = tm.tile_seg[t];
+        if (seg == kNone) {
+            if (threadIdx.x == 0) cnt[t] = 0;
+            continue;
+        }
+        const uint64_t off = (t - tm.tile_base[seg]) * (uint64_t)tm.tile;
+        const uint64_t L = seg_len[seg];
+        const uint64_t n = L - off < tm.tile ? L - off : tm.tile;
+        const uint8_t* p = taken + seg_begin[seg] + off;
+        uint32_t c = 0;
+        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) c += p[i] == 0;
+        c = warp_sum(c);
+        if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = c;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t s = 0;
+            for (int i = 0; i < kThreads / 32; ++i) s += ws[i];
+            cnt[t] = s;
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) rej_write_kernel(
+    TileMap tm, const uint64_t* __restrict__ seg_begin, const uint64_t* __restrict__ seg_len,
+    const uint8_t* __restrict__ taken, const uint32_t* __restrict__ seq_idx,
+    const uint64_t* __restrict__ base, const double* __restrict__ sorted_size,
+    uint64_t out0, uint32_t* __restrict__ out_idx, double* __restrict__ out_sz) {
+    __shared__ uint32_t ws[kThreads / 32];
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (uint64_t t = blockIdx.x; t < tm.max_tiles; t += gridDim.x) {
+        const uint32_t seg = tm.tile_seg[t];
+        if (seg == kNone) break;
+        const uint64_t off = (t - tm.tile_base[seg]) * (uint64_t)tm.tile;
+        const uint64_t L = seg_len[seg];
+        const uint64_t n = L - off < tm.tile ? L - off : tm.tile;
+        const uint64_t g = seg_begin[seg] + off;
+        uint64_t o = out0 + base[t];
+        for (uint32_t r0 = 0; r0 < n; r0 += blockDim.x) {
+            const uint32_t i = r0 + threadIdx.x;
+            const bool rej = i < n && taken[g + i] == 0;
+            const uint32_t bal = __ballot_sync(0xffffffffu, rej);
+            if (lane == 0) ws[warp] = __popc(bal);
+            __syncthreads();
+            uint32_t below = 0, tot = 0;
+#pragma unroll
+            for (int x = 0; x < kThreads / 32; ++x) {
+                below += x < (int)warp ? ws[x] : 0;
+                tot += ws[x];
+            }
+            if (rej) {
+                const uint64_t pos = o + below + __popc(bal & lanemask_lt());
+                const uint32_t si = seq_idx ? seq_idx[g + i] : (uint32_t)(g + i);
+                out_idx[pos] = si;
+                out_sz[pos] = sorted_size[si];
+            }
+            o += tot;
+            __syncthreads();
+        }
+    }
+}
+
+__global__ void rej_segments_kernel(TileMap tm, const uint64_t* __restrict__ base,
+                                    uint64_t out0, uint64_t* __restrict__ nb,
+                                    uint64_t* __restrict__ nl) {
+    for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < tm.nseg; s += gridDim.x * blockDim.x) {
+        const uint64_t a = base[tm.tile_base[s]], b = base[tm.tile_base[s + 1]];
+        nb[s] = out0 + a;
+        nl[s] = b - a;
+    }
+}
+
+// Rejects (taken == 0) of every segment, stable, into [out0, ...) of out_idx / out_sz;
+// their sorted indices (seq_idx maps pass positions to tier order; null = identity) and
+// sizes.  New segment bounds in nb / nl.
+void compact_rejects(cudaStream_t s, const uint64_t* seg_begin, const uint64_t* seg_len,
+                     uint32_t nseg, uint64_t total, const uint8_t* taken, const uint32_t* seq_idx,
+                     const double* sorted_size, uint64_t out0, uint32_t* out_idx, double* out_sz,
+                     uint64_t* nb, uint64_t* nl, Workspace& ws) {
+    TileMap tm;
+    build_tilemap(s, seg_len, nseg, total, kChunk, tm, ws);
+    uint32_t* cnt = ws.scratch<uint32_t>(tm.max_tiles + 1);
+    uint64_t* base = ws.scratch<uint64_t>(tm.max_tiles + 1);
+    const unsigned g = grid_for(tm.max_tiles, 1, 148u * 64u);
+    rej_count_kernel<<<g, kThreads, 0, s>>>(tm, seg_begin, seg_len, taken, cnt);
+    exclusive_scan(s, cnt, tm.max_tiles, base, ws);
+    rej_write_kernel<<<g, kThreads, 0, s>>>(tm, seg_begin, seg_len, taken, seq_idx, base,
+                                            sorted_size, out0, out_idx, out_sz);
+    rej_segments_kernel<<<grid_for(nseg, kThreads), kThreads, 0, s>>>(tm, base, out0, nb, nl);
+}
+
 }  // namespace clairplan

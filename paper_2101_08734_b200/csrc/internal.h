@@ -82,6 +82,10 @@ void first_fit_pass(cudaStream_t s, const uint64_t* seg_begin, const uint64_t* s
                     uint32_t nseg, uint64_t total, const double* sz, double C, uint8_t* taken,
                     Workspace& ws, unsigned long long* taken_count = nullptr);
 
+void compact_rejects(cudaStream_t s, const uint64_t* seg_begin, const uint64_t* seg_len,
+                     uint32_t nseg, uint64_t total, const uint8_t* taken, const uint32_t* seq_idx,
+                     const double* sorted_size, uint64_t out0, uint32_t* out_idx, double* out_sz,
+                     uint64_t* nb, uint64_t* nl, Workspace& ws);
 void launch_gather_sizes(cudaStream_t s, const uint32_t* order, const uint32_t* cand_k,
                          const double* sizes, uint64_t n, double* out);
 void launch_count_keys(cudaStream_t s, const uint32_t* cand_info, uint64_t n, uint32_t maxc,

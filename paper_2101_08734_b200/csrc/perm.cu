@@ -152,7 +152,7 @@ __device__ __noinline__ void fy_group_mid(uint32_t y, uint32_t a0, uint32_t a1, 
     }
 }
 
-__global__ void __launch_bounds__(kThreads, 6) fy_group_kernel(uint32_t F,
+__global__ void __launch_bounds__(kThreads) fy_group_kernel(uint32_t F,
                                                              const uint32_t* __restrict__ head,
                                                              uint32_t* __restrict__ next,
                                                              uint32_t* __restrict__ q,

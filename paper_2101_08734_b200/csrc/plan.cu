@@ -397,47 +397,42 @@ int first_fit_classes(clairplan_plan* p, const double* ssize, uint8_t* cls) {
     const uint32_t* seq_idx = nullptr;
     const double* seq_sz = ssize;
     const uint8_t* prev_taken = cls;  // class 1 writes its flags straight into cls (0/1)
-    uint64_t remaining = D;
+    uint64_t remaining = D, prev_total = D;
     for (uint32_t j = 1; j <= J; ++j) {
         if (remaining == 0) break;
         uint8_t* taken = cls;
         if (j > 1) {
+            // rejects of the previous class, still in tier order, packed for this class
             taken = need<uint8_t>(p->taken, D, ok);
-            uint32_t* keys = need<uint32_t>(p->keys, D, ok);
-            uint32_t* okeys = need<uint32_t>(p->okeys, D, ok);
-            uint32_t* ib0 = need<uint32_t>(p->vals, D, ok);
-            uint32_t* ib1 = need<uint32_t>(p->ovals, D, ok);
-            double* seqsz = need<double>(p->seqsz, D, ok);
+            uint32_t* ib0 = need<uint32_t>(p->vals, remaining, ok);
+            uint32_t* ib1 = need<uint32_t>(p->ovals, remaining, ok);
+            double* seqsz = need<double>(p->seqsz, remaining, ok);
             if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed (first fit)");
-            uint32_t* in_idx = (j % 2) ? ib0 : ib1;
             uint32_t* out_idx = (j % 2) ? ib1 : ib0;
-            launch_reject_keys(s, prev_taken, D, seq_idx, keys, in_idx);
             const size_t m = ws.mark();
-            TileMap tj;
-            build_tilemap(s, sl, nloc, D, kRadixTile, tj, ws);
-            uint64_t* sc = nullptr;
-            radix_pass(s, tj, sb, sl, keys, in_idx, 0, okeys, out_idx, nullptr, &sc, ws);
             uint64_t* nb = ws.scratch<uint64_t>(2 * (uint64_t)nloc);
-            radix_regions(s, tj, sb, sl, sc, 1, nb, nb + nloc);
+            compact_rejects(s, sb, sl, nloc, prev_total, prev_taken, seq_idx, ssize, 0, out_idx,
+                            seqsz, nb, nb + nloc, ws);
             CK(cudaMemcpyAsync(sb, nb, nloc * 8, cudaMemcpyDeviceToDevice, s));
             CK(cudaMemcpyAsync(sl, nb + nloc, nloc * 8, cudaMemcpyDeviceToDevice, s));
             ws.release(m);
-            launch_gather_seq_sizes(s, out_idx, ssize, sb, sl, nloc, seqsz);
             seq_idx = out_idx;
             seq_sz = seqsz;
-            CK(cudaMemsetAsync(taken, 0, D, s));
-            p->launches += 10;
+            CK(cudaMemsetAsync(taken, 0, remaining, s));
+            p->launches += 7;
         }
         CK(cudaMemsetAsync(cnt, 0, 8, s));
         const size_t m = ws.mark();
-        first_fit_pass(s, sb, sl, nloc, D, seq_sz, p->caps[j - 1], taken, ws, cnt);
+        const uint64_t total = (j == 1) ? D : remaining;
+        first_fit_pass(s, sb, sl, nloc, total, seq_sz, p->caps[j - 1], taken, ws, cnt);
         ws.release(m);
         p->launches += 6;
         if (j > 1) {
-            launch_apply_pass(s, taken, D, seq_idx, nullptr, (uint8_t)j, cls);
+            launch_apply_pass(s, taken, remaining, seq_idx, nullptr, (uint8_t)j, cls);
             ++p->launches;
         }
         prev_taken = taken;
+        prev_total = total;
         if (j < J) {
             unsigned long long t = 0;
             CK(cudaMemcpyAsync(&t, cnt, 8, cudaMemcpyDeviceToHost, s));
