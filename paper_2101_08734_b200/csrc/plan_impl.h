@@ -4,6 +4,8 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <stdlib.h>
+
 #include <algorithm>
 #include <mutex>
 #include <string>
@@ -131,6 +133,18 @@ struct clairplan_plan {
     }
     void mark(int i) {
         if (sev[i]) cudaEventRecord(sev[i], stream);
+        static const bool dbg = [] {
+            const char* e = getenv("CLAIRPLAN_DEBUG_SYNC");
+            return e && e[0] == '1';
+        }();
+        if (dbg) {
+            const cudaError_t err = cudaStreamSynchronize(stream);
+            if (err != cudaSuccess) {
+                fprintf(stderr, "clairplan: CUDA error before stage mark %d: %s\n", i,
+                        cudaGetErrorString(err));
+                abort();
+            }
+        }
     }
 };
 

@@ -103,6 +103,10 @@ class DistributedPlan:
         cp._check(self.L.clairplan_generate_perms(self.plan._h, e0, n,
                                                   C.c_void_p(self.local_rows.data_ptr())))
         perms = gather_rows(self.local_rows[:n], self.ranges, self.pad, self.group)
+        # the gather and the concatenation run on torch's stream; the library reads the rows
+        # on its own stream, so order them (every library call synchronises its own stream
+        # before returning, so the reverse direction needs nothing)
+        torch.cuda.current_stream().synchronize()
         cp._check(self.L.clairplan_build_from_perms(self.plan._h, C.c_void_p(perms.data_ptr())))
         del perms
         cp._check(self.L.clairplan_holder_counts(self.plan._h, C.c_void_p(self.counts.data_ptr())))

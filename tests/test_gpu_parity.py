@@ -271,6 +271,7 @@ def test_build_from_perms_matches_build(cp, ref):
         rows = torch.empty((E, F), dtype=torch.int32, device="cuda")
         cp._check(L.clairplan_generate_perms(b._h, 0, 4, C.c_void_p(rows.data_ptr())))
         cp._check(L.clairplan_generate_perms(b._h, 4, E - 4, C.c_void_p(rows[4].data_ptr())))
+        torch.cuda.synchronize()
         for e in (0, 5, 8):
             assert np.array_equal(rows[e].cpu().numpy().astype(np.uint32), ref.epoch_permutation(7, e, F))
         cp._check(L.clairplan_build_from_perms(b._h, C.c_void_p(rows.data_ptr())))
