@@ -137,6 +137,11 @@ int clairplan_build_index(uint32_t num_workers, uint32_t num_classes, uint64_t s
                           const uint32_t* entries, const uint64_t* list_off,
                           uint64_t* offsets_out, uint32_t* holders_out, int device);
 
+/* Re-planning (capacity sweeps): new storage[1..J].capacity_mb for a built handle; reruns
+ * first fit, prefetch orders and holders on the cached streams/tables (simulator.cpp:457-465
+ * rebuilds everything per grid point). */
+int clairplan_reassign(clairplan_t plan, const double* capacities_mb);
+
 /* ---- multi-GPU building blocks (one process per GPU, NCCL between the calls) ---------- */
 /* Permutation rows of epochs [epoch_begin, epoch_begin+count) into a device buffer
  * d_out[count][F] (epoch_permutation for each epoch, rejections resolved). */

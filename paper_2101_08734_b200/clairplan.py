@@ -100,6 +100,7 @@ def lib():
     L.clairplan_assign_from_streams.argtypes = [C.c_uint32, C.c_uint32, u32p, u64p, u32p,
                                                 C.c_uint32, f64p, f64p, C.c_int,
                                                 C.POINTER(C.c_void_p)]
+    L.clairplan_reassign.argtypes = [C.c_void_p, f64p]
     L.clairplan_build_index.argtypes = [C.c_uint32, C.c_uint32, C.c_uint64, u32p, u64p, u64p,
                                         u32p, C.c_int]
     L.clairplan_generate_sizes.argtypes = [C.c_uint64, C.c_double, C.c_double, C.c_int,
@@ -233,6 +234,16 @@ class Plan:
 
     def build(self) -> "Plan":
         _check(lib().clairplan_build(self._h))
+        return self
+
+    def reassign(self, capacities_mb) -> "Plan":
+        """New cache-class capacities on the built plan (sweep re-planning): reruns first fit,
+        prefetch orders and holders only."""
+        caps = np.ascontiguousarray(capacities_mb, np.float64)
+        if len(caps) != self.J:
+            raise ValueError("the number of cache classes is fixed at creation")
+        self._caps = caps
+        _check(lib().clairplan_reassign(self._h, _p(caps, f64p) if len(caps) else None))
         return self
 
     def stats(self) -> dict:

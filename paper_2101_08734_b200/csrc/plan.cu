@@ -443,6 +443,99 @@ int first_fit_classes(clairplan_plan* p, const double* ssize, uint8_t* cls) {
     return 0;
 }
 
+
+// K6-K8 of the v2 path on the cached tier-ordered sizes / block masks: first fit, block class
+// records, class lists, holder CSR.  Also the whole of clairplan_reassign.
+int assign_v2(clairplan_plan* p) {
+    cudaStream_t s = p->stream;
+    const Part& part = p->part;
+    const uint32_t F = part.F, E = part.E, nloc = p->nloc, J = p->cfg.num_classes;
+    const uint32_t MB = p->v2_mb;
+    const uint64_t nblk = p->v2_nblk;
+    const uint64_t D = p->D;
+    uint32_t np = 0;
+    while ((1u << np) <= J) ++np;
+    bool ok = true;
+    uint32_t* stream_buf = p->stream_buf.get<uint32_t>();
+    uint32_t* inv = p->inv.get<uint32_t>();
+    uint16_t* rank16 = p->rank16.get<uint16_t>();
+    uint64_t* poff = p->pair_off.get<uint64_t>();
+    uint32_t* bmask = p->blkmask.get<uint32_t>();
+    uint32_t* bbase = p->blkbase.get<uint32_t>();
+    uint32_t* dest = p->dest.get<uint32_t>();
+    double* ssize = p->sorted_size.get<double>();
+    uint8_t* cls = need<uint8_t>(p->cand_cls, D, ok);
+    uint32_t* htmp = need<uint32_t>(p->holders_tmp, 3 * D, ok);
+    uint32_t* centries = need<uint32_t>(p->class_entries, D, ok);
+    const uint32_t Rp = ((np + J) + 3) & ~3u;
+    uint32_t* rec = need<uint32_t>(p->planes, (uint64_t)std::max<uint32_t>(Rp, 4) * nblk, ok);
+    uint32_t* cbase = need<uint32_t>(p->cbase, (uint64_t)nloc * std::max<uint32_t>(J, 1), ok);
+    uint32_t* ccount = need<uint32_t>(p->ccount, std::max<uint32_t>(J, 1) * nblk, ok);
+    uint64_t* cpre = need<uint64_t>(p->cpre, std::max<uint32_t>(J, 1) * (nblk + 1), ok);
+    uint64_t* clen = need<uint64_t>(p->class_len, (uint64_t)nloc * std::max<uint32_t>(J, 1), ok);
+    uint64_t* cstart = need<uint64_t>(p->class_start, (uint64_t)nloc * std::max<uint32_t>(J, 1) + 1, ok);
+    if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed (tier assignment)");
+    if (J > 0) {
+        // K6: first fit class by class
+        if (int rc = first_fit_classes(p, ssize, cls)) return rc;
+        p->mark(6);
+        // K7: block class records, class lists
+        launch_blk_codes(s, part, MB, bmask, bbase, dest, cls, np, J, Rp, rec, ccount, nblk);
+        for (uint32_t j = 0; j < J; ++j)
+            exclusive_scan(s, ccount + (uint64_t)j * nblk, nblk, cpre + (uint64_t)j * (nblk + 1), p->ws);
+        launch_rec_fill(s, cpre, nblk, np, J, Rp, rec, nloc, E, MB, cbase);
+        launch_class_lens(s, nloc, E, MB, J, cpre, nblk, clen);
+        exclusive_scan(s, clen, (uint64_t)nloc * J, cstart, p->ws);
+        launch_class_write(s, part, MB, stream_buf, rec, np, J, Rp, cbase, cstart, centries, nblk);
+        p->launches += 4 + 3 * J + 3;
+        std::vector<uint64_t> hlen((size_t)nloc * J), hst((size_t)nloc * J);
+        CK(cudaMemcpyAsync(hlen.data(), clen, hlen.size() * 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(hst.data(), cstart, hst.size() * 8, cudaMemcpyDeviceToHost, s));
+        p->mark(7);
+        // K8: holder CSR, sample-major
+        launch_holder_tile(s, part, inv, rank16, MB, rec, np, J, Rp, cbase, poff, htmp);
+        ++p->launches;
+        CK(cudaStreamSynchronize(s));
+        p->class_start_h.assign((size_t)nloc * (J + 1), 0);
+        p->class_len_h.assign((size_t)nloc * (J + 1), 0);
+        uint64_t H = 0;
+        for (uint32_t w = 0; w < nloc; ++w)
+            for (uint32_t j = 0; j < J; ++j) {
+                p->class_start_h[(size_t)w * (J + 1) + j] = hst[(size_t)w * J + j];
+                p->class_len_h[(size_t)w * (J + 1) + j] = hlen[(size_t)w * J + j];
+                H += hlen[(size_t)w * J + j];
+            }
+        p->H = H;
+        if (H == D) {
+            p->holder_off_dev = poff;
+            p->holders_dev = htmp;
+        } else {
+            uint32_t* hc = need<uint32_t>(p->hcount, F, ok);
+            uint64_t* ho = need<uint64_t>(p->hoff, (uint64_t)F + 1, ok);
+            uint32_t* hl = need<uint32_t>(p->holders, 3 * std::max<uint64_t>(H, 1), ok);
+            if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed (holders)");
+            launch_holder_count(s, poff, F, htmp, hc);
+            exclusive_scan(s, hc, F, ho, p->ws);
+            launch_holder_compact(s, poff, F, htmp, ho, hl);
+            p->launches += 5;
+            p->holder_off_dev = ho;
+            p->holders_dev = hl;
+        }
+    } else {
+        p->H = 0;
+        uint64_t* ho = need<uint64_t>(p->hoff, (uint64_t)F + 1, ok);
+        if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed");
+        CK(cudaMemsetAsync(ho, 0, ((uint64_t)F + 1) * 8, s));
+        p->holder_off_dev = ho;
+        p->holders_dev = nullptr;
+        p->class_start_h.assign(nloc, 0);
+        p->class_len_h.assign(nloc, 0);
+        p->mark(6);
+        p->mark(7);
+    }
+    return 0;
+}
+
 int build_seed_path_v2(clairplan_plan* p, const uint32_t* ext_perms) {
     cudaStream_t s = p->stream;
     const Part& part = p->part;
@@ -533,64 +626,9 @@ int build_seed_path_v2(clairplan_plan* p, const uint32_t* ext_perms) {
         p->launches += 2;
         p->mark(4);
         p->mark(5);
-        if (J > 0) {
-            // K6: first fit class by class
-            if (int rc = first_fit_classes(p, ssize, cls)) return rc;
-            p->mark(6);
-            // K7: block class records, class lists
-            launch_blk_codes(s, part, MB, bmask, bbase, dest, cls, np, J, Rp, rec, ccount, nblk);
-            for (uint32_t j = 0; j < J; ++j)
-                exclusive_scan(s, ccount + (uint64_t)j * nblk, nblk, cpre + (uint64_t)j * (nblk + 1), p->ws);
-            launch_rec_fill(s, cpre, nblk, np, J, Rp, rec, nloc, E, MB, cbase);
-            launch_class_lens(s, nloc, E, MB, J, cpre, nblk, clen);
-            exclusive_scan(s, clen, (uint64_t)nloc * J, cstart, p->ws);
-            launch_class_write(s, part, MB, stream_buf, rec, np, J, Rp, cbase, cstart, centries, nblk);
-            p->launches += 4 + 3 * J + 3;
-            std::vector<uint64_t> hlen((size_t)nloc * J), hst((size_t)nloc * J);
-            CK(cudaMemcpyAsync(hlen.data(), clen, hlen.size() * 8, cudaMemcpyDeviceToHost, s));
-            CK(cudaMemcpyAsync(hst.data(), cstart, hst.size() * 8, cudaMemcpyDeviceToHost, s));
-            p->mark(7);
-            // K8: holder CSR, sample-major
-            launch_holder_tile(s, part, inv, rank16, MB, rec, np, J, Rp, cbase, poff, htmp);
-            ++p->launches;
-            CK(cudaStreamSynchronize(s));
-            p->class_start_h.assign((size_t)nloc * (J + 1), 0);
-            p->class_len_h.assign((size_t)nloc * (J + 1), 0);
-            uint64_t H = 0;
-            for (uint32_t w = 0; w < nloc; ++w)
-                for (uint32_t j = 0; j < J; ++j) {
-                    p->class_start_h[(size_t)w * (J + 1) + j] = hst[(size_t)w * J + j];
-                    p->class_len_h[(size_t)w * (J + 1) + j] = hlen[(size_t)w * J + j];
-                    H += hlen[(size_t)w * J + j];
-                }
-            p->H = H;
-            if (H == D) {
-                p->holder_off_dev = poff;
-                p->holders_dev = htmp;
-            } else {
-                uint32_t* hc = need<uint32_t>(p->hcount, F, ok);
-                uint64_t* ho = need<uint64_t>(p->hoff, (uint64_t)F + 1, ok);
-                uint32_t* hl = need<uint32_t>(p->holders, 3 * std::max<uint64_t>(H, 1), ok);
-                if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed (holders)");
-                launch_holder_count(s, poff, F, htmp, hc);
-                exclusive_scan(s, hc, F, ho, p->ws);
-                launch_holder_compact(s, poff, F, htmp, ho, hl);
-                p->launches += 5;
-                p->holder_off_dev = ho;
-                p->holders_dev = hl;
-            }
-        } else {
-            p->H = 0;
-            uint64_t* ho = need<uint64_t>(p->hoff, (uint64_t)F + 1, ok);
-            if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed");
-            CK(cudaMemsetAsync(ho, 0, ((uint64_t)F + 1) * 8, s));
-            p->holder_off_dev = ho;
-            p->holders_dev = nullptr;
-            p->class_start_h.assign(nloc, 0);
-            p->class_len_h.assign(nloc, 0);
-            p->mark(6);
-            p->mark(7);
-        }
+        p->v2_mb = MB;
+        p->v2_nblk = nblk;
+        if (int rc = assign_v2(p)) return rc;
         p->mark(clairplan_plan::kStages);
         CK(cudaEventRecord(p->ev1, s));
         CK(cudaEventSynchronize(p->ev1));
@@ -907,6 +945,29 @@ int clairplan_holder_counts(clairplan_t p, uint32_t* d_out) {
     if (p->cfg.num_classes == 0) CK(cudaMemsetAsync(d_out, 0, (size_t)F * 4, p->stream));
     else CK(cudaMemcpyAsync(d_out, src, (size_t)F * 4, cudaMemcpyDeviceToDevice, p->stream));
     CK(cudaStreamSynchronize(p->stream));
+    return 0;
+}
+
+// Re-planning for capacity sweeps: same streams and tier order, new
+// capacities -> rerun only first fit, class lists and holders (the reference rebuilds the
+// whole assignment per grid point, simulator.cpp:457-465 -> policies.cpp:449-454).
+int clairplan_reassign(clairplan_t p, const double* capacities_mb) {
+    if (!p || !p->built || p->generic) return fail(CLAIRPLAN_EINVAL, "plan not built");
+    if (!p->v2) return fail(CLAIRPLAN_EINVAL, "re-planning needs the v2 device path");
+    if (p->cfg.num_classes && !capacities_mb) return fail(CLAIRPLAN_EINVAL, "null capacities");
+    CK(cudaSetDevice(p->device));
+    p->caps.assign(capacities_mb, capacities_mb + p->cfg.num_classes);
+    p->ws.used = 0;
+    p->launches = 0;
+    CK(cudaEventRecord(p->ev0, p->stream));
+    if (int rc = assign_v2(p)) return rc;
+    CK(cudaEventRecord(p->ev1, p->stream));
+    CK(cudaEventSynchronize(p->ev1));
+    CK(cudaGetLastError());
+    if (p->ws.overflow) return fail(CLAIRPLAN_ENOMEM, "internal workspace overflow");
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
+    p->device_ms = ms;
     return 0;
 }
 

@@ -116,6 +116,8 @@ struct clairplan_plan {
     DevBuf cand_w, dfirst, dcounts;  // explicit-stream (generic) path
     DevBuf inv, info16, rank16, cbase, seghist, sorted_base, blkmask, blkbase, planes, ccount, cpre, hard;
     bool v2 = false;                 // fast seed path in use for the last build
+    uint32_t v2_mb = 0;              // blocks per segment / total blocks of the last v2 build
+    uint64_t v2_nblk = 0;
     uint32_t maxcount = 0;           // generic path: largest frequency value
     Workspace ws;
 

@@ -180,6 +180,21 @@ def test_generic_assign_matches_reference(cp, ref):
         assert plans_equal(r, got, check_streams=False) is None
 
 
+def test_reassign_matches_fresh_plans(cp, ref):
+    """Capacity sweep: one build, then reassign per grid point == a fresh
+    reference plan with those capacities."""
+    F, N, B, E = 20_000, 8, 256, 12
+    sizes = ref.generate_sizes(F, 0.1077, 0.2, None, 1)
+    p = cp.Plan(11, F, cp.PartitionSpec(N, B, E, True), [100.0, 400.0], sizes).build()
+    for caps in ([100.0, 400.0], [30.0, 60.0], [1e6, 1.0], [0.05, 0.2], [250.0, 90.0]):
+        p.reassign(caps)
+        offs, hold = p.holders()
+        got = OPlan(N, 2, [p.stream(w) for w in range(N)], p.class_lists(), offs, hold)
+        want = ref.plan(11, F, N, B, E, True, caps, sizes)
+        assert plans_equal(want, got) is None, caps
+    p.close()
+
+
 def test_build_index_matches_device_csr(cp, ref):
     sizes = ref.generate_sizes(3000, 0.1, 0.1, None, 1)
     p = cp.Plan(5, 3000, cp.PartitionSpec(6, 60, 12, True), [30.0, 100.0], sizes).build()
