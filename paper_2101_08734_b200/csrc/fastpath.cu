@@ -41,7 +41,8 @@ __global__ void __launch_bounds__(128) sample_lanes_kernel(Part part, const uint
                                                            uint16_t* __restrict__ info,
                                                            uint16_t* __restrict__ rank16,
                                                            uint32_t* __restrict__ pair_count,
-                                                           uint32_t W) {
+                                                           uint32_t W,
+                                                           uint32_t* __restrict__ seghist) {
     extern __shared__ uint32_t sm[];
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t E = part.E, F = part.F;
@@ -105,6 +106,8 @@ __global__ void __launch_bounds__(128) sample_lanes_kernel(Part part, const uint
                     const uint32_t r = pre[wd] + __popc(bm[wd] & ((1u << (wl & 31)) - 1u));
                     c = cnt[r * 32 + lane];
                     rk = (uint16_t)r;
+                    // per-(worker, epoch) segment histogram of first accesses by count
+                    if (seghist) atomicAdd(&seghist[((uint64_t)wl * E + (E - c)) * E + e], 1u);
                 }
                 __stcs(info + (size_t)e * F + k, c);
                 __stcs(rank16 + (size_t)e * F + k, rk);
@@ -123,7 +126,8 @@ __global__ void __launch_bounds__(128) sample_hash_kernel(Part part, const uint3
                                                           uint32_t* __restrict__ pair_count,
                                                           const uint32_t* __restrict__ list,
                                                           const uint32_t* __restrict__ nlist,
-                                                          uint32_t hs, uint32_t W) {
+                                                          uint32_t hs, uint32_t W,
+                                                          uint32_t* __restrict__ seghist) {
     extern __shared__ uint32_t sm[];
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint32_t* keys = sm + warp * (2 * hs + 2 * W);
@@ -204,6 +208,7 @@ __global__ void __launch_bounds__(128) sample_hash_kernel(Part part, const uint3
                     if ((v >> 16) == e) {
                         out = (uint16_t)(v & 0xFFFFu);
                         rk = (uint16_t)(pre[w >> 5] + __popc(bm[w >> 5] & ((1u << (w & 31)) - 1u)));
+                        if (seghist) atomicAdd(&seghist[((uint64_t)w * E + (E - out)) * E + e], 1u);
                     }
                 }
             }
@@ -270,6 +275,24 @@ __global__ void __launch_bounds__(kThreads) seg_hist_kernel(Part part, const uin
         if (lane == 0) segcnt[(uint64_t)wl * E + e] = tot;
         __syncwarp();
     }
+}
+
+// per-segment first-access totals from the segment histograms (sum over count values)
+__global__ void segcnt_kernel(uint32_t nloc, uint32_t E, const uint32_t* __restrict__ seghist,
+                              uint32_t* __restrict__ segcnt) {
+    for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < (uint64_t)nloc * E;
+         x += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t wl = x / E, e = x % E;
+        uint32_t s = 0;
+        for (uint32_t i = 0; i < E; ++i) s += seghist[(wl * E + i) * E + e];
+        segcnt[x] = s;
+    }
+}
+
+void launch_segcnt(cudaStream_t s, uint32_t nloc, uint32_t E, const uint32_t* seghist,
+                   uint32_t* segcnt) {
+    segcnt_kernel<<<grid_for((uint64_t)nloc * E, kThreads), kThreads, 0, s>>>(nloc, E, seghist,
+                                                                              segcnt);
 }
 
 // ---------------------------------------------------------------------------- K4c
@@ -600,19 +623,19 @@ void launch_holder_tile(cudaStream_t s, const Part& part, const uint32_t* inv, c
 }
 
 void launch_sample_lanes(cudaStream_t s, const Part& part, const uint32_t* inv, uint16_t* info,
-                         uint16_t* rank16, uint32_t* pair_count) {
+                         uint16_t* rank16, uint32_t* pair_count, uint32_t* seghist) {
     const uint32_t nloc = part.wend - part.wbegin;
     const uint32_t W = (nloc + 31) / 32;
     const size_t smem = (size_t)4 * (64 * W + 32 * part.E) * 4;
     cudaFuncSetAttribute(sample_lanes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const uint64_t groups = ((uint64_t)part.F + 31) / 32;
     sample_lanes_kernel<<<grid_for(groups, 4, 148u * 8u), 128, smem, s>>>(part, inv, info, rank16,
-                                                                         pair_count, W);
+                                                                         pair_count, W, seghist);
 }
 
 void launch_sample_hash(cudaStream_t s, const Part& part, const uint32_t* inv, uint16_t* info,
                         uint16_t* rank16, uint32_t* pair_count, const uint32_t* list,
-                        const uint32_t* nlist, uint64_t max_items) {
+                        const uint32_t* nlist, uint64_t max_items, uint32_t* seghist) {
     const uint32_t nloc = part.wend - part.wbegin;
     const uint32_t d = part.E < nloc ? part.E : nloc;
     uint32_t hs = 32;
@@ -621,7 +644,7 @@ void launch_sample_hash(cudaStream_t s, const Part& part, const uint32_t* inv, u
     const size_t smem = (size_t)4 * (2 * hs + 2 * W) * 4;
     cudaFuncSetAttribute(sample_hash_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     sample_hash_kernel<<<grid_for(max_items, 4, 148u * 16u), 128, smem, s>>>(
-        part, inv, info, rank16, pair_count, list, nlist, hs, W);
+        part, inv, info, rank16, pair_count, list, nlist, hs, W, seghist);
 }
 
 void launch_seg_hist(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info,

@@ -118,10 +118,12 @@ void launch_stream_hist(cudaStream_t s, const uint32_t* st, uint64_t n, uint32_t
 // v2 seed path (fastpath.cu)
 bool lane_path_ok(const Part& part);
 void launch_sample_lanes(cudaStream_t s, const Part& part, const uint32_t* inv, uint16_t* info,
-                         uint16_t* rank16, uint32_t* pair_count);
+                         uint16_t* rank16, uint32_t* pair_count, uint32_t* seghist);
 void launch_sample_hash(cudaStream_t s, const Part& part, const uint32_t* inv, uint16_t* info,
                         uint16_t* rank16, uint32_t* pair_count, const uint32_t* list,
-                        const uint32_t* nlist, uint64_t max_items);
+                        const uint32_t* nlist, uint64_t max_items, uint32_t* seghist);
+void launch_segcnt(cudaStream_t s, uint32_t nloc, uint32_t E, const uint32_t* seghist,
+                   uint32_t* segcnt);
 void launch_seg_hist(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info,
                      uint32_t* seghist, uint32_t* segcnt);
 void launch_seg_write2(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info,

@@ -581,15 +581,21 @@ int build_seed_path_v2(clairplan_plan* p, const uint32_t* ext_perms) {
         }
         p->mark(1);
         // K4a: per-sample (worker, count, first epoch)
+        // Large F: the segment histograms are accumulated by the sample pass itself (REDs
+        // overlap its latency); small F: a separate warp-per-segment pass is cheaper.
+        const bool red_hist = F >= (1u << 22);
+        uint32_t* hist_out = red_hist ? seghist : nullptr;
+        if (red_hist) CK(cudaMemsetAsync(seghist, 0, NEE * 4, s));
         if (lanes) {
-            launch_sample_lanes(s, part, inv, info, rank16, pcount);
+            launch_sample_lanes(s, part, inv, info, rank16, pcount, hist_out);
         } else {
-            launch_sample_hash(s, part, inv, info, rank16, pcount, nullptr, nullptr, F);
+            launch_sample_hash(s, part, inv, info, rank16, pcount, nullptr, nullptr, F, hist_out);
         }
         exclusive_scan(s, pcount, F, poff, p->ws);
         p->mark(2);
         // K4b: per-segment count histograms -> first-order and tier-order bases
-        launch_seg_hist(s, part, stream_buf, info, seghist, segcnt);
+        if (red_hist) launch_segcnt(s, nloc, E, seghist, segcnt);
+        else launch_seg_hist(s, part, stream_buf, info, seghist, segcnt);
         exclusive_scan(s, seghist, NEE, sbase, p->ws);
         exclusive_scan(s, segcnt, (uint64_t)nloc * E, segoff, p->ws);
         p->mark(3);
