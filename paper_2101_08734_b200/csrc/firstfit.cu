@@ -102,12 +102,19 @@ __device__ __forceinline__ Mono warp_compose(Mono m) {
 
 __device__ __forceinline__ int binade(double r) { return ilogb(r); }
 
+__device__ __forceinline__ double warp_min_d(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
 struct FFChunks {
     double *sum, *mn, *mx, *r0;
     int* k;
     long long *d0, *d1;
     uint8_t* pbits;
     uint8_t* status;  // 0 none taken, 1 all taken, 2 explicit flags
+    uint8_t* segfit;  // per segment: provably everything fits (skip the exact chain)
 };
 
 __global__ void __launch_bounds__(kThreads) ff_stats_kernel(TileMap tm,
@@ -159,16 +166,20 @@ __global__ void __launch_bounds__(kThreads) ff_stats_kernel(TileMap tm,
     }
 }
 
-// one warp per segment: r0[t] = C - (sum of the segment's earlier chunk sums)
-__global__ void ff_prefix_kernel(TileMap tm, double C, FFChunks ch) {
+// one warp per segment: r0[t] = C - (sum of the segment's earlier chunk sums).  When the whole
+// segment's sizes sum (with a generous bound on summation and chain rounding) stays below C,
+// every prefix fits, so `s <= remaining` holds at every step and everything is taken.
+__global__ void ff_prefix_kernel(TileMap tm, const uint64_t* __restrict__ seg_len, double C,
+                                 FFChunks ch) {
     const uint32_t lane = threadIdx.x & 31;
     for (uint32_t seg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; seg < tm.nseg;
          seg += (gridDim.x * blockDim.x) >> 5) {
         const uint64_t tb = tm.tile_base[seg], te = tm.tile_base[seg + 1];
-        double carry = 0;
+        double carry = 0, mn = INFINITY;
         for (uint64_t t0 = tb; t0 < te; t0 += 32) {
             const uint64_t t = t0 + lane;
             const double v = t < te ? ch.sum[t] : 0.0;
+            if (t < te) mn = fmin(mn, ch.mn[t]);
             double incl = v;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -177,6 +188,12 @@ __global__ void ff_prefix_kernel(TileMap tm, double C, FFChunks ch) {
             }
             if (t < te) ch.r0[t] = C - (carry + incl - v);
             carry += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        mn = warp_min_d(mn);
+        if (lane == 0) {
+            const double n = (double)seg_len[seg];
+            const double tol = (n + 1024.0) * fmax(C, carry) * 0x1.0p-48;
+            ch.segfit[seg] = (mn >= 0.0 && C - carry > tol) ? 1 : 0;
         }
     }
 }
@@ -190,6 +207,7 @@ __global__ void __launch_bounds__(kThreads) ff_agg_kernel(TileMap tm,
     for (uint64_t t = blockIdx.x; t < tm.max_tiles; t += gridDim.x) {
         const uint32_t seg = tm.tile_seg[t];
         if (seg == kNone) break;
+        if (ch.segfit[seg]) continue;  // block-uniform: whole segment fits
         const uint64_t off = (t - tm.tile_base[seg]) * (uint64_t)tm.tile;
         const uint64_t L = seg_len[seg];
         const uint64_t n = L - off < tm.tile ? L - off : tm.tile;
@@ -262,6 +280,11 @@ __global__ void ff_resolve_kernel(TileMap tm, const uint64_t* __restrict__ seg_b
         uint8_t* flags = taken + seg_begin[seg];
         double r = C;
         unsigned long long ntaken = 0;
+        if (ch.segfit[seg]) {
+            for (uint64_t t = tb + lane; t < te; t += 32) ch.status[t] = 1;
+            if (lane == 0 && taken_count && L) atomicAdd(taken_count, (unsigned long long)L);
+            continue;
+        }
         for (uint64_t t = tb; t < te; ++t) {
             const uint64_t off = (t - tb) * (uint64_t)tm.tile;
             if (r < ch.mn[t]) {
@@ -354,9 +377,10 @@ void first_fit_pass(cudaStream_t s, const uint64_t* seg_begin, const uint64_t* s
     ch.d1 = ws.scratch<long long>(m);
     ch.pbits = ws.scratch<uint8_t>(m);
     ch.status = ws.scratch<uint8_t>(m);
+    ch.segfit = ws.scratch<uint8_t>(nseg + 1);
     const unsigned g = grid_for(m, 1, 148u * 64u);
     ff_stats_kernel<<<g, kThreads, 0, s>>>(tm, seg_begin, seg_len, sz, ch);
-    ff_prefix_kernel<<<grid_for((uint64_t)nseg * 32, kThreads), kThreads, 0, s>>>(tm, C, ch);
+    ff_prefix_kernel<<<grid_for((uint64_t)nseg * 32, kThreads), kThreads, 0, s>>>(tm, seg_len, C, ch);
     ff_agg_kernel<<<g, kThreads, 0, s>>>(tm, seg_begin, seg_len, sz, C, ch);
     ff_resolve_kernel<<<grid_for((uint64_t)nseg * 32, 128), 128, 0, s>>>(tm, seg_begin, seg_len,
                                                                          sz, C, ch, taken,
