@@ -55,6 +55,26 @@ constexpr uint32_t kRadixTile = 2048;
 void launch_fy_link(cudaStream_t s, uint64_t key, uint32_t F, uint32_t e0, uint32_t ne,
                     uint32_t* head, uint32_t* next, const RejTable& rt, uint32_t* rej_flag,
                     bool detect_only, uint32_t i_limit);
+// bucketed Fisher-Yates resolution (perm_bucket.cu)
+struct FyGeom {
+    uint32_t lgTB = 0, lgTS = 0, NB = 0, NT = 0, cap = 0;
+};
+bool fy_geometry(uint32_t F, FyGeom& g);
+void launch_fyb(cudaStream_t s, uint64_t key, const Part& part, uint32_t e0, uint32_t ne,
+                const FyGeom& g, const RejTable& rt, uint32_t* rej_flag, uint32_t* bucket,
+                uint32_t* lst, uint32_t* pool, uint32_t* pool_used, uint32_t* succ, uint32_t* q,
+                uint32_t* inv, uint32_t* stream, uint32_t* perm_out);
+
+void launch_fy_table(cudaStream_t s, uint64_t key, uint32_t F, uint32_t e0, uint32_t ne,
+                     uint4* tbl, uint32_t* ovh, uint32_t* ovn, const RejTable& rt,
+                     uint32_t* rej_flag);
+void launch_fy_qmin(cudaStream_t s, uint32_t F, uint32_t ne, const uint4* tbl, const uint32_t* ovh,
+                    const uint32_t* ovn, uint32_t* q);
+void launch_fy_out(cudaStream_t s, const Part& part, uint32_t e0, uint32_t ne, uint4* tbl,
+                   uint32_t* ovh, const uint32_t* ovn, const uint32_t* q, uint32_t* inv,
+                   uint32_t* stream, uint32_t* perm_out);
+void launch_fy_succ(cudaStream_t s, uint32_t F, uint32_t ne, uint4* tbl, uint32_t* ovh,
+                    const uint32_t* ovn, uint32_t* succ, uint32_t* q);
 void launch_fy_group(cudaStream_t s, uint32_t F, uint32_t ne, const uint32_t* head,
                      uint32_t* next, uint32_t* q, uint32_t* scratch, uint32_t scratch_cap,
                      uint32_t* scratch_used, uint32_t* err);

@@ -1,0 +1,443 @@
+// K1-K3, bucketed resolution (default): the same parallel Fisher-Yates resolution as
+// perm.cu (rng.cpp:15-24, access.cpp:52-57), with the grouping of steps by target done in
+// shared memory instead of with global atomics and linked-list walks.
+//
+//   fyb_tile  (per tile of TS steps)  draw j_i, counting-sort the tile's steps by target
+//             block (TB targets) in shared memory and write them tile-major:
+//             bucket[t*TS + lst[t][b] ...] = (i - t*TS) << lgTB | (j_i mod TB)
+//   fyb_block (per target block)      gather the block's runs from every tile, sort by
+//             target (shared-memory counting sort + per-target insertion sort) and write
+//             q[y] = smallest writer != y, succ[w_k] = w_{k+1} (the last writer keeps none:
+//             its value is its own draw) and inv[y] = w_m for every target with a writer
+//   fyb_emit  (per step)              out[i] = V(succ(i)) (chase through q) or j_i; writes
+//             the worker-stream slot, the permutation row and inv of the chase roots (the
+//             values no step wrote: V's roots are exactly those).
+// Geometry (fy_geometry): TB, TS powers of two with NT*NB cells ~ F/4..F so the runs stay
+// a few elements long; valid for F < 2^31 and NB <= kMaxBlocks (else perm.cu's lists path).
+#include "internal.h"
+
+namespace clairplan {
+
+constexpr uint32_t kTileThreads = 512;
+constexpr uint32_t kBlockThreads = 256;
+constexpr uint32_t kMaxBlocks = 24576;
+constexpr uint32_t kMaxTiles = 4096;
+
+bool fy_geometry(uint32_t F, FyGeom& g) {
+    if (F < 2 || F >= 0x80000000u) return false;
+    uint32_t lgTB = 8;
+    while (lgTB < 12 && (1ull << lgTB) * 2048 < F) ++lgTB;
+    const uint64_t TB = 1ull << lgTB;
+    uint32_t lgTS = 13;
+    while ((1ull << lgTS) * TB < 4ull * F) ++lgTS;
+    if (lgTS + lgTB > 31) return false;
+    g.lgTB = lgTB;
+    g.lgTS = lgTS;
+    g.NB = (uint32_t)((F + TB - 1) >> lgTB);
+    g.NT = (uint32_t)((F + (1ull << lgTS) - 1) >> lgTS);
+    if (g.NB > kMaxBlocks || g.NT > kMaxTiles) return false;
+    // shared-memory capacity of a block's writers (larger blocks use the global pool)
+    g.cap = lgTB <= 10 ? 3072 : 4096;
+    return true;
+}
+
+// In-place exclusive scan of a[0..n) in shared memory (all T threads call); returns the total.
+template <uint32_t T>
+__device__ uint32_t smem_exscan(uint32_t* a, uint32_t n, uint32_t* wsum) {
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t per = (n + T - 1) / T;
+    const uint32_t beg = min(n, tid * per), end = min(n, beg + per);
+    uint32_t loc = 0;
+    for (uint32_t k = beg; k < end; ++k) loc += a[k];
+    uint32_t inc = loc;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= (uint32_t)d) inc += o;
+    }
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        constexpr uint32_t nw = T >> 5;
+        const uint32_t v = lane < nw ? wsum[lane] : 0;
+        uint32_t x = v;
+#pragma unroll
+        for (int d = 1; d < (int)nw; d <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xffffffffu, x, d);
+            if (lane >= (uint32_t)d) x += o;
+        }
+        if (lane < nw) wsum[lane] = x - v;  // exclusive warp offsets
+        if (lane == nw - 1) wsum[32] = x;   // total
+    }
+    __syncthreads();
+    uint32_t run = wsum[warp] + inc - loc;
+    for (uint32_t k = beg; k < end; ++k) {
+        const uint32_t v = a[k];
+        a[k] = run;
+        run += v;
+    }
+    const uint32_t total = wsum[32];
+    __syncthreads();
+    return total;
+}
+
+// In-place inclusive max-scan of a[0..n) in shared or global memory (all T threads call).
+template <uint32_t T>
+__device__ void block_maxscan(uint32_t* a, uint32_t n, uint32_t* wsum) {
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t per = (n + T - 1) / T;
+    const uint32_t beg = min(n, tid * per), end = min(n, beg + per);
+    uint32_t loc = 0;
+    for (uint32_t k = beg; k < end; ++k) loc = max(loc, a[k]);
+    uint32_t inc = loc;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= (uint32_t)d) inc = max(inc, o);
+    }
+    uint32_t exc = __shfl_up_sync(0xffffffffu, inc, 1);
+    if (lane == 0) exc = 0;
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        constexpr uint32_t nw = T >> 5;
+        const uint32_t v = lane < nw ? wsum[lane] : 0;
+        uint32_t x = v;
+#pragma unroll
+        for (int d = 1; d < (int)nw; d <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xffffffffu, x, d);
+            if (lane >= (uint32_t)d) x = max(x, o);
+        }
+        uint32_t xe = __shfl_up_sync(0xffffffffu, x, 1);
+        if (lane == 0) xe = 0;
+        if (lane < nw) wsum[lane] = xe;  // exclusive max over earlier warps
+    }
+    __syncthreads();
+    uint32_t run = max(wsum[warp], exc);
+    for (uint32_t k = beg; k < end; ++k) {
+        run = max(run, a[k]);
+        a[k] = run;
+    }
+    __syncthreads();
+}
+
+struct FyRej {
+    const uint32_t* st;
+    const uint32_t* cu;
+    uint32_t n;
+    __device__ __forceinline__ FyRej(const RejTable& rt, uint32_t er)
+        : st(rt.step + (size_t)er * rt.cap), cu(rt.cum + (size_t)er * rt.cap), n(rt.count[er]) {}
+    __device__ __forceinline__ uint32_t draw(uint64_t key, uint32_t e, uint32_t F, uint32_t i,
+                                             uint32_t* flag) const {
+        uint32_t extra;
+        const uint32_t j = fy_draw(key, e, F, i, n ? rej_shift(st, cu, n, i) : 0, &extra);
+        if (extra && flag) {
+            bool known = false;
+            for (uint32_t t = 0; t < n; ++t) known |= (st[t] == i);
+            if (!known) atomicMax(flag, i + 1);
+        }
+        return j;
+    }
+};
+
+// ---- fyb_tile: one tile of TS steps -> tile-major bucket runs --------------------------------
+// K > 0: each thread owns K = TS / kTileThreads steps and keeps their draws in registers;
+// K == 0: generic tile size, draws recomputed in the second pass.
+template <int K>
+__global__ void __launch_bounds__(kTileThreads) fyb_tile_kernel(uint64_t key, uint32_t F,
+                                                                uint32_t e0, FyGeom g,
+                                                                RejTable rt,
+                                                                uint32_t* __restrict__ rej_flag,
+                                                                uint32_t* __restrict__ bucket,
+                                                                uint32_t* __restrict__ lst) {
+    extern __shared__ uint32_t sm[];
+    __shared__ uint32_t wsum[33];
+    const uint32_t t = blockIdx.x, slot = blockIdx.y, e = e0 + slot;
+    const uint32_t er = e - rt.e_base;
+    const FyRej rj(rt, er);
+    const uint32_t TS = 1u << g.lgTS;
+    const uint32_t i_lo = t * TS, i_hi = min(F, i_lo + TS);
+    const uint32_t nbt = min(g.NB, ((i_hi - 1) >> g.lgTB) + 1);  // j <= i < i_hi
+    uint32_t* hist = sm;  // [NB + 1]
+    for (uint32_t b = threadIdx.x; b <= nbt; b += kTileThreads) hist[b] = 0;
+    __syncthreads();
+    const uint32_t tbmask = (1u << g.lgTB) - 1;
+    uint32_t jr[K > 0 ? K : 1];
+    if constexpr (K > 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const uint32_t i = i_lo + k * kTileThreads + threadIdx.x;
+            jr[k] = (i < i_hi && i > 0) ? rj.draw(key, e, F, i, rej_flag + er) : kNone;
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+            if (jr[k] != kNone) atomicAdd(&hist[jr[k] >> g.lgTB], 1u);
+    } else {
+        constexpr int U = 8;
+        for (uint32_t i0 = i_lo + threadIdx.x; i0 < i_hi; i0 += U * kTileThreads) {
+            uint32_t j[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t i = i0 + u * kTileThreads;
+                j[u] = (i < i_hi && i > 0) ? rj.draw(key, e, F, i, rej_flag + er) : kNone;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (j[u] != kNone) atomicAdd(&hist[j[u] >> g.lgTB], 1u);
+        }
+    }
+    __syncthreads();
+    smem_exscan<kTileThreads>(hist, nbt + 1, wsum);  // hist[nbt] == 0 before: the tile total
+    uint32_t* row = lst + ((size_t)slot * g.NT + t) * (g.NB + 1);
+    const uint32_t total = hist[nbt];
+    for (uint32_t b = threadIdx.x; b <= g.NB; b += kTileThreads) row[b] = b <= nbt ? hist[b] : total;
+    __syncthreads();
+    if constexpr (K > 0) {  // stage the sorted tile in shared memory, then a coalesced copy-out
+        uint32_t* stage = sm + g.NB + 2;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            if (jr[k] == kNone) continue;
+            const uint32_t pos = atomicAdd(&hist[jr[k] >> g.lgTB], 1u);
+            stage[pos] = ((k * kTileThreads + threadIdx.x) << g.lgTB) | (jr[k] & tbmask);
+        }
+        __syncthreads();
+        uint32_t* out = bucket + (size_t)slot * F + i_lo;
+        for (uint32_t k = threadIdx.x; k < total; k += kTileThreads) __stcg(out + k, stage[k]);
+    } else {  // scatter straight into the tile's window (L2 merges the sectors)
+        uint32_t* out = bucket + (size_t)slot * F + i_lo;
+        constexpr int U = 8;
+        for (uint32_t i0 = i_lo + threadIdx.x; i0 < i_hi; i0 += U * kTileThreads) {
+            uint32_t j[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t i = i0 + u * kTileThreads;
+                j[u] = (i < i_hi && i > 0) ? rj.draw(key, e, F, i, nullptr) : kNone;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (j[u] == kNone) continue;
+                const uint32_t i = i0 + u * kTileThreads;
+                const uint32_t pos = atomicAdd(&hist[j[u] >> g.lgTB], 1u);
+                out[pos] = ((i - i_lo) << g.lgTB) | (j[u] & tbmask);
+            }
+        }
+    }
+}
+
+// ---- fyb_block: one block of TB targets -> q, succ, inv ------------------------------------
+// BIG: more writers than the shared-memory capacity (blocks of small targets): W/S/J live in
+// a global pool slab (L2-resident) instead.
+template <bool BIG>
+__device__ __forceinline__ void fyb_block_body(uint32_t F, const FyGeom& g, uint32_t b, uint32_t n,
+                                               uint32_t nt, uint32_t tmin, const uint32_t* tlo,
+                                               const uint32_t* tdst, uint32_t* cnt, uint32_t* W,
+                                               uint32_t* S, uint16_t* JL16, uint32_t* J32,
+                                               uint32_t* wsum, const uint32_t* bk, uint32_t* sc,
+                                               uint32_t* qq, uint32_t* iv) {
+    const uint32_t TB = 1u << g.lgTB, TS = 1u << g.lgTS, tbmask = TB - 1;
+    // owner run of every element: mark run starts, then a max-scan (S is free until the
+    // scatter below)
+    for (uint32_t k = threadIdx.x; k < n; k += kBlockThreads) S[k] = 0;
+    __syncthreads();
+    for (uint32_t k = threadIdx.x; k < nt; k += kBlockThreads)
+        if (tdst[k + 1] > tdst[k]) S[tdst[k]] = k;
+    __syncthreads();
+    block_maxscan<kBlockThreads>(S, n, wsum);
+    // gather: thread per element, consecutive elements mostly share a run (coalesced)
+    for (uint32_t k = threadIdx.x; k < n; k += kBlockThreads) {
+        const uint32_t r = S[k], t = tmin + r;
+        const uint32_t v = __ldcs(bk + (size_t)t * TS + tlo[r] + (k - tdst[r]));
+        const uint32_t jl = v & tbmask;
+        W[k] = t * TS + (v >> g.lgTB);
+        if constexpr (BIG) J32[k] = jl;
+        else JL16[k] = (uint16_t)jl;
+        atomicAdd(&cnt[jl], 1u);
+    }
+    __syncthreads();
+    smem_exscan<kBlockThreads>(cnt, TB + 1, wsum);  // cnt[TB] == 0 before: becomes n
+    // scatter by target; cnt[jl] advances to the end of its group (= start of the next)
+    for (uint32_t k = threadIdx.x; k < n; k += kBlockThreads) {
+        uint32_t jl;
+        if constexpr (BIG) jl = J32[k];
+        else jl = JL16[k];
+        S[atomicAdd(&cnt[jl], 1u)] = W[k];
+    }
+    __syncthreads();
+    const uint32_t y0 = b << g.lgTB;
+    for (uint32_t tt = threadIdx.x; tt < TB; tt += kBlockThreads) {
+        const uint32_t y = y0 + tt;
+        if (y >= F) break;
+        const uint32_t s0 = tt ? cnt[tt - 1] : 0, m = cnt[tt] - s0;
+        uint32_t qv = kNone;
+        if (m == 1) {
+            const uint32_t w = S[s0];
+            if (w != y) qv = w;
+            if (iv) iv[y] = w;
+        } else if (m == 2) {
+            const uint32_t a0 = S[s0], a1 = S[s0 + 1];
+            const uint32_t lo = min(a0, a1), hi = max(a0, a1);
+            qv = lo != y ? lo : hi;
+            sc[lo] = hi;
+            if (iv) iv[y] = hi;
+        } else if (m > 2) {
+            const uint32_t s1 = s0 + m;
+            for (uint32_t a = s0 + 1; a < s1; ++a) {  // short lists: insertion sort
+                const uint32_t v = S[a];
+                uint32_t c = a;
+                while (c > s0 && S[c - 1] > v) {
+                    S[c] = S[c - 1];
+                    --c;
+                }
+                S[c] = v;
+            }
+            const uint32_t w0 = S[s0];
+            qv = w0 != y ? w0 : S[s0 + 1];
+            for (uint32_t a = s0; a + 1 < s1; ++a) sc[S[a]] = S[a + 1];
+            if (iv) iv[y] = S[s1 - 1];  // the last writer places y: out[w_m] = j = y
+        }
+        qq[y] = qv;
+    }
+}
+
+__global__ void __launch_bounds__(kBlockThreads) fyb_block_kernel(uint32_t F, FyGeom g,
+                                                                  const uint32_t* __restrict__ bucket,
+                                                                  const uint32_t* __restrict__ lst,
+                                                                  uint32_t* __restrict__ pool,
+                                                                  uint32_t* __restrict__ pool_used,
+                                                                  uint32_t* __restrict__ succ,
+                                                                  uint32_t* __restrict__ q,
+                                                                  uint32_t e0,
+                                                                  uint32_t* __restrict__ inv) {
+    extern __shared__ uint32_t sm[];
+    __shared__ uint32_t wsum[33];
+    __shared__ uint32_t s_pool;
+    const uint32_t b = blockIdx.x, slot = blockIdx.y;
+    const uint32_t TB = 1u << g.lgTB;
+    const uint32_t tmin = (uint32_t)(((uint64_t)b << g.lgTB) >> g.lgTS);
+    const uint32_t nt = g.NT - tmin;
+    uint32_t* cnt = sm;                 // [TB + 1]
+    uint32_t* tdst = cnt + TB + 1;      // [NT + 1] run offsets within the block
+    uint32_t* tlo = tdst + g.NT + 1;    // [NT] run starts within their tile
+    uint32_t* W = tlo + g.NT;           // [cap]  writer step
+    uint32_t* S = W + g.cap;            // [cap]  owner run, then writers grouped by target
+    uint16_t* JL = reinterpret_cast<uint16_t*>(S + g.cap);  // [cap] target within block
+    const uint32_t* rows = lst + (size_t)slot * g.NT * (g.NB + 1);
+    for (uint32_t k = threadIdx.x; k <= TB; k += kBlockThreads) cnt[k] = 0;
+    for (uint32_t k = threadIdx.x; k < nt; k += kBlockThreads) {
+        const uint32_t* r = rows + (size_t)(tmin + k) * (g.NB + 1) + b;
+        const uint32_t lo = r[0];
+        tlo[k] = lo;
+        tdst[k] = r[1] - lo;
+    }
+    if (threadIdx.x == 0) tdst[nt] = 0;
+    __syncthreads();
+    const uint32_t n = smem_exscan<kBlockThreads>(tdst, nt + 1, wsum);
+    const uint32_t* bk = bucket + (size_t)slot * F;
+    uint32_t* sc = succ + (size_t)slot * F;
+    uint32_t* qq = q + (size_t)slot * F;
+    uint32_t* iv = inv ? inv + (size_t)(e0 + slot) * F : nullptr;
+    if (n <= g.cap) {
+        fyb_block_body<false>(F, g, b, n, nt, tmin, tlo, tdst, cnt, W, S, JL, nullptr, wsum, bk,
+                              sc, qq, iv);
+    } else {  // heavy block (small targets): global pool slab
+        if (threadIdx.x == 0) s_pool = atomicAdd(pool_used + slot, 3 * n);
+        __syncthreads();
+        uint32_t* gW = pool + (size_t)slot * 3 * F + s_pool;
+        fyb_block_body<true>(F, g, b, n, nt, tmin, tlo, tdst, cnt, gW, gW + n, nullptr,
+                             gW + 2 * n, wsum, bk, sc, qq, iv);
+    }
+}
+
+// ---- fyb_emit: per step, chase and write --------------------------------------------------
+__global__ void __launch_bounds__(kThreads) fyb_emit_kernel(uint64_t key, Part part, uint32_t e0,
+                                                            RejTable rt,
+                                                            const uint32_t* __restrict__ succ,
+                                                            const uint32_t* __restrict__ q,
+                                                            uint32_t* __restrict__ inv,
+                                                            uint32_t* __restrict__ stream,
+                                                            uint32_t* __restrict__ perm_out) {
+    const uint32_t slot = blockIdx.y, e = e0 + slot, F = part.F;
+    const FyRej rj(rt, e - rt.e_base);
+    const uint32_t* sc = succ + (size_t)slot * F;
+    const uint32_t* qq = q + (size_t)slot * F;
+    constexpr int U = 4;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < F; i0 += U * stride) {
+        uint32_t cur[U];
+        uint32_t live = 0;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t i = i0 + u * stride;
+            cur[u] = kNone;
+            if (i < F) {
+                const uint32_t s = i ? __ldcs(sc + i) : 0u;
+                if (s == kNone) {
+                    cur[u] = rj.draw(key, e, F, i, nullptr);  // last writer of its target
+                } else {
+                    cur[u] = s;
+                    live |= 1u << u;
+                }
+            }
+        }
+        const uint32_t chased = live;
+        while (live) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (!((live >> u) & 1u)) continue;
+                const uint32_t nq = qq[cur[u]];
+                if (nq == kNone) live &= ~(1u << u);
+                else cur[u] = nq;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t i = i0 + u * stride;
+            if (i >= F) break;
+            const uint32_t v = cur[u];
+            if (perm_out) perm_out[(size_t)slot * F + i] = v;
+            // values with a writer got inv from fyb_block; chase roots have none
+            if (inv && ((chased >> u) & 1u)) inv[(size_t)e * F + v] = i;
+            if (stream && i < part.P) {
+                uint32_t w;
+                uint64_t spos;
+                part.locate(i, e, w, spos);
+                if (w >= part.wbegin && w < part.wend) stream[part.stream_offset(w) + spos] = v;
+            }
+        }
+    }
+}
+
+// ---- launchers --------------------------------------------------------------------------
+size_t fyb_block_smem(const FyGeom& g) {
+    return (size_t)4 * ((1u << g.lgTB) + 1 + 2 * g.NT + 1 + 2 * g.cap) + 2 * (size_t)g.cap;
+}
+
+template <int K>
+void launch_tile(cudaStream_t s, uint64_t key, uint32_t F, uint32_t e0, uint32_t ne,
+                 const FyGeom& g, const RejTable& rt, uint32_t* rej_flag, uint32_t* bucket,
+                 uint32_t* lst) {
+    const size_t sm = (size_t)4 * (g.NB + 2 + (K > 0 ? (1u << g.lgTS) : 0u));
+    cudaFuncSetAttribute(fyb_tile_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    fyb_tile_kernel<K><<<dim3(g.NT, ne), kTileThreads, sm, s>>>(key, F, e0, g, rt, rej_flag,
+                                                                 bucket, lst);
+}
+
+void launch_fyb(cudaStream_t s, uint64_t key, const Part& part, uint32_t e0, uint32_t ne,
+                const FyGeom& g, const RejTable& rt, uint32_t* rej_flag, uint32_t* bucket,
+                uint32_t* lst, uint32_t* pool, uint32_t* pool_used, uint32_t* succ, uint32_t* q,
+                uint32_t* inv, uint32_t* stream, uint32_t* perm_out) {
+    const uint32_t F = part.F;
+    if (g.lgTS == 13) launch_tile<(1 << 13) / kTileThreads>(s, key, F, e0, ne, g, rt, rej_flag, bucket, lst);
+    else if (g.lgTS == 14) launch_tile<(1 << 14) / kTileThreads>(s, key, F, e0, ne, g, rt, rej_flag, bucket, lst);
+    else launch_tile<0>(s, key, F, e0, ne, g, rt, rej_flag, bucket, lst);
+    cudaMemsetAsync(pool_used, 0, ne * sizeof(uint32_t), s);
+    cudaMemsetAsync(succ, 0xFF, (size_t)ne * F * sizeof(uint32_t), s);
+    const size_t sm_block = fyb_block_smem(g);
+    cudaFuncSetAttribute(fyb_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_block);
+    fyb_block_kernel<<<dim3(g.NB, ne), kBlockThreads, sm_block, s>>>(F, g, bucket, lst, pool,
+                                                                      pool_used, succ, q, e0, inv);
+    dim3 grid(grid_for(F, kThreads * 4, 148u * 16u), ne);
+    fyb_emit_kernel<<<grid, kThreads, 0, s>>>(key, part, e0, rt, succ, q, inv, stream, perm_out);
+}
+
+}  // namespace clairplan

@@ -20,8 +20,8 @@ thread_local std::string g_err;
 
 namespace clairplan {
 
-uint32_t epochs_per_batch(uint32_t F, uint32_t E) {
-    const uint64_t per = (uint64_t)F * 12;
+uint32_t epochs_per_batch(uint32_t F, uint32_t E, uint32_t bytes_per_target) {
+    const uint64_t per = (uint64_t)F * bytes_per_target;
     uint64_t budget = 768ull << 20;
     if (const char* env = getenv("CLAIRPLAN_PERM_BUDGET_MB")) budget = strtoull(env, nullptr, 10) << 20;
     uint64_t eb = budget / (per ? per : 1);
@@ -45,8 +45,64 @@ RejTable rej_table(clairplan_plan* p) {
 int enqueue_perms(clairplan_plan* p, uint32_t* stream_out, uint32_t* inv_out, uint32_t* perm_out,
                   uint32_t e_first, uint32_t e_count) {
     const uint32_t F = p->part.F;
-    const uint32_t EB = epochs_per_batch(F, e_count);
     bool ok = true;
+    const RejTable rt = rej_table(p);
+    static const char* mode_env = getenv("CLAIRPLAN_FY");  // "lists" / "table" (A/B only)
+    const std::string mode = mode_env ? mode_env : "bucket";
+    static const bool fy_out_mode = getenv("CLAIRPLAN_FY_OUT") != nullptr;
+    FyGeom g;
+    if (mode == "bucket" && fy_geometry(F, g)) {  // shared-memory bucketed resolution
+        const uint32_t EB = epochs_per_batch(F, e_count, 28);
+        uint32_t* bucket = need<uint32_t>(p->fybucket, (uint64_t)EB * F, ok);
+        uint32_t* lst = need<uint32_t>(p->fylst, (uint64_t)EB * g.NT * (g.NB + 1), ok);
+        uint32_t* pool = need<uint32_t>(p->fypool, (uint64_t)EB * 3 * F, ok);
+        uint32_t* pool_used = need<uint32_t>(p->fypool_used, EB, ok);
+        uint32_t* succ = need<uint32_t>(p->next, (uint64_t)EB * F, ok);
+        uint32_t* q = need<uint32_t>(p->q, (uint64_t)EB * F, ok);
+        if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed (permutation workspace)");
+        for (uint32_t e0 = e_first; e0 < e_first + e_count; e0 += EB) {
+            const uint32_t ne = std::min(EB, e_first + e_count - e0);
+            launch_fyb(p->stream, p->key, p->part, e0, ne, g, rt, p->rej_flag.get<uint32_t>(),
+                       bucket, lst, pool, pool_used, succ, q, inv_out, stream_out,
+                       perm_out ? perm_out + (size_t)(e0 - e_first) * F : nullptr);
+            p->launches += 3;
+        }
+        CK(cudaGetLastError());
+        return 0;
+    }
+    if (mode == "table") {  // slot-table resolution (perm.cu)
+        const uint32_t EB = epochs_per_batch(F, e_count, 32);
+        uint4* tbl = need<uint4>(p->fytbl, (uint64_t)EB * F, ok);
+        uint32_t* ovh = need<uint32_t>(p->fyovh, (uint64_t)EB * F, ok);
+        uint32_t* ovn = need<uint32_t>(p->fyovn, (uint64_t)EB * F, ok);
+        uint32_t* q = need<uint32_t>(p->q, (uint64_t)EB * F, ok);
+        uint32_t* succ = need<uint32_t>(p->next, (uint64_t)EB * F, ok);
+        if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed (permutation workspace)");
+        if (p->fy_clean != p->fytbl.p) {
+            CK(cudaMemsetAsync(tbl, 0, p->fytbl.bytes, p->stream));
+            CK(cudaMemsetAsync(ovh, 0xFF, p->fyovh.bytes, p->stream));
+        }
+        p->fy_clean = nullptr;
+        for (uint32_t e0 = e_first; e0 < e_first + e_count; e0 += EB) {
+            const uint32_t ne = std::min(EB, e_first + e_count - e0);
+            launch_fy_table(p->stream, p->key, F, e0, ne, tbl, ovh, ovn, rt,
+                            p->rej_flag.get<uint32_t>());
+            if (fy_out_mode) {
+                launch_fy_qmin(p->stream, F, ne, tbl, ovh, ovn, q);
+                launch_fy_out(p->stream, p->part, e0, ne, tbl, ovh, ovn, q, inv_out, stream_out,
+                              perm_out ? perm_out + (size_t)(e0 - e_first) * F : nullptr);
+            } else {
+                launch_fy_succ(p->stream, F, ne, tbl, ovh, ovn, succ, q);
+                launch_fy_emit(p->stream, p->key, p->part, e0, ne, succ, q, rt, inv_out, stream_out,
+                               perm_out ? perm_out + (size_t)(e0 - e_first) * F : nullptr);
+            }
+            p->launches += 3;
+        }
+        CK(cudaGetLastError());
+        p->fy_clean = p->fytbl.p;  // fy_out empties every entry it used
+        return 0;
+    }
+    const uint32_t EB = epochs_per_batch(F, e_count, 12);
     uint32_t* head = need<uint32_t>(p->head, (uint64_t)EB * F, ok);
     uint32_t* next = need<uint32_t>(p->next, (uint64_t)EB * F, ok);
     uint32_t* q = need<uint32_t>(p->q, (uint64_t)EB * F, ok);
@@ -54,7 +110,6 @@ int enqueue_perms(clairplan_plan* p, uint32_t* stream_out, uint32_t* inv_out, ui
     uint32_t* scratch = need<uint32_t>(p->scratch, scap, ok);
     uint32_t* counters = need<uint32_t>(p->counters, 4, ok);
     if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed (permutation workspace)");
-    const RejTable rt = rej_table(p);
     for (uint32_t e0 = e_first; e0 < e_first + e_count; e0 += EB) {
         const uint32_t ne = std::min(EB, e_first + e_count - e0);
         CK(cudaMemsetAsync(head, 0xFF, (size_t)ne * F * sizeof(uint32_t), p->stream));
