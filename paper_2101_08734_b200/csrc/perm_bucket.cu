@@ -26,7 +26,8 @@ constexpr uint32_t kMaxTiles = 4096;
 bool fy_geometry(uint32_t F, FyGeom& g) {
     if (F < 2 || F >= 0x80000000u) return false;
     uint32_t lgTB = 8;
-    while (lgTB < 12 && (1ull << lgTB) * 2048 < F) ++lgTB;
+    while ((1ull << lgTB) * 2048 < F) ++lgTB;
+    if (lgTB > 11) return false;  // large F: the linked-list path (perm.cu) is faster today
     const uint64_t TB = 1ull << lgTB;
     uint32_t lgTS = 13;
     while ((1ull << lgTS) * TB < 4ull * F) ++lgTS;

@@ -22,12 +22,12 @@ namespace clairplan {
 
 uint32_t epochs_per_batch(uint32_t F, uint32_t E, uint32_t bytes_per_target) {
     const uint64_t per = (uint64_t)F * bytes_per_target;
-    uint64_t budget = 768ull << 20;
+    uint64_t budget = 4096ull << 20;  // B200: 180 GB HBM; whole-run batches fill the GPU
     if (const char* env = getenv("CLAIRPLAN_PERM_BUDGET_MB")) budget = strtoull(env, nullptr, 10) << 20;
     uint64_t eb = budget / (per ? per : 1);
     if (eb < 1) eb = 1;
     if (eb > E) eb = E;
-    if (eb > 64) eb = 64;
+    if (eb > 128) eb = 128;
     return (uint32_t)eb;
 }
 
