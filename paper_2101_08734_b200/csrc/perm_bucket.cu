@@ -233,7 +233,7 @@ __device__ __forceinline__ void fyb_block_body(uint32_t F, const FyGeom& g, uint
                                                uint32_t nt, uint32_t tmin, const uint32_t* tlo,
                                                const uint32_t* tdst, uint32_t* cnt, uint32_t* W,
                                                uint32_t* S, uint16_t* JL16, uint32_t* J32,
-                                               uint32_t* wsum, const uint32_t* bk, uint32_t* sc,
+                                               uint16_t* SJ16, uint32_t* SJ32, uint32_t* wsum, const uint32_t* bk, uint32_t* sc,
                                                uint32_t* qq, uint32_t* iv) {
     const uint32_t TB = 1u << g.lgTB, TS = 1u << g.lgTS, tbmask = TB - 1;
     // owner run of every element: mark run starts, then a max-scan (S is free until the
@@ -261,42 +261,40 @@ __device__ __forceinline__ void fyb_block_body(uint32_t F, const FyGeom& g, uint
         uint32_t jl;
         if constexpr (BIG) jl = J32[k];
         else jl = JL16[k];
-        S[atomicAdd(&cnt[jl], 1u)] = W[k];
+        const uint32_t pos = atomicAdd(&cnt[jl], 1u);
+        S[pos] = W[k];
+        if constexpr (BIG) SJ32[pos] = jl;
+        else SJ16[pos] = (uint16_t)jl;
     }
     __syncthreads();
     const uint32_t y0 = b << g.lgTB;
+    // targets without a writer: q = none
     for (uint32_t tt = threadIdx.x; tt < TB; tt += kBlockThreads) {
         const uint32_t y = y0 + tt;
         if (y >= F) break;
-        const uint32_t s0 = tt ? cnt[tt - 1] : 0, m = cnt[tt] - s0;
-        uint32_t qv = kNone;
-        if (m == 1) {
-            const uint32_t w = S[s0];
-            if (w != y) qv = w;
-            if (iv) iv[y] = w;
-        } else if (m == 2) {
-            const uint32_t a0 = S[s0], a1 = S[s0 + 1];
-            const uint32_t lo = min(a0, a1), hi = max(a0, a1);
-            qv = lo != y ? lo : hi;
-            sc[lo] = hi;
-            if (iv) iv[y] = hi;
-        } else if (m > 2) {
-            const uint32_t s1 = s0 + m;
-            for (uint32_t a = s0 + 1; a < s1; ++a) {  // short lists: insertion sort
-                const uint32_t v = S[a];
-                uint32_t c = a;
-                while (c > s0 && S[c - 1] > v) {
-                    S[c] = S[c - 1];
-                    --c;
-                }
-                S[c] = v;
-            }
-            const uint32_t w0 = S[s0];
-            qv = w0 != y ? w0 : S[s0 + 1];
-            for (uint32_t a = s0; a + 1 < s1; ++a) sc[S[a]] = S[a + 1];
-            if (iv) iv[y] = S[s1 - 1];  // the last writer places y: out[w_m] = j = y
+        if (cnt[tt] == (tt ? cnt[tt - 1] : 0u)) qq[y] = kNone;
+    }
+    // per writer (no per-group sort): rank among its group and the next larger writer
+    for (uint32_t p = threadIdx.x; p < n; p += kBlockThreads) {
+        const uint32_t w = S[p];
+        uint32_t jl;
+        if constexpr (BIG) jl = SJ32[p];
+        else jl = SJ16[p];
+        const uint32_t s0 = jl ? cnt[jl - 1] : 0u, s1 = cnt[jl];
+        bool first = true;
+        uint32_t nx = kNone;
+        for (uint32_t a = s0; a < s1; ++a) {
+            const uint32_t v = S[a];
+            first &= !(v < w);
+            nx = v > w ? min(nx, v) : nx;
         }
-        qq[y] = qv;
+        const uint32_t y = y0 + jl;
+        if (first) qq[y] = w != y ? w : nx;   // smallest writer != y
+        if (nx == kNone) {
+            if (iv) iv[y] = w;                // the last writer places y (out[w_m] = j = y)
+        } else {
+            sc[w] = nx;
+        }
     }
 }
 
@@ -322,6 +320,7 @@ __global__ void __launch_bounds__(kBlockThreads) fyb_block_kernel(uint32_t F, Fy
     uint32_t* W = tlo + g.NT;           // [cap]  writer step
     uint32_t* S = W + g.cap;            // [cap]  owner run, then writers grouped by target
     uint16_t* JL = reinterpret_cast<uint16_t*>(S + g.cap);  // [cap] target within block
+    uint16_t* SJ = JL + g.cap;                               // [cap] same, grouped order
     const uint32_t* rows = lst + (size_t)slot * g.NT * (g.NB + 1);
     for (uint32_t k = threadIdx.x; k <= TB; k += kBlockThreads) cnt[k] = 0;
     for (uint32_t k = threadIdx.x; k < nt; k += kBlockThreads) {
@@ -338,14 +337,14 @@ __global__ void __launch_bounds__(kBlockThreads) fyb_block_kernel(uint32_t F, Fy
     uint32_t* qq = q + (size_t)slot * F;
     uint32_t* iv = inv ? inv + (size_t)(e0 + slot) * F : nullptr;
     if (n <= g.cap) {
-        fyb_block_body<false>(F, g, b, n, nt, tmin, tlo, tdst, cnt, W, S, JL, nullptr, wsum, bk,
-                              sc, qq, iv);
+        fyb_block_body<false>(F, g, b, n, nt, tmin, tlo, tdst, cnt, W, S, JL, nullptr, SJ,
+                              nullptr, wsum, bk, sc, qq, iv);
     } else {  // heavy block (small targets): global pool slab
-        if (threadIdx.x == 0) s_pool = atomicAdd(pool_used + slot, 3 * n);
+        if (threadIdx.x == 0) s_pool = atomicAdd(pool_used + slot, 4 * n);
         __syncthreads();
-        uint32_t* gW = pool + (size_t)slot * 3 * F + s_pool;
+        uint32_t* gW = pool + (size_t)slot * 4 * F + s_pool;
         fyb_block_body<true>(F, g, b, n, nt, tmin, tlo, tdst, cnt, gW, gW + n, nullptr,
-                             gW + 2 * n, wsum, bk, sc, qq, iv);
+                             gW + 2 * n, nullptr, gW + 3 * n, wsum, bk, sc, qq, iv);
     }
 }
 
@@ -410,7 +409,7 @@ __global__ void __launch_bounds__(kThreads) fyb_emit_kernel(uint64_t key, Part p
 
 // ---- launchers --------------------------------------------------------------------------
 size_t fyb_block_smem(const FyGeom& g) {
-    return (size_t)4 * ((1u << g.lgTB) + 1 + 2 * g.NT + 1 + 2 * g.cap) + 2 * (size_t)g.cap;
+    return (size_t)4 * ((1u << g.lgTB) + 1 + 2 * g.NT + 1 + 2 * g.cap) + 4 * (size_t)g.cap;
 }
 
 template <int K>

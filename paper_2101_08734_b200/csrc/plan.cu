@@ -52,10 +52,10 @@ int enqueue_perms(clairplan_plan* p, uint32_t* stream_out, uint32_t* inv_out, ui
     static const bool fy_out_mode = getenv("CLAIRPLAN_FY_OUT") != nullptr;
     FyGeom g;
     if (mode == "bucket" && fy_geometry(F, g)) {  // shared-memory bucketed resolution
-        const uint32_t EB = epochs_per_batch(F, e_count, 28);
+        const uint32_t EB = epochs_per_batch(F, e_count, 32);
         uint32_t* bucket = need<uint32_t>(p->fybucket, (uint64_t)EB * F, ok);
         uint32_t* lst = need<uint32_t>(p->fylst, (uint64_t)EB * g.NT * (g.NB + 1), ok);
-        uint32_t* pool = need<uint32_t>(p->fypool, (uint64_t)EB * 3 * F, ok);
+        uint32_t* pool = need<uint32_t>(p->fypool, (uint64_t)EB * 4 * F, ok);
         uint32_t* pool_used = need<uint32_t>(p->fypool_used, EB, ok);
         uint32_t* succ = need<uint32_t>(p->next, (uint64_t)EB * F, ok);
         uint32_t* q = need<uint32_t>(p->q, (uint64_t)EB * F, ok);
