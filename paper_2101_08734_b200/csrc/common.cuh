@@ -156,6 +156,17 @@ struct Part {
         slice_of((uint32_t)p, w, h, off);
         spos = (uint64_t)e * epoch_len(w) + (h < full ? (uint64_t)h * len(w) : full * len(w)) + off;
     }
+    // locate plus the number of positions p, p+1, ... that stay in the same batch slice
+    // (consecutive stream positions of the same worker)
+    __host__ __device__ __forceinline__ void locate_run(uint32_t p, uint32_t e, uint32_t& w,
+                                                        uint64_t& spos, uint32_t& left) const {
+        uint32_t h, off;
+        slice_of(p, w, h, off);
+        const bool fl = h < full;
+        const uint64_t L = fl ? len(w) : tlen(w);
+        spos = (uint64_t)e * epoch_len(w) + (fl ? (uint64_t)h * len(w) : full * len(w)) + off;
+        left = (uint32_t)(L - off);
+    }
     __host__ __device__ __forceinline__ uint32_t worker_of(uint64_t p) const {
         uint32_t w, h, off;
         slice_of((uint32_t)p, w, h, off);

@@ -360,14 +360,14 @@ __global__ void __launch_bounds__(kThreads) fyb_emit_kernel(uint64_t key, Part p
     const FyRej rj(rt, e - rt.e_base);
     const uint32_t* sc = succ + (size_t)slot * F;
     const uint32_t* qq = q + (size_t)slot * F;
-    constexpr int U = 4;
-    const uint32_t stride = gridDim.x * blockDim.x;
-    for (uint32_t i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < F; i0 += U * stride) {
+    constexpr int U = 4;  // consecutive positions per thread: one slice lookup serves them
+    const uint32_t nthr = gridDim.x * blockDim.x;
+    for (uint32_t i0 = (blockIdx.x * blockDim.x + threadIdx.x) * U; i0 < F; i0 += U * nthr) {
         uint32_t cur[U];
         uint32_t live = 0;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const uint32_t i = i0 + u * stride;
+            const uint32_t i = i0 + u;
             cur[u] = kNone;
             if (i < F) {
                 const uint32_t s = i ? __ldcs(sc + i) : 0u;
@@ -389,19 +389,34 @@ __global__ void __launch_bounds__(kThreads) fyb_emit_kernel(uint64_t key, Part p
                 else cur[u] = nq;
             }
         }
+        if (perm_out) {
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const uint32_t i = i0 + u * stride;
-            if (i >= F) break;
-            const uint32_t v = cur[u];
-            if (perm_out) perm_out[(size_t)slot * F + i] = v;
-            // values with a writer got inv from fyb_block; chase roots have none
-            if (inv && ((chased >> u) & 1u)) inv[(size_t)e * F + v] = i;
-            if (stream && i < part.P) {
-                uint32_t w;
-                uint64_t spos;
-                part.locate(i, e, w, spos);
-                if (w >= part.wbegin && w < part.wend) stream[part.stream_offset(w) + spos] = v;
+            for (int u = 0; u < U; ++u)
+                if (i0 + u < F) perm_out[(size_t)slot * F + i0 + u] = cur[u];
+        }
+        if (inv) {  // values with a writer got inv from fyb_block; chase roots have none
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if ((chased >> u) & 1u) inv[(size_t)e * F + cur[u]] = i0 + u;
+        }
+        if (stream && i0 < part.P) {
+            uint32_t w, left;
+            uint64_t spos;
+            part.locate_run(i0, e, w, spos, left);
+            if (left >= (uint32_t)U && i0 + U <= part.P) {
+                if (w >= part.wbegin && w < part.wend) {
+                    uint32_t* dst = stream + part.stream_offset(w) + spos;
+#pragma unroll
+                    for (int u = 0; u < U; ++u) dst[u] = cur[u];
+                }
+            } else {
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const uint32_t i = i0 + u;
+                    if (i >= part.P) break;
+                    part.locate(i, e, w, spos);
+                    if (w >= part.wbegin && w < part.wend) stream[part.stream_offset(w) + spos] = cur[u];
+                }
             }
         }
     }
