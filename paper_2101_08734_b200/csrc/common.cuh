@@ -167,6 +167,12 @@ struct Part {
         spos = (uint64_t)e * epoch_len(w) + (fl ? (uint64_t)h * len(w) : full * len(w)) + off;
         left = (uint32_t)(L - off);
     }
+    // worker of position p and the position within that worker's epoch segment
+    __host__ __device__ __forceinline__ uint32_t within_epoch(uint32_t p, uint32_t& w) const {
+        uint32_t h, off;
+        slice_of(p, w, h, off);
+        return (uint32_t)((h < full ? (uint64_t)h : full) * len(w)) + off;
+    }
     __host__ __device__ __forceinline__ uint32_t worker_of(uint64_t p) const {
         uint32_t w, h, off;
         slice_of((uint32_t)p, w, h, off);

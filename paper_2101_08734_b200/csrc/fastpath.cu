@@ -515,13 +515,15 @@ __device__ __forceinline__ uint32_t pick(const uint4& a, uint32_t i) {
     return i == 0 ? a.x : i == 1 ? a.y : i == 2 ? a.z : a.w;
 }
 
+template <int NP>  // class bit-planes per record (0: runtime np)
 __global__ void __launch_bounds__(kThreads) holder_tile_kernel(
     Part part, const uint32_t* __restrict__ inv, const uint16_t* __restrict__ rank16, uint32_t MB,
-    const uint32_t* __restrict__ rec, uint32_t np, uint32_t J, uint32_t Rp,
+    const uint32_t* __restrict__ rec, uint32_t np_rt, uint32_t J, uint32_t Rp,
     const uint32_t* __restrict__ cbase, const uint64_t* __restrict__ pair_off,
     uint32_t* __restrict__ holders) {
     extern __shared__ uint32_t sm[];
     const uint32_t E = part.E, F = part.F;
+    const uint32_t np = NP ? (uint32_t)NP : np_rt;
     uint32_t* tinv = sm;                                            // [E][33]
     uint16_t* trk = reinterpret_cast<uint16_t*>(sm + (size_t)E * 33);  // [E][33]
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
@@ -540,27 +542,34 @@ __global__ void __launch_bounds__(kThreads) holder_tile_kernel(
             for (uint32_t e = lane; e < E; e += 32) {
                 const uint32_t rk = trk[e * 33 + s];
                 if (rk == 0xFFFFu) continue;
-                const uint32_t p = tinv[e * 33 + s];
                 uint32_t w;
-                uint64_t spos;
-                part.locate(p, e, w, spos);
+                const uint32_t tseg = part.within_epoch(tinv[e * 33 + s], w);
                 const uint32_t wl = w - part.wbegin;
-                const uint64_t tseg = spos - (uint64_t)e * part.epoch_len(w);
                 const uint64_t blk = ((uint64_t)wl * E + e) * MB + (tseg >> 5);
-                const uint32_t bit = (uint32_t)(tseg & 31);
+                const uint32_t bit = tseg & 31;
                 const uint4* r4 = reinterpret_cast<const uint4*>(rec + blk * Rp);
                 const uint4 a = r4[0];
-                uint32_t cls = 0;
-                for (uint32_t q = 0; q < np; ++q) cls |= ((pick(a, q) >> bit) & 1u) << q;
-                uint32_t pos = 0;
-                if (cls) {
-                    uint32_t cm = 0xffffffffu;
+                uint32_t cls, cm;
+                if constexpr (NP == 1) {
+                    cls = (a.x >> bit) & 1u;
+                    cm = a.x;
+                } else if constexpr (NP == 2) {
+                    const uint32_t b0 = (a.x >> bit) & 1u, b1 = (a.y >> bit) & 1u;
+                    cls = b0 | (b1 << 1);
+                    cm = (b0 ? a.x : ~a.x) & (b1 ? a.y : ~a.y);
+                } else {
+                    cls = 0;
+                    for (uint32_t q = 0; q < np; ++q) cls |= ((pick(a, q) >> bit) & 1u) << q;
+                    cm = 0xffffffffu;
                     for (uint32_t q = 0; q < np; ++q) {
                         const uint32_t pl = pick(a, q);
                         cm &= ((cls >> q) & 1u) ? pl : ~pl;
                     }
+                }
+                uint32_t pos = 0;
+                if (cls) {
                     const uint32_t wi = np + cls - 1;
-                    const uint32_t prew = wi < 4 ? pick(a, wi) : pick(r4[wi >> 2], wi & 3);
+                    const uint32_t prew = wi < 4 ? pick(a, wi) : rec[blk * Rp + wi];
                     pos = prew - cbase[wl * J + cls - 1] + __popc(cm & ((1u << bit) - 1u));
                 }
                 uint32_t* h = holders + 3 * (slot0 + rk);
@@ -616,10 +625,21 @@ void launch_holder_tile(cudaStream_t s, const Part& part, const uint32_t* inv, c
                         uint32_t MB, const uint32_t* rec, uint32_t np, uint32_t J, uint32_t Rp,
                         const uint32_t* cbase, const uint64_t* pair_off, uint32_t* holders) {
     const size_t smem = (size_t)part.E * 33 * 4 + (size_t)part.E * 33 * 2 + 16;
-    cudaFuncSetAttribute(holder_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const uint64_t tiles = ((uint64_t)part.F + 31) / 32;
-    holder_tile_kernel<<<grid_for(tiles, 1, 148u * 16u), kThreads, smem, s>>>(
-        part, inv, rank16, MB, rec, np, J, Rp, cbase, pair_off, holders);
+    const unsigned grid = grid_for(tiles, 1, 148u * 16u);
+    if (np == 1) {
+        cudaFuncSetAttribute(holder_tile_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        holder_tile_kernel<1><<<grid, kThreads, smem, s>>>(part, inv, rank16, MB, rec, np, J, Rp,
+                                                           cbase, pair_off, holders);
+    } else if (np == 2) {
+        cudaFuncSetAttribute(holder_tile_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        holder_tile_kernel<2><<<grid, kThreads, smem, s>>>(part, inv, rank16, MB, rec, np, J, Rp,
+                                                           cbase, pair_off, holders);
+    } else {
+        cudaFuncSetAttribute(holder_tile_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        holder_tile_kernel<0><<<grid, kThreads, smem, s>>>(part, inv, rank16, MB, rec, np, J, Rp,
+                                                           cbase, pair_off, holders);
+    }
 }
 
 void launch_sample_lanes(cudaStream_t s, const Part& part, const uint32_t* inv, uint16_t* info,
