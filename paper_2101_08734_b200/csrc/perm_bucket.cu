@@ -14,6 +14,8 @@
 //             values no step wrote: V's roots are exactly those).
 // Geometry (fy_geometry): TB, TS powers of two with NT*NB cells ~ F/4..F so the runs stay
 // a few elements long; valid for F < 2^31 and NB <= kMaxBlocks (else perm.cu's lists path).
+#include <cstdlib>
+
 #include "internal.h"
 
 namespace clairplan {
@@ -26,8 +28,9 @@ constexpr uint32_t kMaxTiles = 4096;
 bool fy_geometry(uint32_t F, FyGeom& g) {
     if (F < 2 || F >= 0x80000000u) return false;
     uint32_t lgTB = 8;
-    while ((1ull << lgTB) * 2048 < F) ++lgTB;
+    while ((1ull << lgTB) * 4096 < F) ++lgTB;
     if (lgTB > 11) return false;  // large F: the linked-list path (perm.cu) is faster today
+    if (const char* v = getenv("CLAIRPLAN_FY_LGTB")) lgTB = (uint32_t)atoi(v);
     const uint64_t TB = 1ull << lgTB;
     uint32_t lgTS = 13;
     while ((1ull << lgTS) * TB < 4ull * F) ++lgTS;
@@ -38,7 +41,8 @@ bool fy_geometry(uint32_t F, FyGeom& g) {
     g.NT = (uint32_t)((F + (1ull << lgTS) - 1) >> lgTS);
     if (g.NB > kMaxBlocks || g.NT > kMaxTiles) return false;
     // shared-memory capacity of a block's writers (larger blocks use the global pool)
-    g.cap = lgTB <= 10 ? 3072 : 4096;
+    g.cap = lgTB <= 9 ? 2048 : lgTB == 10 ? 3072 : 4096;
+    if (const char* v = getenv("CLAIRPLAN_FY_CAP")) g.cap = (uint32_t)atoi(v);
     return true;
 }
 
