@@ -32,6 +32,7 @@ def main():
     ap.add_argument("--traffic")
     ap.add_argument("--workload", default="")
     ap.add_argument("--title", default="")
+    ap.add_argument("--reps", type=float, default=1.0, help="plans in the launch list")
     a = ap.parse_args()
     data = load(a.csv)
     agg = collections.OrderedDict()
@@ -47,7 +48,11 @@ def main():
             x["rd"] += v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
         elif m == "dram__bytes_write.sum":
             x["wr"] += v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
-    ours = {k: v for k, v in agg.items() if k.startswith("clairplan::")}
+    # ncu may or may not print the clairplan:: namespace; drop torch's own kernels
+    ours = {k: v for k, v in agg.items() if "at::" not in k and "native::" not in k}
+    for v in ours.values():
+        for f in ("n", "ns", "rd", "wr"):
+            v[f] /= a.reps
     tot = sum(v["ns"] for v in ours.values())
     lines = [f"# {a.title or 'ncu launch list'}", "",
              "Per-launch device times from `ncu --metrics gpu__time_duration.sum,"
@@ -56,7 +61,7 @@ def main():
              "| kernel | launches | total ms | share | DRAM read MB | DRAM write MB |",
              "|---|---:|---:|---:|---:|---:|"]
     for k, v in sorted(ours.items(), key=lambda kv: -kv[1]["ns"]):
-        lines.append(f"| `{k.replace('clairplan::', '')}` | {v['n']} | {v['ns'] / 1e6:.3f} | "
+        lines.append(f"| `{k.replace('clairplan::', '')}` | {v['n']:g} | {v['ns'] / 1e6:.3f} | "
                      f"{100 * v['ns'] / tot:.1f}% | {v['rd'] / 1e6:.1f} | {v['wr'] / 1e6:.1f} |")
     rd = sum(v["rd"] for v in ours.values())
     wr = sum(v["wr"] for v in ours.values())
