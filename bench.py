@@ -289,9 +289,10 @@ def run_ours(args, cfg):
                        "capacities_mb": list(CAPS), "drop_last": True,
                        "l2": "256 MB flush before every timed step",
                        "sharding": ("single GPU" if world == 1 else
-                                    f"epochs sharded over {world} GPUs for the permutations, "
-                                    "NCCL all-gather of the rows, worker ranges for the rest, "
-                                    "holder offsets merged by NCCL all-gather")}, 
+                                    f"epochs sharded over {world} GPUs for the permutations "
+                                    "and stream cutting, one NCCL all-to-all of the stream "
+                                    "slices, worker ranges for the rest, holder offsets "
+                                    "merged by NCCL all-gather")},
             "plan_latency_ms": ms_step,
             "wall_ms_per_step": t_wall * 1e3 / args.steps,
             "accesses": int(A_all), "pairs": int(D_all),

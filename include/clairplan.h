@@ -65,7 +65,13 @@ typedef struct {
     uint64_t holders;         /* assigned pairs = holder records */
     uint64_t rejections;      /* Lemire rejections resolved (rng.hpp:54-60) */
     double device_ms;         /* device time of the last clairplan_build (CUDA events) */
+    uint32_t path;            /* pipeline of the last build: CLAIRPLAN_PATH_* */
+    uint32_t reserved;
 } clairplan_stats;
+
+#define CLAIRPLAN_PATH_V1 0      /* generic / v1 pipeline (explicit streams, large handles) */
+#define CLAIRPLAN_PATH_TIER 1    /* v2: tier order + exact first fit */
+#define CLAIRPLAN_PATH_ALLFIT 2  /* v2: every worker provably fits class 1 (no tier order) */
 
 int clairplan_version(void);
 const char* clairplan_last_error(void);
@@ -150,6 +156,21 @@ int clairplan_generate_perms(clairplan_t plan, uint32_t epoch_begin, uint32_t ep
 /* clairplan_build for the handle's worker range from all E permutation rows d_perms[E][F]
  * (e.g. epoch-sharded rows all-gathered over NVLink). */
 int clairplan_build_from_perms(clairplan_t plan, const uint32_t* d_perms);
+/* Epoch-range streams (the all-to-all exchange of the sharded build): the streams of ALL
+ * workers for epochs [epoch_begin, epoch_begin+count), laid out worker-major as
+ * build_access_streams would for a run of `count` epochs (access.cpp:59-78):
+ * d_out[prefix(w)*count + (e-epoch_begin)*len(w) + t]; the range for the workers of rank d
+ * is contiguous, [count*prefix(wb_d), count*prefix(we_d)), prefix = clairplan_epoch_prefix.
+ * Rejections resolved.  Replaces epoch_permutation x count (access.cpp:52-57). */
+int clairplan_generate_streams(clairplan_t plan, uint32_t epoch_begin, uint32_t epoch_count,
+                               uint32_t* d_out);
+/* Stream entries per epoch of the workers below `worker` (sum of batch_slice lengths). */
+int clairplan_epoch_prefix(clairplan_t plan, uint32_t worker, uint64_t* entries);
+/* clairplan_build for the handle's worker range from the all-to-all output d_recv: for each
+ * source rank r (epochs [epoch_bounds[r], epoch_bounds[r+1])) its block
+ * [local worker][epoch][t], blocks in rank order.  epoch_bounds[nsrc+1] is host memory. */
+int clairplan_build_from_streams(clairplan_t plan, const uint32_t* d_recv,
+                                 const uint32_t* epoch_bounds, uint32_t nsrc);
 /* Per-sample number of holder records of the handle's workers, d_out[F] (device): the
  * input of the cross-GPU holder-offset merge (all-gather + exclusive scan over ranks). */
 int clairplan_holder_counts(clairplan_t plan, uint32_t* d_out);

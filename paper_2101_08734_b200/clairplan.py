@@ -58,6 +58,8 @@ class _Stats(C.Structure):
         ("holders", C.c_uint64),
         ("rejections", C.c_uint64),
         ("device_ms", C.c_double),
+        ("path", C.c_uint32),
+        ("reserved", C.c_uint32),
     ]
 
 
@@ -250,7 +252,8 @@ class Plan:
         s = _Stats()
         _check(lib().clairplan_stats_get(self._h, C.byref(s)))
         return {"accesses": s.accesses, "pairs": s.pairs, "holders": s.holders,
-                "rejections": s.rejections, "device_ms": s.device_ms}
+                "rejections": s.rejections, "device_ms": s.device_ms,
+                "path": {0: "v1", 1: "tier", 2: "allfit"}.get(s.path, str(s.path))}
 
     def launch_count(self) -> int:
         return int(lib().clairplan_launch_count(self._h))

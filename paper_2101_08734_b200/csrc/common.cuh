@@ -114,6 +114,7 @@ struct Part {
     uint64_t tbase, textra;          // batch_slice of the tail batch
     uint32_t wbegin, wend;           // worker range of this handle
     uint64_t off0;                   // stream_offset(wbegin)
+    uint32_t ebase;                  // first epoch held in the stream (epoch-range streams)
     FastDiv dB, dFull1, dFull0, dTail1, dTail0;  // B, base+1, base, tbase+1, tbase
 
     __host__ __device__ uint64_t len(uint32_t w) const { return base + (w < extra ? 1 : 0); }
@@ -154,7 +155,7 @@ struct Part {
                                                     uint64_t& spos) const {
         uint32_t h, off;
         slice_of((uint32_t)p, w, h, off);
-        spos = (uint64_t)e * epoch_len(w) + (h < full ? (uint64_t)h * len(w) : full * len(w)) + off;
+        spos = (uint64_t)(e - ebase) * epoch_len(w) + (h < full ? (uint64_t)h * len(w) : full * len(w)) + off;
     }
     // locate plus the number of positions p, p+1, ... that stay in the same batch slice
     // (consecutive stream positions of the same worker)
@@ -164,7 +165,7 @@ struct Part {
         slice_of(p, w, h, off);
         const bool fl = h < full;
         const uint64_t L = fl ? len(w) : tlen(w);
-        spos = (uint64_t)e * epoch_len(w) + (fl ? (uint64_t)h * len(w) : full * len(w)) + off;
+        spos = (uint64_t)(e - ebase) * epoch_len(w) + (fl ? (uint64_t)h * len(w) : full * len(w)) + off;
         left = (uint32_t)(L - off);
     }
     // worker of position p and the position within that worker's epoch segment
@@ -196,6 +197,7 @@ inline Part make_part(uint32_t F, uint32_t N, uint32_t B, uint32_t E, bool drop_
     p.dTail1 = FastDiv((uint32_t)p.tbase + 1);
     p.dTail0 = FastDiv(p.tbase ? (uint32_t)p.tbase : 1u);
     p.off0 = 0;
+    p.ebase = 0;
     p.off0 = p.stream_offset(wbegin);
     return p;
 }

@@ -22,6 +22,11 @@
 //     class_write    prefetch-ordered class lists (policies.cpp:31-36,162)
 // K8  holder_lanes   lane = sample again: holders written in worker order at the pair slot
 //                    (build_index, policies.cpp:124-142) from the L2-resident block records
+#include <math.h>
+#include <stdlib.h>
+
+#include <type_traits>
+
 #include "internal.h"
 
 namespace clairplan {
@@ -231,10 +236,15 @@ __global__ void __launch_bounds__(128) sample_hash_kernel(Part part, const uint3
 constexpr int kSU = 4;
 
 // seghist[(wl*E + (E - c))*E + e] = first accesses with count c in segment (w, e)
+// With `sizes`: also the sum and minimum of the sizes of the segment's first accesses
+// (segsum/segmin), the input of the whole-worker fit test (fit_check_kernel).
 __global__ void __launch_bounds__(kThreads) seg_hist_kernel(Part part, const uint32_t* __restrict__ stream,
                                                              const uint16_t* __restrict__ info,
                                                              uint32_t* __restrict__ seghist,
-                                                             uint32_t* __restrict__ segcnt) {
+                                                             uint32_t* __restrict__ segcnt,
+                                                             const double* __restrict__ sizes,
+                                                             double* __restrict__ segsum,
+                                                             double* __restrict__ segmin) {
     extern __shared__ uint32_t shist[];  // [warps][E]
     const uint32_t E = part.E, nloc = part.wend - part.wbegin;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -250,6 +260,7 @@ __global__ void __launch_bounds__(kThreads) seg_hist_kernel(Part part, const uin
         const uint64_t g0 = part.stream_offset(w) + (uint64_t)e * Le;
         const uint16_t* row = info + (size_t)e * part.F;
         uint32_t tot = 0;
+        double ssum = 0.0, smin = INFINITY;
         for (uint64_t t0 = 0; t0 < Le; t0 += 32 * kSU) {
             uint32_t k[kSU], c[kSU];
 #pragma unroll
@@ -259,6 +270,16 @@ __global__ void __launch_bounds__(kThreads) seg_hist_kernel(Part part, const uin
             }
 #pragma unroll
             for (int u = 0; u < kSU; ++u) c[u] = k[u] != kNone ? row[k[u]] : 0u;
+            if (segsum) {
+#pragma unroll
+                for (int u = 0; u < kSU; ++u) {
+                    if (c[u] != 0) {
+                        const double v = sizes[k[u]];
+                        ssum += v;
+                        smin = fmin(smin, v);
+                    }
+                }
+            }
 #pragma unroll
             for (int u = 0; u < kSU; ++u) {
                 const bool first = c[u] != 0;
@@ -270,9 +291,22 @@ __global__ void __launch_bounds__(kThreads) seg_hist_kernel(Part part, const uin
             __syncwarp();
         }
         tot = warp_sum(tot);
+        if (segsum) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                ssum += __shfl_xor_sync(0xffffffffu, ssum, o);
+                smin = fmin(smin, __shfl_xor_sync(0xffffffffu, smin, o));
+            }
+        }
         __syncwarp();
         for (uint32_t i = lane; i < E; i += 32) seghist[((uint64_t)wl * E + i) * E + e] = hist[i];
-        if (lane == 0) segcnt[(uint64_t)wl * E + e] = tot;
+        if (lane == 0) {
+            segcnt[(uint64_t)wl * E + e] = tot;
+            if (segsum) {
+                segsum[(uint64_t)wl * E + e] = ssum;
+                segmin[(uint64_t)wl * E + e] = smin;
+            }
+        }
         __syncwarp();
     }
 }
@@ -293,6 +327,120 @@ void launch_segcnt(cudaStream_t s, uint32_t nloc, uint32_t E, const uint32_t* se
                    uint32_t* segcnt) {
     segcnt_kernel<<<grid_for((uint64_t)nloc * E, kThreads), kThreads, 0, s>>>(nloc, E, seghist,
                                                                               segcnt);
+}
+
+// ---------------------------------------------------------------------------- whole-worker fit
+// pack_first_fit (policies.cpp:40-55) takes every candidate of a worker into class 1 when the
+// sizes are non-negative and their sum stays below the capacity by more than the rounding of
+// any summation order and of the chain `remaining -= s` (same bound as ff_prefix_kernel):
+// then `s <= remaining` holds at every step whatever the tier order is.  One warp per worker;
+// *allfit is cleared when some worker does not provably fit.
+__global__ void fit_check_kernel(uint32_t nloc, uint32_t E, const double* __restrict__ segsum,
+                                 const double* __restrict__ segmin,
+                                 const uint32_t* __restrict__ segcnt, double C,
+                                 uint32_t* __restrict__ allfit) {
+    const uint32_t lane = threadIdx.x & 31;
+    for (uint32_t wl = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; wl < nloc;
+         wl += (gridDim.x * blockDim.x) >> 5) {
+        double sum = 0.0, mn = INFINITY;
+        uint64_t n = 0;
+        for (uint32_t e = lane; e < E; e += 32) {
+            sum += segsum[(uint64_t)wl * E + e];
+            mn = fmin(mn, segmin[(uint64_t)wl * E + e]);
+            n += segcnt[(uint64_t)wl * E + e];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            sum += __shfl_xor_sync(0xffffffffu, sum, o);
+            mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+            n += __shfl_xor_sync(0xffffffffu, n, o);
+        }
+        if (lane == 0) {
+            const double tol = ((double)n + 1024.0) * fmax(C, sum) * 0x1.0p-48;
+            const bool fits = n == 0 || (mn >= 0.0 && C - sum > tol);
+            if (!fits) atomicAnd(allfit, 0u);
+        }
+    }
+}
+
+// All-fit variant of seg_write (K4c) + K7: every first access is class 1, the class-1 list of a
+// worker is its first-order candidate list.  Per 32-entry block: the all-fit record uint2
+// {first-access mask, class-1 prefix = first-order index of the block's first candidate} and
+// the class-list entries, written compacted.
+__global__ void __launch_bounds__(kThreads) seg_first_kernel(
+    Part part, const uint32_t* __restrict__ stream, const uint16_t* __restrict__ info,
+    const uint64_t* __restrict__ seg_off, uint32_t MB, uint32_t* __restrict__ rec,
+    uint32_t* __restrict__ class_list) {
+    const uint32_t E = part.E, nloc = part.wend - part.wbegin;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t nseg = (uint64_t)nloc * E;
+    for (uint64_t b = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; b < nseg;
+         b += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+        const uint32_t e = (uint32_t)(b / nloc), wl = (uint32_t)(b - (uint64_t)e * nloc);
+        const uint32_t w = part.wbegin + wl;
+        const uint64_t Le = part.epoch_len(w);
+        const uint64_t g0 = part.stream_offset(w) + (uint64_t)e * Le;
+        const uint16_t* row = info + (size_t)e * part.F;
+        uint64_t frun = seg_off[(uint64_t)wl * E + e];
+        const uint64_t blk0 = ((uint64_t)wl * E + e) * MB;
+        for (uint64_t t0 = 0; t0 < Le; t0 += 32 * kSU) {
+            uint32_t k[kSU], c[kSU];
+#pragma unroll
+            for (int u = 0; u < kSU; ++u) {
+                const uint64_t t = t0 + 32 * u + lane;
+                k[u] = t < Le ? __ldcs(stream + g0 + t) : kNone;
+            }
+#pragma unroll
+            for (int u = 0; u < kSU; ++u) c[u] = k[u] != kNone ? row[k[u]] : 0u;
+#pragma unroll
+            for (int u = 0; u < kSU; ++u) {
+                const uint64_t tb = t0 + 32 * u;
+                if (tb >= Le) break;
+                const bool first = c[u] != 0;
+                const uint32_t bal = __ballot_sync(0xffffffffu, first);
+                if (lane == 0) reinterpret_cast<uint2*>(rec)[blk0 + (tb >> 5)] = make_uint2(bal, (uint32_t)frun);
+                if (first) __stcs(class_list + frun + __popc(bal & lanemask_lt()), k[u]);
+                frun += __popc(bal);
+            }
+        }
+    }
+}
+
+// Class-list geometry of an all-fit handle: list (w, 1) = the worker's candidates, lists
+// (w, j > 1) empty; cbase = class-1 prefix at the worker's first block.
+__global__ void allfit_meta_kernel(uint32_t nloc, uint32_t E, uint32_t J,
+                                   const uint64_t* __restrict__ seg_off, uint64_t* __restrict__ clen,
+                                   uint64_t* __restrict__ cstart, uint32_t* __restrict__ cbase) {
+    for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x <= nloc * J; x += gridDim.x * blockDim.x) {
+        if (x == nloc * J) {
+            cstart[x] = seg_off[(uint64_t)nloc * E];
+            break;
+        }
+        const uint32_t wl = x / J, j = x % J;
+        const uint64_t a = seg_off[(uint64_t)wl * E], b = seg_off[(uint64_t)(wl + 1) * E];
+        clen[x] = j == 0 ? b - a : 0;
+        cstart[x] = j == 0 ? a : b;
+        cbase[x] = j == 0 ? (uint32_t)a : 0u;
+    }
+}
+
+void launch_fit_check(cudaStream_t s, uint32_t nloc, uint32_t E, const double* segsum,
+                      const double* segmin, const uint32_t* segcnt, double C, uint32_t* allfit) {
+    fit_check_kernel<<<grid_for((uint64_t)nloc * 32, kThreads), kThreads, 0, s>>>(
+        nloc, E, segsum, segmin, segcnt, C, allfit);
+}
+
+void launch_seg_first(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info,
+                      const uint64_t* seg_off, uint32_t MB, uint32_t* rec, uint32_t* class_list) {
+    const uint64_t nseg = (uint64_t)(part.wend - part.wbegin) * part.E;
+    seg_first_kernel<<<grid_for(nseg * 32, kThreads, 148u * 64u), kThreads, 0, s>>>(
+        part, stream, info, seg_off, MB, rec, class_list);
+}
+
+void launch_allfit_meta(cudaStream_t s, uint32_t nloc, uint32_t E, uint32_t J, const uint64_t* seg_off,
+                        uint64_t* clen, uint64_t* cstart, uint32_t* cbase) {
+    allfit_meta_kernel<<<grid_for((uint64_t)nloc * J + 1, kThreads), kThreads, 0, s>>>(
+        nloc, E, J, seg_off, clen, cstart, cbase);
 }
 
 // ---------------------------------------------------------------------------- K4c
@@ -509,13 +657,54 @@ __global__ void class_lens_kernel(uint32_t nloc, uint32_t E, uint32_t MB, uint32
 // One CTA takes 32 samples: their inverse-permutation and rank rows are loaded with coalesced
 // 128-B rows into padded shared tiles; then one warp per sample, lanes = epochs: every first
 // access (rank != 0xFFFF) looks up its class and class-list position in the block record and
-// writes its holder record at pair_off[k] + rank — the 32 stores of a warp land in one
-// sample's contiguous holder range (build_index order: workers ascending).
+// writes its holder record {worker, class, position} at pair_off[k] + rank (build_index
+// order, workers ascending): a warp's stores land in one sample's contiguous holder range.
+// (Staging the records in shared memory for fully contiguous stores was measured slower:
+// MIO-throttled, 2.2 vs 1.15 ms for config 2.)
+// NP: class bit-planes per record (0: runtime np); NP == -1: all-fit records (uint2 {first
+// mask, class-1 prefix}, every first access is class 1).
 __device__ __forceinline__ uint32_t pick(const uint4& a, uint32_t i) {
     return i == 0 ? a.x : i == 1 ? a.y : i == 2 ? a.z : a.w;
 }
 
-template <int NP>  // class bit-planes per record (0: runtime np)
+__device__ __forceinline__ uint4 as4(const uint4& a) { return a; }
+__device__ __forceinline__ uint4 as4(const uint2& a) { return make_uint4(a.x, a.y, 0u, 0u); }
+
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+    const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+constexpr uint32_t kHtInv = 33;  // padded row strides of the shared tiles (conflict-free reads)
+constexpr uint32_t kHtRk = 34;   // u16; even, so sample pairs are 4-B aligned for cp.async
+
+// tile k0 of the inverse-permutation / rank rows -> shared buffer (asynchronous, 4-B copies)
+__device__ __forceinline__ void ht_issue(const Part& part, const uint32_t* inv, const uint16_t* rank16,
+                                         uint64_t k0, uint32_t* tinv, uint16_t* trk) {
+    const uint32_t E = part.E, F = part.F;
+    const uint32_t n = (uint32_t)(F - k0 < 32 ? F - k0 : 32);
+    for (uint32_t idx = threadIdx.x; idx < E * 32; idx += blockDim.x) {
+        const uint32_t e = idx >> 5, l = idx & 31;
+        if (l < n) cp_async4(tinv + e * kHtInv + l, inv + (size_t)e * F + k0 + l);
+    }
+    // rank pairs (l, l+1); an odd F leaves a single u16 at the end of each row
+    for (uint32_t idx = threadIdx.x; idx < E * 16; idx += blockDim.x) {
+        const uint32_t e = idx >> 4, l = (idx & 15) * 2;
+        if (l >= n) continue;
+        const uint16_t* g = rank16 + (size_t)e * F + k0 + l;
+        if (l + 1 < n && (((uintptr_t)g) & 3) == 0) cp_async4(trk + e * kHtRk + l, g);
+        else {
+            trk[e * kHtRk + l] = __ldcs(g);
+            if (l + 1 < n) trk[e * kHtRk + l + 1] = __ldcs(g + 1);
+        }
+    }
+    cp_async_commit();
+}
+
+template <int NP, int SU>
 __global__ void __launch_bounds__(kThreads) holder_tile_kernel(
     Part part, const uint32_t* __restrict__ inv, const uint16_t* __restrict__ rank16, uint32_t MB,
     const uint32_t* __restrict__ rec, uint32_t np_rt, uint32_t J, uint32_t Rp,
@@ -523,62 +712,228 @@ __global__ void __launch_bounds__(kThreads) holder_tile_kernel(
     uint32_t* __restrict__ holders) {
     extern __shared__ uint32_t sm[];
     const uint32_t E = part.E, F = part.F;
-    const uint32_t np = NP ? (uint32_t)NP : np_rt;
-    uint32_t* tinv = sm;                                            // [E][33]
-    uint16_t* trk = reinterpret_cast<uint16_t*>(sm + (size_t)E * 33);  // [E][33]
+    const uint32_t np = NP > 0 ? (uint32_t)NP : np_rt;
+    const uint32_t tile_words = E * kHtInv + (E * kHtRk + 1) / 2;
+    uint32_t* tinv_b[2] = {sm, sm + tile_words};
+    uint16_t* trk_b[2] = {reinterpret_cast<uint16_t*>(sm + E * kHtInv),
+                          reinterpret_cast<uint16_t*>(sm + tile_words + E * kHtInv)};
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-    for (uint64_t k0 = (uint64_t)blockIdx.x * 32; k0 < F; k0 += (uint64_t)gridDim.x * 32) {
-        __syncthreads();
-        for (uint32_t idx = threadIdx.x; idx < E * 32; idx += blockDim.x) {
-            const uint32_t e = idx >> 5, l = idx & 31;
-            const bool ok = k0 + l < F;
-            tinv[e * 33 + l] = ok ? __ldcs(inv + (size_t)e * F + k0 + l) : kNone;
-            trk[e * 33 + l] = ok ? __ldcs(rank16 + (size_t)e * F + k0 + l) : (uint16_t)0xFFFFu;
+    // all-fit: uint2 records; NP 0/1/2: the first uint4 of the record (+ overflow words)
+    using RecT = typename std::conditional<NP == -1, uint2, uint4>::type;
+    const uint32_t RW = NP == -1 ? 1u : Rp / 4;  // record stride in RecT units
+    const uint64_t stride = (uint64_t)gridDim.x * 32;
+    uint64_t k0 = (uint64_t)blockIdx.x * 32;
+    if (k0 < F) ht_issue(part, inv, rank16, k0, tinv_b[0], trk_b[0]);
+    for (uint32_t buf = 0; k0 < F; k0 += stride, buf ^= 1) {
+        if (k0 + stride < F) {  // prefetch the next tile into the other buffer
+            ht_issue(part, inv, rank16, k0 + stride, tinv_b[buf ^ 1], trk_b[buf ^ 1]);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
         }
         __syncthreads();
-        for (uint32_t s = warp; s < 32; s += nwarps) {
-            if (k0 + s >= F) break;
-            const uint64_t slot0 = pair_off[k0 + s];
+        const uint32_t* tinv = tinv_b[buf];
+        const uint16_t* trk = trk_b[buf];
+        for (uint32_t s0 = warp; s0 < 32; s0 += nwarps * SU) {
+            uint64_t slot0[SU];
+#pragma unroll
+            for (int u = 0; u < SU; ++u) {
+                const uint32_t s = s0 + u * nwarps;
+                slot0[u] = (s < 32 && k0 + s < F) ? pair_off[k0 + s] : 0;
+            }
             for (uint32_t e = lane; e < E; e += 32) {
-                const uint32_t rk = trk[e * 33 + s];
-                if (rk == 0xFFFFu) continue;
-                uint32_t w;
-                const uint32_t tseg = part.within_epoch(tinv[e * 33 + s], w);
-                const uint32_t wl = w - part.wbegin;
-                const uint64_t blk = ((uint64_t)wl * E + e) * MB + (tseg >> 5);
-                const uint32_t bit = tseg & 31;
-                const uint4* r4 = reinterpret_cast<const uint4*>(rec + blk * Rp);
-                const uint4 a = r4[0];
-                uint32_t cls, cm;
-                if constexpr (NP == 1) {
-                    cls = (a.x >> bit) & 1u;
-                    cm = a.x;
-                } else if constexpr (NP == 2) {
-                    const uint32_t b0 = (a.x >> bit) & 1u, b1 = (a.y >> bit) & 1u;
-                    cls = b0 | (b1 << 1);
-                    cm = (b0 ? a.x : ~a.x) & (b1 ? a.y : ~a.y);
-                } else {
-                    cls = 0;
-                    for (uint32_t q = 0; q < np; ++q) cls |= ((pick(a, q) >> bit) & 1u) << q;
-                    cm = 0xffffffffu;
-                    for (uint32_t q = 0; q < np; ++q) {
-                        const uint32_t pl = pick(a, q);
-                        cm &= ((cls >> q) & 1u) ? pl : ~pl;
+                uint32_t rk[SU], w[SU], bit[SU], wl[SU];
+                uint64_t blk[SU];
+                RecT a[SU];
+#pragma unroll
+                for (int u = 0; u < SU; ++u) {
+                    const uint32_t s = s0 + u * nwarps;
+                    rk[u] = (s < 32 && k0 + s < F) ? trk[e * kHtRk + s] : 0xFFFFu;
+                    if (rk[u] != 0xFFFFu) {
+                        const uint32_t tseg = part.within_epoch(tinv[e * kHtInv + s], w[u]);
+                        wl[u] = w[u] - part.wbegin;
+                        blk[u] = ((uint64_t)wl[u] * E + e) * MB + (tseg >> 5);
+                        bit[u] = tseg & 31;
+                        a[u] = reinterpret_cast<const RecT*>(rec)[blk[u] * RW];
                     }
                 }
-                uint32_t pos = 0;
-                if (cls) {
-                    const uint32_t wi = np + cls - 1;
-                    const uint32_t prew = wi < 4 ? pick(a, wi) : rec[blk * Rp + wi];
-                    pos = prew - cbase[wl * J + cls - 1] + __popc(cm & ((1u << bit) - 1u));
+#pragma unroll
+                for (int u = 0; u < SU; ++u) {
+                    if (rk[u] == 0xFFFFu) continue;
+                    uint32_t cls, pos = 0;
+                    const uint32_t below = (1u << bit[u]) - 1u;
+                    if constexpr (NP == -1) {
+                        cls = (a[u].x >> bit[u]) & 1u;
+                        if (cls) pos = a[u].y - cbase[wl[u] * J] + __popc(a[u].x & below);
+                    } else {
+                        const uint4 v = as4(a[u]);
+                        uint32_t cm;
+                        if constexpr (NP == 1) {
+                            cls = (v.x >> bit[u]) & 1u;
+                            cm = v.x;
+                        } else if constexpr (NP == 2) {
+                            const uint32_t b0 = (v.x >> bit[u]) & 1u, b1 = (v.y >> bit[u]) & 1u;
+                            cls = b0 | (b1 << 1);
+                            cm = (b0 ? v.x : ~v.x) & (b1 ? v.y : ~v.y);
+                        } else {
+                            cls = 0;
+                            for (uint32_t q = 0; q < np; ++q) cls |= ((pick(v, q) >> bit[u]) & 1u) << q;
+                            cm = 0xffffffffu;
+                            for (uint32_t q = 0; q < np; ++q) {
+                                const uint32_t pl = pick(v, q);
+                                cm &= ((cls >> q) & 1u) ? pl : ~pl;
+                            }
+                        }
+                        if (cls) {
+                            const uint32_t wi = np + cls - 1;
+                            const uint32_t prew = wi < 4 ? pick(v, wi) : rec[blk[u] * Rp + wi];
+                            pos = prew - cbase[wl[u] * J + cls - 1] + __popc(cm & below);
+                        }
+                    }
+                    uint32_t* h = holders + 3 * (slot0[u] + rk[u]);
+                    __stcs(h, w[u]);
+                    __stcs(h + 1, cls);
+                    __stcs(h + 2, pos);
                 }
-                uint32_t* h = holders + 3 * (slot0 + rk);
-                __stcs(h, w);
-                __stcs(h + 1, cls);
-                __stcs(h + 2, pos);
             }
         }
+        __syncthreads();  // the buffer is refilled by the prefetch two tiles later
     }
+}
+
+// ---------------------------------------------------------------------------- K4a (tile)
+// CTA = 32 samples: the tile inv[0..E)[k0..k0+32) arrives in shared memory by double-buffered
+// cp.async; one warp per sample, lanes = epochs (R rounds of 32).  Per-warp shared tables
+// indexed by local worker — first epoch (atomicMin), access count (atomicAdd) and a worker
+// bitmap (atomicOr) — give every pair's count and first access; the bitmap's popcount prefix
+// is the pair's rank (build_index worker order).  info / rank rows go back through a shared
+// output tile with coalesced stores.  Needs nloc <= kTileWorkers, E <= 32 R.
+constexpr uint32_t kTileWorkers = 1024;
+constexpr uint32_t kStInv = 33, kStOut = 34;
+
+__device__ __forceinline__ void st_issue(const uint32_t* inv, uint32_t E, uint32_t F, uint64_t k0,
+                                         uint32_t* tinv) {
+    const uint32_t n = (uint32_t)(F - k0 < 32 ? F - k0 : 32);
+    for (uint32_t idx = threadIdx.x; idx < E * 32; idx += blockDim.x) {
+        const uint32_t e = idx >> 5, l = idx & 31;
+        if (l < n) cp_async4(tinv + e * kStInv + l, inv + (size_t)e * F + k0 + l);
+    }
+    cp_async_commit();
+}
+
+template <int R>
+__global__ void __launch_bounds__(kThreads) sample_tile_kernel(Part part, const uint32_t* __restrict__ inv,
+                                                               uint16_t* __restrict__ info,
+                                                               uint16_t* __restrict__ rank16,
+                                                               uint32_t* __restrict__ pair_count,
+                                                               uint32_t W,
+                                                               uint32_t* __restrict__ seghist) {
+    extern __shared__ uint32_t sm[];
+    const uint32_t E = part.E, F = part.F;
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+    const uint32_t nloc = part.wend - part.wbegin;
+    uint32_t* tin[2] = {sm, sm + E * kStInv};
+    uint16_t* oinfo = reinterpret_cast<uint16_t*>(sm + 2 * E * kStInv);  // [E][34]
+    uint16_t* orank = oinfo + E * kStOut;                                 // [E][34]
+    uint32_t* tabs = sm + 2 * E * kStInv + E * kStOut;                    // per warp
+    uint32_t* fe = tabs + warp * (2 * W * 32 + W);  // [nloc] first epoch
+    uint32_t* cnt = fe + W * 32;                     // [nloc] count
+    uint32_t* bm = cnt + W * 32;                     // [W] worker bitmap
+    for (uint32_t x = lane; x < W * 32; x += 32) {
+        fe[x] = kNone;
+        cnt[x] = 0;
+    }
+    if (lane < W) bm[lane] = 0;
+    __syncwarp();
+    const uint64_t stride = (uint64_t)gridDim.x * 32;
+    uint64_t k0 = (uint64_t)blockIdx.x * 32;
+    if (k0 < F) st_issue(inv, E, F, k0, tin[0]);
+    for (uint32_t buf = 0; k0 < F; k0 += stride, buf ^= 1) {
+        if (k0 + stride < F) {
+            st_issue(inv, E, F, k0 + stride, tin[buf ^ 1]);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        const uint32_t* tinv = tin[buf];
+        for (uint32_t s = warp; s < 32; s += nwarps) {
+            const bool live = k0 + s < F;
+            uint32_t wl[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const uint32_t e = r * 32 + lane;
+                wl[r] = kNone;
+                if (live && e < E) {
+                    const uint32_t p = tinv[e * kStInv + s];
+                    if (p < part.P) {
+                        const uint32_t w = part.worker_of(p);
+                        if (w >= part.wbegin && w < part.wend) {
+                            const uint32_t x = w - part.wbegin;
+                            wl[r] = x;
+                            atomicMin(&fe[x], e);
+                            atomicAdd(&cnt[x], 1u);
+                            atomicOr(&bm[x >> 5], 1u << (x & 31));
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+            // exclusive popcount prefix of the bitmap words: lane t holds word t
+            const uint32_t word = lane < W ? bm[lane] : 0u;
+            const uint32_t c = __popc(word);
+            uint32_t inc = c;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+                if (lane >= (uint32_t)d) inc += o;
+            }
+            const uint32_t pre = inc - c;
+            const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
+            if (live && lane == 0) pair_count[k0 + s] = total;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const uint32_t e = r * 32 + lane;
+                const uint32_t x = wl[r];
+                const uint32_t xw = x != kNone ? x >> 5 : 0u;
+                const uint32_t pw = __shfl_sync(0xffffffffu, pre, xw);
+                const uint32_t ww = __shfl_sync(0xffffffffu, word, xw);
+                if (e < E) {
+                    uint16_t ci = 0, rk = 0xFFFFu;
+                    if (x != kNone && fe[x] == e) {
+                        ci = (uint16_t)cnt[x];
+                        rk = (uint16_t)(pw + __popc(ww & ((1u << (x & 31)) - 1u)));
+                        if (seghist) atomicAdd(&seghist[((uint64_t)x * E + (E - ci)) * E + e], 1u);
+                    }
+                    oinfo[e * kStOut + s] = ci;
+                    orank[e * kStOut + s] = rk;
+                }
+            }
+            __syncwarp();
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const uint32_t x = wl[r];
+                if (x != kNone) {
+                    fe[x] = kNone;
+                    cnt[x] = 0;
+                }
+            }
+            if (lane < W) bm[lane] = 0;
+            __syncwarp();
+        }
+        __syncthreads();
+        // coalesced write-back of the info / rank rows (u16 pairs)
+        const uint32_t n = (uint32_t)(F - k0 < 32 ? F - k0 : 32);
+        for (uint32_t idx = threadIdx.x; idx < E * 32; idx += blockDim.x) {
+            const uint32_t e = idx >> 5, l = idx & 31;
+            if (l < n) {
+                __stcs(info + (size_t)e * F + k0 + l, oinfo[e * kStOut + l]);
+                __stcs(rank16 + (size_t)e * F + k0 + l, orank[e * kStOut + l]);
+            }
+        }
+        // the output tile and the input buffer are reused after the next barrier
+    }
+    (void)nloc;
 }
 
 // ---------------------------------------------------------------------------- launchers
@@ -623,23 +978,34 @@ void launch_class_lens(cudaStream_t s, uint32_t nloc, uint32_t E, uint32_t MB, u
 
 void launch_holder_tile(cudaStream_t s, const Part& part, const uint32_t* inv, const uint16_t* rank16,
                         uint32_t MB, const uint32_t* rec, uint32_t np, uint32_t J, uint32_t Rp,
-                        const uint32_t* cbase, const uint64_t* pair_off, uint32_t* holders) {
-    const size_t smem = (size_t)part.E * 33 * 4 + (size_t)part.E * 33 * 2 + 16;
+                        const uint32_t* cbase, const uint64_t* pair_off, uint32_t* holders,
+                        bool allfit) {
+    const size_t smem = 2 * ((size_t)part.E * kHtInv * 4 + ((size_t)part.E * kHtRk * 2 + 3) / 4 * 4) + 16;
     const uint64_t tiles = ((uint64_t)part.F + 31) / 32;
     const unsigned grid = grid_for(tiles, 1, 148u * 16u);
-    if (np == 1) {
-        cudaFuncSetAttribute(holder_tile_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        holder_tile_kernel<1><<<grid, kThreads, smem, s>>>(part, inv, rank16, MB, rec, np, J, Rp,
-                                                           cbase, pair_off, holders);
-    } else if (np == 2) {
-        cudaFuncSetAttribute(holder_tile_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        holder_tile_kernel<2><<<grid, kThreads, smem, s>>>(part, inv, rank16, MB, rec, np, J, Rp,
-                                                           cbase, pair_off, holders);
+#define HT_LAUNCH(NPV, SUV)                                                                      \
+    do {                                                                                         \
+        cudaFuncSetAttribute(holder_tile_kernel<NPV, SUV>,                                       \
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);            \
+        holder_tile_kernel<NPV, SUV><<<grid, kThreads, smem, s>>>(part, inv, rank16, MB, rec, np, J, \
+                                                                  Rp, cbase, pair_off, holders); \
+    } while (0)
+    static const int su = [] {
+        const char* v = getenv("CLAIRPLAN_HT_SU");
+        return v ? atoi(v) : 1;
+    }();
+    if (su >= 2) {
+        if (allfit) HT_LAUNCH(-1, 2);
+        else if (np == 1) HT_LAUNCH(1, 2);
+        else if (np == 2) HT_LAUNCH(2, 2);
+        else HT_LAUNCH(0, 2);
     } else {
-        cudaFuncSetAttribute(holder_tile_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        holder_tile_kernel<0><<<grid, kThreads, smem, s>>>(part, inv, rank16, MB, rec, np, J, Rp,
-                                                           cbase, pair_off, holders);
+        if (allfit) HT_LAUNCH(-1, 1);
+        else if (np == 1) HT_LAUNCH(1, 1);
+        else if (np == 2) HT_LAUNCH(2, 1);
+        else HT_LAUNCH(0, 1);
     }
+#undef HT_LAUNCH
 }
 
 void launch_sample_lanes(cudaStream_t s, const Part& part, const uint32_t* inv, uint16_t* info,
@@ -651,6 +1017,33 @@ void launch_sample_lanes(cudaStream_t s, const Part& part, const uint32_t* inv, 
     const uint64_t groups = ((uint64_t)part.F + 31) / 32;
     sample_lanes_kernel<<<grid_for(groups, 4, 148u * 8u), 128, smem, s>>>(part, inv, info, rank16,
                                                                          pair_count, W, seghist);
+}
+
+bool tile_path_ok(const Part& part) {
+    return (part.wend - part.wbegin) <= kTileWorkers && part.E <= 128;
+}
+
+void launch_sample_tile(cudaStream_t s, const Part& part, const uint32_t* inv, uint16_t* info,
+                        uint16_t* rank16, uint32_t* pair_count, uint32_t* seghist) {
+    const uint32_t nloc = part.wend - part.wbegin;
+    const uint32_t W = (nloc + 31) / 32;
+    const size_t smem = (size_t)4 * (2 * part.E * kStInv + part.E * kStOut +
+                                     (kThreads / 32) * (2 * W * 32 + W));
+    const uint64_t tiles = ((uint64_t)part.F + 31) / 32;
+    const unsigned grid = grid_for(tiles, 1, 148u * 8u);
+#define ST_LAUNCH(RV)                                                                             \
+    do {                                                                                          \
+        cudaFuncSetAttribute(sample_tile_kernel<RV>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
+                             (int)smem);                                                          \
+        sample_tile_kernel<RV><<<grid, kThreads, smem, s>>>(part, inv, info, rank16, pair_count,  \
+                                                            W, seghist);                          \
+    } while (0)
+    const uint32_t R = (part.E + 31) / 32;
+    if (R == 1) ST_LAUNCH(1);
+    else if (R == 2) ST_LAUNCH(2);
+    else if (R == 3) ST_LAUNCH(3);
+    else ST_LAUNCH(4);
+#undef ST_LAUNCH
 }
 
 void launch_sample_hash(cudaStream_t s, const Part& part, const uint32_t* inv, uint16_t* info,
@@ -668,12 +1061,13 @@ void launch_sample_hash(cudaStream_t s, const Part& part, const uint32_t* inv, u
 }
 
 void launch_seg_hist(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info,
-                     uint32_t* seghist, uint32_t* segcnt) {
+                     uint32_t* seghist, uint32_t* segcnt, const double* sizes, double* segsum,
+                     double* segmin) {
     const uint64_t nseg = (uint64_t)(part.wend - part.wbegin) * part.E;
     const size_t smem = (size_t)(kThreads / 32) * part.E * 4;
     cudaFuncSetAttribute(seg_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     seg_hist_kernel<<<grid_for(nseg * 32, kThreads, 148u * 64u), kThreads, smem, s>>>(
-        part, stream, info, seghist, segcnt);
+        part, stream, info, seghist, segcnt, sizes, segsum, segmin);
 }
 
 void launch_seg_write2(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info,

@@ -1,6 +1,8 @@
 // Internal declarations shared by the clairplan translation units (not part of the ABI).
 #pragma once
 #include <cuda_runtime.h>
+
+#include <algorithm>
 #include <stddef.h>
 #include <stdint.h>
 
@@ -82,6 +84,15 @@ void launch_fy_emit(cudaStream_t s, uint64_t key, const Part& part, uint32_t e0,
                     const uint32_t* succ, const uint32_t* q, const RejTable& rt, uint32_t* inv,
                     uint32_t* stream, uint32_t* perm_out);
 
+// epoch ranges of the source ranks of an all-to-all: source r holds [eb[r], eb[r+1])
+constexpr uint32_t kMaxRanks = 64;
+struct EpochSplit {
+    uint32_t G;
+    uint32_t eb[kMaxRanks + 1];
+};
+void launch_stream_relayout(cudaStream_t s, const Part& part, const EpochSplit& es,
+                            const uint32_t* recv, uint32_t* stream);
+void launch_stream_inv(cudaStream_t s, const Part& part, const uint32_t* stream, uint32_t* inv);
 void launch_perm_scatter(cudaStream_t s, const Part& part, const uint32_t* perms, uint32_t* inv,
                          uint32_t* stream);
 
@@ -139,13 +150,23 @@ void launch_stream_hist(cudaStream_t s, const uint32_t* st, uint64_t n, uint32_t
 bool lane_path_ok(const Part& part);
 void launch_sample_lanes(cudaStream_t s, const Part& part, const uint32_t* inv, uint16_t* info,
                          uint16_t* rank16, uint32_t* pair_count, uint32_t* seghist);
+bool tile_path_ok(const Part& part);
+void launch_sample_tile(cudaStream_t s, const Part& part, const uint32_t* inv, uint16_t* info,
+                        uint16_t* rank16, uint32_t* pair_count, uint32_t* seghist);
 void launch_sample_hash(cudaStream_t s, const Part& part, const uint32_t* inv, uint16_t* info,
                         uint16_t* rank16, uint32_t* pair_count, const uint32_t* list,
                         const uint32_t* nlist, uint64_t max_items, uint32_t* seghist);
 void launch_segcnt(cudaStream_t s, uint32_t nloc, uint32_t E, const uint32_t* seghist,
                    uint32_t* segcnt);
 void launch_seg_hist(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info,
-                     uint32_t* seghist, uint32_t* segcnt);
+                     uint32_t* seghist, uint32_t* segcnt, const double* sizes = nullptr,
+                     double* segsum = nullptr, double* segmin = nullptr);
+void launch_fit_check(cudaStream_t s, uint32_t nloc, uint32_t E, const double* segsum,
+                      const double* segmin, const uint32_t* segcnt, double C, uint32_t* allfit);
+void launch_seg_first(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info,
+                      const uint64_t* seg_off, uint32_t MB, uint32_t* rec, uint32_t* class_list);
+void launch_allfit_meta(cudaStream_t s, uint32_t nloc, uint32_t E, uint32_t J, const uint64_t* seg_off,
+                        uint64_t* clen, uint64_t* cstart, uint32_t* cbase);
 void launch_seg_write2(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info,
                        const double* sizes, const uint64_t* seg_off, const uint64_t* sorted_base,
                        uint32_t MB, uint32_t* dest, double* sorted_size, uint32_t* blkmask,
@@ -165,6 +186,7 @@ void launch_class_lens(cudaStream_t s, uint32_t nloc, uint32_t E, uint32_t MB, u
                        const uint64_t* cpre, uint64_t nblk, uint64_t* clen);
 void launch_holder_tile(cudaStream_t s, const Part& part, const uint32_t* inv, const uint16_t* rank16,
                         uint32_t MB, const uint32_t* rec, uint32_t np, uint32_t J, uint32_t Rp,
-                        const uint32_t* cbase, const uint64_t* pair_off, uint32_t* holders);
+                        const uint32_t* cbase, const uint64_t* pair_off, uint32_t* holders,
+                        bool allfit);
 
 }  // namespace clairplan

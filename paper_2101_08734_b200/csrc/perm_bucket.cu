@@ -6,7 +6,7 @@
 //             block (TB targets) in shared memory and write them tile-major:
 //             bucket[t*TS + lst[t][b] ...] = (i - t*TS) << lgTB | (j_i mod TB)
 //   fyb_block (per target block)      gather the block's runs from every tile, sort by
-//             target (shared-memory counting sort + per-target insertion sort) and write
+//             target (shared-memory counting sort; rank/next writer found within the group) and write
 //             q[y] = smallest writer != y, succ[w_k] = w_{k+1} (the last writer keeps none:
 //             its value is its own draw) and inv[y] = w_m for every target with a writer
 //   fyb_emit  (per step)              out[i] = V(succ(i)) (chase through q) or j_i; writes
@@ -46,84 +46,36 @@ bool fy_geometry(uint32_t F, FyGeom& g) {
     return true;
 }
 
-// In-place exclusive scan of a[0..n) in shared memory (all T threads call); returns the total.
+// Exclusive scan of a[0..n) in place, T values per round (one per thread, conflict-free);
+// all T threads call, returns the total.  wsum: T/32 words.
 template <uint32_t T>
-__device__ uint32_t smem_exscan(uint32_t* a, uint32_t n, uint32_t* wsum) {
+__device__ __forceinline__ uint32_t blk_exscan(uint32_t* a, uint32_t n, uint32_t* wsum) {
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t per = (n + T - 1) / T;
-    const uint32_t beg = min(n, tid * per), end = min(n, beg + per);
-    uint32_t loc = 0;
-    for (uint32_t k = beg; k < end; ++k) loc += a[k];
-    uint32_t inc = loc;
+    constexpr uint32_t NW = T / 32;
+    uint32_t carry = 0;
+    for (uint32_t base = 0; base < n; base += T) {
+        const uint32_t k = base + tid;
+        const uint32_t v = k < n ? a[k] : 0u;
+        uint32_t inc = v;
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
-        if (lane >= (uint32_t)d) inc += o;
-    }
-    if (lane == 31) wsum[warp] = inc;
-    __syncthreads();
-    if (warp == 0) {
-        constexpr uint32_t nw = T >> 5;
-        const uint32_t v = lane < nw ? wsum[lane] : 0;
-        uint32_t x = v;
-#pragma unroll
-        for (int d = 1; d < (int)nw; d <<= 1) {
-            const uint32_t o = __shfl_up_sync(0xffffffffu, x, d);
-            if (lane >= (uint32_t)d) x += o;
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+            if (lane >= (uint32_t)d) inc += o;
         }
-        if (lane < nw) wsum[lane] = x - v;  // exclusive warp offsets
-        if (lane == nw - 1) wsum[32] = x;   // total
-    }
-    __syncthreads();
-    uint32_t run = wsum[warp] + inc - loc;
-    for (uint32_t k = beg; k < end; ++k) {
-        const uint32_t v = a[k];
-        a[k] = run;
-        run += v;
-    }
-    const uint32_t total = wsum[32];
-    __syncthreads();
-    return total;
-}
-
-// In-place inclusive max-scan of a[0..n) in shared or global memory (all T threads call).
-template <uint32_t T>
-__device__ void block_maxscan(uint32_t* a, uint32_t n, uint32_t* wsum) {
-    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t per = (n + T - 1) / T;
-    const uint32_t beg = min(n, tid * per), end = min(n, beg + per);
-    uint32_t loc = 0;
-    for (uint32_t k = beg; k < end; ++k) loc = max(loc, a[k]);
-    uint32_t inc = loc;
+        if (lane == 31) wsum[warp] = inc;
+        __syncthreads();
+        uint32_t wofs = 0, tot = 0;
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
-        if (lane >= (uint32_t)d) inc = max(inc, o);
-    }
-    uint32_t exc = __shfl_up_sync(0xffffffffu, inc, 1);
-    if (lane == 0) exc = 0;
-    if (lane == 31) wsum[warp] = inc;
-    __syncthreads();
-    if (warp == 0) {
-        constexpr uint32_t nw = T >> 5;
-        const uint32_t v = lane < nw ? wsum[lane] : 0;
-        uint32_t x = v;
-#pragma unroll
-        for (int d = 1; d < (int)nw; d <<= 1) {
-            const uint32_t o = __shfl_up_sync(0xffffffffu, x, d);
-            if (lane >= (uint32_t)d) x = max(x, o);
+        for (uint32_t w = 0; w < NW; ++w) {
+            const uint32_t s = wsum[w];
+            wofs += w < warp ? s : 0u;
+            tot += s;
         }
-        uint32_t xe = __shfl_up_sync(0xffffffffu, x, 1);
-        if (lane == 0) xe = 0;
-        if (lane < nw) wsum[lane] = xe;  // exclusive max over earlier warps
+        if (k < n) a[k] = carry + wofs + inc - v;
+        carry += tot;
+        __syncthreads();
     }
-    __syncthreads();
-    uint32_t run = max(wsum[warp], exc);
-    for (uint32_t k = beg; k < end; ++k) {
-        run = max(run, a[k]);
-        a[k] = run;
-    }
-    __syncthreads();
+    return carry;
 }
 
 struct FyRej {
@@ -192,7 +144,7 @@ __global__ void __launch_bounds__(kTileThreads) fyb_tile_kernel(uint64_t key, ui
         }
     }
     __syncthreads();
-    smem_exscan<kTileThreads>(hist, nbt + 1, wsum);  // hist[nbt] == 0 before: the tile total
+    blk_exscan<kTileThreads>(hist, nbt + 1, wsum);  // hist[nbt] == 0 before: the tile total
     uint32_t* row = lst + ((size_t)slot * g.NT + t) * (g.NB + 1);
     const uint32_t total = hist[nbt];
     for (uint32_t b = threadIdx.x; b <= g.NB; b += kTileThreads) row[b] = b <= nbt ? hist[b] : total;
@@ -230,72 +182,97 @@ __global__ void __launch_bounds__(kTileThreads) fyb_tile_kernel(uint64_t key, ui
 }
 
 // ---- fyb_block: one block of TB targets -> q, succ, inv ------------------------------------
-// BIG: more writers than the shared-memory capacity (blocks of small targets): W/S/J live in
-// a global pool slab (L2-resident) instead.
+// 1. run table: the block's run in every tile t >= tmin (two words of each lst row) and the
+//    exclusive scan of the run lengths (element k of the block <-> run r, offset k - rdst[r])
+// 2. gather, warp per 32 consecutive elements (balanced, coalesced: consecutive elements
+//    mostly share a run): one warp-uniform binary search finds the run of the first element,
+//    the next 32 run starts sit in the lanes and a 5-step shuffle search places every
+//    element; each element is pushed on its target's list (head[target], nxt[element]) with
+//    a shared atomicExch — no counting sort, no scan
+// 3. per writer: walk its target's list for its rank and the next larger writer ->
+//    q[y] (smallest writer != y), succ[w] (non-last writers; succ is preset to kNone) and
+//    inv[y] = last writer; targets whose list is empty get q = kNone
+// BIG: more writers than the shared-memory capacity (blocks of small targets): W/J/nxt live
+// in a global pool slab (L2-resident) instead.
 template <bool BIG>
 __device__ __forceinline__ void fyb_block_body(uint32_t F, const FyGeom& g, uint32_t b, uint32_t n,
-                                               uint32_t nt, uint32_t tmin, const uint32_t* tlo,
-                                               const uint32_t* tdst, uint32_t* cnt, uint32_t* W,
-                                               uint32_t* S, uint16_t* JL16, uint32_t* J32,
-                                               uint16_t* SJ16, uint32_t* SJ32, uint32_t* wsum, const uint32_t* bk, uint32_t* sc,
+                                               uint32_t nt, uint32_t tmin, const uint32_t* rsrc,
+                                               const uint32_t* rdst, uint32_t* head, uint32_t* W,
+                                               uint16_t* J16, uint16_t* N16, uint32_t* J32,
+                                               uint32_t* N32, const uint32_t* bk, uint32_t* sc,
                                                uint32_t* qq, uint32_t* iv) {
-    const uint32_t TB = 1u << g.lgTB, TS = 1u << g.lgTS, tbmask = TB - 1;
-    // owner run of every element: mark run starts, then a max-scan (S is free until the
-    // scatter below)
-    for (uint32_t k = threadIdx.x; k < n; k += kBlockThreads) S[k] = 0;
-    __syncthreads();
-    for (uint32_t k = threadIdx.x; k < nt; k += kBlockThreads)
-        if (tdst[k + 1] > tdst[k]) S[tdst[k]] = k;
-    __syncthreads();
-    block_maxscan<kBlockThreads>(S, n, wsum);
-    // gather: thread per element, consecutive elements mostly share a run (coalesced)
-    for (uint32_t k = threadIdx.x; k < n; k += kBlockThreads) {
-        const uint32_t r = S[k], t = tmin + r;
-        const uint32_t v = __ldcs(bk + (size_t)t * TS + tlo[r] + (k - tdst[r]));
-        const uint32_t jl = v & tbmask;
-        W[k] = t * TS + (v >> g.lgTB);
-        if constexpr (BIG) J32[k] = jl;
-        else JL16[k] = (uint16_t)jl;
-        atomicAdd(&cnt[jl], 1u);
-    }
-    __syncthreads();
-    smem_exscan<kBlockThreads>(cnt, TB + 1, wsum);  // cnt[TB] == 0 before: becomes n
-    // scatter by target; cnt[jl] advances to the end of its group (= start of the next)
-    for (uint32_t k = threadIdx.x; k < n; k += kBlockThreads) {
-        uint32_t jl;
-        if constexpr (BIG) jl = J32[k];
-        else jl = JL16[k];
-        const uint32_t pos = atomicAdd(&cnt[jl], 1u);
-        S[pos] = W[k];
-        if constexpr (BIG) SJ32[pos] = jl;
-        else SJ16[pos] = (uint16_t)jl;
+    const uint32_t TB = 1u << g.lgTB, tbmask = TB - 1;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr uint32_t kEnd = BIG ? kNone : 0xFFFFu;
+    for (uint32_t x0 = warp * 32; x0 < n; x0 += kBlockThreads) {
+        // r0 = run of element x0 (largest r with rdst[r] <= x0; warp-uniform search)
+        uint32_t lo = 0, hi = nt;
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (rdst[mid] <= x0) lo = mid;
+            else hi = mid;
+        }
+        const uint32_t r0 = lo;
+        const uint32_t r = r0 + lane;
+        const uint32_t beg = r < nt ? rdst[r] : n;
+        const uint32_t src = r < nt ? rsrc[r] : 0u;
+        const uint32_t lim = r0 + 32 < nt ? rdst[r0 + 32] : n;  // runs r0..r0+31 end here
+        const uint32_t k = x0 + lane;
+        uint32_t j = 0;
+#pragma unroll
+        for (uint32_t step = 16; step; step >>= 1) {
+            const uint32_t bc = __shfl_sync(0xffffffffu, beg, j + step);
+            if (bc <= k) j += step;
+        }
+        uint32_t bj = __shfl_sync(0xffffffffu, beg, j);
+        uint32_t sj = __shfl_sync(0xffffffffu, src, j);
+        uint32_t rr = r0 + j;
+        if (k < n) {
+            if (k >= lim) {  // beyond 32 runs (many empty runs): full search
+                uint32_t l2 = r0, h2 = nt;
+                while (h2 - l2 > 1) {
+                    const uint32_t mid = (l2 + h2) >> 1;
+                    if (rdst[mid] <= k) l2 = mid;
+                    else h2 = mid;
+                }
+                rr = l2;
+                bj = rdst[rr];
+                sj = rsrc[rr];
+            }
+            const uint32_t v = __ldcs(bk + sj + (k - bj));
+            const uint32_t jl = v & tbmask;
+            W[k] = ((tmin + rr) << g.lgTS) + (v >> g.lgTB);
+            const uint32_t old = atomicExch(&head[jl], k);
+            if constexpr (BIG) {
+                J32[k] = jl;
+                N32[k] = old;
+            } else {
+                J16[k] = (uint16_t)jl;
+                N16[k] = (uint16_t)old;
+            }
+        }
     }
     __syncthreads();
     const uint32_t y0 = b << g.lgTB;
-    // targets without a writer: q = none
     for (uint32_t tt = threadIdx.x; tt < TB; tt += kBlockThreads) {
         const uint32_t y = y0 + tt;
         if (y >= F) break;
-        if (cnt[tt] == (tt ? cnt[tt - 1] : 0u)) qq[y] = kNone;
+        if (head[tt] == kEnd) qq[y] = kNone;  // no writer
     }
-    // per writer (no per-group sort): rank among its group and the next larger writer
-    for (uint32_t p = threadIdx.x; p < n; p += kBlockThreads) {
-        const uint32_t w = S[p];
-        uint32_t jl;
-        if constexpr (BIG) jl = SJ32[p];
-        else jl = SJ16[p];
-        const uint32_t s0 = jl ? cnt[jl - 1] : 0u, s1 = cnt[jl];
+    for (uint32_t k = threadIdx.x; k < n; k += kBlockThreads) {
+        const uint32_t w = W[k];
+        const uint32_t jl = BIG ? J32[k] : (uint32_t)J16[k];
         bool first = true;
         uint32_t nx = kNone;
-        for (uint32_t a = s0; a < s1; ++a) {
-            const uint32_t v = S[a];
+        for (uint32_t a = head[jl]; a != kEnd; a = BIG ? N32[a] : (uint32_t)N16[a]) {
+            const uint32_t v = W[a];
             first &= !(v < w);
             nx = v > w ? min(nx, v) : nx;
         }
         const uint32_t y = y0 + jl;
         if (first) qq[y] = w != y ? w : nx;   // smallest writer != y
         if (nx == kNone) {
-            if (iv) iv[y] = w;                // the last writer places y (out[w_m] = j = y)
+            if (iv) iv[y] = w;                 // the last writer places y (out[w_m] = j = y)
         } else {
             sc[w] = nx;
         }
@@ -312,43 +289,43 @@ __global__ void __launch_bounds__(kBlockThreads) fyb_block_kernel(uint32_t F, Fy
                                                                   uint32_t e0,
                                                                   uint32_t* __restrict__ inv) {
     extern __shared__ uint32_t sm[];
-    __shared__ uint32_t wsum[33];
+    __shared__ uint32_t wsum[kBlockThreads / 32];
     __shared__ uint32_t s_pool;
     const uint32_t b = blockIdx.x, slot = blockIdx.y;
     const uint32_t TB = 1u << g.lgTB;
     const uint32_t tmin = (uint32_t)(((uint64_t)b << g.lgTB) >> g.lgTS);
     const uint32_t nt = g.NT - tmin;
-    uint32_t* cnt = sm;                 // [TB + 1]
-    uint32_t* tdst = cnt + TB + 1;      // [NT + 1] run offsets within the block
-    uint32_t* tlo = tdst + g.NT + 1;    // [NT] run starts within their tile
-    uint32_t* W = tlo + g.NT;           // [cap]  writer step
-    uint32_t* S = W + g.cap;            // [cap]  owner run, then writers grouped by target
-    uint16_t* JL = reinterpret_cast<uint16_t*>(S + g.cap);  // [cap] target within block
-    uint16_t* SJ = JL + g.cap;                               // [cap] same, grouped order
+    uint32_t* head = sm;                // [TB]
+    uint32_t* rdst = head + TB;         // [NT + 1] run offsets within the block
+    uint32_t* rsrc = rdst + g.NT + 1;   // [NT] run starts within the epoch's bucket row
+    uint32_t* W = rsrc + g.NT;          // [cap]  writer step
+    uint16_t* J16 = reinterpret_cast<uint16_t*>(W + g.cap);  // [cap] target within block
+    uint16_t* N16 = J16 + g.cap;                              // [cap] next on the target's list
     const uint32_t* rows = lst + (size_t)slot * g.NT * (g.NB + 1);
-    for (uint32_t k = threadIdx.x; k <= TB; k += kBlockThreads) cnt[k] = 0;
     for (uint32_t k = threadIdx.x; k < nt; k += kBlockThreads) {
         const uint32_t* r = rows + (size_t)(tmin + k) * (g.NB + 1) + b;
         const uint32_t lo = r[0];
-        tlo[k] = lo;
-        tdst[k] = r[1] - lo;
+        rsrc[k] = ((tmin + k) << g.lgTS) + lo;
+        rdst[k] = r[1] - lo;
     }
-    if (threadIdx.x == 0) tdst[nt] = 0;
     __syncthreads();
-    const uint32_t n = smem_exscan<kBlockThreads>(tdst, nt + 1, wsum);
+    const uint32_t n = blk_exscan<kBlockThreads>(rdst, nt, wsum);
     const uint32_t* bk = bucket + (size_t)slot * F;
     uint32_t* sc = succ + (size_t)slot * F;
     uint32_t* qq = q + (size_t)slot * F;
     uint32_t* iv = inv ? inv + (size_t)(e0 + slot) * F : nullptr;
     if (n <= g.cap) {
-        fyb_block_body<false>(F, g, b, n, nt, tmin, tlo, tdst, cnt, W, S, JL, nullptr, SJ,
-                              nullptr, wsum, bk, sc, qq, iv);
+        for (uint32_t k = threadIdx.x; k < TB; k += kBlockThreads) head[k] = 0xFFFFu;
+        __syncthreads();
+        fyb_block_body<false>(F, g, b, n, nt, tmin, rsrc, rdst, head, W, J16, N16, nullptr,
+                              nullptr, bk, sc, qq, iv);
     } else {  // heavy block (small targets): global pool slab
-        if (threadIdx.x == 0) s_pool = atomicAdd(pool_used + slot, 4 * n);
+        for (uint32_t k = threadIdx.x; k < TB; k += kBlockThreads) head[k] = kNone;
+        if (threadIdx.x == 0) s_pool = atomicAdd(pool_used + slot, 3 * n);
         __syncthreads();
         uint32_t* gW = pool + (size_t)slot * 4 * F + s_pool;
-        fyb_block_body<true>(F, g, b, n, nt, tmin, tlo, tdst, cnt, gW, gW + n, nullptr,
-                             gW + 2 * n, nullptr, gW + 3 * n, wsum, bk, sc, qq, iv);
+        fyb_block_body<true>(F, g, b, n, nt, tmin, rsrc, rdst, head, gW, nullptr, nullptr,
+                             gW + n, gW + 2 * n, bk, sc, qq, iv);
     }
 }
 
@@ -428,7 +405,7 @@ __global__ void __launch_bounds__(kThreads) fyb_emit_kernel(uint64_t key, Part p
 
 // ---- launchers --------------------------------------------------------------------------
 size_t fyb_block_smem(const FyGeom& g) {
-    return (size_t)4 * ((1u << g.lgTB) + 1 + 2 * g.NT + 1 + 2 * g.cap) + 4 * (size_t)g.cap;
+    return (size_t)4 * ((1u << g.lgTB) + 2 * g.NT + 1 + g.cap) + 4 * (size_t)g.cap;
 }
 
 template <int K>

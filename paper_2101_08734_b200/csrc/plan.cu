@@ -41,10 +41,12 @@ RejTable rej_table(clairplan_plan* p) {
     return rt;
 }
 
-// Enqueues the permutations of epochs [0, E): stream + inverse (or plain permutations).
+// Enqueues the permutations of epochs [e_first, e_first + e_count): stream + inverse (or plain
+// permutations).  `spart` (optional) replaces the handle's stream geometry.
 int enqueue_perms(clairplan_plan* p, uint32_t* stream_out, uint32_t* inv_out, uint32_t* perm_out,
-                  uint32_t e_first, uint32_t e_count) {
-    const uint32_t F = p->part.F;
+                  uint32_t e_first, uint32_t e_count, const Part* spart = nullptr) {
+    const Part& part = spart ? *spart : p->part;  // stream geometry (epoch-range streams)
+    const uint32_t F = part.F;
     bool ok = true;
     const RejTable rt = rej_table(p);
     static const char* mode_env = getenv("CLAIRPLAN_FY");  // "lists" / "table" (A/B only)
@@ -62,7 +64,7 @@ int enqueue_perms(clairplan_plan* p, uint32_t* stream_out, uint32_t* inv_out, ui
         if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed (permutation workspace)");
         for (uint32_t e0 = e_first; e0 < e_first + e_count; e0 += EB) {
             const uint32_t ne = std::min(EB, e_first + e_count - e0);
-            launch_fyb(p->stream, p->key, p->part, e0, ne, g, rt, p->rej_flag.get<uint32_t>(),
+            launch_fyb(p->stream, p->key, part, e0, ne, g, rt, p->rej_flag.get<uint32_t>(),
                        bucket, lst, pool, pool_used, succ, q, inv_out, stream_out,
                        perm_out ? perm_out + (size_t)(e0 - e_first) * F : nullptr);
             p->launches += 3;
@@ -89,11 +91,11 @@ int enqueue_perms(clairplan_plan* p, uint32_t* stream_out, uint32_t* inv_out, ui
                             p->rej_flag.get<uint32_t>());
             if (fy_out_mode) {
                 launch_fy_qmin(p->stream, F, ne, tbl, ovh, ovn, q);
-                launch_fy_out(p->stream, p->part, e0, ne, tbl, ovh, ovn, q, inv_out, stream_out,
+                launch_fy_out(p->stream, part, e0, ne, tbl, ovh, ovn, q, inv_out, stream_out,
                               perm_out ? perm_out + (size_t)(e0 - e_first) * F : nullptr);
             } else {
                 launch_fy_succ(p->stream, F, ne, tbl, ovh, ovn, succ, q);
-                launch_fy_emit(p->stream, p->key, p->part, e0, ne, succ, q, rt, inv_out, stream_out,
+                launch_fy_emit(p->stream, p->key, part, e0, ne, succ, q, rt, inv_out, stream_out,
                                perm_out ? perm_out + (size_t)(e0 - e_first) * F : nullptr);
             }
             p->launches += 3;
@@ -117,7 +119,7 @@ int enqueue_perms(clairplan_plan* p, uint32_t* stream_out, uint32_t* inv_out, ui
         launch_fy_link(p->stream, p->key, F, e0, ne, head, next, rt, p->rej_flag.get<uint32_t>(),
                        false, F);
         launch_fy_group(p->stream, F, ne, head, next, q, scratch, scap, counters, counters + 1);
-        launch_fy_emit(p->stream, p->key, p->part, e0, ne, next, q, rt, inv_out, stream_out,
+        launch_fy_emit(p->stream, p->key, part, e0, ne, next, q, rt, inv_out, stream_out,
                        perm_out ? perm_out + (size_t)(e0 - e_first) * F : nullptr);
         p->launches += 3;
     }
@@ -499,12 +501,15 @@ int first_fit_classes(clairplan_plan* p, const double* ssize, uint8_t* cls) {
 }
 
 
+int holders_v2(clairplan_plan* p);
+int no_classes_v2(clairplan_plan* p);
+
 // K6-K8 of the v2 path on the cached tier-ordered sizes / block masks: first fit, block class
 // records, class lists, holder CSR.  Also the whole of clairplan_reassign.
 int assign_v2(clairplan_plan* p) {
     cudaStream_t s = p->stream;
     const Part& part = p->part;
-    const uint32_t F = part.F, E = part.E, nloc = p->nloc, J = p->cfg.num_classes;
+    const uint32_t E = part.E, nloc = p->nloc, J = p->cfg.num_classes;
     const uint32_t MB = p->v2_mb;
     const uint64_t nblk = p->v2_nblk;
     const uint64_t D = p->D;
@@ -512,15 +517,11 @@ int assign_v2(clairplan_plan* p) {
     while ((1u << np) <= J) ++np;
     bool ok = true;
     uint32_t* stream_buf = p->stream_buf.get<uint32_t>();
-    uint32_t* inv = p->inv.get<uint32_t>();
-    uint16_t* rank16 = p->rank16.get<uint16_t>();
-    uint64_t* poff = p->pair_off.get<uint64_t>();
     uint32_t* bmask = p->blkmask.get<uint32_t>();
     uint32_t* bbase = p->blkbase.get<uint32_t>();
     uint32_t* dest = p->dest.get<uint32_t>();
     double* ssize = p->sorted_size.get<double>();
     uint8_t* cls = need<uint8_t>(p->cand_cls, D, ok);
-    uint32_t* htmp = need<uint32_t>(p->holders_tmp, 3 * D, ok);
     uint32_t* centries = need<uint32_t>(p->class_entries, D, ok);
     const uint32_t Rp = ((np + J) + 3) & ~3u;
     uint32_t* rec = need<uint32_t>(p->planes, (uint64_t)std::max<uint32_t>(Rp, 4) * nblk, ok);
@@ -543,12 +544,39 @@ int assign_v2(clairplan_plan* p) {
         exclusive_scan(s, clen, (uint64_t)nloc * J, cstart, p->ws);
         launch_class_write(s, part, MB, stream_buf, rec, np, J, Rp, cbase, cstart, centries, nblk);
         p->launches += 4 + 3 * J + 3;
+        return holders_v2(p);
+    }
+    return no_classes_v2(p);
+}
+
+// K8 and the host-side class-list geometry, after the block records, class bases and class
+// lists exist (general path or all-fit path).
+int holders_v2(clairplan_plan* p) {
+    cudaStream_t s = p->stream;
+    const Part& part = p->part;
+    const uint32_t F = part.F, nloc = p->nloc, J = p->cfg.num_classes;
+    const uint64_t D = p->D;
+    uint32_t np = 0;
+    while ((1u << np) <= J) ++np;
+    const uint32_t Rp = ((np + J) + 3) & ~3u;
+    bool ok = true;
+    uint32_t* inv = p->inv.get<uint32_t>();
+    uint16_t* rank16 = p->rank16.get<uint16_t>();
+    uint64_t* poff = p->pair_off.get<uint64_t>();
+    uint32_t* htmp = need<uint32_t>(p->holders_tmp, 3 * D, ok);
+    uint32_t* rec = p->planes.get<uint32_t>();
+    uint32_t* cbase = p->cbase.get<uint32_t>();
+    uint64_t* clen = p->class_len.get<uint64_t>();
+    uint64_t* cstart = p->class_start.get<uint64_t>();
+    const uint32_t MB = p->v2_mb;
+    if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed (holders)");
+    {
         std::vector<uint64_t> hlen((size_t)nloc * J), hst((size_t)nloc * J);
         CK(cudaMemcpyAsync(hlen.data(), clen, hlen.size() * 8, cudaMemcpyDeviceToHost, s));
         CK(cudaMemcpyAsync(hst.data(), cstart, hst.size() * 8, cudaMemcpyDeviceToHost, s));
         p->mark(7);
         // K8: holder CSR, sample-major
-        launch_holder_tile(s, part, inv, rank16, MB, rec, np, J, Rp, cbase, poff, htmp);
+        launch_holder_tile(s, part, inv, rank16, MB, rec, np, J, Rp, cbase, poff, htmp, p->allfit);
         ++p->launches;
         CK(cudaStreamSynchronize(s));
         p->class_start_h.assign((size_t)nloc * (J + 1), 0);
@@ -576,7 +604,15 @@ int assign_v2(clairplan_plan* p) {
             p->holder_off_dev = ho;
             p->holders_dev = hl;
         }
-    } else {
+    }
+    return 0;
+}
+
+int no_classes_v2(clairplan_plan* p) {
+    cudaStream_t s = p->stream;
+    const uint32_t F = p->part.F, nloc = p->nloc;
+    bool ok = true;
+    {
         p->H = 0;
         uint64_t* ho = need<uint64_t>(p->hoff, (uint64_t)F + 1, ok);
         if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed");
@@ -591,7 +627,55 @@ int assign_v2(clairplan_plan* p) {
     return 0;
 }
 
-int build_seed_path_v2(clairplan_plan* p, const uint32_t* ext_perms) {
+// All-fit path (every worker's candidates provably fit class 1, fit_check_kernel): the tier
+// order cannot change the outcome of pack_first_fit, so it is not materialised; the block
+// records and class-1 lists come straight from the streams (seg_first), then K8.
+int assign_allfit_v2(clairplan_plan* p) {
+    cudaStream_t s = p->stream;
+    const Part& part = p->part;
+    const uint32_t E = part.E, nloc = p->nloc, J = p->cfg.num_classes;
+    uint32_t np = 0;
+    while ((1u << np) <= J) ++np;
+    const uint32_t Rp = ((np + J) + 3) & ~3u;
+    bool ok = true;
+    uint32_t* centries = need<uint32_t>(p->class_entries, p->D, ok);
+    uint32_t* rec = need<uint32_t>(p->planes, (uint64_t)std::max<uint32_t>(Rp, 4) * p->v2_nblk, ok);
+    uint32_t* cbase = need<uint32_t>(p->cbase, (uint64_t)nloc * J, ok);
+    uint64_t* clen = need<uint64_t>(p->class_len, (uint64_t)nloc * J, ok);
+    uint64_t* cstart = need<uint64_t>(p->class_start, (uint64_t)nloc * J + 1, ok);
+    if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed (class lists)");
+    const uint64_t* segoff = p->seg_off.get<uint64_t>();
+    launch_seg_first(s, part, p->stream_buf.get<uint32_t>(), p->info16.get<uint16_t>(), segoff,
+                     p->v2_mb, rec, centries);
+    launch_allfit_meta(s, nloc, E, J, segoff, clen, cstart, cbase);
+    p->launches += 2;
+    p->mark(6);
+    return holders_v2(p);
+}
+
+// K4c: every candidate's first-order index -> tier position (dest), the sizes in tier order,
+// the block first-masks; per-worker candidate ranges (wbeg / wlen).
+int tier_order_v2(clairplan_plan* p) {
+    cudaStream_t s = p->stream;
+    const Part& part = p->part;
+    const uint32_t E = part.E, nloc = p->nloc;
+    const uint64_t D = p->D;
+    bool ok = true;
+    uint32_t* dest = need<uint32_t>(p->dest, D, ok);
+    double* ssize = need<double>(p->sorted_size, D, ok);
+    if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed (candidates)");
+    const uint64_t* segoff = p->seg_off.get<uint64_t>();
+    launch_seg_write2(s, part, p->stream_buf.get<uint32_t>(), p->info16.get<uint16_t>(),
+                      p->sizes.get<double>(), segoff, p->sorted_base.get<uint64_t>(), p->v2_mb, dest,
+                      ssize, p->blkmask.get<uint32_t>(), p->blkbase.get<uint32_t>());
+    launch_worker_segments(s, segoff, nloc, E, p->wbeg.get<uint64_t>(), p->wlen.get<uint64_t>());
+    p->launches += 2;
+    p->tier_ready = true;
+    return 0;
+}
+
+int build_seed_path_v2(clairplan_plan* p, const uint32_t* ext_perms,
+                       const uint32_t* ext_streams = nullptr, const EpochSplit* es = nullptr) {
     cudaStream_t s = p->stream;
     const Part& part = p->part;
     const uint32_t F = part.F, E = part.E, nloc = p->nloc, J = p->cfg.num_classes;
@@ -616,6 +700,9 @@ int build_seed_path_v2(clairplan_plan* p, const uint32_t* ext_perms) {
     uint32_t* bmask = need<uint32_t>(p->blkmask, nblk, ok);
     uint32_t* bbase = need<uint32_t>(p->blkbase, nblk, ok);
     uint32_t* hard = need<uint32_t>(p->hard, (uint64_t)F + 1, ok);
+    double* segsum = need<double>(p->segsum, (uint64_t)nloc * E, ok);
+    double* segmin = need<double>(p->segmin, (uint64_t)nloc * E, ok);
+    uint32_t* allfit_flag = need<uint32_t>(p->allfit_flag, 1, ok);
     if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed (streams / histograms)");
     if (int rc = ensure_ws(p, std::max<uint64_t>(p->A, std::max<uint64_t>(NEE, F)), nloc)) return rc;
     if (int rc = alloc_rej(p, E)) return rc;
@@ -628,7 +715,12 @@ int build_seed_path_v2(clairplan_plan* p, const uint32_t* ext_perms) {
         CK(cudaEventRecord(p->ev0, s));
         p->mark(0);
         // K1-K3: permutations -> streams + inverse permutations
-        if (ext_perms) {
+        if (ext_streams) {  // multi-GPU: epoch-range streams from every rank (all-to-all)
+            launch_stream_relayout(s, part, *es, ext_streams, stream_buf);
+            CK(cudaMemsetAsync(inv, 0xFF, EF * 4, s));
+            launch_stream_inv(s, part, stream_buf, inv);
+            p->launches += 2;
+        } else if (ext_perms) {
             launch_perm_scatter(s, part, ext_perms, inv, stream_buf);
             ++p->launches;
         } else if (int rc = enqueue_perms(p, stream_buf, inv, nullptr, 0, E)) {
@@ -641,7 +733,10 @@ int build_seed_path_v2(clairplan_plan* p, const uint32_t* ext_perms) {
         const bool red_hist = F >= (1u << 22);
         uint32_t* hist_out = red_hist ? seghist : nullptr;
         if (red_hist) CK(cudaMemsetAsync(seghist, 0, NEE * 4, s));
-        if (lanes) {
+        static const bool lanes_only = getenv("CLAIRPLAN_SAMPLE_LANES") != nullptr;  // A/B
+        if (tile_path_ok(part) && !lanes_only) {
+            launch_sample_tile(s, part, inv, info, rank16, pcount, hist_out);
+        } else if (lanes) {
             launch_sample_lanes(s, part, inv, info, rank16, pcount, hist_out);
         } else {
             launch_sample_hash(s, part, inv, info, rank16, pcount, nullptr, nullptr, F, hist_out);
@@ -649,15 +744,28 @@ int build_seed_path_v2(clairplan_plan* p, const uint32_t* ext_perms) {
         exclusive_scan(s, pcount, F, poff, p->ws);
         p->mark(2);
         // K4b: per-segment count histograms -> first-order and tier-order bases
-        if (red_hist) launch_segcnt(s, nloc, E, seghist, segcnt);
-        else launch_seg_hist(s, part, stream_buf, info, seghist, segcnt);
+        // whole-worker fit test (all-fit path) where the segment pass runs anyway
+        const bool no_allfit = getenv("CLAIRPLAN_NO_ALLFIT") != nullptr;
+        const bool try_allfit = !red_hist && J > 0 && !no_allfit;
+        if (red_hist) {
+            launch_segcnt(s, nloc, E, seghist, segcnt);
+        } else if (try_allfit) {
+            CK(cudaMemsetAsync(allfit_flag, 0xFF, 4, s));
+            launch_seg_hist(s, part, stream_buf, info, seghist, segcnt, p->sizes.get<double>(),
+                            segsum, segmin);
+            launch_fit_check(s, nloc, E, segsum, segmin, segcnt, p->caps[0], allfit_flag);
+        } else {
+            launch_seg_hist(s, part, stream_buf, info, seghist, segcnt);
+        }
         exclusive_scan(s, seghist, NEE, sbase, p->ws);
         exclusive_scan(s, segcnt, (uint64_t)nloc * E, segoff, p->ws);
         p->mark(3);
         p->launches += 10;
         std::vector<uint32_t> flags(E);
         uint64_t D = 0;
+        uint32_t allfit = 0;
         CK(cudaMemcpyAsync(&D, segoff + (uint64_t)nloc * E, 8, cudaMemcpyDeviceToHost, s));
+        if (try_allfit) CK(cudaMemcpyAsync(&allfit, allfit_flag, 4, cudaMemcpyDeviceToHost, s));
         CK(cudaMemcpyAsync(flags.data(), p->rej_flag.get<uint32_t>(), E * 4, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         bool any = false;
@@ -667,29 +775,21 @@ int build_seed_path_v2(clairplan_plan* p, const uint32_t* ext_perms) {
         if (D >= 0xFFFFFFFFull)
             return fail(CLAIRPLAN_EOVERFLOW, "more than 2^32-1 (worker, sample) pairs in one handle; "
                                              "shard the workers over several handles");
-        uint32_t* dest = need<uint32_t>(p->dest, D, ok);
-        double* ssize = need<double>(p->sorted_size, D, ok);
-        uint8_t* cls = need<uint8_t>(p->cand_cls, D, ok);
-        uint32_t* htmp = need<uint32_t>(p->holders_tmp, 3 * D, ok);
-        uint32_t* centries = need<uint32_t>(p->class_entries, D, ok);
-        const uint32_t Rp = ((np + J) + 3) & ~3u;
-        uint32_t* rec = need<uint32_t>(p->planes, (uint64_t)std::max<uint32_t>(Rp, 4) * nblk, ok);
-        uint32_t* cbase = need<uint32_t>(p->cbase, (uint64_t)nloc * std::max<uint32_t>(J, 1), ok);
-        uint32_t* ccount = need<uint32_t>(p->ccount, std::max<uint32_t>(J, 1) * nblk, ok);
-        uint64_t* cpre = need<uint64_t>(p->cpre, std::max<uint32_t>(J, 1) * (nblk + 1), ok);
-        uint64_t* clen = need<uint64_t>(p->class_len, (uint64_t)nloc * std::max<uint32_t>(J, 1), ok);
-        uint64_t* cstart = need<uint64_t>(p->class_start, (uint64_t)nloc * std::max<uint32_t>(J, 1) + 1, ok);
-        if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed (candidates)");
-        // K4c: candidates in first order / tier order
-        launch_seg_write2(s, part, stream_buf, info, p->sizes.get<double>(), segoff, sbase, MB, dest,
-                          ssize, bmask, bbase);
-        launch_worker_segments(s, segoff, nloc, E, wbeg, wlen);
-        p->launches += 2;
-        p->mark(4);
-        p->mark(5);
         p->v2_mb = MB;
         p->v2_nblk = nblk;
-        if (int rc = assign_v2(p)) return rc;
+        p->tier_ready = false;
+        if (allfit) {
+            p->mark(4);
+            p->mark(5);
+            p->allfit = true;
+            if (int rc = assign_allfit_v2(p)) return rc;
+        } else {
+            p->allfit = false;
+            if (int rc = tier_order_v2(p)) return rc;
+            p->mark(4);
+            p->mark(5);
+            if (int rc = assign_v2(p)) return rc;
+        }
         p->mark(clairplan_plan::kStages);
         CK(cudaEventRecord(p->ev1, s));
         CK(cudaEventSynchronize(p->ev1));
@@ -802,6 +902,8 @@ int clairplan_stats_get(clairplan_t p, clairplan_stats* s) {
     s->holders = p->H;
     s->rejections = p->rejections;
     s->device_ms = p->device_ms;
+    s->path = !p->v2 ? CLAIRPLAN_PATH_V1 : p->allfit ? CLAIRPLAN_PATH_ALLFIT : CLAIRPLAN_PATH_TIER;
+    s->reserved = 0;
     return 0;
 }
 
@@ -989,6 +1091,66 @@ int clairplan_generate_perms(clairplan_t p, uint32_t epoch_begin, uint32_t epoch
     return fail(CLAIRPLAN_ECUDA, "rejection tables did not converge");
 }
 
+int clairplan_epoch_prefix(clairplan_t p, uint32_t worker, uint64_t* entries) {
+    if (!p || !entries) return fail(CLAIRPLAN_EINVAL, "null argument");
+    if (worker > p->part.N) return fail(CLAIRPLAN_EINVAL, "worker out of range");
+    *entries = p->part.prefix_len(worker);
+    return 0;
+}
+
+int clairplan_generate_streams(clairplan_t p, uint32_t epoch_begin, uint32_t epoch_count,
+                               uint32_t* d_out) {
+    if (!p || p->generic) return fail(CLAIRPLAN_EINVAL, "invalid plan");
+    if (epoch_count == 0) return 0;
+    if (!d_out) return fail(CLAIRPLAN_EINVAL, "null output");
+    if (epoch_begin + epoch_count > p->part.E) return fail(CLAIRPLAN_EINVAL, "epoch range outside plan");
+    CK(cudaSetDevice(p->device));
+    const Part& pp = p->part;
+    if ((uint64_t)epoch_count * pp.P >= (1ull << 32))
+        return fail(CLAIRPLAN_EOVERFLOW, "epoch range holds 2^32 or more stream entries");
+    Part sp = make_part(pp.F, pp.N, pp.B, epoch_count, pp.drop_last != 0, 0, pp.N);
+    sp.ebase = epoch_begin;
+    if (int rc = alloc_rej(p, p->part.E)) return rc;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        p->launches = 0;
+        CK(cudaEventRecord(p->ev0, p->stream));
+        if (int rc = enqueue_perms(p, d_out, nullptr, nullptr, epoch_begin, epoch_count, &sp)) return rc;
+        std::vector<uint32_t> flags(p->part.E);
+        CK(cudaMemcpyAsync(flags.data(), p->rej_flag.get<uint32_t>(), flags.size() * 4,
+                           cudaMemcpyDeviceToHost, p->stream));
+        CK(cudaEventRecord(p->ev1, p->stream));
+        CK(cudaStreamSynchronize(p->stream));
+        bool any = false;
+        if (int rc = resolve_rejections(p, flags, &any)) return rc;
+        if (!any) {
+            float ms = 0;
+            CK(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
+            p->gen_ms = ms;
+            return 0;
+        }
+    }
+    return fail(CLAIRPLAN_ECUDA, "rejection tables did not converge");
+}
+
+int clairplan_build_from_streams(clairplan_t p, const uint32_t* d_recv,
+                                 const uint32_t* epoch_bounds, uint32_t nsrc) {
+    if (!p || p->generic || !d_recv || !epoch_bounds) return fail(CLAIRPLAN_EINVAL, "invalid argument");
+    if (nsrc < 1 || nsrc > kMaxRanks) return fail(CLAIRPLAN_EINVAL, "1..64 source ranks supported");
+    if (epoch_bounds[0] != 0 || epoch_bounds[nsrc] != p->part.E)
+        return fail(CLAIRPLAN_EINVAL, "epoch bounds must cover [0, epochs)");
+    EpochSplit es{};
+    es.G = nsrc;
+    for (uint32_t r = 0; r <= nsrc; ++r) {
+        es.eb[r] = epoch_bounds[r];
+        if (r && es.eb[r] < es.eb[r - 1]) return fail(CLAIRPLAN_EINVAL, "epoch bounds must ascend");
+    }
+    CK(cudaSetDevice(p->device));
+    if (!v2_ok(p)) return fail(CLAIRPLAN_EINVAL, "configuration not supported by the sharded path");
+    p->built = false;
+    p->v2 = false;
+    return build_seed_path_v2(p, nullptr, d_recv, &es);
+}
+
 int clairplan_build_from_perms(clairplan_t p, const uint32_t* d_perms) {
     if (!p || p->generic || !d_perms) return fail(CLAIRPLAN_EINVAL, "invalid argument");
     CK(cudaSetDevice(p->device));
@@ -1021,6 +1183,9 @@ int clairplan_reassign(clairplan_t p, const double* capacities_mb) {
     p->ws.used = 0;
     p->launches = 0;
     CK(cudaEventRecord(p->ev0, p->stream));
+    if (!p->tier_ready)  // the build took the all-fit path: materialise the tier order once
+        if (int rc = tier_order_v2(p)) return rc;
+    p->allfit = false;
     if (int rc = assign_v2(p)) return rc;
     CK(cudaEventRecord(p->ev1, p->stream));
     CK(cudaEventSynchronize(p->ev1));

@@ -102,6 +102,7 @@ struct clairplan_plan {
     uint64_t key = 0;
     uint64_t A = 0, D = 0, H = 0, rejections = 0;
     double device_ms = 0;
+    double gen_ms = 0;               // device time of the last clairplan_generate_streams
     bool built = false;
     bool generic = false;
     uint64_t launches = 0;
@@ -117,6 +118,9 @@ struct clairplan_plan {
     DevBuf wsbuf;
     DevBuf cand_w, dfirst, dcounts;  // explicit-stream (generic) path
     DevBuf inv, info16, rank16, cbase, seghist, sorted_base, blkmask, blkbase, planes, ccount, cpre, hard;
+    DevBuf segsum, segmin, allfit_flag;
+    bool allfit = false;             // last build took the all-fit path (no tier order)
+    bool tier_ready = false;         // dest / sorted_size / block masks hold the tier order
     bool v2 = false;                 // fast seed path in use for the last build
     uint32_t v2_mb = 0;              // blocks per segment / total blocks of the last v2 build
     uint64_t v2_nblk = 0;

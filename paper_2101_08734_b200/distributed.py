@@ -1,15 +1,18 @@
 """Multi-GPU plan build: one process per GPU, torch.distributed (NCCL) for the exchanges.
 
 Decomposition ("Multi-GPU"):
-  1. epoch sharding  — rank r draws the permutations of its epoch range
-                       (clairplan_generate_perms); epochs are independent by construction
+  1. epoch sharding  — rank r draws the permutations of its epoch range and cuts them into
+                       the access streams of ALL workers for those epochs
+                       (clairplan_generate_streams); epochs are independent by construction
                        (access.cpp:52-57: epoch e owns stream positions [e<<34, (e+1)<<34)).
-  2. all-gather      — the permutation rows of every epoch are all-gathered over NVLink
-                       (ncclAllGather through torch.distributed).
-  3. worker sharding — rank r builds streams, (count, first-access) tables, tier assignment,
-                       prefetch orders and holder records for its contiguous worker range
-                       (clairplan_build_from_perms); nopfs_assign_caches has no cross-worker
-                       dependency (policies.cpp:151-163).
+  2. all-to-all      — every rank sends each other rank the stream slices of that rank's
+                       workers (one ncclAllToAll-style exchange through torch.distributed,
+                       4A(G-1)/G bytes in total over NVLink).
+  3. worker sharding — rank r re-lays out its workers' streams, rebuilds the inverse
+                       permutations restricted to its workers and builds the (count,
+                       first-access) tables, tier assignment, prefetch orders and holder
+                       records of its contiguous worker range (clairplan_build_from_streams);
+                       nopfs_assign_caches has no cross-worker dependency (policies.cpp:151-163).
   4. holder merge    — per-sample holder counts are all-gathered; the global CSR offset of
                        sample k is the exclusive scan of the per-sample totals and rank r's
                        records of k start after those of ranks < r (worker ranges ascend, so
@@ -53,6 +56,18 @@ def holder_offsets_from_counts(counts):
     return glob, glob[:-1].unsqueeze(0) + before
 
 
+def stream_splits(prefix, ranges, wranges, rank):
+    """All-to-all split sizes (u32 entries) of the epoch-range streams.
+    prefix[w] = stream entries per epoch of workers < w; ranges[r] = (first epoch, count) of
+    rank r; wranges[d] = worker range of rank d.  Rank `rank` sends rank d the entries of d's
+    workers for its own epochs and receives from rank r r's epochs of its own workers."""
+    n_me = ranges[rank][1]
+    send = [n_me * (prefix[we] - prefix[wb]) for wb, we in wranges]
+    wb, we = wranges[rank]
+    recv = [n * (prefix[we] - prefix[wb]) for _, n in ranges]
+    return send, recv
+
+
 def gather_rows(local, ranges, pad, group=None):
     """All-gather per-rank permutation rows (uneven epoch ranges, padded) -> [E, F]."""
     import torch
@@ -71,14 +86,19 @@ def gather_rows(local, ranges, pad, group=None):
 
 
 class DistributedPlan:
-    """Sharded plan of one rank (call the same sequence on every rank)."""
+    """Sharded plan of one rank (call the same sequence on every rank).
 
-    def __init__(self, seed, samples, part, capacities_mb, sizes_mb, group=None):
+    mode "streams" (default): epoch-range streams + all-to-all (steps 1-3 above);
+    mode "perms": permutation rows all-gathered to every rank (the earlier scheme, kept for
+    A/B measurements)."""
+
+    def __init__(self, seed, samples, part, capacities_mb, sizes_mb, group=None, mode="streams"):
         import torch
         import torch.distributed as dist
         from . import clairplan as cp
         self.cp, self.torch, self.dist = cp, torch, dist
         self.group = group
+        self.mode = mode
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         self.device = torch.cuda.current_device()
@@ -91,8 +111,25 @@ class DistributedPlan:
         L.clairplan_generate_perms.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p]
         L.clairplan_build_from_perms.argtypes = [C.c_void_p, C.c_void_p]
         L.clairplan_holder_counts.argtypes = [C.c_void_p, C.c_void_p]
+        L.clairplan_generate_streams.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p]
+        L.clairplan_build_from_streams.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32]
+        L.clairplan_epoch_prefix.argtypes = [C.c_void_p, C.c_uint32, C.POINTER(C.c_uint64)]
         self.L = L
-        self.local_rows = torch.empty((max(self.pad, 1), samples), dtype=torch.int32, device="cuda")
+        N = part.num_workers
+        if mode == "streams":
+            pre = []
+            for w in range(N + 1):
+                v = C.c_uint64()
+                cp._check(L.clairplan_epoch_prefix(self.plan._h, w, C.byref(v)))
+                pre.append(int(v.value))
+            wr = [worker_range(N, r, self.world) for r in range(self.world)]
+            self.send_splits, self.recv_splits = stream_splits(pre, self.ranges, wr, self.rank)
+            self.send = torch.empty(max(sum(self.send_splits), 1), dtype=torch.int32, device="cuda")
+            self.recv = torch.empty(max(sum(self.recv_splits), 1), dtype=torch.int32, device="cuda")
+            self.bounds = np.array([b for b, _ in self.ranges] + [part.epochs], np.uint32)
+        else:
+            self.local_rows = torch.empty((max(self.pad, 1), samples), dtype=torch.int32,
+                                          device="cuda")
         self.counts = torch.empty(samples, dtype=torch.int32, device="cuda")
         self.global_offsets = None
         self.rank_starts = None
@@ -100,15 +137,28 @@ class DistributedPlan:
     def build(self):
         torch, cp = self.torch, self.cp
         e0, n = self.ranges[self.rank]
-        cp._check(self.L.clairplan_generate_perms(self.plan._h, e0, n,
-                                                  C.c_void_p(self.local_rows.data_ptr())))
-        perms = gather_rows(self.local_rows[:n], self.ranges, self.pad, self.group)
-        # the gather and the concatenation run on torch's stream; the library reads the rows
-        # on its own stream, so order them (every library call synchronises its own stream
-        # before returning, so the reverse direction needs nothing)
-        torch.cuda.current_stream().synchronize()
-        cp._check(self.L.clairplan_build_from_perms(self.plan._h, C.c_void_p(perms.data_ptr())))
-        del perms
+        if self.mode == "streams":
+            cp._check(self.L.clairplan_generate_streams(self.plan._h, e0, n,
+                                                        C.c_void_p(self.send.data_ptr())))
+            # the library synchronises its stream before returning; NCCL runs on torch's
+            self.dist.all_to_all_single(self.recv[:sum(self.recv_splits)],
+                                        self.send[:sum(self.send_splits)],
+                                        self.recv_splits, self.send_splits, group=self.group)
+            torch.cuda.current_stream().synchronize()
+            cp._check(self.L.clairplan_build_from_streams(
+                self.plan._h, C.c_void_p(self.recv.data_ptr()),
+                self.bounds.ctypes.data_as(C.c_void_p), self.world))
+        else:
+            cp._check(self.L.clairplan_generate_perms(self.plan._h, e0, n,
+                                                      C.c_void_p(self.local_rows.data_ptr())))
+            perms = gather_rows(self.local_rows[:n], self.ranges, self.pad, self.group)
+            # the gather and the concatenation run on torch's stream; the library reads the
+            # rows on its own stream, so order them (every library call synchronises its own
+            # stream before returning, so the reverse direction needs nothing)
+            torch.cuda.current_stream().synchronize()
+            cp._check(self.L.clairplan_build_from_perms(self.plan._h,
+                                                        C.c_void_p(perms.data_ptr())))
+            del perms
         cp._check(self.L.clairplan_holder_counts(self.plan._h, C.c_void_p(self.counts.data_ptr())))
         allc = torch.empty((self.world, self.samples), dtype=torch.int32, device="cuda")
         self.dist.all_gather_into_tensor(allc, self.counts, group=self.group)

@@ -13,7 +13,8 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from paper_2101_08734_b200.distributed import (epoch_ranges, gather_rows,
-                                               holder_offsets_from_counts, worker_range)
+                                               holder_offsets_from_counts, stream_splits,
+                                               worker_range)
 
 
 def _free_port():
@@ -58,7 +59,28 @@ def _worker(rank, world, port, q):
                                              np.repeat(np.cumsum(counts.numpy()) - counts.numpy(),
                                                        counts.numpy()))
         ok_pos = np.array_equal(whole.holders[pos], mine)
-        q.put((rank, ok_rows, ok_glob, ok_pos))
+        # 3) epoch-range streams of all workers -> all-to-all -> this rank's worker streams
+        #    (clairplan_generate_streams / _build_from_streams layouts, relayout in numpy)
+        Le = [len(st) // E for st in whole.streams]
+        prefix = np.concatenate([[0], np.cumsum(Le)]).astype(np.int64)
+        wr = [worker_range(N, r, world) for r in range(world)]
+        send_s, recv_s = stream_splits(prefix, ranges, wr, rank)
+        send = np.concatenate([whole.streams[w][e0 * Le[w]:(e0 + n) * Le[w]] for w in range(N)])
+        assert len(send) == sum(send_s) == n * prefix[N]
+        recv = torch.empty(sum(recv_s), dtype=torch.int32)
+        dist.all_to_all_single(recv, torch.tensor(send.astype(np.int32)), recv_s, send_s)
+        recv = recv.numpy()
+        got, off = [], 0
+        parts = {}
+        for r, (er, nr) in enumerate(ranges):
+            for w in range(wb, we):
+                parts[(w, r)] = recv[off:off + nr * Le[w]]
+                off += nr * Le[w]
+        for w in range(wb, we):
+            got.append(np.concatenate([parts[(w, r)] for r in range(world)]))
+        ok_streams = all(np.array_equal(g, whole.streams[w].astype(np.int32))
+                         for g, w in zip(got, range(wb, we)))
+        q.put((rank, ok_rows and ok_streams, ok_glob, ok_pos))
     finally:
         dist.destroy_process_group()
 

@@ -76,6 +76,8 @@ CASES = [
     (13, 5000, 7, 300, 33, True, [25.0, 120.0], (0.1077, 0.2)),
     (21, 4096, 64, 64, 40, False, [3.0, 9.0], (0.1, 0.05)),
     (8, 3000, 5, 5, 300, True, [40.0, 400.0], (0.1, 0.1)),   # E > 255: two radix digits
+    (17, 3000, 6, 60, 12, True, [2.0, 3.0, 5.0, 8.0], (0.1, 0.1)),              # J = 4: 3 planes
+    (19, 2500, 9, 45, 15, False, [1.0, 2.0, 1.5, 4.0, 3.0, 9.0, 2.5], (0.2, 0.1)),  # J = 7
 ]
 
 
@@ -158,6 +160,65 @@ def test_config2_imagenet1k_e90_n256(cp, ref):
     b = device_plan(cp, 42, 1_281_167, 256, 32 * 256, 90, True, [120_000.0, 900_000.0], sizes)
     assert plans_equal(a, b) is None
     assert b.stats["accesses"] == 115_015_680 and b.stats["pairs"] == 97_174_801
+    assert b.stats["path"] == "allfit"  # the benchmarked pipeline
+
+
+ALLFIT_CASES = [
+    (42, 2000, 4, 128, 10, True, [1e6, 1e6], (0.1077, 0.1)),
+    (9, 1000, 16, 16, 6, True, [1e6, 1e6], (1.0, 0.0)),
+    (7, 1500, 3, 7, 5, False, [1e5], (0.1, 0.3)),
+    (13, 5000, 7, 300, 33, True, [1e4, 1.0, 5.0], (0.1077, 0.2)),
+    (77, 7, 1, 3, 2, False, [100.0], (1.0, 0.0)),
+    (8, 3000, 5, 5, 300, True, [1e6, 2.0], (0.1, 0.1)),
+]
+
+
+@pytest.mark.parametrize("case", ALLFIT_CASES)
+def test_allfit_path_matches_reference(cp, ref, case, monkeypatch):
+    """Every worker provably fits class 1: the all-fit pipeline (no tier order) and the full
+    tier-order pipeline both equal the reference."""
+    seed, F, N, B, E, dl, caps, (mu, sd) = case
+    sizes = ref.generate_sizes(F, mu, sd, None, 1)
+    a = ref.plan(seed, F, N, B, E, dl, caps, sizes)
+    b = device_plan(cp, seed, F, N, B, E, dl, caps, sizes)
+    assert b.stats["path"] == "allfit"
+    assert plans_equal(a, b) is None
+    monkeypatch.setenv("CLAIRPLAN_NO_ALLFIT", "1")
+    c = device_plan(cp, seed, F, N, B, E, dl, caps, sizes)
+    assert c.stats["path"] == "tier"
+    assert plans_equal(a, c) is None
+
+
+def test_allfit_capacity_boundary(cp, ref):
+    """Class-1 capacity at, just below and just above the largest per-worker candidate sum:
+    whichever pipeline the fit test picks, the plan equals the reference."""
+    seed, F, N, B, E = 4, 3000, 6, 60, 8
+    sizes = ref.generate_sizes(F, 0.3, 0.2, None, 1)
+    b0 = device_plan(cp, seed, F, N, B, E, True, [1e9], sizes)
+    sums = [float(np.sum(sizes[np.unique(s)])) for s in b0.streams]
+    top = max(sums)
+    paths = set()
+    for C in (top, np.nextafter(top, 0), np.nextafter(top, np.inf), top * (1 - 1e-9),
+              top * (1 + 1e-9), top * (1 + 1e-6), min(sums), 0.5 * top):
+        a = ref.plan(seed, F, N, B, E, True, [float(C), 5.0], sizes)
+        b = device_plan(cp, seed, F, N, B, E, True, [float(C), 5.0], sizes)
+        paths.add(b.stats["path"])
+        assert plans_equal(a, b) is None, C
+    assert paths == {"allfit", "tier"}
+
+
+def test_reassign_after_allfit_build(cp, ref):
+    F, N, B, E = 20_000, 8, 256, 12
+    sizes = ref.generate_sizes(F, 0.1077, 0.2, None, 1)
+    p = cp.Plan(3, F, cp.PartitionSpec(N, B, E, True), [1e7, 1e7], sizes).build()
+    assert p.stats()["path"] == "allfit"
+    for caps in ([30.0, 60.0], [1e7, 1e7], [0.05, 0.2]):
+        p.reassign(caps)
+        offs, hold = p.holders()
+        got = OPlan(N, 2, [p.stream(w) for w in range(N)], p.class_lists(), offs, hold)
+        want = ref.plan(3, F, N, B, E, True, caps, sizes)
+        assert plans_equal(want, got) is None, caps
+    p.close()
 
 
 def test_generic_assign_matches_reference(cp, ref):

@@ -1,8 +1,8 @@
 """Multi-GPU parity check (run with torchrun, one rank per GPU):
     python -m torch.distributed.run --nproc-per-node 2 --master-addr 127.0.0.1 tools/dist_check.py
-Every rank builds its shard through DistributedPlan (epoch-sharded permutations + NCCL
-all-gather + worker-range build + holder-offset merge) and compares it with a single-GPU
-plan of all workers built locally."""
+Every rank builds its shard through DistributedPlan (epoch-range streams + NCCL all-to-all +
+worker-range build + holder-offset merge; and the older permutation all-gather mode) and
+compares it with a single-GPU plan of all workers built locally."""
 import os
 import sys
 
@@ -20,11 +20,15 @@ def main():
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
     dist.init_process_group("nccl", device_id=torch.device("cuda", torch.cuda.current_device()))
     ok = True
-    for (F, N, b, E) in ((1_281_167, 256, 32, 9), (262_144, 64, 16, 10), (20_000, 7, 5, 13)):
+    cases = [(1_281_167, 256, 32, 9, True, "streams"), (262_144, 64, 16, 10, True, "streams"),
+             (20_000, 7, 5, 13, True, "streams"), (20_011, 9, 3, 7, False, "streams"),
+             (30_000, 5, 7, 3, False, "streams"), (1_281_167, 256, 32, 9, True, "perms"),
+             (20_000, 7, 5, 13, True, "perms")]
+    for (F, N, b, E, dl, mode) in cases:
         sizes = cp.generate_sizes(F, 0.1077, 0.1, None, 1)
-        part = cp.PartitionSpec(N, b * N, E, True)
+        part = cp.PartitionSpec(N, b * N, E, dl)
         caps = [120.0 * F / 1e4, 900.0 * F / 1e4]
-        dp = DistributedPlan(42, F, part, caps, sizes).build()
+        dp = DistributedPlan(42, F, part, caps, sizes, mode=mode).build()
         full = cp.Plan(42, F, part, caps, sizes, device=torch.cuda.current_device()).build()
         wb, we = dp.wrange
         st_full = full.streams_flat()
@@ -51,7 +55,7 @@ def main():
             within = np.arange(H, dtype=np.int64) - np.repeat(offs_mine[:-1].astype(np.int64), cnt)
             pos = np.repeat(starts.astype(np.int64), cnt) + within
             ok &= bool(np.array_equal(hold_full[pos], hold_mine))
-        print(f"rank {rank} F={F} ok={ok}", flush=True)
+        print(f"rank {rank} F={F} N={N} E={E} dl={dl} mode={mode} ok={ok}", flush=True)
         dp.close()
         full.close()
     t = torch.tensor([1 if ok else 0], device="cuda")
