@@ -238,6 +238,8 @@ constexpr int kSU = 4;
 // seghist[(wl*E + (E - c))*E + e] = first accesses with count c in segment (w, e)
 // With `sizes`: also the sum and minimum of the sizes of the segment's first accesses
 // (segsum/segmin), the input of the whole-worker fit test (fit_check_kernel).
+// HIST = false: only the per-segment first-access totals (and sums), no count histogram
+template <bool HIST>
 __global__ void __launch_bounds__(kThreads) seg_hist_kernel(Part part, const uint32_t* __restrict__ stream,
                                                              const uint16_t* __restrict__ info,
                                                              uint32_t* __restrict__ seghist,
@@ -254,7 +256,8 @@ __global__ void __launch_bounds__(kThreads) seg_hist_kernel(Part part, const uin
          b += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
         const uint32_t e = (uint32_t)(b / nloc), wl = (uint32_t)(b - (uint64_t)e * nloc);
         const uint32_t w = part.wbegin + wl;
-        for (uint32_t i = lane; i < E; i += 32) hist[i] = 0;
+        if (HIST)
+            for (uint32_t i = lane; i < E; i += 32) hist[i] = 0;
         __syncwarp();
         const uint64_t Le = part.epoch_len(w);
         const uint64_t g0 = part.stream_offset(w) + (uint64_t)e * Le;
@@ -283,9 +286,11 @@ __global__ void __launch_bounds__(kThreads) seg_hist_kernel(Part part, const uin
 #pragma unroll
             for (int u = 0; u < kSU; ++u) {
                 const bool first = c[u] != 0;
-                const uint32_t key = first ? E - c[u] : (0x80000000u | lane);
-                const uint32_t m = __match_any_sync(0xffffffffu, key);
-                if (first && __popc(m & lanemask_lt()) == 0) hist[key] += __popc(m);
+                if (HIST) {
+                    const uint32_t key = first ? E - c[u] : (0x80000000u | lane);
+                    const uint32_t m = __match_any_sync(0xffffffffu, key);
+                    if (first && __popc(m & lanemask_lt()) == 0) hist[key] += __popc(m);
+                }
                 tot += first;
             }
             __syncwarp();
@@ -299,7 +304,8 @@ __global__ void __launch_bounds__(kThreads) seg_hist_kernel(Part part, const uin
             }
         }
         __syncwarp();
-        for (uint32_t i = lane; i < E; i += 32) seghist[((uint64_t)wl * E + i) * E + e] = hist[i];
+        if (HIST)
+            for (uint32_t i = lane; i < E; i += 32) seghist[((uint64_t)wl * E + i) * E + e] = hist[i];
         if (lane == 0) {
             segcnt[(uint64_t)wl * E + e] = tot;
             if (segsum) {
@@ -659,16 +665,14 @@ __global__ void class_lens_kernel(uint32_t nloc, uint32_t E, uint32_t MB, uint32
 // access (rank != 0xFFFF) looks up its class and class-list position in the block record and
 // writes its holder record {worker, class, position} at pair_off[k] + rank (build_index
 // order, workers ascending): a warp's stores land in one sample's contiguous holder range.
-// (Staging the records in shared memory for fully contiguous stores was measured slower:
-// MIO-throttled, 2.2 vs 1.15 ms for config 2.)
+// (Measured slower for config 2 and dropped: staging the records in shared memory for fully
+// contiguous stores — MIO-throttled, 2.2 vs 1.15 ms — and 4 samples per warp in flight with
+// double-buffered cp.async tiles — register-limited occupancy, 1.5-1.7 ms.)
 // NP: class bit-planes per record (0: runtime np); NP == -1: all-fit records (uint2 {first
 // mask, class-1 prefix}, every first access is class 1).
 __device__ __forceinline__ uint32_t pick(const uint4& a, uint32_t i) {
     return i == 0 ? a.x : i == 1 ? a.y : i == 2 ? a.z : a.w;
 }
-
-__device__ __forceinline__ uint4 as4(const uint4& a) { return a; }
-__device__ __forceinline__ uint4 as4(const uint2& a) { return make_uint4(a.x, a.y, 0u, 0u); }
 
 __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
     const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
@@ -678,33 +682,7 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-constexpr uint32_t kHtInv = 33;  // padded row strides of the shared tiles (conflict-free reads)
-constexpr uint32_t kHtRk = 34;   // u16; even, so sample pairs are 4-B aligned for cp.async
-
-// tile k0 of the inverse-permutation / rank rows -> shared buffer (asynchronous, 4-B copies)
-__device__ __forceinline__ void ht_issue(const Part& part, const uint32_t* inv, const uint16_t* rank16,
-                                         uint64_t k0, uint32_t* tinv, uint16_t* trk) {
-    const uint32_t E = part.E, F = part.F;
-    const uint32_t n = (uint32_t)(F - k0 < 32 ? F - k0 : 32);
-    for (uint32_t idx = threadIdx.x; idx < E * 32; idx += blockDim.x) {
-        const uint32_t e = idx >> 5, l = idx & 31;
-        if (l < n) cp_async4(tinv + e * kHtInv + l, inv + (size_t)e * F + k0 + l);
-    }
-    // rank pairs (l, l+1); an odd F leaves a single u16 at the end of each row
-    for (uint32_t idx = threadIdx.x; idx < E * 16; idx += blockDim.x) {
-        const uint32_t e = idx >> 4, l = (idx & 15) * 2;
-        if (l >= n) continue;
-        const uint16_t* g = rank16 + (size_t)e * F + k0 + l;
-        if (l + 1 < n && (((uintptr_t)g) & 3) == 0) cp_async4(trk + e * kHtRk + l, g);
-        else {
-            trk[e * kHtRk + l] = __ldcs(g);
-            if (l + 1 < n) trk[e * kHtRk + l + 1] = __ldcs(g + 1);
-        }
-    }
-    cp_async_commit();
-}
-
-template <int NP, int SU>
+template <int NP>
 __global__ void __launch_bounds__(kThreads) holder_tile_kernel(
     Part part, const uint32_t* __restrict__ inv, const uint16_t* __restrict__ rank16, uint32_t MB,
     const uint32_t* __restrict__ rec, uint32_t np_rt, uint32_t J, uint32_t Rp,
@@ -713,91 +691,66 @@ __global__ void __launch_bounds__(kThreads) holder_tile_kernel(
     extern __shared__ uint32_t sm[];
     const uint32_t E = part.E, F = part.F;
     const uint32_t np = NP > 0 ? (uint32_t)NP : np_rt;
-    const uint32_t tile_words = E * kHtInv + (E * kHtRk + 1) / 2;
-    uint32_t* tinv_b[2] = {sm, sm + tile_words};
-    uint16_t* trk_b[2] = {reinterpret_cast<uint16_t*>(sm + E * kHtInv),
-                          reinterpret_cast<uint16_t*>(sm + tile_words + E * kHtInv)};
+    uint32_t* tinv = sm;                                            // [E][33]
+    uint16_t* trk = reinterpret_cast<uint16_t*>(sm + (size_t)E * 33);  // [E][33]
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-    // all-fit: uint2 records; NP 0/1/2: the first uint4 of the record (+ overflow words)
-    using RecT = typename std::conditional<NP == -1, uint2, uint4>::type;
-    const uint32_t RW = NP == -1 ? 1u : Rp / 4;  // record stride in RecT units
-    const uint64_t stride = (uint64_t)gridDim.x * 32;
-    uint64_t k0 = (uint64_t)blockIdx.x * 32;
-    if (k0 < F) ht_issue(part, inv, rank16, k0, tinv_b[0], trk_b[0]);
-    for (uint32_t buf = 0; k0 < F; k0 += stride, buf ^= 1) {
-        if (k0 + stride < F) {  // prefetch the next tile into the other buffer
-            ht_issue(part, inv, rank16, k0 + stride, tinv_b[buf ^ 1], trk_b[buf ^ 1]);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
+    for (uint64_t k0 = (uint64_t)blockIdx.x * 32; k0 < F; k0 += (uint64_t)gridDim.x * 32) {
+        __syncthreads();
+        for (uint32_t idx = threadIdx.x; idx < E * 32; idx += blockDim.x) {
+            const uint32_t e = idx >> 5, l = idx & 31;
+            const bool ok = k0 + l < F;
+            tinv[e * 33 + l] = ok ? __ldcs(inv + (size_t)e * F + k0 + l) : kNone;
+            trk[e * 33 + l] = ok ? __ldcs(rank16 + (size_t)e * F + k0 + l) : (uint16_t)0xFFFFu;
         }
         __syncthreads();
-        const uint32_t* tinv = tinv_b[buf];
-        const uint16_t* trk = trk_b[buf];
-        for (uint32_t s0 = warp; s0 < 32; s0 += nwarps * SU) {
-            uint64_t slot0[SU];
-#pragma unroll
-            for (int u = 0; u < SU; ++u) {
-                const uint32_t s = s0 + u * nwarps;
-                slot0[u] = (s < 32 && k0 + s < F) ? pair_off[k0 + s] : 0;
-            }
+        for (uint32_t s = warp; s < 32; s += nwarps) {
+            if (k0 + s >= F) break;
+            const uint64_t slot0 = pair_off[k0 + s];
             for (uint32_t e = lane; e < E; e += 32) {
-                uint32_t rk[SU], w[SU], bit[SU], wl[SU];
-                uint64_t blk[SU];
-                RecT a[SU];
-#pragma unroll
-                for (int u = 0; u < SU; ++u) {
-                    const uint32_t s = s0 + u * nwarps;
-                    rk[u] = (s < 32 && k0 + s < F) ? trk[e * kHtRk + s] : 0xFFFFu;
-                    if (rk[u] != 0xFFFFu) {
-                        const uint32_t tseg = part.within_epoch(tinv[e * kHtInv + s], w[u]);
-                        wl[u] = w[u] - part.wbegin;
-                        blk[u] = ((uint64_t)wl[u] * E + e) * MB + (tseg >> 5);
-                        bit[u] = tseg & 31;
-                        a[u] = reinterpret_cast<const RecT*>(rec)[blk[u] * RW];
+                const uint32_t rk = trk[e * 33 + s];
+                if (rk == 0xFFFFu) continue;
+                uint32_t w;
+                const uint32_t tseg = part.within_epoch(tinv[e * 33 + s], w);
+                const uint32_t wl = w - part.wbegin;
+                const uint64_t blk = ((uint64_t)wl * E + e) * MB + (tseg >> 5);
+                const uint32_t bit = tseg & 31;
+                uint32_t cls, pos = 0;
+                if constexpr (NP == -1) {
+                    const uint2 a2 = reinterpret_cast<const uint2*>(rec)[blk];
+                    cls = (a2.x >> bit) & 1u;
+                    if (cls) pos = a2.y - cbase[wl * J] + __popc(a2.x & ((1u << bit) - 1u));
+                } else {
+                const uint4* r4 = reinterpret_cast<const uint4*>(rec + blk * Rp);
+                const uint4 a = r4[0];
+                uint32_t cm;
+                if constexpr (NP == 1) {
+                    cls = (a.x >> bit) & 1u;
+                    cm = a.x;
+                } else if constexpr (NP == 2) {
+                    const uint32_t b0 = (a.x >> bit) & 1u, b1 = (a.y >> bit) & 1u;
+                    cls = b0 | (b1 << 1);
+                    cm = (b0 ? a.x : ~a.x) & (b1 ? a.y : ~a.y);
+                } else {
+                    cls = 0;
+                    for (uint32_t q = 0; q < np; ++q) cls |= ((pick(a, q) >> bit) & 1u) << q;
+                    cm = 0xffffffffu;
+                    for (uint32_t q = 0; q < np; ++q) {
+                        const uint32_t pl = pick(a, q);
+                        cm &= ((cls >> q) & 1u) ? pl : ~pl;
                     }
                 }
-#pragma unroll
-                for (int u = 0; u < SU; ++u) {
-                    if (rk[u] == 0xFFFFu) continue;
-                    uint32_t cls, pos = 0;
-                    const uint32_t below = (1u << bit[u]) - 1u;
-                    if constexpr (NP == -1) {
-                        cls = (a[u].x >> bit[u]) & 1u;
-                        if (cls) pos = a[u].y - cbase[wl[u] * J] + __popc(a[u].x & below);
-                    } else {
-                        const uint4 v = as4(a[u]);
-                        uint32_t cm;
-                        if constexpr (NP == 1) {
-                            cls = (v.x >> bit[u]) & 1u;
-                            cm = v.x;
-                        } else if constexpr (NP == 2) {
-                            const uint32_t b0 = (v.x >> bit[u]) & 1u, b1 = (v.y >> bit[u]) & 1u;
-                            cls = b0 | (b1 << 1);
-                            cm = (b0 ? v.x : ~v.x) & (b1 ? v.y : ~v.y);
-                        } else {
-                            cls = 0;
-                            for (uint32_t q = 0; q < np; ++q) cls |= ((pick(v, q) >> bit[u]) & 1u) << q;
-                            cm = 0xffffffffu;
-                            for (uint32_t q = 0; q < np; ++q) {
-                                const uint32_t pl = pick(v, q);
-                                cm &= ((cls >> q) & 1u) ? pl : ~pl;
-                            }
-                        }
-                        if (cls) {
-                            const uint32_t wi = np + cls - 1;
-                            const uint32_t prew = wi < 4 ? pick(v, wi) : rec[blk[u] * Rp + wi];
-                            pos = prew - cbase[wl[u] * J + cls - 1] + __popc(cm & below);
-                        }
-                    }
-                    uint32_t* h = holders + 3 * (slot0[u] + rk[u]);
-                    __stcs(h, w[u]);
-                    __stcs(h + 1, cls);
-                    __stcs(h + 2, pos);
+                if (cls) {
+                    const uint32_t wi = np + cls - 1;
+                    const uint32_t prew = wi < 4 ? pick(a, wi) : rec[blk * Rp + wi];
+                    pos = prew - cbase[wl * J + cls - 1] + __popc(cm & ((1u << bit) - 1u));
                 }
+                }
+                uint32_t* h = holders + 3 * (slot0 + rk);
+                __stcs(h, w);
+                __stcs(h + 1, cls);
+                __stcs(h + 2, pos);
             }
         }
-        __syncthreads();  // the buffer is refilled by the prefetch two tiles later
     }
 }
 
@@ -980,31 +933,20 @@ void launch_holder_tile(cudaStream_t s, const Part& part, const uint32_t* inv, c
                         uint32_t MB, const uint32_t* rec, uint32_t np, uint32_t J, uint32_t Rp,
                         const uint32_t* cbase, const uint64_t* pair_off, uint32_t* holders,
                         bool allfit) {
-    const size_t smem = 2 * ((size_t)part.E * kHtInv * 4 + ((size_t)part.E * kHtRk * 2 + 3) / 4 * 4) + 16;
+    const size_t smem = (size_t)part.E * 33 * 4 + (size_t)part.E * 33 * 2 + 16;
     const uint64_t tiles = ((uint64_t)part.F + 31) / 32;
     const unsigned grid = grid_for(tiles, 1, 148u * 16u);
-#define HT_LAUNCH(NPV, SUV)                                                                      \
+#define HT_LAUNCH(NPV)                                                                           \
     do {                                                                                         \
-        cudaFuncSetAttribute(holder_tile_kernel<NPV, SUV>,                                       \
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);            \
-        holder_tile_kernel<NPV, SUV><<<grid, kThreads, smem, s>>>(part, inv, rank16, MB, rec, np, J, \
-                                                                  Rp, cbase, pair_off, holders); \
+        cudaFuncSetAttribute(holder_tile_kernel<NPV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                             (int)smem);                                                         \
+        holder_tile_kernel<NPV><<<grid, kThreads, smem, s>>>(part, inv, rank16, MB, rec, np, J, Rp, \
+                                                             cbase, pair_off, holders);          \
     } while (0)
-    static const int su = [] {
-        const char* v = getenv("CLAIRPLAN_HT_SU");
-        return v ? atoi(v) : 1;
-    }();
-    if (su >= 2) {
-        if (allfit) HT_LAUNCH(-1, 2);
-        else if (np == 1) HT_LAUNCH(1, 2);
-        else if (np == 2) HT_LAUNCH(2, 2);
-        else HT_LAUNCH(0, 2);
-    } else {
-        if (allfit) HT_LAUNCH(-1, 1);
-        else if (np == 1) HT_LAUNCH(1, 1);
-        else if (np == 2) HT_LAUNCH(2, 1);
-        else HT_LAUNCH(0, 1);
-    }
+    if (allfit) HT_LAUNCH(-1);
+    else if (np == 1) HT_LAUNCH(1);
+    else if (np == 2) HT_LAUNCH(2);
+    else HT_LAUNCH(0);
 #undef HT_LAUNCH
 }
 
@@ -1064,10 +1006,34 @@ void launch_seg_hist(cudaStream_t s, const Part& part, const uint32_t* stream, c
                      uint32_t* seghist, uint32_t* segcnt, const double* sizes, double* segsum,
                      double* segmin) {
     const uint64_t nseg = (uint64_t)(part.wend - part.wbegin) * part.E;
-    const size_t smem = (size_t)(kThreads / 32) * part.E * 4;
-    cudaFuncSetAttribute(seg_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    seg_hist_kernel<<<grid_for(nseg * 32, kThreads, 148u * 64u), kThreads, smem, s>>>(
-        part, stream, info, seghist, segcnt, sizes, segsum, segmin);
+    const unsigned grid = grid_for(nseg * 32, kThreads, 148u * 64u);
+    if (seghist) {
+        const size_t smem = (size_t)(kThreads / 32) * part.E * 4;
+        cudaFuncSetAttribute(seg_hist_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        seg_hist_kernel<true><<<grid, kThreads, smem, s>>>(part, stream, info, seghist, segcnt, sizes,
+                                                            segsum, segmin);
+    } else {
+        seg_hist_kernel<false><<<grid, kThreads, 0, s>>>(part, stream, info, nullptr, segcnt, sizes,
+                                                          segsum, segmin);
+    }
+}
+
+// sum_k sizes[k] * pair_count[k] (all workers' candidate sizes) -> *out (atomic, unordered:
+// only the all-fit gate reads it)
+__global__ void pair_size_total_kernel(uint32_t F, const double* __restrict__ sizes,
+                                       const uint32_t* __restrict__ pair_count, double* out) {
+    double acc = 0.0;
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < F; k += gridDim.x * blockDim.x)
+        acc += sizes[k] * (double)pair_count[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
+}
+
+void launch_pair_size_total(cudaStream_t s, uint32_t F, const double* sizes,
+                            const uint32_t* pair_count, double* out) {
+    cudaMemsetAsync(out, 0, sizeof(double), s);
+    pair_size_total_kernel<<<grid_for(F, kThreads, 148u * 4u), kThreads, 0, s>>>(F, sizes, pair_count, out);
 }
 
 void launch_seg_write2(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info,

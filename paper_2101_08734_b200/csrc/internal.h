@@ -161,6 +161,8 @@ void launch_segcnt(cudaStream_t s, uint32_t nloc, uint32_t E, const uint32_t* se
 void launch_seg_hist(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info,
                      uint32_t* seghist, uint32_t* segcnt, const double* sizes = nullptr,
                      double* segsum = nullptr, double* segmin = nullptr);
+void launch_pair_size_total(cudaStream_t s, uint32_t F, const double* sizes,
+                            const uint32_t* pair_count, double* out);
 void launch_fit_check(cudaStream_t s, uint32_t nloc, uint32_t E, const double* segsum,
                       const double* segmin, const uint32_t* segcnt, double C, uint32_t* allfit);
 void launch_seg_first(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info,

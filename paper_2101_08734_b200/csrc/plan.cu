@@ -665,6 +665,14 @@ int tier_order_v2(clairplan_plan* p) {
     double* ssize = need<double>(p->sorted_size, D, ok);
     if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed (candidates)");
     const uint64_t* segoff = p->seg_off.get<uint64_t>();
+    if (!p->hist_ready) {  // all-fit build: the count histograms were not needed then
+        const uint64_t NEE = (uint64_t)nloc * E * E;
+        launch_seg_hist(s, part, p->stream_buf.get<uint32_t>(), p->info16.get<uint16_t>(),
+                        p->seghist.get<uint32_t>(), p->segcnt.get<uint32_t>());
+        exclusive_scan(s, p->seghist.get<uint32_t>(), NEE, p->sorted_base.get<uint64_t>(), p->ws);
+        p->launches += 3;
+        p->hist_ready = true;
+    }
     launch_seg_write2(s, part, p->stream_buf.get<uint32_t>(), p->info16.get<uint16_t>(),
                       p->sizes.get<double>(), segoff, p->sorted_base.get<uint64_t>(), p->v2_mb, dest,
                       ssize, p->blkmask.get<uint32_t>(), p->blkbase.get<uint32_t>());
@@ -743,34 +751,45 @@ int build_seed_path_v2(clairplan_plan* p, const uint32_t* ext_perms,
         }
         exclusive_scan(s, pcount, F, poff, p->ws);
         p->mark(2);
-        // K4b: per-segment count histograms -> first-order and tier-order bases
-        // whole-worker fit test (all-fit path) where the segment pass runs anyway
+        // All-fit gate (necessary condition, on the host): the mean per-worker candidate size
+        // sum_k size_k * pairs_k / nloc must not exceed the class-1 capacity.
         const bool no_allfit = getenv("CLAIRPLAN_NO_ALLFIT") != nullptr;
-        const bool try_allfit = !red_hist && J > 0 && !no_allfit;
-        if (red_hist) {
-            launch_segcnt(s, nloc, E, seghist, segcnt);
-        } else if (try_allfit) {
-            CK(cudaMemsetAsync(allfit_flag, 0xFF, 4, s));
-            launch_seg_hist(s, part, stream_buf, info, seghist, segcnt, p->sizes.get<double>(),
-                            segsum, segmin);
-            launch_fit_check(s, nloc, E, segsum, segmin, segcnt, p->caps[0], allfit_flag);
-        } else {
-            launch_seg_hist(s, part, stream_buf, info, seghist, segcnt);
-        }
-        exclusive_scan(s, seghist, NEE, sbase, p->ws);
-        exclusive_scan(s, segcnt, (uint64_t)nloc * E, segoff, p->ws);
-        p->mark(3);
-        p->launches += 10;
+        const bool gate = !red_hist && J > 0 && !no_allfit;
+        double* ptot = segsum;  // scratch scalar until the segment pass runs
+        if (gate) launch_pair_size_total(s, F, p->sizes.get<double>(), pcount, ptot);
         std::vector<uint32_t> flags(E);
         uint64_t D = 0;
-        uint32_t allfit = 0;
-        CK(cudaMemcpyAsync(&D, segoff + (uint64_t)nloc * E, 8, cudaMemcpyDeviceToHost, s));
-        if (try_allfit) CK(cudaMemcpyAsync(&allfit, allfit_flag, 4, cudaMemcpyDeviceToHost, s));
+        double pair_size_total = 0;
+        CK(cudaMemcpyAsync(&D, poff + F, 8, cudaMemcpyDeviceToHost, s));
+        if (gate) CK(cudaMemcpyAsync(&pair_size_total, ptot, 8, cudaMemcpyDeviceToHost, s));
         CK(cudaMemcpyAsync(flags.data(), p->rej_flag.get<uint32_t>(), E * 4, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         bool any = false;
         if (int rc = resolve_rejections(p, flags, &any)) return rc;
         if (any) continue;
+        // K4b: per-segment first-access totals (+ sizes: whole-worker fit test) or count
+        // histograms -> first-order and tier-order bases
+        const bool try_allfit = gate && pair_size_total / nloc <= p->caps[0];
+        uint32_t allfit = 0;
+        if (try_allfit) {
+            CK(cudaMemsetAsync(allfit_flag, 0xFF, 4, s));
+            launch_seg_hist(s, part, stream_buf, info, nullptr, segcnt, p->sizes.get<double>(),
+                            segsum, segmin);
+            launch_fit_check(s, nloc, E, segsum, segmin, segcnt, p->caps[0], allfit_flag);
+            exclusive_scan(s, segcnt, (uint64_t)nloc * E, segoff, p->ws);
+            CK(cudaMemcpyAsync(&allfit, allfit_flag, 4, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+        }
+        p->hist_ready = false;
+        if (!allfit) {
+            if (red_hist) launch_segcnt(s, nloc, E, seghist, segcnt);
+            else launch_seg_hist(s, part, stream_buf, info, seghist, segcnt);
+            exclusive_scan(s, seghist, NEE, sbase, p->ws);
+            exclusive_scan(s, segcnt, (uint64_t)nloc * E, segoff, p->ws);
+            p->hist_ready = true;
+        }
+        p->mark(3);
+        p->launches += 10;
         p->D = D;
         if (D >= 0xFFFFFFFFull)
             return fail(CLAIRPLAN_EOVERFLOW, "more than 2^32-1 (worker, sample) pairs in one handle; "

@@ -121,6 +121,7 @@ struct clairplan_plan {
     DevBuf segsum, segmin, allfit_flag;
     bool allfit = false;             // last build took the all-fit path (no tier order)
     bool tier_ready = false;         // dest / sorted_size / block masks hold the tier order
+    bool hist_ready = false;         // seghist / sorted_base hold the count histograms
     bool v2 = false;                 // fast seed path in use for the last build
     uint32_t v2_mb = 0;              // blocks per segment / total blocks of the last v2 build
     uint64_t v2_nblk = 0;
