@@ -271,15 +271,19 @@ __global__ void __launch_bounds__(kThreads) seg_hist_kernel(Part part, const uin
                 const uint64_t t = t0 + 32 * u + lane;
                 k[u] = t < Le ? __ldcs(stream + g0 + t) : kNone;
             }
+            double sz[kSU];
 #pragma unroll
-            for (int u = 0; u < kSU; ++u) c[u] = k[u] != kNone ? row[k[u]] : 0u;
+            for (int u = 0; u < kSU; ++u) {
+                c[u] = k[u] != kNone ? row[k[u]] : 0u;
+                // issued with the info gather (both depend on k only), used for first accesses
+                sz[u] = (segsum && k[u] != kNone) ? __ldg(sizes + k[u]) : 0.0;
+            }
             if (segsum) {
 #pragma unroll
                 for (int u = 0; u < kSU; ++u) {
                     if (c[u] != 0) {
-                        const double v = sizes[k[u]];
-                        ssum += v;
-                        smin = fmin(smin, v);
+                        ssum += sz[u];
+                        smin = fmin(smin, sz[u]);
                     }
                 }
             }
@@ -696,11 +700,27 @@ __global__ void __launch_bounds__(kThreads) holder_tile_kernel(
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
     for (uint64_t k0 = (uint64_t)blockIdx.x * 32; k0 < F; k0 += (uint64_t)gridDim.x * 32) {
         __syncthreads();
-        for (uint32_t idx = threadIdx.x; idx < E * 32; idx += blockDim.x) {
-            const uint32_t e = idx >> 5, l = idx & 31;
-            const bool ok = k0 + l < F;
-            tinv[e * 33 + l] = ok ? __ldcs(inv + (size_t)e * F + k0 + l) : kNone;
-            trk[e * 33 + l] = ok ? __ldcs(rank16 + (size_t)e * F + k0 + l) : (uint16_t)0xFFFFu;
+        constexpr int TU = 4;  // rows in flight per thread
+        for (uint32_t i0 = threadIdx.x; i0 < E * 32; i0 += TU * blockDim.x) {
+            uint32_t iv[TU];
+            uint16_t rv[TU];
+#pragma unroll
+            for (int u = 0; u < TU; ++u) {
+                const uint32_t idx = i0 + u * blockDim.x;
+                const uint32_t e = idx >> 5, l = idx & 31;
+                const bool ok = idx < E * 32 && k0 + l < F;
+                iv[u] = ok ? __ldcs(inv + (size_t)e * F + k0 + l) : kNone;
+                rv[u] = ok ? __ldcs(rank16 + (size_t)e * F + k0 + l) : (uint16_t)0xFFFFu;
+            }
+#pragma unroll
+            for (int u = 0; u < TU; ++u) {
+                const uint32_t idx = i0 + u * blockDim.x;
+                if (idx < E * 32) {
+                    const uint32_t e = idx >> 5, l = idx & 31;
+                    tinv[e * 33 + l] = iv[u];
+                    trk[e * 33 + l] = rv[u];
+                }
+            }
         }
         __syncthreads();
         for (uint32_t s = warp; s < 32; s += nwarps) {
@@ -716,12 +736,20 @@ __global__ void __launch_bounds__(kThreads) holder_tile_kernel(
                 const uint32_t bit = tseg & 31;
                 uint32_t cls, pos = 0;
                 if constexpr (NP == -1) {
-                    const uint2 a2 = reinterpret_cast<const uint2*>(rec)[blk];
+                    // one 64-bit load and the class base issued together (a plain uint2 read
+                    // was split into two dependent 32-bit loads)
+                    const uint2 a2 = __ldg(reinterpret_cast<const uint2*>(rec) + blk);
+                    const uint32_t cb = __ldg(cbase + wl * J);
                     cls = (a2.x >> bit) & 1u;
-                    if (cls) pos = a2.y - cbase[wl * J] + __popc(a2.x & ((1u << bit) - 1u));
+                    pos = cls ? a2.y - cb + __popc(a2.x & ((1u << bit) - 1u)) : 0u;
                 } else {
-                const uint4* r4 = reinterpret_cast<const uint4*>(rec + blk * Rp);
-                const uint4 a = r4[0];
+                const uint4 a = __ldg(reinterpret_cast<const uint4*>(rec + blk * Rp));
+                uint32_t cb0 = 0, cb1 = 0, cb2 = 0;  // class bases issued with the record (J <= 3)
+                if constexpr (NP == 1 || NP == 2) {
+                    cb0 = __ldg(cbase + wl * J);
+                    if (J > 1) cb1 = __ldg(cbase + wl * J + 1);
+                    if (J > 2) cb2 = __ldg(cbase + wl * J + 2);
+                }
                 uint32_t cm;
                 if constexpr (NP == 1) {
                     cls = (a.x >> bit) & 1u;
@@ -742,7 +770,10 @@ __global__ void __launch_bounds__(kThreads) holder_tile_kernel(
                 if (cls) {
                     const uint32_t wi = np + cls - 1;
                     const uint32_t prew = wi < 4 ? pick(a, wi) : rec[blk * Rp + wi];
-                    pos = prew - cbase[wl * J + cls - 1] + __popc(cm & ((1u << bit) - 1u));
+                    uint32_t cb;
+                    if constexpr (NP == 1 || NP == 2) cb = cls == 1 ? cb0 : cls == 2 ? cb1 : cb2;
+                    else cb = cbase[wl * J + cls - 1];
+                    pos = prew - cb + __popc(cm & ((1u << bit) - 1u));
                 }
                 }
                 uint32_t* h = holders + 3 * (slot0 + rk);
