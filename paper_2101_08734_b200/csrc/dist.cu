@@ -41,34 +41,37 @@ __global__ void __launch_bounds__(kThreads) stream_relayout_kernel(Part part, Ep
     }
 }
 
-// one warp per (worker, epoch) segment, lanes over the segment's entries
-__global__ void __launch_bounds__(kThreads) stream_inv_kernel(Part part, const uint32_t* __restrict__ stream,
+// Position-major: thread per permutation position p of the handle's workers in epochs
+// [e_lo, e_hi) (epoch-major, so the inv rows being written stay L2-resident and their sectors
+// are completed there): k = the stream entry at p, inv[e][k] = p.  Positions of the handle's
+// workers in a full batch are contiguous: [h*B + sb(wb), h*B + sb(we)).
+__global__ void __launch_bounds__(kThreads) stream_inv_kernel(Part part, uint32_t e_lo, uint32_t e_hi,
+                                                              uint32_t lb, FastDiv dlb, uint32_t lt,
+                                                              const uint32_t* __restrict__ stream,
                                                               uint32_t* __restrict__ inv) {
-    const uint32_t E = part.E, F = part.F, nloc = part.wend - part.wbegin;
-    const uint32_t lane = threadIdx.x & 31;
-    const uint64_t nseg = (uint64_t)nloc * E;
-    for (uint64_t sg = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; sg < nseg;
-         sg += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
-        const uint32_t e = (uint32_t)(sg / nloc), wl = (uint32_t)(sg - (uint64_t)e * nloc);
-        const uint32_t w = part.wbegin + wl;
-        const uint32_t L = (uint32_t)part.len(w);
-        const FastDiv& dl = w < part.extra ? part.dFull1 : part.dFull0;
-        const uint32_t fb = (uint32_t)(w * part.base + (w < part.extra ? w : part.extra));
-        const uint32_t tb = (uint32_t)(w * part.tbase + (w < part.textra ? w : part.textra));
-        const uint32_t nfull = (uint32_t)(part.full * L);
-        const uint32_t Le = (uint32_t)part.epoch_len(w);
-        const uint32_t* seg = stream + part.stream_offset(w) + (uint64_t)e * Le;
-        uint32_t* row = inv + (size_t)e * F;
-        for (uint32_t t = lane; t < Le; t += 32) {
-            uint32_t pos;
-            if (t < nfull) {
-                const uint32_t h = dl.div(t);
-                pos = h * part.B + fb + (t - h * L);
-            } else {
-                pos = (uint32_t)(part.full * part.B) + tb + (t - nfull);
-            }
-            row[__ldcs(seg + t)] = pos;
+    const uint32_t F = part.F;
+    const uint32_t sb = (uint32_t)(part.wbegin * part.base + min((uint64_t)part.wbegin, part.extra));
+    const uint32_t tsb = (uint32_t)(part.wbegin * part.tbase + min((uint64_t)part.wbegin, part.textra));
+    const uint64_t lfull = (uint64_t)part.full * lb;
+    const uint64_t lep = lfull + lt;  // positions per epoch
+    const uint64_t total = lep * (e_hi - e_lo);
+    for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < total;
+         x += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t el = (uint32_t)(x / lep);
+        const uint32_t xe = (uint32_t)(x - (uint64_t)el * lep);
+        const uint32_t e = e_lo + el;
+        uint32_t pos;
+        if (xe < lfull) {
+            const uint32_t h = dlb.div(xe);
+            pos = h * part.B + sb + (xe - h * lb);
+        } else {
+            pos = (uint32_t)(part.full * part.B) + tsb + (uint32_t)(xe - lfull);
         }
+        uint32_t w;
+        uint64_t spos;
+        part.locate(pos, e, w, spos);
+        const uint32_t k = __ldcs(stream + part.stream_offset(w) + spos);
+        inv[(size_t)e * F + k] = pos;
     }
 }
 
@@ -80,8 +83,22 @@ void launch_stream_relayout(cudaStream_t s, const Part& part, const EpochSplit& 
 }
 
 void launch_stream_inv(cudaStream_t s, const Part& part, const uint32_t* stream, uint32_t* inv) {
-    const uint64_t nseg = (uint64_t)(part.wend - part.wbegin) * part.E;
-    stream_inv_kernel<<<grid_for(nseg * 32, kThreads, 148u * 64u), kThreads, 0, s>>>(part, stream, inv);
+    // epoch batches of ~40 MB of inv rows: the none-fill and the scatter of a batch meet in L2
+    const uint32_t F = part.F, E = part.E;
+    // local positions per full batch / in the tail batch
+    const uint32_t lfb = (uint32_t)((part.wend * part.base + std::min<uint64_t>(part.wend, part.extra)) -
+                                    (part.wbegin * part.base + std::min<uint64_t>(part.wbegin, part.extra)));
+    const uint32_t ltb = part.tail ? (uint32_t)((part.wend * part.tbase + std::min<uint64_t>(part.wend, part.textra)) -
+                                                (part.wbegin * part.tbase + std::min<uint64_t>(part.wbegin, part.textra)))
+                                   : 0u;
+    const uint32_t eb = std::max<uint32_t>(1, (uint32_t)((40ull << 20) / ((uint64_t)F * 4)));
+    for (uint32_t e0 = 0; e0 < E; e0 += eb) {
+        const uint32_t e1 = std::min(E, e0 + eb);
+        cudaMemsetAsync(inv + (size_t)e0 * F, 0xFF, (size_t)(e1 - e0) * F * 4, s);
+        const uint64_t n = ((uint64_t)part.full * lfb + ltb) * (e1 - e0);
+        stream_inv_kernel<<<grid_for(n, kThreads, 148u * 16u), kThreads, 0, s>>>(
+            part, e0, e1, lfb, FastDiv(lfb ? lfb : 1), ltb, stream, inv);
+    }
 }
 
 }  // namespace clairplan

@@ -241,7 +241,7 @@ constexpr int kSU = 4;
 // HIST = false: only the per-segment first-access totals (and sums), no count histogram
 template <bool HIST>
 __global__ void __launch_bounds__(kThreads) seg_hist_kernel(Part part, const uint32_t* __restrict__ stream,
-                                                             const uint16_t* __restrict__ info,
+                                                             const uint16_t* __restrict__ info, bool ent,
                                                              uint32_t* __restrict__ seghist,
                                                              uint32_t* __restrict__ segcnt,
                                                              const double* __restrict__ sizes,
@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(kThreads) seg_hist_kernel(Part part, const uin
             double sz[kSU];
 #pragma unroll
             for (int u = 0; u < kSU; ++u) {
-                c[u] = k[u] != kNone ? row[k[u]] : 0u;
+                c[u] = k[u] == kNone ? 0u : ent ? info[g0 + t0 + 32 * u + lane] : row[k[u]];
                 // issued with the info gather (both depend on k only), used for first accesses
                 sz[u] = (segsum && k[u] != kNone) ? __ldg(sizes + k[u]) : 0.0;
             }
@@ -378,40 +378,105 @@ __global__ void fit_check_kernel(uint32_t nloc, uint32_t E, const double* __rest
 // {first-access mask, class-1 prefix = first-order index of the block's first candidate} and
 // the class-list entries, written compacted.
 __global__ void __launch_bounds__(kThreads) seg_first_kernel(
-    Part part, const uint32_t* __restrict__ stream, const uint16_t* __restrict__ info,
-    const uint64_t* __restrict__ seg_off, uint32_t MB, uint32_t* __restrict__ rec,
+    Part part, const uint32_t* __restrict__ stream, const uint16_t* __restrict__ info, bool ent,
+    const uint64_t* __restrict__ chunk_off, uint32_t MB, uint32_t C, uint32_t* __restrict__ rec,
     uint32_t* __restrict__ class_list) {
     const uint32_t E = part.E, nloc = part.wend - part.wbegin;
     const uint32_t lane = threadIdx.x & 31;
-    const uint64_t nseg = (uint64_t)nloc * E;
-    for (uint64_t b = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; b < nseg;
+    const uint64_t nch = (uint64_t)nloc * E * C;
+    for (uint64_t b = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; b < nch;
          b += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
-        const uint32_t e = (uint32_t)(b / nloc), wl = (uint32_t)(b - (uint64_t)e * nloc);
+        // epoch-major chunk order (the info row of one epoch stays L2-resident)
+        const uint32_t e = (uint32_t)(b / ((uint64_t)nloc * C));
+        const uint32_t r = (uint32_t)(b - (uint64_t)e * nloc * C);
+        const uint32_t wl = r / C, ci = r - wl * C;
         const uint32_t w = part.wbegin + wl;
         const uint64_t Le = part.epoch_len(w);
+        const uint64_t t_lo = (uint64_t)ci * kAllfitChunk, t_hi = t_lo + kAllfitChunk < Le ? t_lo + kAllfitChunk : Le;
+        if (t_lo >= t_hi) continue;
         const uint64_t g0 = part.stream_offset(w) + (uint64_t)e * Le;
         const uint16_t* row = info + (size_t)e * part.F;
-        uint64_t frun = seg_off[(uint64_t)wl * E + e];
+        uint64_t frun = chunk_off[((uint64_t)wl * E + e) * C + ci];
         const uint64_t blk0 = ((uint64_t)wl * E + e) * MB;
-        for (uint64_t t0 = 0; t0 < Le; t0 += 32 * kSU) {
+        for (uint64_t t0 = t_lo; t0 < t_hi; t0 += 32 * kSU) {
             uint32_t k[kSU], c[kSU];
 #pragma unroll
             for (int u = 0; u < kSU; ++u) {
                 const uint64_t t = t0 + 32 * u + lane;
-                k[u] = t < Le ? __ldcs(stream + g0 + t) : kNone;
+                k[u] = t < t_hi ? __ldcs(stream + g0 + t) : kNone;
             }
 #pragma unroll
-            for (int u = 0; u < kSU; ++u) c[u] = k[u] != kNone ? row[k[u]] : 0u;
+            for (int u = 0; u < kSU; ++u)
+                c[u] = k[u] == kNone ? 0u : ent ? info[g0 + t0 + 32 * u + lane] : row[k[u]];
 #pragma unroll
             for (int u = 0; u < kSU; ++u) {
                 const uint64_t tb = t0 + 32 * u;
-                if (tb >= Le) break;
+                if (tb >= t_hi) break;
                 const bool first = c[u] != 0;
                 const uint32_t bal = __ballot_sync(0xffffffffu, first);
                 if (lane == 0) reinterpret_cast<uint2*>(rec)[blk0 + (tb >> 5)] = make_uint2(bal, (uint32_t)frun);
                 if (first) __stcs(class_list + frun + __popc(bal & lanemask_lt()), k[u]);
                 frun += __popc(bal);
             }
+        }
+    }
+}
+
+// All-fit counting pass: per chunk of kAllfitChunk stream entries, the first accesses and the sum /
+// minimum of their sizes (warp per chunk, epoch-major; chunks keep every warp busy when a
+// shard has few workers).  Chunk order of the outputs: (worker, epoch, chunk).
+__global__ void __launch_bounds__(kThreads) chunk_count_kernel(
+    Part part, const uint32_t* __restrict__ stream, const uint16_t* __restrict__ info, bool ent,
+    const double* __restrict__ sizes, uint32_t C, uint32_t* __restrict__ cnt,
+    double* __restrict__ csum, double* __restrict__ cmin) {
+    const uint32_t E = part.E, nloc = part.wend - part.wbegin;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t nch = (uint64_t)nloc * E * C;
+    for (uint64_t b = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; b < nch;
+         b += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+        const uint32_t e = (uint32_t)(b / ((uint64_t)nloc * C));
+        const uint32_t r = (uint32_t)(b - (uint64_t)e * nloc * C);
+        const uint32_t wl = r / C, ci = r - wl * C;
+        const uint32_t w = part.wbegin + wl;
+        const uint64_t Le = part.epoch_len(w);
+        const uint64_t t_lo = (uint64_t)ci * kAllfitChunk, t_hi = t_lo + kAllfitChunk < Le ? t_lo + kAllfitChunk : Le;
+        const uint64_t g0 = part.stream_offset(w) + (uint64_t)e * Le;
+        const uint16_t* row = info + (size_t)e * part.F;
+        uint32_t tot = 0;
+        double ssum = 0.0, smin = INFINITY;
+        for (uint64_t t0 = t_lo; t0 < t_hi; t0 += 32 * kSU) {
+            uint32_t k[kSU], c[kSU];
+            double sz[kSU];
+#pragma unroll
+            for (int u = 0; u < kSU; ++u) {
+                const uint64_t t = t0 + 32 * u + lane;
+                k[u] = t < t_hi ? __ldcs(stream + g0 + t) : kNone;
+            }
+#pragma unroll
+            for (int u = 0; u < kSU; ++u) {
+                c[u] = k[u] == kNone ? 0u : ent ? info[g0 + t0 + 32 * u + lane] : row[k[u]];
+                sz[u] = k[u] != kNone ? __ldg(sizes + k[u]) : 0.0;  // issued with the info gather
+            }
+#pragma unroll
+            for (int u = 0; u < kSU; ++u) {
+                if (c[u] != 0) {
+                    ++tot;
+                    ssum += sz[u];
+                    smin = fmin(smin, sz[u]);
+                }
+            }
+        }
+        tot = warp_sum(tot);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            ssum += __shfl_xor_sync(0xffffffffu, ssum, o);
+            smin = fmin(smin, __shfl_xor_sync(0xffffffffu, smin, o));
+        }
+        if (lane == 0) {
+            const uint64_t x = ((uint64_t)wl * E + e) * C + ci;
+            cnt[x] = tot;
+            csum[x] = ssum;
+            cmin[x] = smin;
         }
     }
 }
@@ -440,11 +505,19 @@ void launch_fit_check(cudaStream_t s, uint32_t nloc, uint32_t E, const double* s
         nloc, E, segsum, segmin, segcnt, C, allfit);
 }
 
-void launch_seg_first(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info,
-                      const uint64_t* seg_off, uint32_t MB, uint32_t* rec, uint32_t* class_list) {
-    const uint64_t nseg = (uint64_t)(part.wend - part.wbegin) * part.E;
-    seg_first_kernel<<<grid_for(nseg * 32, kThreads, 148u * 64u), kThreads, 0, s>>>(
-        part, stream, info, seg_off, MB, rec, class_list);
+void launch_seg_first(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info, bool ent,
+                      const uint64_t* chunk_off, uint32_t MB, uint32_t C, uint32_t* rec,
+                      uint32_t* class_list) {
+    const uint64_t nch = (uint64_t)(part.wend - part.wbegin) * part.E * C;
+    seg_first_kernel<<<grid_for(nch * 32, kThreads, 148u * 64u), kThreads, 0, s>>>(
+        part, stream, info, ent, chunk_off, MB, C, rec, class_list);
+}
+
+void launch_chunk_count(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info, bool ent,
+                        const double* sizes, uint32_t C, uint32_t* cnt, double* csum, double* cmin) {
+    const uint64_t nch = (uint64_t)(part.wend - part.wbegin) * part.E * C;
+    chunk_count_kernel<<<grid_for(nch * 32, kThreads, 148u * 64u), kThreads, 0, s>>>(
+        part, stream, info, ent, sizes, C, cnt, csum, cmin);
 }
 
 void launch_allfit_meta(cudaStream_t s, uint32_t nloc, uint32_t E, uint32_t J, const uint64_t* seg_off,
@@ -455,7 +528,7 @@ void launch_allfit_meta(cudaStream_t s, uint32_t nloc, uint32_t E, uint32_t J, c
 
 // ---------------------------------------------------------------------------- K4c
 __global__ void __launch_bounds__(kThreads) seg_write_kernel2(
-    Part part, const uint32_t* __restrict__ stream, const uint16_t* __restrict__ info,
+    Part part, const uint32_t* __restrict__ stream, const uint16_t* __restrict__ info, bool ent,
     const double* __restrict__ sizes, const uint64_t* __restrict__ seg_off,
     const uint64_t* __restrict__ sorted_base, uint32_t MB, uint32_t* __restrict__ dest,
     double* __restrict__ sorted_size, uint32_t* __restrict__ blkmask,
@@ -486,7 +559,8 @@ __global__ void __launch_bounds__(kThreads) seg_write_kernel2(
                 k[u] = t < Le ? __ldcs(stream + g0 + t) : kNone;
             }
 #pragma unroll
-            for (int u = 0; u < kSU; ++u) c[u] = k[u] != kNone ? row[k[u]] : 0u;
+            for (int u = 0; u < kSU; ++u)
+                c[u] = k[u] == kNone ? 0u : ent ? info[g0 + t0 + 32 * u + lane] : row[k[u]];
 #pragma unroll
             for (int u = 0; u < kSU; ++u) {
                 const uint64_t tb = t0 + 32 * u;
@@ -1033,7 +1107,7 @@ void launch_sample_hash(cudaStream_t s, const Part& part, const uint32_t* inv, u
         part, inv, info, rank16, pair_count, list, nlist, hs, W, seghist);
 }
 
-void launch_seg_hist(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info,
+void launch_seg_hist(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info, bool ent,
                      uint32_t* seghist, uint32_t* segcnt, const double* sizes, double* segsum,
                      double* segmin) {
     const uint64_t nseg = (uint64_t)(part.wend - part.wbegin) * part.E;
@@ -1041,10 +1115,10 @@ void launch_seg_hist(cudaStream_t s, const Part& part, const uint32_t* stream, c
     if (seghist) {
         const size_t smem = (size_t)(kThreads / 32) * part.E * 4;
         cudaFuncSetAttribute(seg_hist_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        seg_hist_kernel<true><<<grid, kThreads, smem, s>>>(part, stream, info, seghist, segcnt, sizes,
+        seg_hist_kernel<true><<<grid, kThreads, smem, s>>>(part, stream, info, ent, seghist, segcnt, sizes,
                                                             segsum, segmin);
     } else {
-        seg_hist_kernel<false><<<grid, kThreads, 0, s>>>(part, stream, info, nullptr, segcnt, sizes,
+        seg_hist_kernel<false><<<grid, kThreads, 0, s>>>(part, stream, info, ent, nullptr, segcnt, sizes,
                                                           segsum, segmin);
     }
 }
@@ -1067,7 +1141,7 @@ void launch_pair_size_total(cudaStream_t s, uint32_t F, const double* sizes,
     pair_size_total_kernel<<<grid_for(F, kThreads, 148u * 4u), kThreads, 0, s>>>(F, sizes, pair_count, out);
 }
 
-void launch_seg_write2(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info,
+void launch_seg_write2(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info, bool ent,
                        const double* sizes, const uint64_t* seg_off, const uint64_t* sorted_base,
                        uint32_t MB, uint32_t* dest, double* sorted_size, uint32_t* blkmask,
                        uint32_t* blkbase) {
@@ -1075,7 +1149,7 @@ void launch_seg_write2(cudaStream_t s, const Part& part, const uint32_t* stream,
     const size_t smem = (size_t)(kThreads / 32) * part.E * 4;
     cudaFuncSetAttribute(seg_write_kernel2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     seg_write_kernel2<<<grid_for(nseg * 32, kThreads, 148u * 64u), kThreads, smem, s>>>(
-        part, stream, info, sizes, seg_off, sorted_base, MB, dest, sorted_size, blkmask, blkbase);
+        part, stream, info, ent, sizes, seg_off, sorted_base, MB, dest, sorted_size, blkmask, blkbase);
 }
 
 }  // namespace clairplan

@@ -184,10 +184,10 @@ __global__ void __launch_bounds__(kTileThreads) fyb_tile_kernel(uint64_t key, ui
 // ---- fyb_block: one block of TB targets -> q, succ, inv ------------------------------------
 // 1. run table: the block's run in every tile t >= tmin (two words of each lst row) and the
 //    exclusive scan of the run lengths (element k of the block <-> run r, offset k - rdst[r])
-// 2. gather, warp per 32 consecutive elements (balanced, coalesced: consecutive elements
-//    mostly share a run): one warp-uniform binary search finds the run of the first element,
-//    the next 32 run starts sit in the lanes and a 5-step shuffle search places every
-//    element; each element is pushed on its target's list (head[target], nxt[element]) with
+// 2. gather, each warp a contiguous eighth of the elements, 32 at a time (balanced,
+//    coalesced: consecutive elements mostly share a run): one binary search per warp finds
+//    the first run, the next 32 run starts sit in the lanes and a 5-step shuffle search
+//    places every element; each element is pushed on its target's list (head[target], nxt[element]) with
 //    a shared atomicExch — no counting sort, no scan
 // 3. per writer: walk its target's list for its rank and the next larger writer ->
 //    q[y] (smallest writer != y), succ[w] (non-last writers; succ is preset to kNone) and
@@ -204,15 +204,21 @@ __device__ __forceinline__ void fyb_block_body(uint32_t F, const FyGeom& g, uint
     const uint32_t TB = 1u << g.lgTB, tbmask = TB - 1;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     constexpr uint32_t kEnd = BIG ? kNone : 0xFFFFu;
-    for (uint32_t x0 = warp * 32; x0 < n; x0 += kBlockThreads) {
-        // r0 = run of element x0 (largest r with rdst[r] <= x0; warp-uniform search)
-        uint32_t lo = 0, hi = nt;
-        while (hi - lo > 1) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (rdst[mid] <= x0) lo = mid;
+    // each warp gathers a contiguous range of the block's elements, 32 at a time; one
+    // warp-uniform binary search finds the run of its first element, later chunks advance it
+    constexpr uint32_t NW = kBlockThreads / 32;
+    const uint32_t xa = (uint32_t)(((uint64_t)n * warp) / NW), xb = (uint32_t)(((uint64_t)n * (warp + 1)) / NW);
+    uint32_t r0 = 0;
+    if (xa < xb) {
+        uint32_t hi = nt;
+        while (hi - r0 > 1) {
+            const uint32_t mid = (r0 + hi) >> 1;
+            if (rdst[mid] <= xa) r0 = mid;
             else hi = mid;
         }
-        const uint32_t r0 = lo;
+    }
+    for (uint32_t x0 = xa; x0 < xb; x0 += 32) {
+        while (r0 + 1 < nt && rdst[r0 + 1] <= x0) ++r0;  // warp-uniform, usually 0-1 steps
         const uint32_t r = r0 + lane;
         const uint32_t beg = r < nt ? rdst[r] : n;
         const uint32_t src = r < nt ? rsrc[r] : 0u;
@@ -227,7 +233,7 @@ __device__ __forceinline__ void fyb_block_body(uint32_t F, const FyGeom& g, uint
         uint32_t bj = __shfl_sync(0xffffffffu, beg, j);
         uint32_t sj = __shfl_sync(0xffffffffu, src, j);
         uint32_t rr = r0 + j;
-        if (k < n) {
+        if (k < xb) {
             if (k >= lim) {  // beyond 32 runs (many empty runs): full search
                 uint32_t l2 = r0, h2 = nt;
                 while (h2 - l2 > 1) {
@@ -251,6 +257,7 @@ __device__ __forceinline__ void fyb_block_body(uint32_t F, const FyGeom& g, uint
                 N16[k] = (uint16_t)old;
             }
         }
+        r0 = __shfl_sync(0xffffffffu, rr, 31);  // run of the chunk's last element
     }
     __syncthreads();
     const uint32_t y0 = b << g.lgTB;
@@ -315,12 +322,14 @@ __global__ void __launch_bounds__(kBlockThreads) fyb_block_kernel(uint32_t F, Fy
     uint32_t* qq = q + (size_t)slot * F;
     uint32_t* iv = inv ? inv + (size_t)(e0 + slot) * F : nullptr;
     if (n <= g.cap) {
-        for (uint32_t k = threadIdx.x; k < TB; k += kBlockThreads) head[k] = 0xFFFFu;
+        for (uint32_t k = threadIdx.x; k < TB / 4; k += kBlockThreads)
+            reinterpret_cast<uint4*>(head)[k] = make_uint4(0xFFFFu, 0xFFFFu, 0xFFFFu, 0xFFFFu);
         __syncthreads();
         fyb_block_body<false>(F, g, b, n, nt, tmin, rsrc, rdst, head, W, J16, N16, nullptr,
                               nullptr, bk, sc, qq, iv);
     } else {  // heavy block (small targets): global pool slab
-        for (uint32_t k = threadIdx.x; k < TB; k += kBlockThreads) head[k] = kNone;
+        for (uint32_t k = threadIdx.x; k < TB / 4; k += kBlockThreads)
+            reinterpret_cast<uint4*>(head)[k] = make_uint4(kNone, kNone, kNone, kNone);
         if (threadIdx.x == 0) s_pool = atomicAdd(pool_used + slot, 3 * n);
         __syncthreads();
         uint32_t* gW = pool + (size_t)slot * 4 * F + s_pool;

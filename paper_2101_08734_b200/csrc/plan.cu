@@ -501,6 +501,12 @@ int first_fit_classes(clairplan_plan* p, const double* ssize, uint8_t* cls) {
 }
 
 
+// (count at first access) source of the segment passes: info[e][k] (dense sample pass) or
+// einfo[stream index] (sparse sample pass of a sharded handle)
+inline const uint16_t* info_src(clairplan_plan* p) {
+    return p->sparse ? p->einfo.get<uint16_t>() : p->info16.get<uint16_t>();
+}
+
 int holders_v2(clairplan_plan* p);
 int no_classes_v2(clairplan_plan* p);
 
@@ -576,7 +582,12 @@ int holders_v2(clairplan_plan* p) {
         CK(cudaMemcpyAsync(hst.data(), cstart, hst.size() * 8, cudaMemcpyDeviceToHost, s));
         p->mark(7);
         // K8: holder CSR, sample-major
-        launch_holder_tile(s, part, inv, rank16, MB, rec, np, J, Rp, cbase, poff, htmp, p->allfit);
+        if (p->sparse)
+            launch_holder_sparse(s, part, p->soff.get<uint64_t>(), p->koff.get<uint64_t>(),
+                                 p->csr.get<uint32_t>(), p->erank.get<uint16_t>(), MB, rec, np, J, Rp,
+                                 cbase, poff, htmp, p->allfit);
+        else
+            launch_holder_tile(s, part, inv, rank16, MB, rec, np, J, Rp, cbase, poff, htmp, p->allfit);
         ++p->launches;
         CK(cudaStreamSynchronize(s));
         p->class_start_h.assign((size_t)nloc * (J + 1), 0);
@@ -644,10 +655,11 @@ int assign_allfit_v2(clairplan_plan* p) {
     uint64_t* clen = need<uint64_t>(p->class_len, (uint64_t)nloc * J, ok);
     uint64_t* cstart = need<uint64_t>(p->class_start, (uint64_t)nloc * J + 1, ok);
     if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed (class lists)");
-    const uint64_t* segoff = p->seg_off.get<uint64_t>();
-    launch_seg_first(s, part, p->stream_buf.get<uint32_t>(), p->info16.get<uint16_t>(), segoff,
-                     p->v2_mb, rec, centries);
-    launch_allfit_meta(s, nloc, E, J, segoff, clen, cstart, cbase);
+    const uint64_t* choff = p->choff.get<uint64_t>();
+    const uint32_t C = p->allfit_chunks;
+    launch_seg_first(s, part, p->stream_buf.get<uint32_t>(), info_src(p), p->sparse, choff,
+                     p->v2_mb, C, rec, centries);
+    launch_allfit_meta(s, nloc, E * C, J, choff, clen, cstart, cbase);
     p->launches += 2;
     p->mark(6);
     return holders_v2(p);
@@ -667,13 +679,14 @@ int tier_order_v2(clairplan_plan* p) {
     const uint64_t* segoff = p->seg_off.get<uint64_t>();
     if (!p->hist_ready) {  // all-fit build: the count histograms were not needed then
         const uint64_t NEE = (uint64_t)nloc * E * E;
-        launch_seg_hist(s, part, p->stream_buf.get<uint32_t>(), p->info16.get<uint16_t>(),
+        launch_seg_hist(s, part, p->stream_buf.get<uint32_t>(), info_src(p), p->sparse,
                         p->seghist.get<uint32_t>(), p->segcnt.get<uint32_t>());
         exclusive_scan(s, p->seghist.get<uint32_t>(), NEE, p->sorted_base.get<uint64_t>(), p->ws);
-        p->launches += 3;
+        exclusive_scan(s, p->segcnt.get<uint32_t>(), (uint64_t)nloc * E, p->seg_off.get<uint64_t>(), p->ws);
+        p->launches += 4;
         p->hist_ready = true;
     }
-    launch_seg_write2(s, part, p->stream_buf.get<uint32_t>(), p->info16.get<uint16_t>(),
+    launch_seg_write2(s, part, p->stream_buf.get<uint32_t>(), info_src(p), p->sparse,
                       p->sizes.get<double>(), segoff, p->sorted_base.get<uint64_t>(), p->v2_mb, dest,
                       ssize, p->blkmask.get<uint32_t>(), p->blkbase.get<uint32_t>());
     launch_worker_segments(s, segoff, nloc, E, p->wbeg.get<uint64_t>(), p->wlen.get<uint64_t>());
@@ -708,9 +721,28 @@ int build_seed_path_v2(clairplan_plan* p, const uint32_t* ext_perms,
     uint32_t* bmask = need<uint32_t>(p->blkmask, nblk, ok);
     uint32_t* bbase = need<uint32_t>(p->blkbase, nblk, ok);
     uint32_t* hard = need<uint32_t>(p->hard, (uint64_t)F + 1, ok);
-    double* segsum = need<double>(p->segsum, (uint64_t)nloc * E, ok);
-    double* segmin = need<double>(p->segmin, (uint64_t)nloc * E, ok);
+    const uint32_t C = (uint32_t)((part.epoch_len(part.wbegin) + kAllfitChunk - 1) / kAllfitChunk);
+    const uint64_t NCH = (uint64_t)nloc * E * C;  // all-fit chunks (worker, epoch, chunk)
+    double* segsum = need<double>(p->segsum, NCH, ok);
+    double* segmin = need<double>(p->segmin, NCH, ok);
+    uint32_t* chcnt = need<uint32_t>(p->chcnt, NCH, ok);
+    uint64_t* choff = need<uint64_t>(p->choff, NCH + 1, ok);
     uint32_t* allfit_flag = need<uint32_t>(p->allfit_flag, 1, ok);
+    // sparse sample-major passes (sharded handle fed by the all-to-all; CLAIRPLAN_DENSE=1: A/B)
+    const bool sparse = ext_streams && sparse_path_ok(part) && getenv("CLAIRPLAN_DENSE") == nullptr;
+    p->sparse = sparse;
+    uint32_t *sp_cnt = nullptr, *sp_cur = nullptr, *sp_csr = nullptr;
+    uint64_t *sp_koff = nullptr, *sp_soff = nullptr;
+    uint16_t *sp_einfo = nullptr, *sp_erank = nullptr;
+    if (sparse) {
+        sp_cnt = need<uint32_t>(p->hcount, F, ok);
+        sp_cur = need<uint32_t>(p->sp_cur, F, ok);
+        sp_koff = need<uint64_t>(p->koff, (uint64_t)F + 1, ok);
+        sp_csr = need<uint32_t>(p->csr, p->A, ok);
+        sp_soff = need<uint64_t>(p->soff, (uint64_t)nloc + 1, ok);
+        sp_einfo = need<uint16_t>(p->einfo, p->A, ok);
+        sp_erank = need<uint16_t>(p->erank, p->A, ok);
+    }
     if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed (streams / histograms)");
     if (int rc = ensure_ws(p, std::max<uint64_t>(p->A, std::max<uint64_t>(NEE, F)), nloc)) return rc;
     if (int rc = alloc_rej(p, E)) return rc;
@@ -725,9 +757,11 @@ int build_seed_path_v2(clairplan_plan* p, const uint32_t* ext_perms,
         // K1-K3: permutations -> streams + inverse permutations
         if (ext_streams) {  // multi-GPU: epoch-range streams from every rank (all-to-all)
             launch_stream_relayout(s, part, *es, ext_streams, stream_buf);
-            CK(cudaMemsetAsync(inv, 0xFF, EF * 4, s));
-            launch_stream_inv(s, part, stream_buf, inv);
-            p->launches += 2;
+            ++p->launches;
+            if (!sparse) {
+                launch_stream_inv(s, part, stream_buf, inv);  // none-fills inv batch by batch
+                ++p->launches;
+            }
         } else if (ext_perms) {
             launch_perm_scatter(s, part, ext_perms, inv, stream_buf);
             ++p->launches;
@@ -738,11 +772,16 @@ int build_seed_path_v2(clairplan_plan* p, const uint32_t* ext_perms,
         // K4a: per-sample (worker, count, first epoch)
         // Large F: the segment histograms are accumulated by the sample pass itself (REDs
         // overlap its latency); small F: a separate warp-per-segment pass is cheaper.
-        const bool red_hist = F >= (1u << 22);
+        const bool red_hist = F >= (1u << 22) && !sparse;
         uint32_t* hist_out = red_hist ? seghist : nullptr;
         if (red_hist) CK(cudaMemsetAsync(seghist, 0, NEE * 4, s));
         static const bool lanes_only = getenv("CLAIRPLAN_SAMPLE_LANES") != nullptr;  // A/B
-        if (tile_path_ok(part) && !lanes_only) {
+        if (sparse) {
+            launch_sparse_csr(s, part, stream_buf, p->A, sp_cnt, sp_koff, sp_cur, sp_csr, sp_soff,
+                              p->ws);
+            launch_sparse_sample(s, part, sp_soff, sp_koff, sp_csr, pcount, sp_einfo, sp_erank);
+            p->launches += 7;
+        } else if (tile_path_ok(part) && !lanes_only) {
             launch_sample_tile(s, part, inv, info, rank16, pcount, hist_out);
         } else if (lanes) {
             launch_sample_lanes(s, part, inv, info, rank16, pcount, hist_out);
@@ -773,17 +812,18 @@ int build_seed_path_v2(clairplan_plan* p, const uint32_t* ext_perms,
         uint32_t allfit = 0;
         if (try_allfit) {
             CK(cudaMemsetAsync(allfit_flag, 0xFF, 4, s));
-            launch_seg_hist(s, part, stream_buf, info, nullptr, segcnt, p->sizes.get<double>(),
-                            segsum, segmin);
-            launch_fit_check(s, nloc, E, segsum, segmin, segcnt, p->caps[0], allfit_flag);
-            exclusive_scan(s, segcnt, (uint64_t)nloc * E, segoff, p->ws);
+            launch_chunk_count(s, part, stream_buf, info_src(p), p->sparse, p->sizes.get<double>(), C, chcnt, segsum,
+                               segmin);
+            launch_fit_check(s, nloc, E * C, segsum, segmin, chcnt, p->caps[0], allfit_flag);
+            exclusive_scan(s, chcnt, NCH, choff, p->ws);
+            p->allfit_chunks = C;
             CK(cudaMemcpyAsync(&allfit, allfit_flag, 4, cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
         }
         p->hist_ready = false;
         if (!allfit) {
             if (red_hist) launch_segcnt(s, nloc, E, seghist, segcnt);
-            else launch_seg_hist(s, part, stream_buf, info, seghist, segcnt);
+            else launch_seg_hist(s, part, stream_buf, info_src(p), p->sparse, seghist, segcnt);
             exclusive_scan(s, seghist, NEE, sbase, p->ws);
             exclusive_scan(s, segcnt, (uint64_t)nloc * E, segoff, p->ws);
             p->hist_ready = true;

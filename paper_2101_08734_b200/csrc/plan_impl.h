@@ -118,7 +118,10 @@ struct clairplan_plan {
     DevBuf wsbuf;
     DevBuf cand_w, dfirst, dcounts;  // explicit-stream (generic) path
     DevBuf inv, info16, rank16, cbase, seghist, sorted_base, blkmask, blkbase, planes, ccount, cpre, hard;
-    DevBuf segsum, segmin, allfit_flag;
+    DevBuf segsum, segmin, allfit_flag, chcnt, choff;
+    DevBuf koff, sp_cur, csr, soff, einfo, erank;  // sparse sample-major passes (sharded)
+    bool sparse = false;             // last build used the sparse passes
+    uint32_t allfit_chunks = 1;      // chunks per (worker, epoch) segment of the all-fit passes
     bool allfit = false;             // last build took the all-fit path (no tier order)
     bool tier_ready = false;         // dest / sorted_size / block masks hold the tier order
     bool hist_ready = false;         // seghist / sorted_base hold the count histograms

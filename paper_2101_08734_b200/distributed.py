@@ -131,23 +131,32 @@ class DistributedPlan:
             self.local_rows = torch.empty((max(self.pad, 1), samples), dtype=torch.int32,
                                           device="cuda")
         self.counts = torch.empty(samples, dtype=torch.int32, device="cuda")
+        self.timings = {}
         self.global_offsets = None
         self.rank_starts = None
 
     def build(self):
+        import time
         torch, cp = self.torch, self.cp
         e0, n = self.ranges[self.rank]
+        t0 = time.perf_counter()
         if self.mode == "streams":
             cp._check(self.L.clairplan_generate_streams(self.plan._h, e0, n,
                                                         C.c_void_p(self.send.data_ptr())))
+            t1 = time.perf_counter()
             # the library synchronises its stream before returning; NCCL runs on torch's
             self.dist.all_to_all_single(self.recv[:sum(self.recv_splits)],
                                         self.send[:sum(self.send_splits)],
                                         self.recv_splits, self.send_splits, group=self.group)
             torch.cuda.current_stream().synchronize()
+            t2 = time.perf_counter()
             cp._check(self.L.clairplan_build_from_streams(
                 self.plan._h, C.c_void_p(self.recv.data_ptr()),
                 self.bounds.ctypes.data_as(C.c_void_p), self.world))
+            t3 = time.perf_counter()
+            self.timings = {"generate_ms": round((t1 - t0) * 1e3, 3),
+                            "all_to_all_ms": round((t2 - t1) * 1e3, 3),
+                            "build_ms": round((t3 - t2) * 1e3, 3)}
         else:
             cp._check(self.L.clairplan_generate_perms(self.plan._h, e0, n,
                                                       C.c_void_p(self.local_rows.data_ptr())))
