@@ -186,6 +186,15 @@ uint64_t clairplan_launch_count(clairplan_t plan);
  * returns the number of stages; names via clairplan_stage_name. */
 int clairplan_stage_times(clairplan_t plan, double* ms, uint32_t n);
 const char* clairplan_stage_name(uint32_t stage);
+/* End to end in one call (the reference's build_policy returns host vectors,
+ * policies.cpp:446-456): sizes from host memory (optional, NULL keeps the handle's), the
+ * build, and every output copied to host buffers — streams (layout of
+ * clairplan_export_streams), class lists (clairplan_export_class_lists), holder CSR
+ * (clairplan_export_holders).  The stream copy starts as soon as the streams are final and
+ * overlaps the rest of the build on a second CUDA stream; pinned buffers make it asynchronous. */
+int clairplan_build_export(clairplan_t plan, const double* host_sizes, uint32_t* streams_out,
+                           uint64_t streams_cap, uint32_t* class_lists_out, uint64_t cl_cap,
+                           uint64_t* offsets_out, uint32_t* holders_out, uint64_t holders_cap);
 /* Replaces the sample sizes (DatasetModel::sizes_mb) of a handle, e.g. from pinned host
  * memory for an end-to-end step; the copy is ordered before the next build. */
 int clairplan_set_sizes(clairplan_t plan, const double* sizes_mb, int on_device);

@@ -241,7 +241,7 @@ constexpr int kSU = 4;
 // HIST = false: only the per-segment first-access totals (and sums), no count histogram
 template <bool HIST>
 __global__ void __launch_bounds__(kThreads) seg_hist_kernel(Part part, const uint32_t* __restrict__ stream,
-                                                             const uint16_t* __restrict__ info, bool ent,
+                                                             const uint16_t* __restrict__ info, const uint32_t* __restrict__ cpos,
                                                              uint32_t* __restrict__ seghist,
                                                              uint32_t* __restrict__ segcnt,
                                                              const double* __restrict__ sizes,
@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(kThreads) seg_hist_kernel(Part part, const uin
             double sz[kSU];
 #pragma unroll
             for (int u = 0; u < kSU; ++u) {
-                c[u] = k[u] == kNone ? 0u : ent ? info[g0 + t0 + 32 * u + lane] : row[k[u]];
+                c[u] = k[u] == kNone ? 0u : cpos ? info[cpos[g0 + t0 + 32 * u + lane]] : row[k[u]];
                 // issued with the info gather (both depend on k only), used for first accesses
                 sz[u] = (segsum && k[u] != kNone) ? __ldg(sizes + k[u]) : 0.0;
             }
@@ -339,65 +339,50 @@ void launch_segcnt(cudaStream_t s, uint32_t nloc, uint32_t E, const uint32_t* se
                                                                               segcnt);
 }
 
-// ---------------------------------------------------------------------------- whole-worker fit
+// ---------------------------------------------------------------------------- all-fit path
 // pack_first_fit (policies.cpp:40-55) takes every candidate of a worker into class 1 when the
 // sizes are non-negative and their sum stays below the capacity by more than the rounding of
-// any summation order and of the chain `remaining -= s` (same bound as ff_prefix_kernel):
-// then `s <= remaining` holds at every step whatever the tier order is.  One warp per worker;
-// *allfit is cleared when some worker does not provably fit.
-__global__ void fit_check_kernel(uint32_t nloc, uint32_t E, const double* __restrict__ segsum,
-                                 const double* __restrict__ segmin,
-                                 const uint32_t* __restrict__ segcnt, double C,
-                                 uint32_t* __restrict__ allfit) {
-    const uint32_t lane = threadIdx.x & 31;
-    for (uint32_t wl = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; wl < nloc;
-         wl += (gridDim.x * blockDim.x) >> 5) {
-        double sum = 0.0, mn = INFINITY;
-        uint64_t n = 0;
-        for (uint32_t e = lane; e < E; e += 32) {
-            sum += segsum[(uint64_t)wl * E + e];
-            mn = fmin(mn, segmin[(uint64_t)wl * E + e]);
-            n += segcnt[(uint64_t)wl * E + e];
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            sum += __shfl_xor_sync(0xffffffffu, sum, o);
-            mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-            n += __shfl_xor_sync(0xffffffffu, n, o);
-        }
-        if (lane == 0) {
-            const double tol = ((double)n + 1024.0) * fmax(C, sum) * 0x1.0p-48;
-            const bool fits = n == 0 || (mn >= 0.0 && C - sum > tol);
-            if (!fits) atomicAnd(allfit, 0u);
-        }
-    }
-}
+// any summation order and of the chain `remaining -= s`: `s <= remaining` then holds at every
+// step whatever the tier order is.  The per-worker sums come from the sample pass
+// (WorkerSums); the host decides (allfit_decide, plan.cu).  Then one pass over the streams:
+//
+// seg_allfit   warp per chunk of kAllfitChunk stream entries, chunks taken from a ticket
+//              counter in epoch-major order (the info row of one epoch stays L2-resident).
+//              Pass A: first accesses (ballots kept one per lane); the chunk's count is
+//              published and the worker-local first-order prefix found by a decoupled
+//              look-back over the worker's earlier chunks (all hold smaller tickets, so they
+//              are running or done: no deadlock).  Pass B re-reads the chunk (L2) and writes
+//              per 32-entry block the record {first-access mask, worker-local first-order
+//              index} and the class-1 list (= first-access order = prefetch order) at the
+//              worker's stream offset.
+constexpr unsigned long long kStAgg = 1ull << 62, kStInc = 2ull << 62, kStMask = (1ull << 62) - 1;
 
-// All-fit variant of seg_write (K4c) + K7: every first access is class 1, the class-1 list of a
-// worker is its first-order candidate list.  Per 32-entry block: the all-fit record uint2
-// {first-access mask, class-1 prefix = first-order index of the block's first candidate} and
-// the class-list entries, written compacted.
-__global__ void __launch_bounds__(kThreads) seg_first_kernel(
-    Part part, const uint32_t* __restrict__ stream, const uint16_t* __restrict__ info, bool ent,
-    const uint64_t* __restrict__ chunk_off, uint32_t MB, uint32_t C, uint32_t* __restrict__ rec,
-    uint32_t* __restrict__ class_list) {
+__global__ void __launch_bounds__(kThreads) seg_allfit_kernel(
+    Part part, const uint32_t* __restrict__ stream, const uint16_t* __restrict__ info,
+    const uint32_t* __restrict__ cpos, uint32_t MB, uint32_t C,
+    unsigned long long* __restrict__ status, uint32_t* __restrict__ ticket,
+    uint32_t* __restrict__ rec, uint32_t* __restrict__ class_list) {
     const uint32_t E = part.E, nloc = part.wend - part.wbegin;
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t nch = (uint64_t)nloc * E * C;
-    for (uint64_t b = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; b < nch;
-         b += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
-        // epoch-major chunk order (the info row of one epoch stays L2-resident)
-        const uint32_t e = (uint32_t)(b / ((uint64_t)nloc * C));
-        const uint32_t r = (uint32_t)(b - (uint64_t)e * nloc * C);
+    while (true) {
+        uint32_t tk = 0;
+        if (lane == 0) tk = atomicAdd(ticket, 1u);
+        tk = __shfl_sync(0xffffffffu, tk, 0);
+        if (tk >= nch) break;
+        const uint32_t e = (uint32_t)(tk / ((uint64_t)nloc * C));
+        const uint32_t r = (uint32_t)(tk - (uint64_t)e * nloc * C);
         const uint32_t wl = r / C, ci = r - wl * C;
         const uint32_t w = part.wbegin + wl;
         const uint64_t Le = part.epoch_len(w);
-        const uint64_t t_lo = (uint64_t)ci * kAllfitChunk, t_hi = t_lo + kAllfitChunk < Le ? t_lo + kAllfitChunk : Le;
-        if (t_lo >= t_hi) continue;
-        const uint64_t g0 = part.stream_offset(w) + (uint64_t)e * Le;
+        const uint64_t t_lo = (uint64_t)ci * kAllfitChunk;
+        const uint64_t t_hi = t_lo + kAllfitChunk < Le ? t_lo + kAllfitChunk : Le;
+        const uint64_t sw = part.stream_offset(w);
+        const uint64_t g0 = sw + (uint64_t)e * Le;
         const uint16_t* row = info + (size_t)e * part.F;
-        uint64_t frun = chunk_off[((uint64_t)wl * E + e) * C + ci];
-        const uint64_t blk0 = ((uint64_t)wl * E + e) * MB;
+        const uint64_t x = ((uint64_t)wl * E + e) * C + ci;  // worker-major chunk index
+        // pass A: first-access ballots, lane b keeps block b's
+        uint32_t mymask = 0, tot = 0;
         for (uint64_t t0 = t_lo; t0 < t_hi; t0 += 32 * kSU) {
             uint32_t k[kSU], c[kSU];
 #pragma unroll
@@ -407,128 +392,99 @@ __global__ void __launch_bounds__(kThreads) seg_first_kernel(
             }
 #pragma unroll
             for (int u = 0; u < kSU; ++u)
-                c[u] = k[u] == kNone ? 0u : ent ? info[g0 + t0 + 32 * u + lane] : row[k[u]];
+                c[u] = k[u] == kNone ? 0u : cpos ? info[cpos[g0 + t0 + 32 * u + lane]] : row[k[u]];
 #pragma unroll
             for (int u = 0; u < kSU; ++u) {
                 const uint64_t tb = t0 + 32 * u;
-                if (tb >= t_hi) break;
-                const bool first = c[u] != 0;
-                const uint32_t bal = __ballot_sync(0xffffffffu, first);
-                if (lane == 0) reinterpret_cast<uint2*>(rec)[blk0 + (tb >> 5)] = make_uint2(bal, (uint32_t)frun);
-                if (first) __stcs(class_list + frun + __popc(bal & lanemask_lt()), k[u]);
-                frun += __popc(bal);
+                const uint32_t bal = __ballot_sync(0xffffffffu, c[u] != 0);
+                if (tb < t_hi && lane == (uint32_t)((tb - t_lo) >> 5)) mymask = bal;
+                tot += __popc(bal);
             }
         }
-    }
-}
-
-// All-fit counting pass: per chunk of kAllfitChunk stream entries, the first accesses and the sum /
-// minimum of their sizes (warp per chunk, epoch-major; chunks keep every warp busy when a
-// shard has few workers).  Chunk order of the outputs: (worker, epoch, chunk).
-__global__ void __launch_bounds__(kThreads) chunk_count_kernel(
-    Part part, const uint32_t* __restrict__ stream, const uint16_t* __restrict__ info, bool ent,
-    const double* __restrict__ sizes, uint32_t C, uint32_t* __restrict__ cnt,
-    double* __restrict__ csum, double* __restrict__ cmin) {
-    const uint32_t E = part.E, nloc = part.wend - part.wbegin;
-    const uint32_t lane = threadIdx.x & 31;
-    const uint64_t nch = (uint64_t)nloc * E * C;
-    for (uint64_t b = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; b < nch;
-         b += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
-        const uint32_t e = (uint32_t)(b / ((uint64_t)nloc * C));
-        const uint32_t r = (uint32_t)(b - (uint64_t)e * nloc * C);
-        const uint32_t wl = r / C, ci = r - wl * C;
-        const uint32_t w = part.wbegin + wl;
-        const uint64_t Le = part.epoch_len(w);
-        const uint64_t t_lo = (uint64_t)ci * kAllfitChunk, t_hi = t_lo + kAllfitChunk < Le ? t_lo + kAllfitChunk : Le;
-        const uint64_t g0 = part.stream_offset(w) + (uint64_t)e * Le;
-        const uint16_t* row = info + (size_t)e * part.F;
-        uint32_t tot = 0;
-        double ssum = 0.0, smin = INFINITY;
+        // publish, look back within the worker's chain of chunks
+        unsigned long long prefix = 0;
+        if (lane == 0) {
+            const uint64_t first_x = (uint64_t)wl * E * C;
+            if (x == first_x) {
+                atomicExch(status + x, kStInc | tot);
+            } else {
+                atomicExch(status + x, kStAgg | tot);
+                for (uint64_t j = x - 1;; --j) {
+                    unsigned long long v;
+                    do {
+                        v = *reinterpret_cast<volatile unsigned long long*>(status + j);
+                    } while (v == 0);
+                    prefix += v & kStMask;
+                    if ((v & kStInc) || j == first_x) break;
+                }
+                atomicExch(status + x, kStInc | (prefix + tot));
+            }
+        }
+        prefix = __shfl_sync(0xffffffffu, prefix, 0);
+        // pass B: block records and the class-1 list
+        uint64_t run = prefix;
+        const uint64_t blk0 = ((uint64_t)wl * E + e) * MB;
         for (uint64_t t0 = t_lo; t0 < t_hi; t0 += 32 * kSU) {
-            uint32_t k[kSU], c[kSU];
-            double sz[kSU];
+            uint32_t k[kSU];
 #pragma unroll
             for (int u = 0; u < kSU; ++u) {
                 const uint64_t t = t0 + 32 * u + lane;
-                k[u] = t < t_hi ? __ldcs(stream + g0 + t) : kNone;
+                k[u] = t < t_hi ? stream[g0 + t] : kNone;
             }
 #pragma unroll
             for (int u = 0; u < kSU; ++u) {
-                c[u] = k[u] == kNone ? 0u : ent ? info[g0 + t0 + 32 * u + lane] : row[k[u]];
-                sz[u] = k[u] != kNone ? __ldg(sizes + k[u]) : 0.0;  // issued with the info gather
-            }
-#pragma unroll
-            for (int u = 0; u < kSU; ++u) {
-                if (c[u] != 0) {
-                    ++tot;
-                    ssum += sz[u];
-                    smin = fmin(smin, sz[u]);
+                const uint64_t tb = t0 + 32 * u;
+                const uint32_t bal = __shfl_sync(0xffffffffu, mymask, (uint32_t)((tb - t_lo) >> 5) & 31);
+                if (tb < t_hi) {
+                    if (lane == 0)
+                        reinterpret_cast<uint2*>(rec)[blk0 + (tb >> 5)] = make_uint2(bal, (uint32_t)run);
+                    if ((bal >> lane) & 1u)
+                        __stcs(class_list + sw + run + __popc(bal & lanemask_lt()), k[u]);
+                    run += __popc(bal);
                 }
             }
         }
-        tot = warp_sum(tot);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            ssum += __shfl_xor_sync(0xffffffffu, ssum, o);
-            smin = fmin(smin, __shfl_xor_sync(0xffffffffu, smin, o));
-        }
-        if (lane == 0) {
-            const uint64_t x = ((uint64_t)wl * E + e) * C + ci;
-            cnt[x] = tot;
-            csum[x] = ssum;
-            cmin[x] = smin;
-        }
     }
 }
 
-// Class-list geometry of an all-fit handle: list (w, 1) = the worker's candidates, lists
-// (w, j > 1) empty; cbase = class-1 prefix at the worker's first block.
-__global__ void allfit_meta_kernel(uint32_t nloc, uint32_t E, uint32_t J,
-                                   const uint64_t* __restrict__ seg_off, uint64_t* __restrict__ clen,
-                                   uint64_t* __restrict__ cstart, uint32_t* __restrict__ cbase) {
+// class-list geometry of an all-fit handle: list (w, 1) = the worker's candidates at its stream
+// offset, lists (w, j > 1) empty; class bases 0 (records hold worker-local indices)
+__global__ void allfit_meta_kernel(Part part, uint32_t J, const uint32_t* __restrict__ wcnt,
+                                   uint64_t* __restrict__ clen, uint64_t* __restrict__ cstart,
+                                   uint32_t* __restrict__ cbase) {
+    const uint32_t nloc = part.wend - part.wbegin;
     for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x <= nloc * J; x += gridDim.x * blockDim.x) {
         if (x == nloc * J) {
-            cstart[x] = seg_off[(uint64_t)nloc * E];
+            cstart[x] = part.stream_offset(part.wend);
             break;
         }
         const uint32_t wl = x / J, j = x % J;
-        const uint64_t a = seg_off[(uint64_t)wl * E], b = seg_off[(uint64_t)(wl + 1) * E];
-        clen[x] = j == 0 ? b - a : 0;
-        cstart[x] = j == 0 ? a : b;
-        cbase[x] = j == 0 ? (uint32_t)a : 0u;
+        const uint64_t a = part.stream_offset(part.wbegin + wl);
+        clen[x] = j == 0 ? wcnt[wl] : 0;
+        cstart[x] = j == 0 ? a : a + wcnt[wl];
+        cbase[x] = 0;
     }
 }
 
-void launch_fit_check(cudaStream_t s, uint32_t nloc, uint32_t E, const double* segsum,
-                      const double* segmin, const uint32_t* segcnt, double C, uint32_t* allfit) {
-    fit_check_kernel<<<grid_for((uint64_t)nloc * 32, kThreads), kThreads, 0, s>>>(
-        nloc, E, segsum, segmin, segcnt, C, allfit);
-}
-
-void launch_seg_first(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info, bool ent,
-                      const uint64_t* chunk_off, uint32_t MB, uint32_t C, uint32_t* rec,
-                      uint32_t* class_list) {
+void launch_seg_allfit(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info,
+                       const uint32_t* cpos, uint32_t MB, uint32_t C, unsigned long long* status,
+                       uint32_t* ticket, uint32_t* rec, uint32_t* class_list) {
     const uint64_t nch = (uint64_t)(part.wend - part.wbegin) * part.E * C;
-    seg_first_kernel<<<grid_for(nch * 32, kThreads, 148u * 64u), kThreads, 0, s>>>(
-        part, stream, info, ent, chunk_off, MB, C, rec, class_list);
+    cudaMemsetAsync(status, 0, nch * 8, s);
+    cudaMemsetAsync(ticket, 0, 4, s);
+    seg_allfit_kernel<<<grid_for(nch * 32, kThreads, 148u * 8u), kThreads, 0, s>>>(
+        part, stream, info, cpos, MB, C, status, ticket, rec, class_list);
 }
 
-void launch_chunk_count(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info, bool ent,
-                        const double* sizes, uint32_t C, uint32_t* cnt, double* csum, double* cmin) {
-    const uint64_t nch = (uint64_t)(part.wend - part.wbegin) * part.E * C;
-    chunk_count_kernel<<<grid_for(nch * 32, kThreads, 148u * 64u), kThreads, 0, s>>>(
-        part, stream, info, ent, sizes, C, cnt, csum, cmin);
-}
-
-void launch_allfit_meta(cudaStream_t s, uint32_t nloc, uint32_t E, uint32_t J, const uint64_t* seg_off,
+void launch_allfit_meta(cudaStream_t s, const Part& part, uint32_t J, const uint32_t* wcnt,
                         uint64_t* clen, uint64_t* cstart, uint32_t* cbase) {
-    allfit_meta_kernel<<<grid_for((uint64_t)nloc * J + 1, kThreads), kThreads, 0, s>>>(
-        nloc, E, J, seg_off, clen, cstart, cbase);
+    allfit_meta_kernel<<<grid_for((uint64_t)(part.wend - part.wbegin) * J + 1, kThreads), kThreads, 0, s>>>(
+        part, J, wcnt, clen, cstart, cbase);
 }
 
 // ---------------------------------------------------------------------------- K4c
 __global__ void __launch_bounds__(kThreads) seg_write_kernel2(
-    Part part, const uint32_t* __restrict__ stream, const uint16_t* __restrict__ info, bool ent,
+    Part part, const uint32_t* __restrict__ stream, const uint16_t* __restrict__ info, const uint32_t* __restrict__ cpos,
     const double* __restrict__ sizes, const uint64_t* __restrict__ seg_off,
     const uint64_t* __restrict__ sorted_base, uint32_t MB, uint32_t* __restrict__ dest,
     double* __restrict__ sorted_size, uint32_t* __restrict__ blkmask,
@@ -560,7 +516,7 @@ __global__ void __launch_bounds__(kThreads) seg_write_kernel2(
             }
 #pragma unroll
             for (int u = 0; u < kSU; ++u)
-                c[u] = k[u] == kNone ? 0u : ent ? info[g0 + t0 + 32 * u + lane] : row[k[u]];
+                c[u] = k[u] == kNone ? 0u : cpos ? info[cpos[g0 + t0 + 32 * u + lane]] : row[k[u]];
 #pragma unroll
             for (int u = 0; u < kSU; ++u) {
                 const uint64_t tb = t0 + 32 * u;
@@ -885,7 +841,8 @@ __global__ void __launch_bounds__(kThreads) sample_tile_kernel(Part part, const 
                                                                uint16_t* __restrict__ rank16,
                                                                uint32_t* __restrict__ pair_count,
                                                                uint32_t W,
-                                                               uint32_t* __restrict__ seghist) {
+                                                               uint32_t* __restrict__ seghist,
+                                                               WorkerSums ws) {
     extern __shared__ uint32_t sm[];
     const uint32_t E = part.E, F = part.F;
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
@@ -897,12 +854,21 @@ __global__ void __launch_bounds__(kThreads) sample_tile_kernel(Part part, const 
     uint32_t* fe = tabs + warp * (2 * W * 32 + W);  // [nloc] first epoch
     uint32_t* cnt = fe + W * 32;                     // [nloc] count
     uint32_t* bm = cnt + W * 32;                     // [W] worker bitmap
+    // per-CTA candidate size sums / counts per local worker (the whole-worker fit test)
+    double* csum = reinterpret_cast<double*>(tabs + nwarps * (2 * W * 32 + W) + 1) ;
+    csum = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(csum) + 7) & ~(uintptr_t)7);
+    uint32_t* ccnt = reinterpret_cast<uint32_t*>(csum + W * 32);
+    if (ws.sum)
+        for (uint32_t x = threadIdx.x; x < W * 32; x += blockDim.x) {
+            csum[x] = 0.0;
+            ccnt[x] = 0;
+        }
     for (uint32_t x = lane; x < W * 32; x += 32) {
         fe[x] = kNone;
         cnt[x] = 0;
     }
     if (lane < W) bm[lane] = 0;
-    __syncwarp();
+    __syncthreads();
     const uint64_t stride = (uint64_t)gridDim.x * 32;
     uint64_t k0 = (uint64_t)blockIdx.x * 32;
     if (k0 < F) st_issue(inv, E, F, k0, tin[0]);
@@ -949,6 +915,11 @@ __global__ void __launch_bounds__(kThreads) sample_tile_kernel(Part part, const 
             const uint32_t pre = inc - c;
             const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
             if (live && lane == 0) pair_count[k0 + s] = total;
+            double sz = 0.0;
+            if (ws.sum && live) {
+                sz = __ldg(ws.sizes + k0 + s);
+                if (lane == 0 && !(sz >= 0.0)) atomicOr(ws.neg, 1u);
+            }
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 const uint32_t e = r * 32 + lane;
@@ -962,6 +933,10 @@ __global__ void __launch_bounds__(kThreads) sample_tile_kernel(Part part, const 
                         ci = (uint16_t)cnt[x];
                         rk = (uint16_t)(pw + __popc(ww & ((1u << (x & 31)) - 1u)));
                         if (seghist) atomicAdd(&seghist[((uint64_t)x * E + (E - ci)) * E + e], 1u);
+                        if (ws.sum) {
+                            atomicAdd(&csum[x], sz);
+                            atomicAdd(&ccnt[x], 1u);
+                        }
                     }
                     oinfo[e * kStOut + s] = ci;
                     orank[e * kStOut + s] = rk;
@@ -991,7 +966,15 @@ __global__ void __launch_bounds__(kThreads) sample_tile_kernel(Part part, const 
         }
         // the output tile and the input buffer are reused after the next barrier
     }
-    (void)nloc;
+    if (ws.sum) {
+        __syncthreads();
+        for (uint32_t x = threadIdx.x; x < nloc; x += blockDim.x) {
+            if (ccnt[x]) {
+                atomicAdd(&ws.sum[x], csum[x]);
+                atomicAdd(&ws.cnt[x], ccnt[x]);
+            }
+        }
+    }
 }
 
 // ---------------------------------------------------------------------------- launchers
@@ -1071,11 +1054,13 @@ bool tile_path_ok(const Part& part) {
 }
 
 void launch_sample_tile(cudaStream_t s, const Part& part, const uint32_t* inv, uint16_t* info,
-                        uint16_t* rank16, uint32_t* pair_count, uint32_t* seghist) {
+                        uint16_t* rank16, uint32_t* pair_count, uint32_t* seghist,
+                        const WorkerSums& ws) {
     const uint32_t nloc = part.wend - part.wbegin;
     const uint32_t W = (nloc + 31) / 32;
     const size_t smem = (size_t)4 * (2 * part.E * kStInv + part.E * kStOut +
-                                     (kThreads / 32) * (2 * W * 32 + W));
+                                     (kThreads / 32) * (2 * W * 32 + W) + 2) +
+                        (ws.sum ? (size_t)W * 32 * 12 : 0);
     const uint64_t tiles = ((uint64_t)part.F + 31) / 32;
     const unsigned grid = grid_for(tiles, 1, 148u * 8u);
 #define ST_LAUNCH(RV)                                                                             \
@@ -1083,7 +1068,7 @@ void launch_sample_tile(cudaStream_t s, const Part& part, const uint32_t* inv, u
         cudaFuncSetAttribute(sample_tile_kernel<RV>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
                              (int)smem);                                                          \
         sample_tile_kernel<RV><<<grid, kThreads, smem, s>>>(part, inv, info, rank16, pair_count,  \
-                                                            W, seghist);                          \
+                                                            W, seghist, ws);                      \
     } while (0)
     const uint32_t R = (part.E + 31) / 32;
     if (R == 1) ST_LAUNCH(1);
@@ -1107,41 +1092,20 @@ void launch_sample_hash(cudaStream_t s, const Part& part, const uint32_t* inv, u
         part, inv, info, rank16, pair_count, list, nlist, hs, W, seghist);
 }
 
-void launch_seg_hist(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info, bool ent,
+void launch_seg_hist(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info, const uint32_t* cpos,
                      uint32_t* seghist, uint32_t* segcnt, const double* sizes, double* segsum,
                      double* segmin) {
     const uint64_t nseg = (uint64_t)(part.wend - part.wbegin) * part.E;
     const unsigned grid = grid_for(nseg * 32, kThreads, 148u * 64u);
-    if (seghist) {
-        const size_t smem = (size_t)(kThreads / 32) * part.E * 4;
-        cudaFuncSetAttribute(seg_hist_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        seg_hist_kernel<true><<<grid, kThreads, smem, s>>>(part, stream, info, ent, seghist, segcnt, sizes,
-                                                            segsum, segmin);
-    } else {
-        seg_hist_kernel<false><<<grid, kThreads, 0, s>>>(part, stream, info, ent, nullptr, segcnt, sizes,
-                                                          segsum, segmin);
-    }
+    // (the all-fit totals come from chunk_count_kernel; only the histogram variant is used)
+    const size_t smem = (size_t)(kThreads / 32) * part.E * 4;
+    cudaFuncSetAttribute(seg_hist_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    seg_hist_kernel<true><<<grid, kThreads, smem, s>>>(part, stream, info, cpos, seghist, segcnt, sizes,
+                                                        segsum, segmin);
 }
 
-// sum_k sizes[k] * pair_count[k] (all workers' candidate sizes) -> *out (atomic, unordered:
-// only the all-fit gate reads it)
-__global__ void pair_size_total_kernel(uint32_t F, const double* __restrict__ sizes,
-                                       const uint32_t* __restrict__ pair_count, double* out) {
-    double acc = 0.0;
-    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < F; k += gridDim.x * blockDim.x)
-        acc += sizes[k] * (double)pair_count[k];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
-}
 
-void launch_pair_size_total(cudaStream_t s, uint32_t F, const double* sizes,
-                            const uint32_t* pair_count, double* out) {
-    cudaMemsetAsync(out, 0, sizeof(double), s);
-    pair_size_total_kernel<<<grid_for(F, kThreads, 148u * 4u), kThreads, 0, s>>>(F, sizes, pair_count, out);
-}
-
-void launch_seg_write2(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info, bool ent,
+void launch_seg_write2(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info, const uint32_t* cpos,
                        const double* sizes, const uint64_t* seg_off, const uint64_t* sorted_base,
                        uint32_t MB, uint32_t* dest, double* sorted_size, uint32_t* blkmask,
                        uint32_t* blkbase) {
@@ -1149,7 +1113,7 @@ void launch_seg_write2(cudaStream_t s, const Part& part, const uint32_t* stream,
     const size_t smem = (size_t)(kThreads / 32) * part.E * 4;
     cudaFuncSetAttribute(seg_write_kernel2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     seg_write_kernel2<<<grid_for(nseg * 32, kThreads, 148u * 64u), kThreads, smem, s>>>(
-        part, stream, info, ent, sizes, seg_off, sorted_base, MB, dest, sorted_size, blkmask, blkbase);
+        part, stream, info, cpos, sizes, seg_off, sorted_base, MB, dest, sorted_size, blkmask, blkbase);
 }
 
 }  // namespace clairplan

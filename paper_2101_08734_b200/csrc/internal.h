@@ -40,6 +40,14 @@ struct TileMap {
     uint32_t* tile_seg = nullptr;  // [max_tiles]
 };
 
+// per local worker: sum / count of its candidates' sizes (all-fit test); sum == nullptr: off
+struct WorkerSums {
+    const double* sizes = nullptr;
+    double* sum = nullptr;
+    uint32_t* cnt = nullptr;
+    uint32_t* neg = nullptr;  // set when a size is negative (or NaN)
+};
+
 void exclusive_scan(cudaStream_t s, const uint32_t* in, uint64_t n, uint64_t* out, Workspace& ws);
 void exclusive_scan(cudaStream_t s, const uint64_t* in, uint64_t n, uint64_t* out, Workspace& ws);
 
@@ -92,17 +100,20 @@ struct EpochSplit {
 };
 void launch_stream_relayout(cudaStream_t s, const Part& part, const EpochSplit& es,
                             const uint32_t* recv, uint32_t* stream);
-bool sparse_path_ok(const Part& part);
+bool sparse_path_ok(const Part& part, uint64_t local_entries);
+bool sparse_path_fits(const Part& part);
+uint64_t csr_windows(uint64_t n);
 void launch_sparse_csr(cudaStream_t s, const Part& part, const uint32_t* stream, uint64_t n,
-                       uint32_t* cnt, uint64_t* koff, uint32_t* cur, uint32_t* csr, uint64_t* soff,
-                       Workspace& ws);
+                       uint32_t* cnt, uint64_t* koff, uint32_t* cur, uint32_t* csr, uint32_t* cpos,
+                       uint64_t* soff, Workspace& ws);
 void launch_sparse_sample(cudaStream_t s, const Part& part, const uint64_t* soff, const uint64_t* koff,
                           const uint32_t* csr, uint32_t* pair_count, uint16_t* einfo,
-                          uint16_t* erank);
-void launch_holder_sparse(cudaStream_t s, const Part& part, const uint64_t* soff, const uint64_t* koff,
-                          const uint32_t* csr, const uint16_t* erank, uint32_t MB, const uint32_t* rec,
-                          uint32_t np, uint32_t J, uint32_t Rp, const uint32_t* cbase,
-                          const uint64_t* pair_off, uint32_t* holders, bool allfit);
+                          uint16_t* erank, const WorkerSums& ws);
+void launch_holder_sparse(cudaStream_t s, const Part& part, uint64_t n, const uint64_t* soff,
+                          const uint32_t* stream, const uint32_t* csr, const uint16_t* erank,
+                          uint32_t MB, const uint32_t* rec, uint32_t np, uint32_t J, uint32_t Rp,
+                          const uint32_t* cbase, const uint64_t* pair_off, uint32_t* holders,
+                          bool allfit);
 void launch_stream_inv(cudaStream_t s, const Part& part, const uint32_t* stream, uint32_t* inv);
 void launch_perm_scatter(cudaStream_t s, const Part& part, const uint32_t* perms, uint32_t* inv,
                          uint32_t* stream);
@@ -163,28 +174,23 @@ void launch_sample_lanes(cudaStream_t s, const Part& part, const uint32_t* inv, 
                          uint16_t* rank16, uint32_t* pair_count, uint32_t* seghist);
 bool tile_path_ok(const Part& part);
 void launch_sample_tile(cudaStream_t s, const Part& part, const uint32_t* inv, uint16_t* info,
-                        uint16_t* rank16, uint32_t* pair_count, uint32_t* seghist);
+                        uint16_t* rank16, uint32_t* pair_count, uint32_t* seghist,
+                        const WorkerSums& ws);
 void launch_sample_hash(cudaStream_t s, const Part& part, const uint32_t* inv, uint16_t* info,
                         uint16_t* rank16, uint32_t* pair_count, const uint32_t* list,
                         const uint32_t* nlist, uint64_t max_items, uint32_t* seghist);
 void launch_segcnt(cudaStream_t s, uint32_t nloc, uint32_t E, const uint32_t* seghist,
                    uint32_t* segcnt);
-void launch_seg_hist(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info, bool ent,
+void launch_seg_hist(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info, const uint32_t* cpos,
                      uint32_t* seghist, uint32_t* segcnt, const double* sizes = nullptr,
                      double* segsum = nullptr, double* segmin = nullptr);
-void launch_pair_size_total(cudaStream_t s, uint32_t F, const double* sizes,
-                            const uint32_t* pair_count, double* out);
-void launch_fit_check(cudaStream_t s, uint32_t nloc, uint32_t E, const double* segsum,
-                      const double* segmin, const uint32_t* segcnt, double C, uint32_t* allfit);
-void launch_seg_first(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info, bool ent,
-                      const uint64_t* chunk_off, uint32_t MB, uint32_t C, uint32_t* rec,
-                      uint32_t* class_list);
-void launch_chunk_count(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info, bool ent,
-                        const double* sizes, uint32_t C, uint32_t* cnt, double* csum, double* cmin);
 constexpr uint32_t kAllfitChunk = 1024;
-void launch_allfit_meta(cudaStream_t s, uint32_t nloc, uint32_t E, uint32_t J, const uint64_t* seg_off,
+void launch_seg_allfit(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info,
+                       const uint32_t* cpos, uint32_t MB, uint32_t C, unsigned long long* status,
+                       uint32_t* ticket, uint32_t* rec, uint32_t* class_list);
+void launch_allfit_meta(cudaStream_t s, const Part& part, uint32_t J, const uint32_t* wcnt,
                         uint64_t* clen, uint64_t* cstart, uint32_t* cbase);
-void launch_seg_write2(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info, bool ent,
+void launch_seg_write2(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info, const uint32_t* cpos,
                        const double* sizes, const uint64_t* seg_off, const uint64_t* sorted_base,
                        uint32_t MB, uint32_t* dest, double* sorted_size, uint32_t* blkmask,
                        uint32_t* blkbase);

@@ -502,7 +502,7 @@ int first_fit_classes(clairplan_plan* p, const double* ssize, uint8_t* cls) {
 
 
 // (count at first access) source of the segment passes: info[e][k] (dense sample pass) or
-// einfo[stream index] (sparse sample pass of a sharded handle)
+// einfo[csr slot] with cpos[stream index] = csr slot (sparse sample pass of a sharded handle)
 inline const uint16_t* info_src(clairplan_plan* p) {
     return p->sparse ? p->einfo.get<uint16_t>() : p->info16.get<uint16_t>();
 }
@@ -550,6 +550,7 @@ int assign_v2(clairplan_plan* p) {
         exclusive_scan(s, clen, (uint64_t)nloc * J, cstart, p->ws);
         launch_class_write(s, part, MB, stream_buf, rec, np, J, Rp, cbase, cstart, centries, nblk);
         p->launches += 4 + 3 * J + 3;
+        p->cl_contig = true;
         return holders_v2(p);
     }
     return no_classes_v2(p);
@@ -583,7 +584,7 @@ int holders_v2(clairplan_plan* p) {
         p->mark(7);
         // K8: holder CSR, sample-major
         if (p->sparse)
-            launch_holder_sparse(s, part, p->soff.get<uint64_t>(), p->koff.get<uint64_t>(),
+            launch_holder_sparse(s, part, p->A, p->soff.get<uint64_t>(), p->stream_buf.get<uint32_t>(),
                                  p->csr.get<uint32_t>(), p->erank.get<uint16_t>(), MB, rec, np, J, Rp,
                                  cbase, poff, htmp, p->allfit);
         else
@@ -648,21 +649,35 @@ int assign_allfit_v2(clairplan_plan* p) {
     uint32_t np = 0;
     while ((1u << np) <= J) ++np;
     const uint32_t Rp = ((np + J) + 3) & ~3u;
+    const uint32_t C = (uint32_t)((part.epoch_len(part.wbegin) + kAllfitChunk - 1) / kAllfitChunk);
     bool ok = true;
-    uint32_t* centries = need<uint32_t>(p->class_entries, p->D, ok);
+    uint32_t* centries = need<uint32_t>(p->class_entries, p->A, ok);  // lists at stream offsets
     uint32_t* rec = need<uint32_t>(p->planes, (uint64_t)std::max<uint32_t>(Rp, 4) * p->v2_nblk, ok);
     uint32_t* cbase = need<uint32_t>(p->cbase, (uint64_t)nloc * J, ok);
     uint64_t* clen = need<uint64_t>(p->class_len, (uint64_t)nloc * J, ok);
     uint64_t* cstart = need<uint64_t>(p->class_start, (uint64_t)nloc * J + 1, ok);
+    unsigned long long* status = need<unsigned long long>(p->chstatus, (uint64_t)nloc * E * C, ok);
+    uint32_t* ticket = need<uint32_t>(p->counters, 4, ok);
     if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed (class lists)");
-    const uint64_t* choff = p->choff.get<uint64_t>();
-    const uint32_t C = p->allfit_chunks;
-    launch_seg_first(s, part, p->stream_buf.get<uint32_t>(), info_src(p), p->sparse, choff,
-                     p->v2_mb, C, rec, centries);
-    launch_allfit_meta(s, nloc, E * C, J, choff, clen, cstart, cbase);
-    p->launches += 2;
+    launch_seg_allfit(s, part, p->stream_buf.get<uint32_t>(), info_src(p),
+                      p->sparse ? p->cpos.get<uint32_t>() : nullptr, p->v2_mb, C, status, ticket,
+                      rec, centries);
+    launch_allfit_meta(s, part, J, p->wcnt.get<uint32_t>(), clen, cstart, cbase);
+    p->launches += 4;
+    p->cl_contig = false;
     p->mark(6);
     return holders_v2(p);
+}
+
+// Whole-worker fit test on the host from the sample pass's per-worker sums: every worker's
+// candidates fit class 1 whatever the order (bound as in firstfit.cu ff_prefix_kernel).
+bool allfit_decide(double C, const std::vector<double>& sum, const std::vector<uint32_t>& cnt) {
+    for (size_t w = 0; w < sum.size(); ++w) {
+        if (cnt[w] == 0) continue;
+        const double tol = ((double)cnt[w] + 1024.0) * std::max(C, sum[w]) * 0x1.0p-48;
+        if (!(C - sum[w] > tol)) return false;
+    }
+    return true;
 }
 
 // K4c: every candidate's first-order index -> tier position (dest), the sizes in tier order,
@@ -679,14 +694,14 @@ int tier_order_v2(clairplan_plan* p) {
     const uint64_t* segoff = p->seg_off.get<uint64_t>();
     if (!p->hist_ready) {  // all-fit build: the count histograms were not needed then
         const uint64_t NEE = (uint64_t)nloc * E * E;
-        launch_seg_hist(s, part, p->stream_buf.get<uint32_t>(), info_src(p), p->sparse,
+        launch_seg_hist(s, part, p->stream_buf.get<uint32_t>(), info_src(p), p->sparse ? p->cpos.get<uint32_t>() : nullptr,
                         p->seghist.get<uint32_t>(), p->segcnt.get<uint32_t>());
         exclusive_scan(s, p->seghist.get<uint32_t>(), NEE, p->sorted_base.get<uint64_t>(), p->ws);
         exclusive_scan(s, p->segcnt.get<uint32_t>(), (uint64_t)nloc * E, p->seg_off.get<uint64_t>(), p->ws);
         p->launches += 4;
         p->hist_ready = true;
     }
-    launch_seg_write2(s, part, p->stream_buf.get<uint32_t>(), info_src(p), p->sparse,
+    launch_seg_write2(s, part, p->stream_buf.get<uint32_t>(), info_src(p), p->sparse ? p->cpos.get<uint32_t>() : nullptr,
                       p->sizes.get<double>(), segoff, p->sorted_base.get<uint64_t>(), p->v2_mb, dest,
                       ssize, p->blkmask.get<uint32_t>(), p->blkbase.get<uint32_t>());
     launch_worker_segments(s, segoff, nloc, E, p->wbeg.get<uint64_t>(), p->wlen.get<uint64_t>());
@@ -721,15 +736,13 @@ int build_seed_path_v2(clairplan_plan* p, const uint32_t* ext_perms,
     uint32_t* bmask = need<uint32_t>(p->blkmask, nblk, ok);
     uint32_t* bbase = need<uint32_t>(p->blkbase, nblk, ok);
     uint32_t* hard = need<uint32_t>(p->hard, (uint64_t)F + 1, ok);
-    const uint32_t C = (uint32_t)((part.epoch_len(part.wbegin) + kAllfitChunk - 1) / kAllfitChunk);
-    const uint64_t NCH = (uint64_t)nloc * E * C;  // all-fit chunks (worker, epoch, chunk)
-    double* segsum = need<double>(p->segsum, NCH, ok);
-    double* segmin = need<double>(p->segmin, NCH, ok);
-    uint32_t* chcnt = need<uint32_t>(p->chcnt, NCH, ok);
-    uint64_t* choff = need<uint64_t>(p->choff, NCH + 1, ok);
-    uint32_t* allfit_flag = need<uint32_t>(p->allfit_flag, 1, ok);
+    double* wsum = need<double>(p->wsum, nloc, ok);
+    uint32_t* wcnt = need<uint32_t>(p->wcnt, (uint64_t)nloc + 1, ok);  // + the negative-size flag
+    uint32_t* wneg = wcnt + nloc;
     // sparse sample-major passes (sharded handle fed by the all-to-all; CLAIRPLAN_DENSE=1: A/B)
-    const bool sparse = ext_streams && sparse_path_ok(part) && getenv("CLAIRPLAN_DENSE") == nullptr;
+    const char* dense_env = getenv("CLAIRPLAN_DENSE");  // "1": dense, "0": sparse, unset: cost model
+    const bool sparse = ext_streams && (dense_env ? dense_env[0] == '0' && sparse_path_fits(part)
+                                                  : sparse_path_ok(part, p->A));
     p->sparse = sparse;
     uint32_t *sp_cnt = nullptr, *sp_cur = nullptr, *sp_csr = nullptr;
     uint64_t *sp_koff = nullptr, *sp_soff = nullptr;
@@ -742,6 +755,7 @@ int build_seed_path_v2(clairplan_plan* p, const uint32_t* ext_perms,
         sp_soff = need<uint64_t>(p->soff, (uint64_t)nloc + 1, ok);
         sp_einfo = need<uint16_t>(p->einfo, p->A, ok);
         sp_erank = need<uint16_t>(p->erank, p->A, ok);
+        need<uint32_t>(p->cpos, p->A, ok);
     }
     if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed (streams / histograms)");
     if (int rc = ensure_ws(p, std::max<uint64_t>(p->A, std::max<uint64_t>(NEE, F)), nloc)) return rc;
@@ -776,13 +790,25 @@ int build_seed_path_v2(clairplan_plan* p, const uint32_t* ext_perms,
         uint32_t* hist_out = red_hist ? seghist : nullptr;
         if (red_hist) CK(cudaMemsetAsync(seghist, 0, NEE * 4, s));
         static const bool lanes_only = getenv("CLAIRPLAN_SAMPLE_LANES") != nullptr;  // A/B
+        // per-worker candidate size sums for the whole-worker fit test (all-fit path)
+        const bool no_allfit = getenv("CLAIRPLAN_NO_ALLFIT") != nullptr;
+        const bool sums = J > 0 && !no_allfit && (sparse || (tile_path_ok(part) && !lanes_only));
+        WorkerSums wsm;
+        if (sums) {
+            wsm.sizes = p->sizes.get<double>();
+            wsm.sum = wsum;
+            wsm.cnt = wcnt;
+            wsm.neg = wneg;
+            CK(cudaMemsetAsync(wsum, 0, (size_t)nloc * 8, s));
+            CK(cudaMemsetAsync(wcnt, 0, (size_t)nloc * 4 + 4, s));  // wcnt and wneg
+        }
         if (sparse) {
-            launch_sparse_csr(s, part, stream_buf, p->A, sp_cnt, sp_koff, sp_cur, sp_csr, sp_soff,
-                              p->ws);
-            launch_sparse_sample(s, part, sp_soff, sp_koff, sp_csr, pcount, sp_einfo, sp_erank);
+            launch_sparse_csr(s, part, stream_buf, p->A, sp_cnt, sp_koff, sp_cur, sp_csr,
+                              p->cpos.get<uint32_t>(), sp_soff, p->ws);
+            launch_sparse_sample(s, part, sp_soff, sp_koff, sp_csr, pcount, sp_einfo, sp_erank, wsm);
             p->launches += 7;
         } else if (tile_path_ok(part) && !lanes_only) {
-            launch_sample_tile(s, part, inv, info, rank16, pcount, hist_out);
+            launch_sample_tile(s, part, inv, info, rank16, pcount, hist_out, wsm);
         } else if (lanes) {
             launch_sample_lanes(s, part, inv, info, rank16, pcount, hist_out);
         } else {
@@ -790,40 +816,36 @@ int build_seed_path_v2(clairplan_plan* p, const uint32_t* ext_perms,
         }
         exclusive_scan(s, pcount, F, poff, p->ws);
         p->mark(2);
-        // All-fit gate (necessary condition, on the host): the mean per-worker candidate size
-        // sum_k size_k * pairs_k / nloc must not exceed the class-1 capacity.
-        const bool no_allfit = getenv("CLAIRPLAN_NO_ALLFIT") != nullptr;
-        const bool gate = !red_hist && J > 0 && !no_allfit;
-        double* ptot = segsum;  // scratch scalar until the segment pass runs
-        if (gate) launch_pair_size_total(s, F, p->sizes.get<double>(), pcount, ptot);
         std::vector<uint32_t> flags(E);
         uint64_t D = 0;
-        double pair_size_total = 0;
+        std::vector<double> hsum(sums ? nloc : 0);
+        std::vector<uint32_t> hcnt(sums ? nloc + 1 : 0);
         CK(cudaMemcpyAsync(&D, poff + F, 8, cudaMemcpyDeviceToHost, s));
-        if (gate) CK(cudaMemcpyAsync(&pair_size_total, ptot, 8, cudaMemcpyDeviceToHost, s));
+        if (sums) {
+            CK(cudaMemcpyAsync(hsum.data(), wsum, (size_t)nloc * 8, cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(hcnt.data(), wcnt, (size_t)nloc * 4 + 4, cudaMemcpyDeviceToHost, s));
+        }
         CK(cudaMemcpyAsync(flags.data(), p->rej_flag.get<uint32_t>(), E * 4, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         bool any = false;
         if (int rc = resolve_rejections(p, flags, &any)) return rc;
         if (any) continue;
-        // K4b: per-segment first-access totals (+ sizes: whole-worker fit test) or count
-        // histograms -> first-order and tier-order bases
-        const bool try_allfit = gate && pair_size_total / nloc <= p->caps[0];
-        uint32_t allfit = 0;
-        if (try_allfit) {
-            CK(cudaMemsetAsync(allfit_flag, 0xFF, 4, s));
-            launch_chunk_count(s, part, stream_buf, info_src(p), p->sparse, p->sizes.get<double>(), C, chcnt, segsum,
-                               segmin);
-            launch_fit_check(s, nloc, E * C, segsum, segmin, chcnt, p->caps[0], allfit_flag);
-            exclusive_scan(s, chcnt, NCH, choff, p->ws);
-            p->allfit_chunks = C;
-            CK(cudaMemcpyAsync(&allfit, allfit_flag, 4, cudaMemcpyDeviceToHost, s));
-            CK(cudaStreamSynchronize(s));
+        if (p->x_streams) {  // build_export: the streams are final, copy them out meanwhile
+            CK(cudaEventRecord(p->xev, s));
+            CK(cudaStreamWaitEvent(p->xstream, p->xev, 0));
+            CK(cudaMemcpyAsync(p->x_streams, stream_buf, p->A * 4, cudaMemcpyDeviceToHost, p->xstream));
+        }
+        // all-fit test (host); otherwise K4b: per-segment count histograms -> first-order and
+        // tier-order bases
+        bool allfit = false;
+        if (sums && hcnt[nloc] == 0) {
+            hcnt.resize(nloc);
+            allfit = allfit_decide(p->caps[0], hsum, hcnt);
         }
         p->hist_ready = false;
         if (!allfit) {
             if (red_hist) launch_segcnt(s, nloc, E, seghist, segcnt);
-            else launch_seg_hist(s, part, stream_buf, info_src(p), p->sparse, seghist, segcnt);
+            else launch_seg_hist(s, part, stream_buf, info_src(p), p->sparse ? p->cpos.get<uint32_t>() : nullptr, seghist, segcnt);
             exclusive_scan(s, seghist, NEE, sbase, p->ws);
             exclusive_scan(s, segcnt, (uint64_t)nloc * E, segoff, p->ws);
             p->hist_ready = true;
@@ -954,6 +976,41 @@ int clairplan_build(clairplan_t p) {
     return build_seed_path(p);
 }
 
+int clairplan_build_export(clairplan_t p, const double* host_sizes, uint32_t* streams_out,
+                           uint64_t streams_cap, uint32_t* class_lists_out, uint64_t cl_cap,
+                           uint64_t* offsets_out, uint32_t* holders_out, uint64_t holders_cap) {
+    if (!p || !streams_out || !offsets_out) return fail(CLAIRPLAN_EINVAL, "null argument");
+    if (p->generic) return fail(CLAIRPLAN_EINVAL, "plan was created from explicit streams");
+    CK(cudaSetDevice(p->device));
+    if (streams_cap < p->part.E * (p->part.prefix_len(p->part.wend) - p->part.prefix_len(p->part.wbegin)))
+        return fail(CLAIRPLAN_ERANGE, "stream buffer too small");
+    if (!p->xstream) {
+        CK(cudaStreamCreateWithFlags(&p->xstream, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&p->xev, cudaEventDisableTiming));
+    }
+    if (host_sizes)
+        if (int rc = clairplan_set_sizes(p, host_sizes, 0)) return rc;
+    p->x_streams = streams_out;
+    int rc = clairplan_build(p);
+    const bool copied = p->v2;  // the v2 build issued the stream copy on xstream
+    p->x_streams = nullptr;
+    if (rc) {
+        cudaStreamSynchronize(p->xstream);
+        return rc;
+    }
+    if (!copied)
+        CK(cudaMemcpyAsync(streams_out, p->stream_buf.get<uint32_t>(), p->A * 4, cudaMemcpyDeviceToHost,
+                           p->stream));
+    if (int rc2 = clairplan_export_class_lists_async(p, class_lists_out, cl_cap)) return rc2;
+    if (holders_cap < p->H) return fail(CLAIRPLAN_ERANGE, "holder buffer too small");
+    CK(cudaMemcpyAsync(offsets_out, p->holder_off_dev, ((uint64_t)p->part.F + 1) * 8,
+                       cudaMemcpyDeviceToHost, p->stream));
+    if (p->H) CK(cudaMemcpyAsync(holders_out, p->holders_dev, p->H * 12, cudaMemcpyDeviceToHost, p->stream));
+    CK(cudaStreamSynchronize(p->stream));
+    CK(cudaStreamSynchronize(p->xstream));
+    return 0;
+}
+
 int clairplan_stats_get(clairplan_t p, clairplan_stats* s) {
     if (!p || !s) return fail(CLAIRPLAN_EINVAL, "null argument");
     s->accesses = p->A;
@@ -1027,6 +1084,39 @@ int clairplan_export_streams(clairplan_t p, uint32_t* out, uint64_t cap) {
     return 0;
 }
 
+}  // extern "C"
+
+namespace clairplan {
+// class lists back to back in (worker, class) order, on the handle's stream
+int clairplan_export_class_lists_async(clairplan_t p, uint32_t* out, uint64_t cap) {
+    const uint32_t J = p->cfg.num_classes;
+    uint64_t need_n = 0;
+    for (uint32_t w = 0; w < p->nloc; ++w)
+        for (uint32_t j = 0; j < J; ++j) need_n += p->class_len_h[(size_t)w * (J + 1) + j];
+    if (cap < need_n) return fail(CLAIRPLAN_ERANGE, "output buffer too small");
+    if (need_n == 0) return 0;
+    if (!out) return fail(CLAIRPLAN_EINVAL, "null class-list buffer");
+    if (p->v2 && p->cl_contig) {
+        CK(cudaMemcpyAsync(out, p->class_entries.get<uint32_t>(), need_n * 4, cudaMemcpyDeviceToHost,
+                           p->stream));
+        return 0;
+    }
+    uint64_t o = 0;
+    for (uint32_t w = 0; w < p->nloc; ++w) {
+        const uint64_t a = p->class_start_h[(size_t)w * (J + 1)];
+        uint64_t n = 0;
+        for (uint32_t j = 0; j < J; ++j) n += p->class_len_h[(size_t)w * (J + 1) + j];
+        if (n)
+            CK(cudaMemcpyAsync(out + o, p->class_entries.get<uint32_t>() + a, n * 4,
+                               cudaMemcpyDeviceToHost, p->stream));
+        o += n;
+    }
+    return 0;
+}
+}  // namespace clairplan
+
+extern "C" {
+
 int clairplan_export_class_lists(clairplan_t p, uint32_t* out, uint64_t cap) {
     if (!p || !p->built) return fail(CLAIRPLAN_EINVAL, "plan not built");
     const uint32_t J = p->cfg.num_classes;
@@ -1036,7 +1126,7 @@ int clairplan_export_class_lists(clairplan_t p, uint32_t* out, uint64_t cap) {
     if (cap < need_n) return fail(CLAIRPLAN_ERANGE, "output buffer too small");
     if (need_n == 0) return 0;
     CK(cudaSetDevice(p->device));
-    if (p->v2) {  // class lists are stored back to back in (worker, class) order
+    if (p->v2 && p->cl_contig) {  // class lists are stored back to back in (worker, class) order
         CK(cudaMemcpy(out, p->class_entries.get<uint32_t>(), need_n * 4, cudaMemcpyDeviceToHost));
         return 0;
     }

@@ -118,10 +118,10 @@ struct clairplan_plan {
     DevBuf wsbuf;
     DevBuf cand_w, dfirst, dcounts;  // explicit-stream (generic) path
     DevBuf inv, info16, rank16, cbase, seghist, sorted_base, blkmask, blkbase, planes, ccount, cpre, hard;
-    DevBuf segsum, segmin, allfit_flag, chcnt, choff;
-    DevBuf koff, sp_cur, csr, soff, einfo, erank;  // sparse sample-major passes (sharded)
+    DevBuf wsum, wcnt, chstatus;     // all-fit: per-worker size sums / counts, chunk look-back
+    bool cl_contig = true;           // class lists back to back (tier path) or at stream offsets
+    DevBuf koff, sp_cur, csr, cpos, soff, einfo, erank;  // sparse sample-major passes (sharded)
     bool sparse = false;             // last build used the sparse passes
-    uint32_t allfit_chunks = 1;      // chunks per (worker, epoch) segment of the all-fit passes
     bool allfit = false;             // last build took the all-fit path (no tier order)
     bool tier_ready = false;         // dest / sorted_size / block masks hold the tier order
     bool hist_ready = false;         // seghist / sorted_base hold the count histograms
@@ -136,7 +136,12 @@ struct clairplan_plan {
     const uint64_t* holder_off_dev = nullptr;
     const uint32_t* holders_dev = nullptr;
 
+    cudaStream_t xstream = nullptr;   // build_export: stream of the overlapped output copy
+    cudaEvent_t xev = nullptr;
+    uint32_t* x_streams = nullptr;     // build_export: host stream buffer of the running build
     ~clairplan_plan() {
+        if (xstream) cudaStreamDestroy(xstream);
+        if (xev) cudaEventDestroy(xev);
         if (stream) cudaStreamDestroy(stream);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
@@ -174,4 +179,5 @@ int generic_holders(clairplan_plan* p);
 void launch_generic_count_keys(cudaStream_t s, const uint32_t* cnt, uint64_t n, uint32_t maxc,
                                uint32_t* keys);
 int ensure_ws(clairplan_plan* p, uint64_t n_elems, uint32_t nseg);
+int clairplan_export_class_lists_async(clairplan_t p, uint32_t* out, uint64_t cap);
 }  // namespace clairplan

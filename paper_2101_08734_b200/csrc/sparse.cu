@@ -7,12 +7,14 @@
 //   sparse_sample            warp per sample over its entries: per local worker the first
 //                            access (smallest stream index = earliest epoch, access.cpp:59-78
 //                            order), the access count, the worker bitmap -> pair_count[k],
-//                            einfo[s] = count at a pair's first access (0 elsewhere) and
-//                            erank[s] = the pair's rank among the sample's local workers
-//                            (build_index worker order, policies.cpp:124-142)
-//   holder_sparse            warp per sample: holder records at pair_off[k] + rank from the
-//                            block records of the tier / all-fit paths
-// The segment passes read einfo in stream order instead of gathering info[e][k].
+//                            einfo[slot] = count at a pair's first access (0 elsewhere) and
+//                            erank[slot] = the pair's rank among the sample's local workers
+//                            (build_index worker order, policies.cpp:124-142), in CSR order;
+//                            cpos[s] (stream index -> CSR slot) lets the segment passes find
+//                            an entry's value
+//   holder_sparse            thread per CSR entry: holder records at pair_off[k] + rank from
+//                            the block records of the tier / all-fit paths
+// The CSR is written in sample windows that fit L2 (the random slot writes then merge there).
 #include "internal.h"
 
 namespace clairplan {
@@ -42,137 +44,181 @@ __global__ void __launch_bounds__(kThreads) csr_cursor_kernel(const uint64_t* __
         cur[k] = (uint32_t)koff[k];
 }
 
+// entries whose sample lies in [k_lo, k_hi) (a window of the CSR that stays L2-resident while
+// it is written): csr[slot] = s, cpos[s] = slot
 __global__ void __launch_bounds__(kThreads) csr_scatter_kernel(const uint32_t* __restrict__ stream,
-                                                               uint64_t n, uint32_t* __restrict__ cur,
-                                                               uint32_t* __restrict__ csr) {
+                                                               uint64_t n, uint32_t k_lo, uint32_t k_hi,
+                                                               uint32_t* __restrict__ cur,
+                                                               uint32_t* __restrict__ csr,
+                                                               uint32_t* __restrict__ cpos) {
     for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < n;
-         s += (uint64_t)gridDim.x * blockDim.x)
-        csr[atomicAdd(&cur[__ldcs(stream + s)], 1u)] = (uint32_t)s;
+         s += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t k = __ldcs(stream + s);
+        if (k < k_lo || k >= k_hi) continue;
+        const uint32_t slot = atomicAdd(&cur[k], 1u);
+        csr[slot] = (uint32_t)s;
+        cpos[s] = slot;
+    }
 }
 
-// warp per sample; per-warp shared tables indexed by local worker (nloc <= 32 W)
+// warp per sample, lanes over its entries (R rounds of 32, entries kept in registers); per-warp
+// shared tables indexed by local worker (nloc <= 32 W)
+template <int R>
 __global__ void __launch_bounds__(kThreads) sparse_sample_kernel(
     uint32_t F, uint32_t nloc, uint32_t W, const uint64_t* __restrict__ soff,
     const uint64_t* __restrict__ koff, const uint32_t* __restrict__ csr,
-    uint32_t* __restrict__ pair_count, uint16_t* __restrict__ einfo, uint16_t* __restrict__ erank) {
+    uint32_t* __restrict__ pair_count, uint16_t* __restrict__ einfo, uint16_t* __restrict__ erank,
+    WorkerSums ws) {
     extern __shared__ uint32_t sm[];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr uint32_t NW = kThreads / 32;
     uint32_t* fs = sm + warp * (2 * W * 32 + W);  // [nloc] smallest stream index
     uint32_t* cnt = fs + W * 32;                   // [nloc] accesses
     uint32_t* bm = cnt + W * 32;                   // [W]
+    // per-CTA candidate size sums / counts per local worker (the whole-worker fit test)
+    double* csum = reinterpret_cast<double*>(sm + NW * (2 * W * 32 + W) + 1);
+    csum = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(csum) + 7) & ~(uintptr_t)7);
+    uint32_t* ccnt = reinterpret_cast<uint32_t*>(csum + W * 32);
+    if (ws.sum)
+        for (uint32_t x = threadIdx.x; x < W * 32; x += blockDim.x) {
+            csum[x] = 0.0;
+            ccnt[x] = 0;
+        }
     for (uint32_t x = lane; x < W * 32; x += 32) {
         fs[x] = kNone;
         cnt[x] = 0;
     }
     if (lane < W) bm[lane] = 0;
-    __syncwarp();
+    __syncthreads();
     for (uint32_t k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < F;
          k += (gridDim.x * blockDim.x) >> 5) {
         const uint64_t a = koff[k], b = koff[k + 1];
-        for (uint64_t i = a + lane; i < b; i += 32) {
-            {
-                const uint32_t s = __ldcs(csr + i);
-                const uint32_t x = worker_of_entry(soff, nloc, s);
-                atomicMin(&fs[x], s);
-                atomicAdd(&cnt[x], 1u);
-                atomicOr(&bm[x >> 5], 1u << (x & 31));
+        uint32_t sv[R], xv[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const uint64_t i = a + r * 32 + lane;
+            xv[r] = kNone;
+            if (i < b) {
+                sv[r] = __ldcs(csr + i);
+                xv[r] = worker_of_entry(soff, nloc, sv[r]);
+                atomicMin(&fs[xv[r]], sv[r]);
+                atomicAdd(&cnt[xv[r]], 1u);
+                atomicOr(&bm[xv[r] >> 5], 1u << (xv[r] & 31));
             }
         }
         __syncwarp();
         const uint32_t word = lane < W ? bm[lane] : 0u;
-        const uint32_t c = __popc(word);
-        uint32_t inc = c;
+        uint32_t pre = 0, total;
+        if (W == 1) {
+            total = __shfl_sync(0xffffffffu, __popc(word), 0);
+        } else {
+            const uint32_t c = __popc(word);
+            uint32_t inc = c;
 #pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
-            if (lane >= (uint32_t)d) inc += o;
-        }
-        const uint32_t pre = inc - c;
-        if (lane == 31) pair_count[k] = inc;
-        for (uint64_t i0 = a; i0 < b; i0 += 32) {  // warp-uniform trip count (shuffles)
-            const uint64_t i = i0 + lane;
-            uint32_t s = 0, x = 0;
-            const bool live = i < b;
-            if (live) {
-                s = __ldcs(csr + i);
-                x = worker_of_entry(soff, nloc, s);
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+                if (lane >= (uint32_t)d) inc += o;
             }
-            const uint32_t pw = __shfl_sync(0xffffffffu, pre, live ? x >> 5 : 0u);
-            const uint32_t ww = __shfl_sync(0xffffffffu, word, live ? x >> 5 : 0u);
-            if (live) {
+            pre = inc - c;
+            total = __shfl_sync(0xffffffffu, inc, 31);
+        }
+        if (lane == 0) pair_count[k] = total;
+        double sz = 0.0;
+        if (ws.sum && b > a) {
+            sz = __ldg(ws.sizes + k);
+            if (lane == 0 && !(sz >= 0.0)) atomicOr(ws.neg, 1u);
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const uint32_t x = xv[r];
+            const uint32_t xw = x != kNone ? x >> 5 : 0u;
+            const uint32_t pw = W == 1 ? 0u : __shfl_sync(0xffffffffu, pre, xw);
+            const uint32_t ww = W == 1 ? __shfl_sync(0xffffffffu, word, 0) : __shfl_sync(0xffffffffu, word, xw);
+            if (x != kNone) {
                 uint16_t ci = 0, rk = 0xFFFFu;
-                if (fs[x] == s) {
+                if (fs[x] == sv[r]) {
                     ci = (uint16_t)cnt[x];
                     rk = (uint16_t)(pw + __popc(ww & ((1u << (x & 31)) - 1u)));
+                    if (ws.sum) {
+                        atomicAdd(&csum[x], sz);
+                        atomicAdd(&ccnt[x], 1u);
+                    }
                 }
-                einfo[s] = ci;
-                erank[s] = rk;
+                const uint64_t i = a + r * 32 + lane;
+                einfo[i] = ci;  // CSR order: coalesced (cpos maps stream index -> slot)
+                erank[i] = rk;
             }
         }
         __syncwarp();
-        for (uint64_t i = a + lane; i < b; i += 32) {
-            const uint32_t x = worker_of_entry(soff, nloc, __ldcs(csr + i));
-            fs[x] = kNone;
-            cnt[x] = 0;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            if (xv[r] != kNone) {
+                fs[xv[r]] = kNone;
+                cnt[xv[r]] = 0;
+            }
         }
         if (lane < W) bm[lane] = 0;
         __syncwarp();
     }
+    if (ws.sum) {
+        __syncthreads();
+        for (uint32_t x = threadIdx.x; x < nloc; x += blockDim.x) {
+            if (ccnt[x]) {
+                atomicAdd(&ws.sum[x], csum[x]);
+                atomicAdd(&ws.cnt[x], ccnt[x]);
+            }
+        }
+    }
 }
 
-// warp per sample: holder records {worker, class, position} at pair_off[k] + rank.
-// NP as holder_tile (-1: all-fit uint2 records).
+// thread per CSR entry: holder records {worker, class, position} at pair_off[k] + rank for the
+// pairs' first accesses (k = the stream entry itself).  NP as holder_tile (-1: all-fit uint2).
 template <int NP>
 __global__ void __launch_bounds__(kThreads) holder_sparse_kernel(
-    Part part, const uint64_t* __restrict__ soff, const uint64_t* __restrict__ koff,
+    Part part, uint64_t n, const uint64_t* __restrict__ soff, const uint32_t* __restrict__ stream,
     const uint32_t* __restrict__ csr, const uint16_t* __restrict__ erank, uint32_t MB,
     const uint32_t* __restrict__ rec, uint32_t np_rt, uint32_t J, uint32_t Rp,
     const uint32_t* __restrict__ cbase, const uint64_t* __restrict__ pair_off,
     uint32_t* __restrict__ holders) {
-    const uint32_t E = part.E, F = part.F, nloc = part.wend - part.wbegin;
-    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t E = part.E, nloc = part.wend - part.wbegin;
     const uint32_t np = NP > 0 ? (uint32_t)NP : np_rt;
-    for (uint32_t k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < F;
-         k += (gridDim.x * blockDim.x) >> 5) {
-        const uint64_t a = koff[k], b = koff[k + 1];
-        if (a == b) continue;
-        const uint64_t slot0 = pair_off[k];
-        for (uint64_t i = a + lane; i < b; i += 32) {
-            const uint32_t s = __ldcs(csr + i);
-            const uint32_t rk = erank[s];
-            if (rk == 0xFFFFu) continue;
-            const uint32_t wl = worker_of_entry(soff, nloc, s);
-            const uint32_t w = part.wbegin + wl;
-            const uint32_t Le = (uint32_t)part.epoch_len(w);
-            const uint32_t rel = (uint32_t)(s - soff[wl]);
-            const uint32_t e = rel / Le;
-            const uint32_t t = rel - e * Le;
-            const uint64_t blk = ((uint64_t)wl * E + e) * MB + (t >> 5);
-            const uint32_t bit = t & 31;
-            uint32_t cls, pos = 0;
-            if constexpr (NP == -1) {
-                const uint2 a2 = __ldg(reinterpret_cast<const uint2*>(rec) + blk);
-                const uint32_t cb = __ldg(cbase + wl * J);
-                cls = (a2.x >> bit) & 1u;
-                pos = cls ? a2.y - cb + __popc(a2.x & ((1u << bit) - 1u)) : 0u;
-            } else {
-                const uint4 v = __ldg(reinterpret_cast<const uint4*>(rec + blk * Rp));
-                const uint32_t pl[4] = {v.x, v.y, v.z, v.w};
-                cls = 0;
-                for (uint32_t q = 0; q < np; ++q) cls |= ((pl[q & 3] >> bit) & 1u) << q;
-                uint32_t cm = 0xffffffffu;
-                for (uint32_t q = 0; q < np; ++q) cm &= ((cls >> q) & 1u) ? pl[q & 3] : ~pl[q & 3];
-                if (cls) {
-                    const uint32_t wi = np + cls - 1;
-                    const uint32_t prew = wi < 4 ? pl[wi] : rec[blk * Rp + wi];
-                    pos = prew - cbase[wl * J + cls - 1] + __popc(cm & ((1u << bit) - 1u));
-                }
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t rk = erank[i];
+        if (rk == 0xFFFFu) continue;
+        const uint32_t s = __ldcs(csr + i);
+        const uint32_t k = __ldg(stream + s);
+        const uint32_t wl = worker_of_entry(soff, nloc, s);
+        const uint32_t w = part.wbegin + wl;
+        const uint32_t Le = (uint32_t)part.epoch_len(w);
+        const uint32_t rel = (uint32_t)(s - soff[wl]);
+        const uint32_t e = rel / Le;
+        const uint32_t t = rel - e * Le;
+        const uint64_t blk = ((uint64_t)wl * E + e) * MB + (t >> 5);
+        const uint32_t bit = t & 31;
+        uint32_t cls, pos = 0;
+        if constexpr (NP == -1) {
+            const uint2 a2 = __ldg(reinterpret_cast<const uint2*>(rec) + blk);
+            const uint32_t cb = __ldg(cbase + wl * J);
+            cls = (a2.x >> bit) & 1u;
+            pos = cls ? a2.y - cb + __popc(a2.x & ((1u << bit) - 1u)) : 0u;
+        } else {
+            const uint4 v = __ldg(reinterpret_cast<const uint4*>(rec + blk * Rp));
+            const uint32_t pl[4] = {v.x, v.y, v.z, v.w};
+            cls = 0;
+            for (uint32_t q = 0; q < np; ++q) cls |= ((pl[q & 3] >> bit) & 1u) << q;
+            uint32_t cm = 0xffffffffu;
+            for (uint32_t q = 0; q < np; ++q) cm &= ((cls >> q) & 1u) ? pl[q & 3] : ~pl[q & 3];
+            if (cls) {
+                const uint32_t wi = np + cls - 1;
+                const uint32_t prew = wi < 4 ? pl[wi] : rec[blk * Rp + wi];
+                pos = prew - cbase[wl * J + cls - 1] + __popc(cm & ((1u << bit) - 1u));
             }
-            uint32_t* h = holders + 3 * (slot0 + rk);
-            __stcs(h, w);
-            __stcs(h + 1, cls);
-            __stcs(h + 2, pos);
         }
+        uint32_t* h = holders + 3 * (pair_off[k] + rk);
+        __stcs(h, w);
+        __stcs(h + 1, cls);
+        __stcs(h + 2, pos);
     }
 }
 
@@ -183,40 +229,72 @@ __global__ void stream_offsets_kernel(Part part, uint64_t* __restrict__ soff) {
 }
 
 void launch_sparse_csr(cudaStream_t s, const Part& part, const uint32_t* stream, uint64_t n,
-                       uint32_t* cnt, uint64_t* koff, uint32_t* cur, uint32_t* csr, uint64_t* soff,
-                       Workspace& ws) {
+                       uint32_t* cnt, uint64_t* koff, uint32_t* cur, uint32_t* csr, uint32_t* cpos,
+                       uint64_t* soff, Workspace& ws) {
     const uint32_t F = part.F, nloc = part.wend - part.wbegin;
     stream_offsets_kernel<<<grid_for(nloc + 1, kThreads), kThreads, 0, s>>>(part, soff);
     cudaMemsetAsync(cnt, 0, (size_t)F * 4, s);
     csr_hist_kernel<<<grid_for(n, kThreads, 148u * 16u), kThreads, 0, s>>>(stream, n, cnt);
     exclusive_scan(s, cnt, F, koff, ws);
     csr_cursor_kernel<<<grid_for(F, kThreads), kThreads, 0, s>>>(koff, F, cur);
-    csr_scatter_kernel<<<grid_for(n, kThreads, 148u * 16u), kThreads, 0, s>>>(stream, n, cur, csr);
+    // sample windows of ~48 MB of CSR (samples are uniform over the entries)
+    const uint64_t windows = csr_windows(n);
+    for (uint64_t j = 0; j < windows; ++j) {
+        const uint32_t lo = (uint32_t)(F * j / windows), hi = (uint32_t)(F * (j + 1) / windows);
+        csr_scatter_kernel<<<grid_for(n, kThreads, 148u * 16u), kThreads, 0, s>>>(stream, n, lo, hi,
+                                                                               cur, csr, cpos);
+    }
 }
 
-bool sparse_path_ok(const Part& part) { return (part.wend - part.wbegin) <= 1024; }
+uint64_t csr_windows(uint64_t n) {
+    return std::max<uint64_t>(1, (n * 4 + (48ull << 20) - 1) / (48ull << 20));
+}
+
+// Sparse passes when they beat the dense E*F ones (B200 measurements, config 2: dense ~14 ps
+// per (epoch, sample) cell; sparse ~40 ps per local entry + ~10 ps per entry per CSR window).
+bool sparse_path_fits(const Part& part) { return (part.wend - part.wbegin) <= 1024 && part.E <= 128; }
+
+bool sparse_path_ok(const Part& part, uint64_t local_entries) {
+    if (!sparse_path_fits(part)) return false;
+    const double sparse = (double)local_entries * (40.0 + 10.0 * (double)csr_windows(local_entries));
+    const double dense = 14.0 * (double)part.E * (double)part.F;
+    return sparse < dense;
+}
 
 void launch_sparse_sample(cudaStream_t s, const Part& part, const uint64_t* soff, const uint64_t* koff,
                           const uint32_t* csr, uint32_t* pair_count, uint16_t* einfo,
-                          uint16_t* erank) {
+                          uint16_t* erank, const WorkerSums& ws) {
     const uint32_t nloc = part.wend - part.wbegin, W = (nloc + 31) / 32;
-    const size_t smem = (size_t)(kThreads / 32) * (2 * W * 32 + W) * 4;
-    cudaFuncSetAttribute(sparse_sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    sparse_sample_kernel<<<grid_for((uint64_t)part.F * 32, kThreads, 148u * 8u), kThreads, smem, s>>>(
-        part.F, nloc, W, soff, koff, csr, pair_count, einfo, erank);
+    const size_t smem = ((size_t)(kThreads / 32) * (2 * W * 32 + W) + 2) * 4 +
+                        (ws.sum ? (size_t)W * 32 * 12 : 0);
+    const unsigned grid = grid_for((uint64_t)part.F * 32, kThreads, 148u * 8u);
+#define SS_LAUNCH(RV)                                                                              \
+    do {                                                                                           \
+        cudaFuncSetAttribute(sparse_sample_kernel<RV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                             (int)smem);                                                           \
+        sparse_sample_kernel<RV><<<grid, kThreads, smem, s>>>(part.F, nloc, W, soff, koff, csr,      \
+                                                              pair_count, einfo, erank, ws);       \
+    } while (0)
+    const uint32_t R = (part.E + 31) / 32;  // a sample has at most one entry per epoch
+    if (R == 1) SS_LAUNCH(1);
+    else if (R == 2) SS_LAUNCH(2);
+    else if (R == 3) SS_LAUNCH(3);
+    else SS_LAUNCH(4);
+#undef SS_LAUNCH
 }
 
-void launch_holder_sparse(cudaStream_t s, const Part& part, const uint64_t* soff, const uint64_t* koff,
-                          const uint32_t* csr, const uint16_t* erank, uint32_t MB, const uint32_t* rec,
-                          uint32_t np, uint32_t J, uint32_t Rp, const uint32_t* cbase,
-                          const uint64_t* pair_off, uint32_t* holders, bool allfit) {
-    const unsigned grid = grid_for((uint64_t)part.F * 32, kThreads, 148u * 16u);
+void launch_holder_sparse(cudaStream_t s, const Part& part, uint64_t n, const uint64_t* soff,
+                          const uint32_t* stream, const uint32_t* csr, const uint16_t* erank,
+                          uint32_t MB, const uint32_t* rec, uint32_t np, uint32_t J, uint32_t Rp,
+                          const uint32_t* cbase, const uint64_t* pair_off, uint32_t* holders,
+                          bool allfit) {
+    const unsigned grid = grid_for(n, kThreads, 148u * 16u);
     if (allfit)
-        holder_sparse_kernel<-1><<<grid, kThreads, 0, s>>>(part, soff, koff, csr, erank, MB, rec, np,
-                                                           J, Rp, cbase, pair_off, holders);
+        holder_sparse_kernel<-1><<<grid, kThreads, 0, s>>>(part, n, soff, stream, csr, erank, MB, rec,
+                                                           np, J, Rp, cbase, pair_off, holders);
     else
-        holder_sparse_kernel<0><<<grid, kThreads, 0, s>>>(part, soff, koff, csr, erank, MB, rec, np, J,
-                                                          Rp, cbase, pair_off, holders);
+        holder_sparse_kernel<0><<<grid, kThreads, 0, s>>>(part, n, soff, stream, csr, erank, MB, rec, np,
+                                                          J, Rp, cbase, pair_off, holders);
 }
 
 }  // namespace clairplan

@@ -395,3 +395,34 @@ def test_config4_imagenet22k_against_reference_worker_subset(cp, ref):
     sub_offs[1:] = np.cumsum(np.bincount(owner[keep], minlength=F))
     assert np.array_equal(sub_offs, a.holder_offsets.astype(np.int64))
     assert np.array_equal(hold[keep], a.holders)
+
+
+def test_build_export_matches_separate_exports(cp, ref):
+    """clairplan_build_export (sizes H2D + build + overlapped D2H) == build + the export calls."""
+    import ctypes as C
+    F, N, B, E = 30_000, 12, 240, 9
+    sizes = ref.generate_sizes(F, 0.1077, 0.2, None, 1)
+    for caps in ([1e6, 1e6], [20.0, 60.0]):
+        p = cp.Plan(5, F, cp.PartitionSpec(N, B, E, True), caps, sizes).build()
+        st = p.stats()
+        want_streams = np.concatenate([p.stream(w) for w in range(N)])
+        want_cl = np.concatenate([x for lists in p.class_lists() for x in lists])
+        want_off, want_hold = p.holders()
+        L = cp.lib()
+        u32, u64 = C.POINTER(C.c_uint32), C.POINTER(C.c_uint64)
+        L.clairplan_build_export.argtypes = [C.c_void_p, C.c_void_p, u32, C.c_uint64, u32,
+                                             C.c_uint64, u64, u32, C.c_uint64]
+        hs = np.zeros(st["accesses"], np.uint32)
+        hc = np.zeros(max(st["holders"], 1), np.uint32)
+        ho = np.zeros(F + 1, np.uint64)
+        hh = np.zeros(3 * max(st["holders"], 1), np.uint32)
+        hsz = np.ascontiguousarray(sizes, np.float64)
+        cp._check(L.clairplan_build_export(p._h, hsz.ctypes.data_as(C.c_void_p),
+                                           hs.ctypes.data_as(u32), len(hs), hc.ctypes.data_as(u32),
+                                           len(hc), ho.ctypes.data_as(u64), hh.ctypes.data_as(u32),
+                                           st["holders"]))
+        assert np.array_equal(hs, want_streams)
+        assert np.array_equal(hc[:len(want_cl)], want_cl)
+        assert np.array_equal(ho, want_off.astype(np.uint64))
+        assert np.array_equal(hh[:3 * st["holders"]], want_hold.reshape(-1))
+        p.close()
