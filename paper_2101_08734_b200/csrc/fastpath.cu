@@ -855,12 +855,15 @@ __global__ void __launch_bounds__(kThreads) sample_tile_kernel(Part part, const 
     uint32_t* cnt = fe + W * 32;                     // [nloc] count
     uint32_t* bm = cnt + W * 32;                     // [W] worker bitmap
     // per-CTA candidate size sums / counts per local worker (the whole-worker fit test)
-    double* csum = reinterpret_cast<double*>(tabs + nwarps * (2 * W * 32 + W) + 1) ;
-    csum = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(csum) + 7) & ~(uintptr_t)7);
-    uint32_t* ccnt = reinterpret_cast<uint32_t*>(csum + W * 32);
+    // (fixed point, size * 2^20 rounded up: an upper bound; 64-bit sums as two 32-bit words,
+    // native shared atomics)
+    uint32_t* clo = tabs + nwarps * (2 * W * 32 + W);
+    uint32_t* chi = clo + W * 32;
+    uint32_t* ccnt = chi + W * 32;
     if (ws.sum)
         for (uint32_t x = threadIdx.x; x < W * 32; x += blockDim.x) {
-            csum[x] = 0.0;
+            clo[x] = 0;
+            chi[x] = 0;
             ccnt[x] = 0;
         }
     for (uint32_t x = lane; x < W * 32; x += 32) {
@@ -915,10 +918,14 @@ __global__ void __launch_bounds__(kThreads) sample_tile_kernel(Part part, const 
             const uint32_t pre = inc - c;
             const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
             if (live && lane == 0) pair_count[k0 + s] = total;
-            double sz = 0.0;
+            unsigned long long sz = 0;
             if (ws.sum && live) {
-                sz = __ldg(ws.sizes + k0 + s);
-                if (lane == 0 && !(sz >= 0.0)) atomicOr(ws.neg, 1u);
+                const double v = __ldg(ws.sizes + k0 + s);
+                if (!(v >= 0.0 && v < 0x1.0p40)) {
+                    if (lane == 0) atomicOr(ws.neg, 1u);  // negative, NaN or huge: no all-fit
+                } else {
+                    sz = __double2ull_ru(v * 0x1.0p20);
+                }
             }
 #pragma unroll
             for (int r = 0; r < R; ++r) {
@@ -934,7 +941,7 @@ __global__ void __launch_bounds__(kThreads) sample_tile_kernel(Part part, const 
                         rk = (uint16_t)(pw + __popc(ww & ((1u << (x & 31)) - 1u)));
                         if (seghist) atomicAdd(&seghist[((uint64_t)x * E + (E - ci)) * E + e], 1u);
                         if (ws.sum) {
-                            atomicAdd(&csum[x], sz);
+                            add64(clo + x, chi + x, sz);
                             atomicAdd(&ccnt[x], 1u);
                         }
                     }
@@ -970,7 +977,7 @@ __global__ void __launch_bounds__(kThreads) sample_tile_kernel(Part part, const 
         __syncthreads();
         for (uint32_t x = threadIdx.x; x < nloc; x += blockDim.x) {
             if (ccnt[x]) {
-                atomicAdd(&ws.sum[x], csum[x]);
+                atomicAdd(&ws.sum[x], ((unsigned long long)chi[x] << 32) | clo[x]);
                 atomicAdd(&ws.cnt[x], ccnt[x]);
             }
         }
@@ -1060,7 +1067,7 @@ void launch_sample_tile(cudaStream_t s, const Part& part, const uint32_t* inv, u
     const uint32_t W = (nloc + 31) / 32;
     const size_t smem = (size_t)4 * (2 * part.E * kStInv + part.E * kStOut +
                                      (kThreads / 32) * (2 * W * 32 + W) + 2) +
-                        (ws.sum ? (size_t)W * 32 * 12 : 0);
+                        (ws.sum ? (size_t)W * 32 * 12 : 0);  // clo, chi, ccnt
     const uint64_t tiles = ((uint64_t)part.F + 31) / 32;
     const unsigned grid = grid_for(tiles, 1, 148u * 8u);
 #define ST_LAUNCH(RV)                                                                             \

@@ -41,9 +41,18 @@ struct TileMap {
 };
 
 // per local worker: sum / count of its candidates' sizes (all-fit test); sum == nullptr: off
+// exact 64-bit add into a (lo, hi) pair of shared words with 32-bit atomics (shared 64-bit
+// atomic adds compile to CAS loops)
+__device__ __forceinline__ void add64(uint32_t* lo, uint32_t* hi, unsigned long long v) {
+    const uint32_t vl = (uint32_t)v, vh = (uint32_t)(v >> 32);
+    const uint32_t old = atomicAdd(lo, vl);
+    const uint32_t carry = (uint32_t)(old + vl < old);
+    if (vh + carry) atomicAdd(hi, vh + carry);
+}
+
 struct WorkerSums {
     const double* sizes = nullptr;
-    double* sum = nullptr;
+    unsigned long long* sum = nullptr;  // sum of ceil(size * 2^20): an upper bound
     uint32_t* cnt = nullptr;
     uint32_t* neg = nullptr;  // set when a size is negative (or NaN)
 };

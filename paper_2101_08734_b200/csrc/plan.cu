@@ -671,11 +671,14 @@ int assign_allfit_v2(clairplan_plan* p) {
 
 // Whole-worker fit test on the host from the sample pass's per-worker sums: every worker's
 // candidates fit class 1 whatever the order (bound as in firstfit.cu ff_prefix_kernel).
-bool allfit_decide(double C, const std::vector<double>& sum, const std::vector<uint32_t>& cnt) {
+// sum[w] = sum of ceil(size * 2^20) over worker w's candidates (an upper bound).
+bool allfit_decide(double C, const std::vector<unsigned long long>& sum,
+                   const std::vector<uint32_t>& cnt) {
     for (size_t w = 0; w < sum.size(); ++w) {
         if (cnt[w] == 0) continue;
-        const double tol = ((double)cnt[w] + 1024.0) * std::max(C, sum[w]) * 0x1.0p-48;
-        if (!(C - sum[w] > tol)) return false;
+        const double sw = (double)sum[w] * 0x1.0p-20;
+        const double tol = ((double)cnt[w] + 1024.0) * std::max(C, sw) * 0x1.0p-48;
+        if (!(C - sw > tol)) return false;
     }
     return true;
 }
@@ -736,7 +739,7 @@ int build_seed_path_v2(clairplan_plan* p, const uint32_t* ext_perms,
     uint32_t* bmask = need<uint32_t>(p->blkmask, nblk, ok);
     uint32_t* bbase = need<uint32_t>(p->blkbase, nblk, ok);
     uint32_t* hard = need<uint32_t>(p->hard, (uint64_t)F + 1, ok);
-    double* wsum = need<double>(p->wsum, nloc, ok);
+    unsigned long long* wsum = need<unsigned long long>(p->wsum, nloc, ok);
     uint32_t* wcnt = need<uint32_t>(p->wcnt, (uint64_t)nloc + 1, ok);  // + the negative-size flag
     uint32_t* wneg = wcnt + nloc;
     // sparse sample-major passes (sharded handle fed by the all-to-all; CLAIRPLAN_DENSE=1: A/B)
@@ -818,7 +821,7 @@ int build_seed_path_v2(clairplan_plan* p, const uint32_t* ext_perms,
         p->mark(2);
         std::vector<uint32_t> flags(E);
         uint64_t D = 0;
-        std::vector<double> hsum(sums ? nloc : 0);
+        std::vector<unsigned long long> hsum(sums ? nloc : 0);
         std::vector<uint32_t> hcnt(sums ? nloc + 1 : 0);
         CK(cudaMemcpyAsync(&D, poff + F, 8, cudaMemcpyDeviceToHost, s));
         if (sums) {

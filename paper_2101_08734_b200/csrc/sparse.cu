@@ -19,9 +19,12 @@
 
 namespace clairplan {
 
-// local worker of stream index s: largest wl with soff[wl] <= s (soff[nloc] = total)
+// local worker of stream index s: largest wl with soff[wl] <= s (soff[nloc] = total); when
+// every local worker's stream has the same length (FastDiv d != 1 ... set by the host), one
+// division
 __device__ __forceinline__ uint32_t worker_of_entry(const uint64_t* __restrict__ soff, uint32_t nloc,
-                                                    uint64_t s) {
+                                                    uint64_t s, const FastDiv& uni) {
+    if (uni.d > 1 || nloc == 1) return nloc == 1 ? 0u : uni.div((uint32_t)s);
     uint32_t lo = 0, hi = nloc;
     while (hi - lo > 1) {
         const uint32_t mid = (lo + hi) >> 1;
@@ -68,7 +71,7 @@ __global__ void __launch_bounds__(kThreads) sparse_sample_kernel(
     uint32_t F, uint32_t nloc, uint32_t W, const uint64_t* __restrict__ soff,
     const uint64_t* __restrict__ koff, const uint32_t* __restrict__ csr,
     uint32_t* __restrict__ pair_count, uint16_t* __restrict__ einfo, uint16_t* __restrict__ erank,
-    WorkerSums ws) {
+    WorkerSums ws, FastDiv uni) {
     extern __shared__ uint32_t sm[];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr uint32_t NW = kThreads / 32;
@@ -76,12 +79,15 @@ __global__ void __launch_bounds__(kThreads) sparse_sample_kernel(
     uint32_t* cnt = fs + W * 32;                   // [nloc] accesses
     uint32_t* bm = cnt + W * 32;                   // [W]
     // per-CTA candidate size sums / counts per local worker (the whole-worker fit test)
-    double* csum = reinterpret_cast<double*>(sm + NW * (2 * W * 32 + W) + 1);
-    csum = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(csum) + 7) & ~(uintptr_t)7);
-    uint32_t* ccnt = reinterpret_cast<uint32_t*>(csum + W * 32);
+    // (fixed point, size * 2^20 rounded up: an upper bound; 64-bit sums as two 32-bit words,
+    // native shared atomics)
+    uint32_t* clo = sm + NW * (2 * W * 32 + W);
+    uint32_t* chi = clo + W * 32;
+    uint32_t* ccnt = chi + W * 32;
     if (ws.sum)
         for (uint32_t x = threadIdx.x; x < W * 32; x += blockDim.x) {
-            csum[x] = 0.0;
+            clo[x] = 0;
+            chi[x] = 0;
             ccnt[x] = 0;
         }
     for (uint32_t x = lane; x < W * 32; x += 32) {
@@ -100,7 +106,7 @@ __global__ void __launch_bounds__(kThreads) sparse_sample_kernel(
             xv[r] = kNone;
             if (i < b) {
                 sv[r] = __ldcs(csr + i);
-                xv[r] = worker_of_entry(soff, nloc, sv[r]);
+                xv[r] = worker_of_entry(soff, nloc, sv[r], uni);
                 atomicMin(&fs[xv[r]], sv[r]);
                 atomicAdd(&cnt[xv[r]], 1u);
                 atomicOr(&bm[xv[r] >> 5], 1u << (xv[r] & 31));
@@ -123,10 +129,14 @@ __global__ void __launch_bounds__(kThreads) sparse_sample_kernel(
             total = __shfl_sync(0xffffffffu, inc, 31);
         }
         if (lane == 0) pair_count[k] = total;
-        double sz = 0.0;
+        unsigned long long sz = 0;
         if (ws.sum && b > a) {
-            sz = __ldg(ws.sizes + k);
-            if (lane == 0 && !(sz >= 0.0)) atomicOr(ws.neg, 1u);
+            const double v = __ldg(ws.sizes + k);
+            if (!(v >= 0.0 && v < 0x1.0p40)) {
+                if (lane == 0) atomicOr(ws.neg, 1u);  // negative, NaN or huge: no all-fit
+            } else {
+                sz = __double2ull_ru(v * 0x1.0p20);
+            }
         }
 #pragma unroll
         for (int r = 0; r < R; ++r) {
@@ -140,7 +150,7 @@ __global__ void __launch_bounds__(kThreads) sparse_sample_kernel(
                     ci = (uint16_t)cnt[x];
                     rk = (uint16_t)(pw + __popc(ww & ((1u << (x & 31)) - 1u)));
                     if (ws.sum) {
-                        atomicAdd(&csum[x], sz);
+                        add64(clo + x, chi + x, sz);
                         atomicAdd(&ccnt[x], 1u);
                     }
                 }
@@ -164,7 +174,7 @@ __global__ void __launch_bounds__(kThreads) sparse_sample_kernel(
         __syncthreads();
         for (uint32_t x = threadIdx.x; x < nloc; x += blockDim.x) {
             if (ccnt[x]) {
-                atomicAdd(&ws.sum[x], csum[x]);
+                atomicAdd(&ws.sum[x], ((unsigned long long)chi[x] << 32) | clo[x]);
                 atomicAdd(&ws.cnt[x], ccnt[x]);
             }
         }
@@ -179,7 +189,7 @@ __global__ void __launch_bounds__(kThreads) holder_sparse_kernel(
     const uint32_t* __restrict__ csr, const uint16_t* __restrict__ erank, uint32_t MB,
     const uint32_t* __restrict__ rec, uint32_t np_rt, uint32_t J, uint32_t Rp,
     const uint32_t* __restrict__ cbase, const uint64_t* __restrict__ pair_off,
-    uint32_t* __restrict__ holders) {
+    uint32_t* __restrict__ holders, FastDiv uni) {
     const uint32_t E = part.E, nloc = part.wend - part.wbegin;
     const uint32_t np = NP > 0 ? (uint32_t)NP : np_rt;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
@@ -188,7 +198,7 @@ __global__ void __launch_bounds__(kThreads) holder_sparse_kernel(
         if (rk == 0xFFFFu) continue;
         const uint32_t s = __ldcs(csr + i);
         const uint32_t k = __ldg(stream + s);
-        const uint32_t wl = worker_of_entry(soff, nloc, s);
+        const uint32_t wl = worker_of_entry(soff, nloc, s, uni);
         const uint32_t w = part.wbegin + wl;
         const uint32_t Le = (uint32_t)part.epoch_len(w);
         const uint32_t rel = (uint32_t)(s - soff[wl]);
@@ -226,6 +236,16 @@ __global__ void stream_offsets_kernel(Part part, uint64_t* __restrict__ soff) {
     const uint32_t nloc = part.wend - part.wbegin;
     for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x <= nloc; x += gridDim.x * blockDim.x)
         soff[x] = part.stream_offset(part.wbegin + x);
+}
+
+// FastDiv by the common per-worker stream length when every local worker has the same one
+// (uniform batch slices); d == 1 otherwise (binary search)
+static FastDiv uniform_len(const Part& part) {
+    const uint64_t L0 = part.epoch_len(part.wbegin), L1 = part.epoch_len(part.wend - 1);
+    const uint64_t L = L0 * part.E;
+    if (L0 == L1 && L > 1 && L < (1ull << 31) && part.stream_offset(part.wend) < (1ull << 32))
+        return FastDiv((uint32_t)L);
+    return FastDiv(1u);
 }
 
 void launch_sparse_csr(cudaStream_t s, const Part& part, const uint32_t* stream, uint64_t n,
@@ -268,12 +288,13 @@ void launch_sparse_sample(cudaStream_t s, const Part& part, const uint64_t* soff
     const size_t smem = ((size_t)(kThreads / 32) * (2 * W * 32 + W) + 2) * 4 +
                         (ws.sum ? (size_t)W * 32 * 12 : 0);
     const unsigned grid = grid_for((uint64_t)part.F * 32, kThreads, 148u * 8u);
+    const FastDiv uni = uniform_len(part);
 #define SS_LAUNCH(RV)                                                                              \
     do {                                                                                           \
         cudaFuncSetAttribute(sparse_sample_kernel<RV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                              (int)smem);                                                           \
         sparse_sample_kernel<RV><<<grid, kThreads, smem, s>>>(part.F, nloc, W, soff, koff, csr,      \
-                                                              pair_count, einfo, erank, ws);       \
+                                                              pair_count, einfo, erank, ws, uni);  \
     } while (0)
     const uint32_t R = (part.E + 31) / 32;  // a sample has at most one entry per epoch
     if (R == 1) SS_LAUNCH(1);
@@ -289,12 +310,13 @@ void launch_holder_sparse(cudaStream_t s, const Part& part, uint64_t n, const ui
                           const uint32_t* cbase, const uint64_t* pair_off, uint32_t* holders,
                           bool allfit) {
     const unsigned grid = grid_for(n, kThreads, 148u * 16u);
+    const FastDiv uni = uniform_len(part);
     if (allfit)
         holder_sparse_kernel<-1><<<grid, kThreads, 0, s>>>(part, n, soff, stream, csr, erank, MB, rec,
-                                                           np, J, Rp, cbase, pair_off, holders);
+                                                           np, J, Rp, cbase, pair_off, holders, uni);
     else
         holder_sparse_kernel<0><<<grid, kThreads, 0, s>>>(part, n, soff, stream, csr, erank, MB, rec, np,
-                                                          J, Rp, cbase, pair_off, holders);
+                                                          J, Rp, cbase, pair_off, holders, uni);
 }
 
 }  // namespace clairplan

@@ -181,7 +181,9 @@ def test_allfit_path_matches_reference(cp, ref, case, monkeypatch):
     sizes = ref.generate_sizes(F, mu, sd, None, 1)
     a = ref.plan(seed, F, N, B, E, dl, caps, sizes)
     b = device_plan(cp, seed, F, N, B, E, dl, caps, sizes)
-    assert b.stats["path"] == "allfit"
+    # the worker sums come from the tile sample pass (E <= 128); the lane fallback takes the
+    # tier path
+    assert b.stats["path"] == ("allfit" if E <= 128 else "tier")
     assert plans_equal(a, b) is None
     monkeypatch.setenv("CLAIRPLAN_NO_ALLFIT", "1")
     c = device_plan(cp, seed, F, N, B, E, dl, caps, sizes)
@@ -199,7 +201,7 @@ def test_allfit_capacity_boundary(cp, ref):
     top = max(sums)
     paths = set()
     for C in (top, np.nextafter(top, 0), np.nextafter(top, np.inf), top * (1 - 1e-9),
-              top * (1 + 1e-9), top * (1 + 1e-6), min(sums), 0.5 * top):
+              top * (1 + 1e-9), top * (1 + 1e-6), top * (1 + 1e-3), min(sums), 0.5 * top):
         a = ref.plan(seed, F, N, B, E, True, [float(C), 5.0], sizes)
         b = device_plan(cp, seed, F, N, B, E, True, [float(C), 5.0], sizes)
         paths.add(b.stats["path"])
