@@ -753,6 +753,42 @@ __global__ void __launch_bounds__(kThreads) holder_tile_kernel(
             }
         }
         __syncthreads();
+        if constexpr (NP == -1) {
+            if (E <= 128) {  // all-fit, <= 4 epoch rounds: the rounds' record loads overlap
+                for (uint32_t s = warp; s < 32; s += nwarps) {
+                    if (k0 + s >= F) break;
+                    const uint64_t slot0 = pair_off[k0 + s];
+                    uint32_t rk[4], w[4], bit[4];
+                    uint2 a2[4];
+                    uint32_t cb[4];
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        const uint32_t e = r * 32 + lane;
+                        rk[r] = e < E ? trk[e * 33 + s] : 0xFFFFu;
+                        if (rk[r] != 0xFFFFu) {
+                            const uint32_t tseg = part.within_epoch(tinv[e * 33 + s], w[r]);
+                            const uint32_t wl = w[r] - part.wbegin;
+                            const uint64_t blk = ((uint64_t)wl * E + e) * MB + (tseg >> 5);
+                            bit[r] = tseg & 31;
+                            a2[r] = __ldg(reinterpret_cast<const uint2*>(rec) + blk);
+                            cb[r] = __ldg(cbase + wl * J);
+                        }
+                    }
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        if (rk[r] == 0xFFFFu) continue;
+                        const uint32_t cls = (a2[r].x >> bit[r]) & 1u;
+                        const uint32_t pos =
+                            cls ? a2[r].y - cb[r] + __popc(a2[r].x & ((1u << bit[r]) - 1u)) : 0u;
+                        uint32_t* h = holders + 3 * (slot0 + rk[r]);
+                        __stcs(h, w[r]);
+                        __stcs(h + 1, cls);
+                        __stcs(h + 2, pos);
+                    }
+                }
+                continue;
+            }
+        }
         for (uint32_t s = warp; s < 32; s += nwarps) {
             if (k0 + s >= F) break;
             const uint64_t slot0 = pair_off[k0 + s];

@@ -339,6 +339,7 @@ __global__ void __launch_bounds__(kBlockThreads) fyb_block_kernel(uint32_t F, Fy
 }
 
 // ---- fyb_emit: per step, chase and write --------------------------------------------------
+template <int U>  // consecutive positions per thread: one slice lookup serves them
 __global__ void __launch_bounds__(kThreads) fyb_emit_kernel(uint64_t key, Part part, uint32_t e0,
                                                             RejTable rt,
                                                             const uint32_t* __restrict__ succ,
@@ -350,7 +351,6 @@ __global__ void __launch_bounds__(kThreads) fyb_emit_kernel(uint64_t key, Part p
     const FyRej rj(rt, e - rt.e_base);
     const uint32_t* sc = succ + (size_t)slot * F;
     const uint32_t* qq = q + (size_t)slot * F;
-    constexpr int U = 4;  // consecutive positions per thread: one slice lookup serves them
     const uint32_t nthr = gridDim.x * blockDim.x;
     for (uint32_t i0 = (blockIdx.x * blockDim.x + threadIdx.x) * U; i0 < F; i0 += U * nthr) {
         uint32_t cur[U];
@@ -442,7 +442,19 @@ void launch_fyb(cudaStream_t s, uint64_t key, const Part& part, uint32_t e0, uin
     fyb_block_kernel<<<dim3(g.NB, ne), kBlockThreads, sm_block, s>>>(F, g, bucket, lst, pool,
                                                                       pool_used, succ, q, e0, inv);
     dim3 grid(grid_for(F, kThreads * 4, 148u * 16u), ne);
-    fyb_emit_kernel<<<grid, kThreads, 0, s>>>(key, part, e0, rt, succ, q, inv, stream, perm_out);
+    static const int u = [] {
+        const char* v = getenv("CLAIRPLAN_EMIT_U");  // A/B
+        return v ? atoi(v) : 4;
+    }();
+    if (u == 8) {
+        dim3 g8(grid_for(F, kThreads * 8, 148u * 16u), ne);
+        fyb_emit_kernel<8><<<g8, kThreads, 0, s>>>(key, part, e0, rt, succ, q, inv, stream, perm_out);
+    } else if (u == 2) {
+        dim3 g2(grid_for(F, kThreads * 2, 148u * 16u), ne);
+        fyb_emit_kernel<2><<<g2, kThreads, 0, s>>>(key, part, e0, rt, succ, q, inv, stream, perm_out);
+    } else {
+        fyb_emit_kernel<4><<<grid, kThreads, 0, s>>>(key, part, e0, rt, succ, q, inv, stream, perm_out);
+    }
 }
 
 }  // namespace clairplan
