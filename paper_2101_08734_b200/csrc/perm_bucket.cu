@@ -34,6 +34,7 @@ bool fy_geometry(uint32_t F, FyGeom& g) {
     const uint64_t TB = 1ull << lgTB;
     uint32_t lgTS = 13;
     while ((1ull << lgTS) * TB < 4ull * F) ++lgTS;
+    if (const char* v = getenv("CLAIRPLAN_FY_LGTS")) lgTS = (uint32_t)atoi(v);  // A/B
     if (lgTS + lgTB > 31) return false;
     g.lgTB = lgTB;
     g.lgTS = lgTS;
@@ -443,8 +444,8 @@ void launch_fyb(cudaStream_t s, uint64_t key, const Part& part, uint32_t e0, uin
                                                                       pool_used, succ, q, e0, inv);
     dim3 grid(grid_for(F, kThreads * 4, 148u * 16u), ne);
     static const int u = [] {
-        const char* v = getenv("CLAIRPLAN_EMIT_U");  // A/B
-        return v ? atoi(v) : 4;
+        const char* v = getenv("CLAIRPLAN_EMIT_U");  // A/B (2 measured best for config 2)
+        return v ? atoi(v) : 2;
     }();
     if (u == 8) {
         dim3 g8(grid_for(F, kThreads * 8, 148u * 16u), ne);

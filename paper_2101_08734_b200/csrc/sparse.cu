@@ -270,14 +270,15 @@ uint64_t csr_windows(uint64_t n) {
     return std::max<uint64_t>(1, (n * 4 + (48ull << 20) - 1) / (48ull << 20));
 }
 
-// Sparse passes when they beat the dense E*F ones (B200 measurements, config 2: dense ~14 ps
-// per (epoch, sample) cell; sparse ~40 ps per local entry + ~10 ps per entry per CSR window).
+// Sparse passes when they beat the dense E*F ones (B200, config 2 sharded 2/4/8 ways: dense
+// ~16 ps per (epoch, sample) cell — inverse rebuild, sample and holder passes; sparse ~55 ps
+// per local entry — CSR build, sparse sample and holder passes — growing with the windows).
 bool sparse_path_fits(const Part& part) { return (part.wend - part.wbegin) <= 1024 && part.E <= 128; }
 
 bool sparse_path_ok(const Part& part, uint64_t local_entries) {
     if (!sparse_path_fits(part)) return false;
-    const double sparse = (double)local_entries * (40.0 + 10.0 * (double)csr_windows(local_entries));
-    const double dense = 14.0 * (double)part.E * (double)part.F;
+    const double sparse = (double)local_entries * (40.0 + 5.0 * (double)csr_windows(local_entries));
+    const double dense = 16.0 * (double)part.E * (double)part.F;
     return sparse < dense;
 }
 
