@@ -245,6 +245,70 @@ void* ref_plan_build_subset(uint64_t seed, uint32_t F, uint32_t N, uint32_t B, u
     }
 }
 
+// Worker-subset plan for datasets whose permutations do not fit host memory together
+// (config 5: 100 x 100 M samples): epochs are generated one per thread at a time and only the
+// subset workers' slices are kept; the other workers' streams stay empty.
+void* ref_plan_build_subset_lowmem(uint64_t seed, uint32_t F, uint32_t N, uint32_t B, uint32_t E,
+                                   int drop_last, uint32_t J, const double* caps,
+                                   const double* sizes, int threads, const uint32_t* subset,
+                                   uint32_t nsubset) {
+    try {
+        auto p = std::make_unique<RefPlan>();
+        p->F = F;
+        PartitionSpec part{N, B, E, drop_last != 0};
+        const DatasetModel dataset = DatasetModel::from_sizes(std::vector<double>(sizes, sizes + F));
+        part.validate(F);
+        const uint64_t full = F / B;
+        const uint64_t tail = part.drop_last ? 0 : F % B;
+        const uint64_t nb = full + (tail > 0 ? 1 : 0);
+        // per (subset worker, epoch) slices, the same insert order as build_access_streams
+        std::vector<std::vector<std::vector<uint32_t>>> part_e(nsubset,
+                                                               std::vector<std::vector<uint32_t>>(E));
+        parallel_for(E, threads, [&](uint64_t e) {
+            const auto perm = epoch_permutation(Seed{seed}, static_cast<uint32_t>(e), F);
+            for (uint32_t i = 0; i < nsubset; ++i) {
+                auto& out = part_e[i][e];
+                for (uint64_t h = 0; h < nb; ++h) {
+                    const uint64_t bs = h < full ? B : tail;
+                    const auto [sb, se] = batch_slice(bs, N, subset[i]);
+                    out.insert(out.end(), perm.begin() + h * B + sb, perm.begin() + h * B + se);
+                }
+            }
+        });
+        p->streams.resize(N);
+        for (uint32_t w = 0; w < N; ++w) {
+            p->streams[w].worker_id = w;
+            p->streams[w].epoch_offsets.push_back(0);
+            p->streams[w].batch_offsets.push_back(0);
+        }
+        for (uint32_t i = 0; i < nsubset; ++i) {
+            auto& st = p->streams[subset[i]];
+            st.epoch_offsets.clear();
+            st.epoch_offsets.push_back(0);
+            for (uint32_t e = 0; e < E; ++e) {
+                st.entries.insert(st.entries.end(), part_e[i][e].begin(), part_e[i][e].end());
+                st.epoch_offsets.push_back(st.entries.size());
+                std::vector<uint32_t>().swap(part_e[i][e]);
+            }
+        }
+        p->assign.class_lists.assign(N, std::vector<std::vector<uint32_t>>(J));
+        const SystemConfig cfg1 = make_cfg(1, J, caps);
+        parallel_for(nsubset, threads, [&](uint64_t i) {
+            const uint32_t w = subset[i];
+            const auto& st = p->streams[w];
+            const auto freq = access_frequencies(st, F, 0, st.epoch_count());
+            auto one = nopfs_assign_caches({freq}, cfg1, dataset, {st});
+            if (J > 0) p->assign.class_lists[w] = std::move(one.class_lists[0]);
+        });
+        p->assign.build_index(F);
+        flatten_holders(*p);
+        return p.release();
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+
 // nopfs_assign_caches on caller-provided streams + dense frequency tables (policies.hpp:88-90).
 // streams: concatenated entries with per-worker offsets [N+1]; counts: N x F dense.
 void* ref_assign_from_streams(uint32_t N, uint32_t F, const uint32_t* entries,

@@ -922,6 +922,8 @@ __global__ void __launch_bounds__(kThreads) sample_tile_kernel(Part part, const 
         const uint32_t* tinv = tin[buf];
         for (uint32_t s = warp; s < 32; s += nwarps) {
             const bool live = k0 + s < F;
+            // the sample's size, issued early (used after the rounds)
+            const double szv = (ws.sum && live) ? __ldg(ws.sizes + k0 + s) : 0.0;
             uint32_t wl[R];
 #pragma unroll
             for (int r = 0; r < R; ++r) {
@@ -956,7 +958,7 @@ __global__ void __launch_bounds__(kThreads) sample_tile_kernel(Part part, const 
             if (live && lane == 0) pair_count[k0 + s] = total;
             unsigned long long sz = 0;
             if (ws.sum && live) {
-                const double v = __ldg(ws.sizes + k0 + s);
+                const double v = szv;
                 if (!(v >= 0.0 && v < 0x1.0p40)) {
                     if (lane == 0) atomicOr(ws.neg, 1u);  // negative, NaN or huge: no all-fit
                 } else {

@@ -724,10 +724,15 @@ int build_seed_path_v2(clairplan_plan* p, const uint32_t* ext_perms,
     while ((1u << np) <= J) ++np;  // bits to hold classes 0..J
     const uint64_t EF = (uint64_t)E * F, NEE = (uint64_t)nloc * E * E;
     bool ok = true;
+    // sparse sample-major passes (sharded handle fed by the all-to-all; CLAIRPLAN_DENSE=1: A/B)
+    const char* dense_env = getenv("CLAIRPLAN_DENSE");  // "1": dense, "0": sparse, unset: cost model
+    const bool sparse = ext_streams && (dense_env ? dense_env[0] == '0' && sparse_path_fits(part)
+                                                  : sparse_path_ok(part, p->A));
     uint32_t* stream_buf = need<uint32_t>(p->stream_buf, p->A, ok);
-    uint32_t* inv = need<uint32_t>(p->inv, EF, ok);
-    uint16_t* info = need<uint16_t>(p->info16, EF, ok);
-    uint16_t* rank16 = need<uint16_t>(p->rank16, EF, ok);
+    // the dense [E][F] sample-major arrays (not needed by the sparse passes)
+    uint32_t* inv = sparse ? nullptr : need<uint32_t>(p->inv, EF, ok);
+    uint16_t* info = sparse ? nullptr : need<uint16_t>(p->info16, EF, ok);
+    uint16_t* rank16 = sparse ? nullptr : need<uint16_t>(p->rank16, EF, ok);
     uint32_t* pcount = need<uint32_t>(p->pair_count, F, ok);
     uint64_t* poff = need<uint64_t>(p->pair_off, (uint64_t)F + 1, ok);
     uint32_t* seghist = need<uint32_t>(p->seghist, NEE, ok);
@@ -742,10 +747,6 @@ int build_seed_path_v2(clairplan_plan* p, const uint32_t* ext_perms,
     unsigned long long* wsum = need<unsigned long long>(p->wsum, nloc, ok);
     uint32_t* wcnt = need<uint32_t>(p->wcnt, (uint64_t)nloc + 1, ok);  // + the negative-size flag
     uint32_t* wneg = wcnt + nloc;
-    // sparse sample-major passes (sharded handle fed by the all-to-all; CLAIRPLAN_DENSE=1: A/B)
-    const char* dense_env = getenv("CLAIRPLAN_DENSE");  // "1": dense, "0": sparse, unset: cost model
-    const bool sparse = ext_streams && (dense_env ? dense_env[0] == '0' && sparse_path_fits(part)
-                                                  : sparse_path_ok(part, p->A));
     p->sparse = sparse;
     uint32_t *sp_cnt = nullptr, *sp_cur = nullptr, *sp_csr = nullptr;
     uint64_t *sp_koff = nullptr, *sp_soff = nullptr;

@@ -113,12 +113,15 @@ __global__ void __launch_bounds__(kThreads) sparse_sample_kernel(
             }
         }
         __syncwarp();
-        const uint32_t word = lane < W ? bm[lane] : 0u;
+        // bitmap words: lane l holds word l (W <= 32) or words 2l, 2l+1 (W <= 64)
+        const bool two = W > 32;
+        const uint32_t w0 = two ? (2 * lane < W ? bm[2 * lane] : 0u) : (lane < W ? bm[lane] : 0u);
+        const uint32_t w1 = two && 2 * lane + 1 < W ? bm[2 * lane + 1] : 0u;
         uint32_t pre = 0, total;
         if (W == 1) {
-            total = __shfl_sync(0xffffffffu, __popc(word), 0);
+            total = __shfl_sync(0xffffffffu, __popc(w0), 0);
         } else {
-            const uint32_t c = __popc(word);
+            const uint32_t c = __popc(w0) + __popc(w1);
             uint32_t inc = c;
 #pragma unroll
             for (int d = 1; d < 32; d <<= 1) {
@@ -142,8 +145,13 @@ __global__ void __launch_bounds__(kThreads) sparse_sample_kernel(
         for (int r = 0; r < R; ++r) {
             const uint32_t x = xv[r];
             const uint32_t xw = x != kNone ? x >> 5 : 0u;
-            const uint32_t pw = W == 1 ? 0u : __shfl_sync(0xffffffffu, pre, xw);
-            const uint32_t ww = W == 1 ? __shfl_sync(0xffffffffu, word, 0) : __shfl_sync(0xffffffffu, word, xw);
+            const uint32_t src = two ? xw >> 1 : xw;
+            const uint32_t a0 = __shfl_sync(0xffffffffu, w0, W == 1 ? 0u : src);
+            const uint32_t a1 = __shfl_sync(0xffffffffu, w1, src);
+            const uint32_t pl = W == 1 ? 0u : __shfl_sync(0xffffffffu, pre, src);
+            const bool hi = two && (xw & 1u);
+            const uint32_t ww = hi ? a1 : a0;
+            const uint32_t pw = pl + (hi ? __popc(a0) : 0u);
             if (x != kNone) {
                 uint16_t ci = 0, rk = 0xFFFFu;
                 if (fs[x] == sv[r]) {
@@ -267,17 +275,22 @@ void launch_sparse_csr(cudaStream_t s, const Part& part, const uint32_t* stream,
 }
 
 uint64_t csr_windows(uint64_t n) {
-    return std::max<uint64_t>(1, (n * 4 + (48ull << 20) - 1) / (48ull << 20));
+    const uint64_t w = std::max<uint64_t>(1, (n * 4 + (48ull << 20) - 1) / (48ull << 20));
+    return w <= 16 ? w : 1;  // a CSR of many L2 sizes: one pass (the writes miss L2 anyway)
 }
 
 // Sparse passes when they beat the dense E*F ones (B200, config 2 sharded 2/4/8 ways: dense
 // ~16 ps per (epoch, sample) cell — inverse rebuild, sample and holder passes; sparse ~55 ps
 // per local entry — CSR build, sparse sample and holder passes — growing with the windows).
-bool sparse_path_fits(const Part& part) { return (part.wend - part.wbegin) <= 1024 && part.E <= 128; }
+bool sparse_path_fits(const Part& part) { return (part.wend - part.wbegin) <= 2048 && part.E <= 128; }
 
 bool sparse_path_ok(const Part& part, uint64_t local_entries) {
     if (!sparse_path_fits(part)) return false;
-    const double sparse = (double)local_entries * (40.0 + 5.0 * (double)csr_windows(local_entries));
+    // the dense inverse / info / rank arrays (8 B per (epoch, sample) cell) would crowd HBM
+    if ((double)part.E * (double)part.F * 8.0 > 40e9) return true;
+    const uint64_t W = csr_windows(local_entries);
+    const double sparse = (double)local_entries * (W == 1 && local_entries * 4 > (48ull << 20) ? 120.0
+                                                                                             : 40.0 + 5.0 * (double)W);
     const double dense = 16.0 * (double)part.E * (double)part.F;
     return sparse < dense;
 }

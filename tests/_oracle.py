@@ -166,6 +166,8 @@ class Ref:
         L.ref_plan_build_subset.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
                                             C.c_uint32, C.c_int, C.c_uint32, f64p, f64p, C.c_int,
                                             u32p, C.c_uint32]
+        L.ref_plan_build_subset_lowmem.restype = C.c_void_p
+        L.ref_plan_build_subset_lowmem.argtypes = L.ref_plan_build_subset.argtypes
         L.ref_assign_from_streams.restype = C.c_void_p
         L.ref_assign_from_streams.argtypes = [C.c_uint32, C.c_uint32, u32p, u64p, u32p,
                                               C.c_uint32, f64p, f64p]
@@ -267,6 +269,18 @@ class Ref:
         h = self.L.ref_plan_build_subset(seed, F, N, B, E, int(drop_last), len(caps),
                                          _ptr(caps, f64p), _ptr(sizes, f64p), threads,
                                          _ptr(ws, u32p), len(ws))
+        if not h:
+            raise ValueError(self.err())
+        return self._collect(h, N, len(caps), F)
+
+    def plan_subset_lowmem(self, seed, F, N, B, E, drop_last, caps, sizes, workers, threads):
+        """Worker-subset plan that never holds all permutations (config 5)."""
+        caps = np.ascontiguousarray(caps, np.float64)
+        sizes = np.ascontiguousarray(sizes, np.float64)
+        ws = np.ascontiguousarray(workers, np.uint32)
+        h = self.L.ref_plan_build_subset_lowmem(seed, F, N, B, E, int(drop_last), len(caps),
+                                                _ptr(caps, f64p), _ptr(sizes, f64p), threads,
+                                                _ptr(ws, u32p), len(ws))
         if not h:
             raise ValueError(self.err())
         return self._collect(h, N, len(caps), F)

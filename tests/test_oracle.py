@@ -118,6 +118,23 @@ def test_reference_per_worker_harness_matches_verbatim(ref, case):
     assert plans_equal(a, b) is None
 
 
+@pytest.mark.parametrize("case", CASES[:4])
+def test_reference_lowmem_subset_harness(ref, case):
+    """The epoch-by-epoch subset harness (config 5 checks) == the subset harness: subset
+    streams, class lists and the subset-restricted holder CSR."""
+    seed, F, N, B, E, dl, caps, (mu, sd) = case
+    sizes = ref.generate_sizes(F, mu, sd, None, 1)
+    subset = np.array(sorted({0, N - 1, N // 2}), np.uint32)
+    a = ref.plan_subset(seed, F, N, B, E, dl, caps, sizes, subset, 4)
+    b = ref.plan_subset_lowmem(seed, F, N, B, E, dl, caps, sizes, subset, 4)
+    for w in subset:
+        assert np.array_equal(a.streams[w], b.streams[w])
+        for j in range(len(caps)):
+            assert np.array_equal(a.class_lists[w][j], b.class_lists[w][j])
+    assert np.array_equal(a.holder_offsets, b.holder_offsets)
+    assert np.array_equal(a.holders, b.holders)
+
+
 def test_port_generic_assign_matches_reference(port, ref):
     # test_policies.cpp:54-67: hand-built stream, counts {5, 2}, class 1 fits one sample
     streams = [np.array([0, 1, 0, 0, 1, 0, 0], np.uint32)]
