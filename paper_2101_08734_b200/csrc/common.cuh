@@ -115,6 +115,7 @@ struct Part {
     uint32_t wbegin, wend;           // worker range of this handle
     uint64_t off0;                   // stream_offset(wbegin)
     uint32_t ebase;                  // first epoch held in the stream (epoch-range streams)
+    uint32_t pow2, lgB, lgBase;      // B and base powers of two, no remainder, no tail: shifts
     FastDiv dB, dFull1, dFull0, dTail1, dTail0;  // B, base+1, base, tbase+1, tbase
 
     __host__ __device__ uint64_t len(uint32_t w) const { return base + (w < extra ? 1 : 0); }
@@ -135,6 +136,13 @@ struct Part {
     // perm position p (< P < 2^32) of epoch e -> worker and position within its stream
     __host__ __device__ __forceinline__ void slice_of(uint32_t p, uint32_t& w, uint32_t& h,
                                                       uint32_t& off) const {
+        if (pow2) {  // every slice is `base` long: shifts and masks
+            h = p >> lgB;
+            const uint32_t o = p & (B - 1);
+            w = o >> lgBase;
+            off = o & ((1u << lgBase) - 1);
+            return;
+        }
         h = dB.div(p);
         const uint32_t o = p - h * B;
         const bool tl = h >= full;
@@ -199,6 +207,15 @@ inline Part make_part(uint32_t F, uint32_t N, uint32_t B, uint32_t E, bool drop_
     p.off0 = 0;
     p.ebase = 0;
     p.off0 = p.stream_offset(wbegin);
+    auto lg = [](uint64_t v) {
+        uint32_t l = 0;
+        while ((1ull << l) < v) ++l;
+        return l;
+    };
+    p.lgB = lg(B);
+    p.lgBase = lg(p.base);
+    p.pow2 = (p.extra == 0 && p.tail == 0 && p.base >= 1 && (1ull << p.lgB) == B &&
+              (1ull << p.lgBase) == p.base) ? 1u : 0u;
     return p;
 }
 

@@ -787,6 +787,14 @@ int build_seed_path_v2(clairplan_plan* p, const uint32_t* ext_perms,
             return rc;
         }
         p->mark(1);
+        if (p->x_streams) {
+            // build_export: the streams are final (unless a Lemire rejection turns up at the
+            // check below; the retry then issues a second copy behind this one on the same
+            // stream), so copy them out while the rest of the plan builds
+            CK(cudaEventRecord(p->xev, s));
+            CK(cudaStreamWaitEvent(p->xstream, p->xev, 0));
+            CK(cudaMemcpyAsync(p->x_streams, stream_buf, p->A * 4, cudaMemcpyDeviceToHost, p->xstream));
+        }
         // K4a: per-sample (worker, count, first epoch)
         // Large F: the segment histograms are accumulated by the sample pass itself (REDs
         // overlap its latency); small F: a separate warp-per-segment pass is cheaper.
@@ -834,11 +842,6 @@ int build_seed_path_v2(clairplan_plan* p, const uint32_t* ext_perms,
         bool any = false;
         if (int rc = resolve_rejections(p, flags, &any)) return rc;
         if (any) continue;
-        if (p->x_streams) {  // build_export: the streams are final, copy them out meanwhile
-            CK(cudaEventRecord(p->xev, s));
-            CK(cudaStreamWaitEvent(p->xstream, p->xev, 0));
-            CK(cudaMemcpyAsync(p->x_streams, stream_buf, p->A * 4, cudaMemcpyDeviceToHost, p->xstream));
-        }
         // all-fit test (host); otherwise K4b: per-segment count histograms -> first-order and
         // tier-order bases
         bool allfit = false;
