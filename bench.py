@@ -198,6 +198,9 @@ def run_ours(args, cfg):
 
         def build():
             dplan.build()
+
+        def dplan_timings():  # host wall time of the last build's phases on this rank
+            return dict(dplan.timings)
     else:
         plan = cp.Plan(SEED, cfg["F"], part, list(CAPS), sizes, device=local, worker_range=(wb, we))
 
@@ -319,6 +322,7 @@ def run_ours(args, cfg):
                          "peak_kind": f"{peak_kind} copy bandwidth x {world}",
                          "dominant_stage": dominant_stage(stage_ms, A_loc, hbm)},
             "stages_ms": stage_ms,
+            "rank0_phases_ms": (dplan_timings() if world > 1 else None),
             "e2e": e2e,
             "cpu_baseline": cpu,
             "gpu_launches": launches,

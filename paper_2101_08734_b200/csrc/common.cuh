@@ -116,6 +116,7 @@ struct Part {
     uint64_t off0;                   // stream_offset(wbegin)
     uint32_t ebase;                  // first epoch held in the stream (epoch-range streams)
     uint32_t pow2, lgB, lgBase;      // B and base powers of two, no remainder, no tail: shifts
+    uint32_t Fp;                     // row pitch of the u16 [E][F] arrays (info, rank): F to 8
     FastDiv dB, dFull1, dFull0, dTail1, dTail0;  // B, base+1, base, tbase+1, tbase
 
     __host__ __device__ uint64_t len(uint32_t w) const { return base + (w < extra ? 1 : 0); }
@@ -214,6 +215,7 @@ inline Part make_part(uint32_t F, uint32_t N, uint32_t B, uint32_t E, bool drop_
     };
     p.lgB = lg(B);
     p.lgBase = lg(p.base);
+    p.Fp = (F + 7u) & ~7u;
     p.pow2 = (p.extra == 0 && p.tail == 0 && p.base >= 1 && (1ull << p.lgB) == B &&
               (1ull << p.lgBase) == p.base) ? 1u : 0u;
     return p;

@@ -114,8 +114,8 @@ __global__ void __launch_bounds__(128) sample_lanes_kernel(Part part, const uint
                     // per-(worker, epoch) segment histogram of first accesses by count
                     if (seghist) atomicAdd(&seghist[((uint64_t)wl * E + (E - c)) * E + e], 1u);
                 }
-                __stcs(info + (size_t)e * F + k, c);
-                __stcs(rank16 + (size_t)e * F + k, rk);
+                __stcs(info + (size_t)e * part.Fp + k, c);
+                __stcs(rank16 + (size_t)e * part.Fp + k, rk);
             }
         }
         for (uint32_t t = 0; t < W; ++t) bm[t * 32 + lane] = 0;
@@ -217,8 +217,8 @@ __global__ void __launch_bounds__(128) sample_hash_kernel(Part part, const uint3
                     }
                 }
             }
-            info[(size_t)e * F + k] = out;
-            rank16[(size_t)e * F + k] = rk;
+            info[(size_t)e * part.Fp + k] = out;
+            rank16[(size_t)e * part.Fp + k] = rk;
         }
         __syncwarp();
         for (uint32_t t = lane; t < hs; t += 32) keys[t] = kNone;
@@ -261,7 +261,7 @@ __global__ void __launch_bounds__(kThreads) seg_hist_kernel(Part part, const uin
         __syncwarp();
         const uint64_t Le = part.epoch_len(w);
         const uint64_t g0 = part.stream_offset(w) + (uint64_t)e * Le;
-        const uint16_t* row = info + (size_t)e * part.F;
+        const uint16_t* row = info + (size_t)e * part.Fp;
         uint32_t tot = 0;
         double ssum = 0.0, smin = INFINITY;
         for (uint64_t t0 = 0; t0 < Le; t0 += 32 * kSU) {
@@ -379,7 +379,7 @@ __global__ void __launch_bounds__(kThreads) seg_allfit_kernel(
         const uint64_t t_hi = t_lo + kAllfitChunk < Le ? t_lo + kAllfitChunk : Le;
         const uint64_t sw = part.stream_offset(w);
         const uint64_t g0 = sw + (uint64_t)e * Le;
-        const uint16_t* row = info + (size_t)e * part.F;
+        const uint16_t* row = info + (size_t)e * part.Fp;
         const uint64_t x = ((uint64_t)wl * E + e) * C + ci;  // worker-major chunk index
         // pass A: first-access ballots, lane b keeps block b's
         uint32_t mymask = 0, tot = 0;
@@ -502,7 +502,7 @@ __global__ void __launch_bounds__(kThreads) seg_write_kernel2(
         __syncwarp();
         const uint64_t Le = part.epoch_len(w);
         const uint64_t g0 = part.stream_offset(w) + (uint64_t)e * Le;
-        const uint16_t* row = info + (size_t)e * part.F;
+        const uint16_t* row = info + (size_t)e * part.Fp;
         const uint64_t fbase = seg_off[(uint64_t)wl * E + e];
         const uint64_t* sbase = sorted_base + (uint64_t)wl * E * E + e;  // + (E-c)*E
         const uint64_t blk0 = ((uint64_t)wl * E + e) * MB;
@@ -740,7 +740,7 @@ __global__ void __launch_bounds__(kThreads) holder_tile_kernel(
                 const uint32_t e = idx >> 5, l = idx & 31;
                 const bool ok = idx < E * 32 && k0 + l < F;
                 iv[u] = ok ? __ldcs(inv + (size_t)e * F + k0 + l) : kNone;
-                rv[u] = ok ? __ldcs(rank16 + (size_t)e * F + k0 + l) : (uint16_t)0xFFFFu;
+                rv[u] = ok ? __ldcs(rank16 + (size_t)e * part.Fp + k0 + l) : (uint16_t)0xFFFFu;
             }
 #pragma unroll
             for (int u = 0; u < TU; ++u) {
@@ -1000,13 +1000,26 @@ __global__ void __launch_bounds__(kThreads) sample_tile_kernel(Part part, const 
             __syncwarp();
         }
         __syncthreads();
-        // coalesced write-back of the info / rank rows (u16 pairs)
+        // coalesced write-back of the info / rank rows: 16-B stores of 8 samples (the rows
+        // are pitched to Fp, a multiple of 8 samples), scalar for a partial last tile
         const uint32_t n = (uint32_t)(F - k0 < 32 ? F - k0 : 32);
-        for (uint32_t idx = threadIdx.x; idx < E * 32; idx += blockDim.x) {
-            const uint32_t e = idx >> 5, l = idx & 31;
-            if (l < n) {
-                __stcs(info + (size_t)e * F + k0 + l, oinfo[e * kStOut + l]);
-                __stcs(rank16 + (size_t)e * F + k0 + l, orank[e * kStOut + l]);
+        if (n == 32) {
+            for (uint32_t idx = threadIdx.x; idx < E * 4; idx += blockDim.x) {
+                const uint32_t e = idx >> 2, q = (idx & 3) * 8;
+                const uint32_t* si = reinterpret_cast<const uint32_t*>(oinfo + e * kStOut + q);
+                const uint32_t* sr = reinterpret_cast<const uint32_t*>(orank + e * kStOut + q);
+                __stcs(reinterpret_cast<uint4*>(info + (size_t)e * part.Fp + k0 + q),
+                       make_uint4(si[0], si[1], si[2], si[3]));
+                __stcs(reinterpret_cast<uint4*>(rank16 + (size_t)e * part.Fp + k0 + q),
+                       make_uint4(sr[0], sr[1], sr[2], sr[3]));
+            }
+        } else {
+            for (uint32_t idx = threadIdx.x; idx < E * 32; idx += blockDim.x) {
+                const uint32_t e = idx >> 5, l = idx & 31;
+                if (l < n) {
+                    __stcs(info + (size_t)e * part.Fp + k0 + l, oinfo[e * kStOut + l]);
+                    __stcs(rank16 + (size_t)e * part.Fp + k0 + l, orank[e * kStOut + l]);
+                }
             }
         }
         // the output tile and the input buffer are reused after the next barrier

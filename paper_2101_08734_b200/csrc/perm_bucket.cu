@@ -299,9 +299,7 @@ __global__ void __launch_bounds__(kBlockThreads) fyb_block_kernel(uint32_t F, Fy
     extern __shared__ uint32_t sm[];
     __shared__ uint32_t wsum[kBlockThreads / 32];
     __shared__ uint32_t s_pool;
-    // epochs in reverse: fyb_tile wrote the last epochs' buckets most recently (still in L2),
-    // and fyb_emit (forward) then starts on the q / succ rows written last here
-    const uint32_t b = blockIdx.x, slot = gridDim.y - 1 - blockIdx.y;
+    const uint32_t b = blockIdx.x, slot = blockIdx.y;
     const uint32_t TB = 1u << g.lgTB;
     const uint32_t tmin = (uint32_t)(((uint64_t)b << g.lgTB) >> g.lgTS);
     const uint32_t nt = g.NT - tmin;

@@ -731,8 +731,9 @@ int build_seed_path_v2(clairplan_plan* p, const uint32_t* ext_perms,
     uint32_t* stream_buf = need<uint32_t>(p->stream_buf, p->A, ok);
     // the dense [E][F] sample-major arrays (not needed by the sparse passes)
     uint32_t* inv = sparse ? nullptr : need<uint32_t>(p->inv, EF, ok);
-    uint16_t* info = sparse ? nullptr : need<uint16_t>(p->info16, EF, ok);
-    uint16_t* rank16 = sparse ? nullptr : need<uint16_t>(p->rank16, EF, ok);
+    const uint64_t EFp = (uint64_t)E * part.Fp;  // pitched u16 rows
+    uint16_t* info = sparse ? nullptr : need<uint16_t>(p->info16, EFp, ok);
+    uint16_t* rank16 = sparse ? nullptr : need<uint16_t>(p->rank16, EFp, ok);
     uint32_t* pcount = need<uint32_t>(p->pair_count, F, ok);
     uint64_t* poff = need<uint64_t>(p->pair_off, (uint64_t)F + 1, ok);
     uint32_t* seghist = need<uint32_t>(p->seghist, NEE, ok);

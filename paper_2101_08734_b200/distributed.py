@@ -168,11 +168,15 @@ class DistributedPlan:
             cp._check(self.L.clairplan_build_from_perms(self.plan._h,
                                                         C.c_void_p(perms.data_ptr())))
             del perms
+        t4 = time.perf_counter()
         cp._check(self.L.clairplan_holder_counts(self.plan._h, C.c_void_p(self.counts.data_ptr())))
         allc = torch.empty((self.world, self.samples), dtype=torch.int32, device="cuda")
         self.dist.all_gather_into_tensor(allc, self.counts, group=self.group)
         self.global_offsets, starts = holder_offsets_from_counts(allc)
         self.rank_starts = starts[self.rank]
+        if self.mode == "streams":
+            torch.cuda.current_stream().synchronize()
+            self.timings["merge_ms"] = round((time.perf_counter() - t4) * 1e3, 3)
         return self
 
     def stats(self):
