@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(kTileThreads) fyb_tile_kernel(uint64_t key, ui
 //    inv[y] = last writer; targets whose list is empty get q = kNone
 // BIG: more writers than the shared-memory capacity (blocks of small targets): W/J/nxt live
 // in a global pool slab (L2-resident) instead.
-template <bool BIG>
+template <bool BIG, uint32_t BT>
 __device__ __forceinline__ void fyb_block_body(uint32_t F, const FyGeom& g, uint32_t b, uint32_t n,
                                                uint32_t nt, uint32_t tmin, const uint32_t* rsrc,
                                                const uint32_t* rdst, uint32_t* head, uint32_t* W,
@@ -207,7 +207,7 @@ __device__ __forceinline__ void fyb_block_body(uint32_t F, const FyGeom& g, uint
     constexpr uint32_t kEnd = BIG ? kNone : 0xFFFFu;
     // each warp gathers a contiguous range of the block's elements, 32 at a time; one
     // warp-uniform binary search finds the run of its first element, later chunks advance it
-    constexpr uint32_t NW = kBlockThreads / 32;
+    constexpr uint32_t NW = BT / 32;
     const uint32_t xa = (uint32_t)(((uint64_t)n * warp) / NW), xb = (uint32_t)(((uint64_t)n * (warp + 1)) / NW);
     uint32_t r0 = 0;
     if (xa < xb) {
@@ -262,12 +262,12 @@ __device__ __forceinline__ void fyb_block_body(uint32_t F, const FyGeom& g, uint
     }
     __syncthreads();
     const uint32_t y0 = b << g.lgTB;
-    for (uint32_t tt = threadIdx.x; tt < TB; tt += kBlockThreads) {
+    for (uint32_t tt = threadIdx.x; tt < TB; tt += BT) {
         const uint32_t y = y0 + tt;
         if (y >= F) break;
         if (head[tt] == kEnd) qq[y] = kNone;  // no writer
     }
-    for (uint32_t k = threadIdx.x; k < n; k += kBlockThreads) {
+    for (uint32_t k = threadIdx.x; k < n; k += BT) {
         const uint32_t w = W[k];
         const uint32_t jl = BIG ? J32[k] : (uint32_t)J16[k];
         bool first = true;
@@ -287,7 +287,8 @@ __device__ __forceinline__ void fyb_block_body(uint32_t F, const FyGeom& g, uint
     }
 }
 
-__global__ void __launch_bounds__(kBlockThreads) fyb_block_kernel(uint32_t F, FyGeom g,
+template <uint32_t BT>
+__global__ void __launch_bounds__(BT) fyb_block_kernel(uint32_t F, FyGeom g,
                                                                   const uint32_t* __restrict__ bucket,
                                                                   const uint32_t* __restrict__ lst,
                                                                   uint32_t* __restrict__ pool,
@@ -297,7 +298,7 @@ __global__ void __launch_bounds__(kBlockThreads) fyb_block_kernel(uint32_t F, Fy
                                                                   uint32_t e0,
                                                                   uint32_t* __restrict__ inv) {
     extern __shared__ uint32_t sm[];
-    __shared__ uint32_t wsum[kBlockThreads / 32];
+    __shared__ uint32_t wsum[BT / 32];
     __shared__ uint32_t s_pool;
     const uint32_t b = blockIdx.x, slot = blockIdx.y;
     const uint32_t TB = 1u << g.lgTB;
@@ -310,31 +311,31 @@ __global__ void __launch_bounds__(kBlockThreads) fyb_block_kernel(uint32_t F, Fy
     uint16_t* J16 = reinterpret_cast<uint16_t*>(W + g.cap);  // [cap] target within block
     uint16_t* N16 = J16 + g.cap;                              // [cap] next on the target's list
     const uint32_t* rows = lst + (size_t)slot * g.NT * (g.NB + 1);
-    for (uint32_t k = threadIdx.x; k < nt; k += kBlockThreads) {
+    for (uint32_t k = threadIdx.x; k < nt; k += BT) {
         const uint32_t* r = rows + (size_t)(tmin + k) * (g.NB + 1) + b;
         const uint32_t lo = r[0];
         rsrc[k] = ((tmin + k) << g.lgTS) + lo;
         rdst[k] = r[1] - lo;
     }
     __syncthreads();
-    const uint32_t n = blk_exscan<kBlockThreads>(rdst, nt, wsum);
+    const uint32_t n = blk_exscan<BT>(rdst, nt, wsum);
     const uint32_t* bk = bucket + (size_t)slot * F;
     uint32_t* sc = succ + (size_t)slot * F;
     uint32_t* qq = q + (size_t)slot * F;
     uint32_t* iv = inv ? inv + (size_t)(e0 + slot) * F : nullptr;
     if (n <= g.cap) {
-        for (uint32_t k = threadIdx.x; k < TB / 4; k += kBlockThreads)
+        for (uint32_t k = threadIdx.x; k < TB / 4; k += BT)
             reinterpret_cast<uint4*>(head)[k] = make_uint4(0xFFFFu, 0xFFFFu, 0xFFFFu, 0xFFFFu);
         __syncthreads();
-        fyb_block_body<false>(F, g, b, n, nt, tmin, rsrc, rdst, head, W, J16, N16, nullptr,
+        fyb_block_body<false, BT>(F, g, b, n, nt, tmin, rsrc, rdst, head, W, J16, N16, nullptr,
                               nullptr, bk, sc, qq, iv);
     } else {  // heavy block (small targets): global pool slab
-        for (uint32_t k = threadIdx.x; k < TB / 4; k += kBlockThreads)
+        for (uint32_t k = threadIdx.x; k < TB / 4; k += BT)
             reinterpret_cast<uint4*>(head)[k] = make_uint4(kNone, kNone, kNone, kNone);
         if (threadIdx.x == 0) s_pool = atomicAdd(pool_used + slot, 3 * n);
         __syncthreads();
         uint32_t* gW = pool + (size_t)slot * 4 * F + s_pool;
-        fyb_block_body<true>(F, g, b, n, nt, tmin, rsrc, rdst, head, gW, nullptr, nullptr,
+        fyb_block_body<true, BT>(F, g, b, n, nt, tmin, rsrc, rdst, head, gW, nullptr, nullptr,
                              gW + n, gW + 2 * n, bk, sc, qq, iv);
     }
 }
@@ -439,9 +440,21 @@ void launch_fyb(cudaStream_t s, uint64_t key, const Part& part, uint32_t e0, uin
     cudaMemsetAsync(pool_used, 0, ne * sizeof(uint32_t), s);
     cudaMemsetAsync(succ, 0xFF, (size_t)ne * F * sizeof(uint32_t), s);
     const size_t sm_block = fyb_block_smem(g);
-    cudaFuncSetAttribute(fyb_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_block);
-    fyb_block_kernel<<<dim3(g.NB, ne), kBlockThreads, sm_block, s>>>(F, g, bucket, lst, pool,
-                                                                      pool_used, succ, q, e0, inv);
+    static const int bt = [] {
+        const char* v = getenv("CLAIRPLAN_FYB_THREADS");  // A/B
+        return v ? atoi(v) : (int)kBlockThreads;
+    }();
+#define FYB_LAUNCH(BTV)                                                                           \
+    do {                                                                                          \
+        cudaFuncSetAttribute(fyb_block_kernel<BTV>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
+                             (int)sm_block);                                                      \
+        fyb_block_kernel<BTV><<<dim3(g.NB, ne), BTV, sm_block, s>>>(F, g, bucket, lst, pool,       \
+                                                                    pool_used, succ, q, e0, inv);  \
+    } while (0)
+    if (bt == 128) FYB_LAUNCH(128);
+    else if (bt == 512) FYB_LAUNCH(512);
+    else FYB_LAUNCH(256);
+#undef FYB_LAUNCH
     dim3 grid(grid_for(F, kThreads * 4, 148u * 16u), ne);
     static const int u = [] {
         const char* v = getenv("CLAIRPLAN_EMIT_U");  // A/B (2 measured best for config 2)

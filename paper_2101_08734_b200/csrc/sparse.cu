@@ -15,6 +15,8 @@
 //   holder_sparse            thread per CSR entry: holder records at pair_off[k] + rank from
 //                            the block records of the tier / all-fit paths
 // The CSR is written in sample windows that fit L2 (the random slot writes then merge there).
+#include <cstdlib>
+
 #include "internal.h"
 
 namespace clairplan {
@@ -275,6 +277,7 @@ void launch_sparse_csr(cudaStream_t s, const Part& part, const uint32_t* stream,
 }
 
 uint64_t csr_windows(uint64_t n) {
+    if (const char* v = getenv("CLAIRPLAN_CSR_WINDOWS")) return std::max(1, atoi(v));  // A/B
     const uint64_t w = std::max<uint64_t>(1, (n * 4 + (48ull << 20) - 1) / (48ull << 20));
     return w <= 16 ? w : 1;  // a CSR of many L2 sizes: one pass (the writes miss L2 anyway)
 }
