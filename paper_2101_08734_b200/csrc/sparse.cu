@@ -56,20 +56,33 @@ __global__ void __launch_bounds__(kThreads) csr_scatter_kernel(const uint32_t* _
                                                                uint32_t* __restrict__ cur,
                                                                uint32_t* __restrict__ csr,
                                                                uint32_t* __restrict__ cpos) {
-    for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < n;
-         s += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t k = __ldcs(stream + s);
-        if (k < k_lo || k >= k_hi) continue;
-        const uint32_t slot = atomicAdd(&cur[k], 1u);
-        csr[slot] = (uint32_t)s;
-        cpos[s] = slot;
+    // 4 entries per thread and round: their cursor atomics are independent and overlap
+    constexpr int U = 4;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t s0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s0 < n; s0 += U * stride) {
+        uint32_t k[U], slot[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t s = s0 + u * stride;
+            k[u] = s < n ? __ldcs(stream + s) : kNone;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            slot[u] = (k[u] >= k_lo && k[u] < k_hi) ? atomicAdd(&cur[k[u]], 1u) : kNone;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (slot[u] == kNone) continue;
+            const uint64_t s = s0 + u * stride;
+            csr[slot[u]] = (uint32_t)s;
+            cpos[s] = slot[u];
+        }
     }
 }
 
 // warp per sample, lanes over its entries (R rounds of 32, entries kept in registers); per-warp
 // shared tables indexed by local worker (nloc <= 32 W)
 template <int R>
-__global__ void __launch_bounds__(kThreads) sparse_sample_kernel(
+__global__ void __launch_bounds__(kThreads, 6) sparse_sample_kernel(
     uint32_t F, uint32_t nloc, uint32_t W, const uint64_t* __restrict__ soff,
     const uint64_t* __restrict__ koff, const uint32_t* __restrict__ csr,
     uint32_t* __restrict__ pair_count, uint16_t* __restrict__ einfo, uint16_t* __restrict__ erank,
@@ -104,6 +117,7 @@ __global__ void __launch_bounds__(kThreads) sparse_sample_kernel(
         uint32_t sv[R], xv[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
+            if ((uint64_t)r * 32 >= b - a) break;  // warp-uniform: only the rounds in use
             const uint64_t i = a + r * 32 + lane;
             xv[r] = kNone;
             if (i < b) {
@@ -145,6 +159,7 @@ __global__ void __launch_bounds__(kThreads) sparse_sample_kernel(
         }
 #pragma unroll
         for (int r = 0; r < R; ++r) {
+            if ((uint64_t)r * 32 >= b - a) break;  // warp-uniform: only the rounds in use
             const uint32_t x = xv[r];
             const uint32_t xw = x != kNone ? x >> 5 : 0u;
             const uint32_t src = two ? xw >> 1 : xw;
@@ -172,6 +187,7 @@ __global__ void __launch_bounds__(kThreads) sparse_sample_kernel(
         __syncwarp();
 #pragma unroll
         for (int r = 0; r < R; ++r) {
+            if ((uint64_t)r * 32 >= b - a) break;  // warp-uniform: only the rounds in use
             if (xv[r] != kNone) {
                 fs[xv[r]] = kNone;
                 cnt[xv[r]] = 0;
@@ -267,7 +283,8 @@ void launch_sparse_csr(cudaStream_t s, const Part& part, const uint32_t* stream,
     csr_hist_kernel<<<grid_for(n, kThreads, 148u * 16u), kThreads, 0, s>>>(stream, n, cnt);
     exclusive_scan(s, cnt, F, koff, ws);
     csr_cursor_kernel<<<grid_for(F, kThreads), kThreads, 0, s>>>(koff, F, cur);
-    // sample windows of ~48 MB of CSR (samples are uniform over the entries)
+    // sample windows of ~64 MB of CSR (samples are uniform over the entries; 64 MB measured
+    // best at 115 MB of CSR: 2 windows 1.24 ms, 1 window 1.42, 3 windows 1.29)
     const uint64_t windows = csr_windows(n);
     for (uint64_t j = 0; j < windows; ++j) {
         const uint32_t lo = (uint32_t)(F * j / windows), hi = (uint32_t)(F * (j + 1) / windows);
@@ -278,7 +295,7 @@ void launch_sparse_csr(cudaStream_t s, const Part& part, const uint32_t* stream,
 
 uint64_t csr_windows(uint64_t n) {
     if (const char* v = getenv("CLAIRPLAN_CSR_WINDOWS")) return std::max(1, atoi(v));  // A/B
-    const uint64_t w = std::max<uint64_t>(1, (n * 4 + (48ull << 20) - 1) / (48ull << 20));
+    const uint64_t w = std::max<uint64_t>(1, (n * 4 + (64ull << 20) - 1) / (64ull << 20));
     return w <= 16 ? w : 1;  // a CSR of many L2 sizes: one pass (the writes miss L2 anyway)
 }
 
@@ -292,7 +309,7 @@ bool sparse_path_ok(const Part& part, uint64_t local_entries) {
     // the dense inverse / info / rank arrays (8 B per (epoch, sample) cell) would crowd HBM
     if ((double)part.E * (double)part.F * 8.0 > 40e9) return true;
     const uint64_t W = csr_windows(local_entries);
-    const double sparse = (double)local_entries * (W == 1 && local_entries * 4 > (48ull << 20) ? 120.0
+    const double sparse = (double)local_entries * (W == 1 && local_entries * 4 > (64ull << 20) ? 120.0
                                                                                              : 40.0 + 5.0 * (double)W);
     const double dense = 16.0 * (double)part.E * (double)part.F;
     return sparse < dense;

@@ -56,6 +56,18 @@ def holder_offsets_from_counts(counts):
     return glob, glob[:-1].unsqueeze(0) + before
 
 
+def rank_offsets_from_counts(counts, rank):
+    """holder_offsets_from_counts for one rank: (global_offsets[F+1], rank_starts[F]) with a
+    few kernels over the [world, F] counts (no [world, F] int64 intermediates)."""
+    import torch
+    tot = counts.sum(dim=0, dtype=torch.int64)
+    glob = torch.zeros(counts.shape[1] + 1, dtype=torch.int64, device=counts.device)
+    torch.cumsum(tot, dim=0, out=glob[1:])
+    if rank == 0:
+        return glob, glob[:-1]
+    return glob, glob[:-1] + counts[:rank].sum(dim=0, dtype=torch.int64)
+
+
 def stream_splits(prefix, ranges, wranges, rank):
     """All-to-all split sizes (u32 entries) of the epoch-range streams.
     prefix[w] = stream entries per epoch of workers < w; ranges[r] = (first epoch, count) of
@@ -172,8 +184,7 @@ class DistributedPlan:
         cp._check(self.L.clairplan_holder_counts(self.plan._h, C.c_void_p(self.counts.data_ptr())))
         allc = torch.empty((self.world, self.samples), dtype=torch.int32, device="cuda")
         self.dist.all_gather_into_tensor(allc, self.counts, group=self.group)
-        self.global_offsets, starts = holder_offsets_from_counts(allc)
-        self.rank_starts = starts[self.rank]
+        self.global_offsets, self.rank_starts = rank_offsets_from_counts(allc, self.rank)
         if self.mode == "streams":
             torch.cuda.current_stream().synchronize()
             self.timings["merge_ms"] = round((time.perf_counter() - t4) * 1e3, 3)

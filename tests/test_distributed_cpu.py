@@ -13,7 +13,8 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from paper_2101_08734_b200.distributed import (epoch_ranges, gather_rows,
-                                               holder_offsets_from_counts, stream_splits,
+                                               holder_offsets_from_counts,
+                                               rank_offsets_from_counts, stream_splits,
                                                worker_range)
 
 
@@ -54,6 +55,9 @@ def _worker(rank, world, port, q):
         dist.all_gather(allc, counts)
         glob, starts = holder_offsets_from_counts(torch.stack(allc))
         ok_glob = np.array_equal(glob.numpy(), whole.holder_offsets.astype(np.int64))
+        g2, s2 = rank_offsets_from_counts(torch.stack(allc), rank)
+        ok_glob &= np.array_equal(g2.numpy(), glob.numpy()) and np.array_equal(
+            s2.numpy(), starts[rank].numpy())
         # place this rank's records at their global positions: must equal the global slice
         pos = starts[rank].numpy()[mine_k] + (np.arange(len(mine_k)) -
                                              np.repeat(np.cumsum(counts.numpy()) - counts.numpy(),
