@@ -123,30 +123,6 @@ __global__ void holder_compact_kernel(const uint64_t* __restrict__ pair_off, uin
     }
 }
 
-// dense counts of one worker (FrequencyTable::counts, access.cpp:80-88) from its pairs
-__global__ void dense_counts_kernel(const uint32_t* __restrict__ cand_k,
-                                    const uint32_t* __restrict__ cand_info, uint64_t b,
-                                    uint64_t L, uint32_t* __restrict__ counts) {
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < L;
-         i += (uint64_t)gridDim.x * blockDim.x)
-        counts[cand_k[b + i]] = cand_info[b + i] >> 16;
-}
-
-__global__ void count_nonzero_kernel(const uint8_t* __restrict__ a, uint64_t n,
-                                     unsigned long long* __restrict__ out) {
-    uint32_t c = 0;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-         i += (uint64_t)gridDim.x * blockDim.x)
-        c += a[i] != 0;
-    c = warp_sum(c);
-    if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, (unsigned long long)c);
-}
-
-void launch_count_nonzero(cudaStream_t s, const uint8_t* a, uint64_t n, unsigned long long* out) {
-    cudaMemsetAsync(out, 0, sizeof(unsigned long long), s);
-    count_nonzero_kernel<<<grid_for(n, kThreads * 8, 148u * 8u), kThreads, 0, s>>>(a, n, out);
-}
-
 __global__ void stream_hist_kernel(const uint32_t* __restrict__ st, uint64_t n,
                                    uint32_t* __restrict__ counts) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
@@ -204,10 +180,6 @@ void launch_holder_compact(cudaStream_t s, const uint64_t* pair_off, uint32_t F,
                            const uint32_t* tmp, const uint64_t* hoff, uint32_t* holders) {
     holder_compact_kernel<<<grid_for(F, kThreads), kThreads, 0, s>>>(pair_off, F, tmp, hoff,
                                                                      holders);
-}
-void launch_dense_counts(cudaStream_t s, const uint32_t* cand_k, const uint32_t* cand_info,
-                         uint64_t b, uint64_t L, uint32_t* counts) {
-    dense_counts_kernel<<<grid_for(L, kThreads), kThreads, 0, s>>>(cand_k, cand_info, b, L, counts);
 }
 
 }  // namespace clairplan

@@ -1,27 +1,32 @@
 // Seed-path kernels of the plan build after the permutations (K4-K8), v2.
 //
 // Data layout (one handle = a worker range [wb, we), nloc workers):
-//   inv   [E][F] u32   position of sample k in epoch e's permutation (K3 output)
-//   info  [E][F] u16   access count of (w,k) at the epoch of its first access, else 0
+//   inv   [E][F]  u32  position of sample k in epoch e's permutation (K3 output)
+//   info  [E][Fp] u16  access count of (w,k) at the epoch of its first access, else 0
+//   rank  [E][Fp] u16  rank of w among k's workers at that access, else 0xFFFF
+//                      (Fp = F rounded up to 8: 16-B aligned rows)
 //   stream         u32 worker-major access streams; segment (w,e) = worker w's epoch e,
 //                      contiguous, length Le(w); split into 32-entry blocks
 //                      blk(w,e,t) = ((w-wb)*E + e)*MB + t/32, MB = ceil(max Le / 32)
 //   candidates     per worker in first-access order ("first order", c)   -- dest[c]
 //   sorted         per worker in tier order (count desc, first asc)      -- sorted_size[s]
 //   block records  blkmask/blkbase (first-access bits, first-order index of the first one),
-//                  np class bit-planes and per-class prefix counts
+//                  np class bit-planes and per-class prefix counts; all-fit path: uint2
+//                  {first-access mask, worker-local first-order index}
 //
-// K4a sample_lanes   lane = sample: per-lane worker bitmap in shared memory (conflict-free
-//                    [word][lane] layout) gives first accesses and the distinct count; the
-//                    few repeated workers go to a short per-lane list for their counts.
-// K4b seg_hist       per (w,e) segment: histogram of first accesses by count
+// K4a sample_tile    CTA = 32 samples, warp per sample, lanes = epochs; per-warp shared
+//                    tables (first epoch, count, worker bitmap) -> info / rank, pair counts,
+//                    per-worker candidate size sums (all-fit test).  sample_lanes /
+//                    sample_hash: fallbacks for nloc > 1024 or E > 128.
+// all-fit seg_allfit one pass: class-1 lists + block records, decoupled look-back (§4.3)
+// K4b seg_hist       per (w,e) segment: histogram of first accesses by count (tier path)
 // K4c seg_write      per segment: first-order index, tier-order index (stable counting sort
 //                    by count desc = policies.cpp:157-160), sizes gathered in tier order,
 //                    block first-masks
 // K7  blk_codes      class bit-planes + per-class counts per block (after first fit)
 //     class_write    prefetch-ordered class lists (policies.cpp:31-36,162)
-// K8  holder_lanes   lane = sample again: holders written in worker order at the pair slot
-//                    (build_index, policies.cpp:124-142) from the L2-resident block records
+// K8  holder_tile    CTA = 32 samples, warp per sample: holders written in worker order at
+//                    the pair slot (build_index, policies.cpp:124-142) from the block records
 #include <math.h>
 #include <stdlib.h>
 
@@ -238,15 +243,12 @@ constexpr int kSU = 4;
 // seghist[(wl*E + (E - c))*E + e] = first accesses with count c in segment (w, e)
 // With `sizes`: also the sum and minimum of the sizes of the segment's first accesses
 // (segsum/segmin), the input of the whole-worker fit test (fit_check_kernel).
-// HIST = false: only the per-segment first-access totals (and sums), no count histogram
-template <bool HIST>
+// seghist[(wl*E + (E - c))*E + e] = first accesses with count c in segment (w, e)
 __global__ void __launch_bounds__(kThreads) seg_hist_kernel(Part part, const uint32_t* __restrict__ stream,
-                                                             const uint16_t* __restrict__ info, const uint32_t* __restrict__ cpos,
+                                                             const uint16_t* __restrict__ info,
+                                                             const uint32_t* __restrict__ cpos,
                                                              uint32_t* __restrict__ seghist,
-                                                             uint32_t* __restrict__ segcnt,
-                                                             const double* __restrict__ sizes,
-                                                             double* __restrict__ segsum,
-                                                             double* __restrict__ segmin) {
+                                                             uint32_t* __restrict__ segcnt) {
     extern __shared__ uint32_t shist[];  // [warps][E]
     const uint32_t E = part.E, nloc = part.wend - part.wbegin;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -256,14 +258,12 @@ __global__ void __launch_bounds__(kThreads) seg_hist_kernel(Part part, const uin
          b += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
         const uint32_t e = (uint32_t)(b / nloc), wl = (uint32_t)(b - (uint64_t)e * nloc);
         const uint32_t w = part.wbegin + wl;
-        if (HIST)
-            for (uint32_t i = lane; i < E; i += 32) hist[i] = 0;
+        for (uint32_t i = lane; i < E; i += 32) hist[i] = 0;
         __syncwarp();
         const uint64_t Le = part.epoch_len(w);
         const uint64_t g0 = part.stream_offset(w) + (uint64_t)e * Le;
         const uint16_t* row = info + (size_t)e * part.Fp;
         uint32_t tot = 0;
-        double ssum = 0.0, smin = INFINITY;
         for (uint64_t t0 = 0; t0 < Le; t0 += 32 * kSU) {
             uint32_t k[kSU], c[kSU];
 #pragma unroll
@@ -271,52 +271,23 @@ __global__ void __launch_bounds__(kThreads) seg_hist_kernel(Part part, const uin
                 const uint64_t t = t0 + 32 * u + lane;
                 k[u] = t < Le ? __ldcs(stream + g0 + t) : kNone;
             }
-            double sz[kSU];
 #pragma unroll
-            for (int u = 0; u < kSU; ++u) {
+            for (int u = 0; u < kSU; ++u)
                 c[u] = k[u] == kNone ? 0u : cpos ? info[cpos[g0 + t0 + 32 * u + lane]] : row[k[u]];
-                // issued with the info gather (both depend on k only), used for first accesses
-                sz[u] = (segsum && k[u] != kNone) ? __ldg(sizes + k[u]) : 0.0;
-            }
-            if (segsum) {
-#pragma unroll
-                for (int u = 0; u < kSU; ++u) {
-                    if (c[u] != 0) {
-                        ssum += sz[u];
-                        smin = fmin(smin, sz[u]);
-                    }
-                }
-            }
 #pragma unroll
             for (int u = 0; u < kSU; ++u) {
                 const bool first = c[u] != 0;
-                if (HIST) {
-                    const uint32_t key = first ? E - c[u] : (0x80000000u | lane);
-                    const uint32_t m = __match_any_sync(0xffffffffu, key);
-                    if (first && __popc(m & lanemask_lt()) == 0) hist[key] += __popc(m);
-                }
+                const uint32_t key = first ? E - c[u] : (0x80000000u | lane);
+                const uint32_t m = __match_any_sync(0xffffffffu, key);
+                if (first && __popc(m & lanemask_lt()) == 0) hist[key] += __popc(m);
                 tot += first;
             }
             __syncwarp();
         }
         tot = warp_sum(tot);
-        if (segsum) {
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                ssum += __shfl_xor_sync(0xffffffffu, ssum, o);
-                smin = fmin(smin, __shfl_xor_sync(0xffffffffu, smin, o));
-            }
-        }
         __syncwarp();
-        if (HIST)
-            for (uint32_t i = lane; i < E; i += 32) seghist[((uint64_t)wl * E + i) * E + e] = hist[i];
-        if (lane == 0) {
-            segcnt[(uint64_t)wl * E + e] = tot;
-            if (segsum) {
-                segsum[(uint64_t)wl * E + e] = ssum;
-                segmin[(uint64_t)wl * E + e] = smin;
-            }
-        }
+        for (uint32_t i = lane; i < E; i += 32) seghist[((uint64_t)wl * E + i) * E + e] = hist[i];
+        if (lane == 0) segcnt[(uint64_t)wl * E + e] = tot;
         __syncwarp();
     }
 }
@@ -1150,16 +1121,13 @@ void launch_sample_hash(cudaStream_t s, const Part& part, const uint32_t* inv, u
         part, inv, info, rank16, pair_count, list, nlist, hs, W, seghist);
 }
 
-void launch_seg_hist(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info, const uint32_t* cpos,
-                     uint32_t* seghist, uint32_t* segcnt, const double* sizes, double* segsum,
-                     double* segmin) {
+void launch_seg_hist(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info,
+                     const uint32_t* cpos, uint32_t* seghist, uint32_t* segcnt) {
     const uint64_t nseg = (uint64_t)(part.wend - part.wbegin) * part.E;
-    const unsigned grid = grid_for(nseg * 32, kThreads, 148u * 64u);
-    // (the all-fit totals come from chunk_count_kernel; only the histogram variant is used)
     const size_t smem = (size_t)(kThreads / 32) * part.E * 4;
-    cudaFuncSetAttribute(seg_hist_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    seg_hist_kernel<true><<<grid, kThreads, smem, s>>>(part, stream, info, cpos, seghist, segcnt, sizes,
-                                                        segsum, segmin);
+    cudaFuncSetAttribute(seg_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    seg_hist_kernel<<<grid_for(nseg * 32, kThreads, 148u * 64u), kThreads, smem, s>>>(
+        part, stream, info, cpos, seghist, segcnt);
 }
 
 

@@ -171,10 +171,6 @@ void launch_holder_count(cudaStream_t s, const uint64_t* pair_off, uint32_t F, c
                          uint32_t* cnt);
 void launch_holder_compact(cudaStream_t s, const uint64_t* pair_off, uint32_t F,
                            const uint32_t* tmp, const uint64_t* hoff, uint32_t* holders);
-void launch_dense_counts(cudaStream_t s, const uint32_t* cand_k, const uint32_t* cand_info,
-                         uint64_t b, uint64_t L, uint32_t* counts);
-
-void launch_count_nonzero(cudaStream_t s, const uint8_t* a, uint64_t n, unsigned long long* out);
 void launch_stream_hist(cudaStream_t s, const uint32_t* st, uint64_t n, uint32_t* counts);
 
 // v2 seed path (fastpath.cu)
@@ -190,9 +186,8 @@ void launch_sample_hash(cudaStream_t s, const Part& part, const uint32_t* inv, u
                         const uint32_t* nlist, uint64_t max_items, uint32_t* seghist);
 void launch_segcnt(cudaStream_t s, uint32_t nloc, uint32_t E, const uint32_t* seghist,
                    uint32_t* segcnt);
-void launch_seg_hist(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info, const uint32_t* cpos,
-                     uint32_t* seghist, uint32_t* segcnt, const double* sizes = nullptr,
-                     double* segsum = nullptr, double* segmin = nullptr);
+void launch_seg_hist(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info,
+                     const uint32_t* cpos, uint32_t* seghist, uint32_t* segcnt);
 constexpr uint32_t kAllfitChunk = 1024;
 void launch_seg_allfit(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info,
                        const uint32_t* cpos, uint32_t MB, uint32_t C, unsigned long long* status,

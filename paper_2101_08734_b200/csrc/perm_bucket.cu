@@ -29,7 +29,11 @@ bool fy_geometry(uint32_t F, FyGeom& g) {
     if (F < 2 || F >= 0x80000000u) return false;
     uint32_t lgTB = 8;
     while ((1ull << lgTB) * 4096 < F) ++lgTB;
-    if (lgTB > 11) return false;  // large F: the linked-list path (perm.cu) is faster today
+    static const uint32_t max_lgtb = [] {
+        const char* v = getenv("CLAIRPLAN_FY_MAXLGTB");  // A/B: bucketed path for larger F
+        return v ? (uint32_t)atoi(v) : 11u;
+    }();
+    if (lgTB > max_lgtb) return false;  // large F: the linked-list path (perm.cu)
     if (const char* v = getenv("CLAIRPLAN_FY_LGTB")) lgTB = (uint32_t)atoi(v);
     const uint64_t TB = 1ull << lgTB;
     uint32_t lgTS = 13;
@@ -42,7 +46,7 @@ bool fy_geometry(uint32_t F, FyGeom& g) {
     g.NT = (uint32_t)((F + (1ull << lgTS) - 1) >> lgTS);
     if (g.NB > kMaxBlocks || g.NT > kMaxTiles) return false;
     // shared-memory capacity of a block's writers (larger blocks use the global pool)
-    g.cap = lgTB <= 9 ? 2048 : lgTB == 10 ? 3072 : 4096;
+    g.cap = lgTB <= 9 ? 2048 : lgTB == 10 ? 3072 : lgTB == 11 ? 4096 : 8192;
     if (const char* v = getenv("CLAIRPLAN_FY_CAP")) g.cap = (uint32_t)atoi(v);
     return true;
 }
