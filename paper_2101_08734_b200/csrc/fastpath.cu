@@ -671,8 +671,9 @@ __global__ void class_lens_kernel(uint32_t nloc, uint32_t E, uint32_t MB, uint32
 // writes its holder record {worker, class, position} at pair_off[k] + rank (build_index
 // order, workers ascending): a warp's stores land in one sample's contiguous holder range.
 // (Measured slower for config 2 and dropped: staging the records in shared memory for fully
-// contiguous stores — MIO-throttled, 2.2 vs 1.15 ms — and 4 samples per warp in flight with
-// double-buffered cp.async tiles — register-limited occupancy, 1.5-1.7 ms.)
+// contiguous stores — MIO-throttled, 2.2 vs 1.15 ms — 4 samples per warp in flight with
+// double-buffered cp.async tiles — register-limited occupancy, 1.5-1.7 ms — and the cp.async
+// double buffer alone, 1.13 vs 1.05 ms.)
 // NP: class bit-planes per record (0: runtime np); NP == -1: all-fit records (uint2 {first
 // mask, class-1 prefix}, every first access is class 1).
 __device__ __forceinline__ uint32_t pick(const uint4& a, uint32_t i) {
@@ -687,33 +688,6 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-constexpr uint32_t kHtInv = 33;  // padded row strides of the holder tiles (conflict-free
-constexpr uint32_t kHtRk = 34;   // column reads; 34 u16 keeps sample pairs 4-B aligned)
-
-// tile k0 of the inverse-permutation / rank rows -> shared buffer (cp.async, 4-B copies; the
-// rank rows are pitched (Fp even), so sample pairs are 4-B aligned in global memory too)
-__device__ __forceinline__ void ht_issue(const Part& part, const uint32_t* inv, const uint16_t* rank16,
-                                         uint64_t k0, uint32_t* tinv, uint16_t* trk) {
-    const uint32_t E = part.E, F = part.F;
-    const uint32_t n = (uint32_t)(F - k0 < 32 ? F - k0 : 32);
-    for (uint32_t idx = threadIdx.x; idx < E * 32; idx += blockDim.x) {
-        const uint32_t e = idx >> 5, l = idx & 31;
-        if (l < n) cp_async4(tinv + e * kHtInv + l, inv + (size_t)e * F + k0 + l);
-        else tinv[e * kHtInv + l] = kNone;
-    }
-    for (uint32_t idx = threadIdx.x; idx < E * 16; idx += blockDim.x) {
-        const uint32_t e = idx >> 4, l = (idx & 15) * 2;
-        const uint16_t* g = rank16 + (size_t)e * part.Fp + k0 + l;
-        if (l + 1 < n) {
-            cp_async4(trk + e * kHtRk + l, g);
-        } else {
-            trk[e * kHtRk + l] = l < n ? g[0] : (uint16_t)0xFFFFu;
-            trk[e * kHtRk + l + 1] = (uint16_t)0xFFFFu;
-        }
-    }
-    cp_async_commit();
-}
-
 template <int NP>
 __global__ void __launch_bounds__(kThreads) holder_tile_kernel(
     Part part, const uint32_t* __restrict__ inv, const uint16_t* __restrict__ rank16, uint32_t MB,
@@ -723,24 +697,34 @@ __global__ void __launch_bounds__(kThreads) holder_tile_kernel(
     extern __shared__ uint32_t sm[];
     const uint32_t E = part.E, F = part.F;
     const uint32_t np = NP > 0 ? (uint32_t)NP : np_rt;
-    const uint32_t tile_words = E * kHtInv + (E * kHtRk + 1) / 2;
+    uint32_t* tinv = sm;                                            // [E][33]
+    uint16_t* trk = reinterpret_cast<uint16_t*>(sm + (size_t)E * 33);  // [E][33]
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-    const uint64_t stride = (uint64_t)gridDim.x * 32;
-    uint64_t k0 = (uint64_t)blockIdx.x * 32;
-    if (k0 < F) ht_issue(part, inv, rank16, k0, sm, reinterpret_cast<uint16_t*>(sm + E * kHtInv));
-    for (uint32_t buf = 0; k0 < F; k0 += stride, buf ^= 1) {
-        // double buffer: the next tile's rows arrive (cp.async) while this one is processed
-        uint32_t* tinv = sm + buf * tile_words;
-        uint16_t* trk = reinterpret_cast<uint16_t*>(tinv + E * kHtInv);
-        if (k0 + stride < F) {
-            uint32_t* nx = sm + (buf ^ 1) * tile_words;
-            ht_issue(part, inv, rank16, k0 + stride, nx, reinterpret_cast<uint16_t*>(nx + E * kHtInv));
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
+    for (uint64_t k0 = (uint64_t)blockIdx.x * 32; k0 < F; k0 += (uint64_t)gridDim.x * 32) {
+        __syncthreads();
+        constexpr int TU = 4;  // rows in flight per thread
+        for (uint32_t i0 = threadIdx.x; i0 < E * 32; i0 += TU * blockDim.x) {
+            uint32_t iv[TU];
+            uint16_t rv[TU];
+#pragma unroll
+            for (int u = 0; u < TU; ++u) {
+                const uint32_t idx = i0 + u * blockDim.x;
+                const uint32_t e = idx >> 5, l = idx & 31;
+                const bool ok = idx < E * 32 && k0 + l < F;
+                iv[u] = ok ? __ldcs(inv + (size_t)e * F + k0 + l) : kNone;
+                rv[u] = ok ? __ldcs(rank16 + (size_t)e * part.Fp + k0 + l) : (uint16_t)0xFFFFu;
+            }
+#pragma unroll
+            for (int u = 0; u < TU; ++u) {
+                const uint32_t idx = i0 + u * blockDim.x;
+                if (idx < E * 32) {
+                    const uint32_t e = idx >> 5, l = idx & 31;
+                    tinv[e * 33 + l] = iv[u];
+                    trk[e * 33 + l] = rv[u];
+                }
+            }
         }
         __syncthreads();
-        bool tile_done = false;
         if constexpr (NP == -1) {
             if (E <= 128) {  // all-fit, <= 4 epoch rounds: the rounds' record loads overlap
                 for (uint32_t s = warp; s < 32; s += nwarps) {
@@ -752,9 +736,9 @@ __global__ void __launch_bounds__(kThreads) holder_tile_kernel(
 #pragma unroll
                     for (int r = 0; r < 4; ++r) {
                         const uint32_t e = r * 32 + lane;
-                        rk[r] = e < E ? trk[e * kHtRk + s] : 0xFFFFu;
+                        rk[r] = e < E ? trk[e * 33 + s] : 0xFFFFu;
                         if (rk[r] != 0xFFFFu) {
-                            const uint32_t tseg = part.within_epoch(tinv[e * kHtInv + s], w[r]);
+                            const uint32_t tseg = part.within_epoch(tinv[e * 33 + s], w[r]);
                             const uint32_t wl = w[r] - part.wbegin;
                             const uint64_t blk = ((uint64_t)wl * E + e) * MB + (tseg >> 5);
                             bit[r] = tseg & 31;
@@ -774,17 +758,17 @@ __global__ void __launch_bounds__(kThreads) holder_tile_kernel(
                         __stcs(h + 2, pos);
                     }
                 }
-                tile_done = true;
+                continue;
             }
         }
-        for (uint32_t s = warp; s < 32 && !tile_done; s += nwarps) {
+        for (uint32_t s = warp; s < 32; s += nwarps) {
             if (k0 + s >= F) break;
             const uint64_t slot0 = pair_off[k0 + s];
             for (uint32_t e = lane; e < E; e += 32) {
-                const uint32_t rk = trk[e * kHtRk + s];
+                const uint32_t rk = trk[e * 33 + s];
                 if (rk == 0xFFFFu) continue;
                 uint32_t w;
-                const uint32_t tseg = part.within_epoch(tinv[e * kHtInv + s], w);
+                const uint32_t tseg = part.within_epoch(tinv[e * 33 + s], w);
                 const uint32_t wl = w - part.wbegin;
                 const uint64_t blk = ((uint64_t)wl * E + e) * MB + (tseg >> 5);
                 const uint32_t bit = tseg & 31;
@@ -836,7 +820,6 @@ __global__ void __launch_bounds__(kThreads) holder_tile_kernel(
                 __stcs(h + 2, pos);
             }
         }
-        __syncthreads();  // this buffer is refilled by the prefetch two tiles later
     }
 }
 
@@ -1068,7 +1051,7 @@ void launch_holder_tile(cudaStream_t s, const Part& part, const uint32_t* inv, c
                         uint32_t MB, const uint32_t* rec, uint32_t np, uint32_t J, uint32_t Rp,
                         const uint32_t* cbase, const uint64_t* pair_off, uint32_t* holders,
                         bool allfit) {
-    const size_t smem = 2 * ((size_t)part.E * kHtInv + ((size_t)part.E * kHtRk + 1) / 2) * 4 + 16;
+    const size_t smem = (size_t)part.E * 33 * 4 + (size_t)part.E * 33 * 2 + 16;
     const uint64_t tiles = ((uint64_t)part.F + 31) / 32;
     const unsigned grid = grid_for(tiles, 1, 148u * 16u);
 #define HT_LAUNCH(NPV)                                                                           \

@@ -352,7 +352,8 @@ __global__ void __launch_bounds__(kThreads) fyb_emit_kernel(uint64_t key, Part p
                                                             const uint32_t* __restrict__ q,
                                                             uint32_t* __restrict__ inv,
                                                             uint32_t* __restrict__ stream,
-                                                            uint32_t* __restrict__ perm_out) {
+                                                            uint32_t* __restrict__ perm_out,
+                                                            bool inv_all) {
     const uint32_t slot = blockIdx.y, e = e0 + slot, F = part.F;
     const FyRej rj(rt, e - rt.e_base);
     const uint32_t* sc = succ + (size_t)slot * F;
@@ -390,10 +391,12 @@ __global__ void __launch_bounds__(kThreads) fyb_emit_kernel(uint64_t key, Part p
             for (int u = 0; u < U; ++u)
                 if (i0 + u < F) perm_out[(size_t)slot * F + i0 + u] = cur[u];
         }
-        if (inv) {  // values with a writer got inv from fyb_block; chase roots have none
+        if (inv) {
+            // inv_all: every value's position is written here (the epoch's inv row is filled
+            // while it is L2-resident); otherwise only the chase roots (fyb_block wrote the rest)
 #pragma unroll
             for (int u = 0; u < U; ++u)
-                if ((chased >> u) & 1u) inv[(size_t)e * F + cur[u]] = i0 + u;
+                if ((inv_all && i0 + u < F) || ((chased >> u) & 1u)) inv[(size_t)e * F + cur[u]] = i0 + u;
         }
         if (stream && i0 < part.P) {
             uint32_t w, left;
@@ -444,6 +447,13 @@ void launch_fyb(cudaStream_t s, uint64_t key, const Part& part, uint32_t e0, uin
     cudaMemsetAsync(pool_used, 0, ne * sizeof(uint32_t), s);
     cudaMemsetAsync(succ, 0xFF, (size_t)ne * F * sizeof(uint32_t), s);
     const size_t sm_block = fyb_block_smem(g);
+    // inv written entirely by fyb_emit (each epoch's row is filled while it is L2-resident;
+    // measured 3.46 vs 3.64 ms for the config-2 shuffle stage); CLAIRPLAN_INV_ALL=0: fyb_block
+    // writes inv of the targets with a writer, fyb_emit the chase roots (A/B)
+    static const bool inv_all = [] {
+        const char* v = getenv("CLAIRPLAN_INV_ALL");
+        return !(v && v[0] == '0');
+    }();
     static const int bt = [] {
         const char* v = getenv("CLAIRPLAN_FYB_THREADS");  // A/B
         return v ? atoi(v) : (int)kBlockThreads;
@@ -453,7 +463,8 @@ void launch_fyb(cudaStream_t s, uint64_t key, const Part& part, uint32_t e0, uin
         cudaFuncSetAttribute(fyb_block_kernel<BTV>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
                              (int)sm_block);                                                      \
         fyb_block_kernel<BTV><<<dim3(g.NB, ne), BTV, sm_block, s>>>(F, g, bucket, lst, pool,       \
-                                                                    pool_used, succ, q, e0, inv);  \
+                                                                    pool_used, succ, q, e0,        \
+                                                                    inv_all ? nullptr : inv);      \
     } while (0)
     if (bt == 128) FYB_LAUNCH(128);
     else if (bt == 512) FYB_LAUNCH(512);
@@ -466,12 +477,12 @@ void launch_fyb(cudaStream_t s, uint64_t key, const Part& part, uint32_t e0, uin
     }();
     if (u == 8) {
         dim3 g8(grid_for(F, kThreads * 8, 148u * 16u), ne);
-        fyb_emit_kernel<8><<<g8, kThreads, 0, s>>>(key, part, e0, rt, succ, q, inv, stream, perm_out);
+        fyb_emit_kernel<8><<<g8, kThreads, 0, s>>>(key, part, e0, rt, succ, q, inv, stream, perm_out, inv_all);
     } else if (u == 2) {
         dim3 g2(grid_for(F, kThreads * 2, 148u * 16u), ne);
-        fyb_emit_kernel<2><<<g2, kThreads, 0, s>>>(key, part, e0, rt, succ, q, inv, stream, perm_out);
+        fyb_emit_kernel<2><<<g2, kThreads, 0, s>>>(key, part, e0, rt, succ, q, inv, stream, perm_out, inv_all);
     } else {
-        fyb_emit_kernel<4><<<grid, kThreads, 0, s>>>(key, part, e0, rt, succ, q, inv, stream, perm_out);
+        fyb_emit_kernel<4><<<grid, kThreads, 0, s>>>(key, part, e0, rt, succ, q, inv, stream, perm_out, inv_all);
     }
 }
 
