@@ -205,7 +205,7 @@ __device__ __forceinline__ void fyb_block_body(uint32_t F, const FyGeom& g, uint
                                                const uint32_t* rdst, uint32_t* head, uint32_t* W,
                                                uint16_t* J16, uint16_t* N16, uint32_t* J32,
                                                uint32_t* N32, const uint32_t* bk, uint32_t* sc,
-                                               uint32_t* qq, uint32_t* iv) {
+                                               uint32_t* qq, uint32_t* iv, bool succ_all) {
     const uint32_t TB = 1u << g.lgTB, tbmask = TB - 1;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     constexpr uint32_t kEnd = BIG ? kNone : 0xFFFFu;
@@ -285,6 +285,7 @@ __device__ __forceinline__ void fyb_block_body(uint32_t F, const FyGeom& g, uint
         if (first) qq[y] = w != y ? w : nx;   // smallest writer != y
         if (nx == kNone) {
             if (iv) iv[y] = w;                 // the last writer places y (out[w_m] = j = y)
+            if (succ_all) sc[w] = kNone;       // every writer's succ written: no preset
         } else {
             sc[w] = nx;
         }
@@ -300,7 +301,8 @@ __global__ void __launch_bounds__(BT) fyb_block_kernel(uint32_t F, FyGeom g,
                                                                   uint32_t* __restrict__ succ,
                                                                   uint32_t* __restrict__ q,
                                                                   uint32_t e0,
-                                                                  uint32_t* __restrict__ inv) {
+                                                                  uint32_t* __restrict__ inv,
+                                                                  bool succ_all) {
     extern __shared__ uint32_t sm[];
     __shared__ uint32_t wsum[BT / 32];
     __shared__ uint32_t s_pool;
@@ -332,7 +334,7 @@ __global__ void __launch_bounds__(BT) fyb_block_kernel(uint32_t F, FyGeom g,
             reinterpret_cast<uint4*>(head)[k] = make_uint4(0xFFFFu, 0xFFFFu, 0xFFFFu, 0xFFFFu);
         __syncthreads();
         fyb_block_body<false, BT>(F, g, b, n, nt, tmin, rsrc, rdst, head, W, J16, N16, nullptr,
-                              nullptr, bk, sc, qq, iv);
+                              nullptr, bk, sc, qq, iv, succ_all);
     } else {  // heavy block (small targets): global pool slab
         for (uint32_t k = threadIdx.x; k < TB / 4; k += BT)
             reinterpret_cast<uint4*>(head)[k] = make_uint4(kNone, kNone, kNone, kNone);
@@ -340,7 +342,7 @@ __global__ void __launch_bounds__(BT) fyb_block_kernel(uint32_t F, FyGeom g,
         __syncthreads();
         uint32_t* gW = pool + (size_t)slot * 4 * F + s_pool;
         fyb_block_body<true, BT>(F, g, b, n, nt, tmin, rsrc, rdst, head, gW, nullptr, nullptr,
-                             gW + n, gW + 2 * n, bk, sc, qq, iv);
+                             gW + n, gW + 2 * n, bk, sc, qq, iv, succ_all);
     }
 }
 
@@ -445,7 +447,11 @@ void launch_fyb(cudaStream_t s, uint64_t key, const Part& part, uint32_t e0, uin
     else if (g.lgTS == 14) launch_tile<(1 << 14) / kTileThreads>(s, key, F, e0, ne, g, rt, rej_flag, bucket, lst);
     else launch_tile<0>(s, key, F, e0, ne, g, rt, rej_flag, bucket, lst);
     cudaMemsetAsync(pool_used, 0, ne * sizeof(uint32_t), s);
-    cudaMemsetAsync(succ, 0xFF, (size_t)ne * F * sizeof(uint32_t), s);
+    static const bool succ_all = [] {
+        const char* v = getenv("CLAIRPLAN_SUCC_ALL");  // A/B: every succ entry from fyb_block
+        return v && v[0] == '1';
+    }();
+    if (!succ_all) cudaMemsetAsync(succ, 0xFF, (size_t)ne * F * sizeof(uint32_t), s);
     const size_t sm_block = fyb_block_smem(g);
     // inv written entirely by fyb_emit (each epoch's row is filled while it is L2-resident;
     // measured 3.46 vs 3.64 ms for the config-2 shuffle stage); CLAIRPLAN_INV_ALL=0: fyb_block
@@ -464,7 +470,8 @@ void launch_fyb(cudaStream_t s, uint64_t key, const Part& part, uint32_t e0, uin
                              (int)sm_block);                                                      \
         fyb_block_kernel<BTV><<<dim3(g.NB, ne), BTV, sm_block, s>>>(F, g, bucket, lst, pool,       \
                                                                     pool_used, succ, q, e0,        \
-                                                                    inv_all ? nullptr : inv);      \
+                                                                    inv_all ? nullptr : inv,       \
+                                                                    succ_all);                     \
     } while (0)
     if (bt == 128) FYB_LAUNCH(128);
     else if (bt == 512) FYB_LAUNCH(512);
