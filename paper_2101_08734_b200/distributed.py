@@ -104,7 +104,8 @@ class DistributedPlan:
     mode "perms": permutation rows all-gathered to every rank (the earlier scheme, kept for
     A/B measurements)."""
 
-    def __init__(self, seed, samples, part, capacities_mb, sizes_mb, group=None, mode="streams"):
+    def __init__(self, seed, samples, part, capacities_mb, sizes_mb, group=None, mode="streams",
+                 pipeline=False):
         import torch
         import torch.distributed as dist
         from . import clairplan as cp
@@ -136,10 +137,40 @@ class DistributedPlan:
                 pre.append(int(v.value))
             wr = [worker_range(N, r, self.world) for r in range(self.world)]
             self.send_splits, self.recv_splits = stream_splits(pre, self.ranges, wr, self.rank)
-            self.send = torch.empty(max(sum(self.send_splits), 1), dtype=torch.int32, device="cuda")
+            self.pipeline = pipeline and dist.get_backend(group) == "nccl"
+            self.send = None if self.pipeline else torch.empty(max(sum(self.send_splits), 1),
+                                                               dtype=torch.int32, device="cuda")
             self.recv = torch.empty(max(sum(self.recv_splits), 1), dtype=torch.int32, device="cuda")
             self.bounds = np.array([b for b, _ in self.ranges] + [part.epochs], np.uint32)
+            # pipelined variant (NCCL): every rank's epochs in two halves, the first half's
+            # all-to-all overlapping the second half's shuffle (measured at 4 ranks: generate +
+            # exchange 1.31 vs 1.21 ms unpipelined — the exchange competes for SMs — so off by
+            # default)
+            if self.pipeline:
+                wb, we = self.wrange
+                lloc = pre[we] - pre[wb]
+                self.halves = [[(b, (n + 1) // 2), (b + (n + 1) // 2, n - (n + 1) // 2)]
+                               for b, n in self.ranges]
+                self.bounds2 = np.array([c[0] for h in self.halves for c in h] + [part.epochs],
+                                        np.uint32)
+                mine = self.halves[self.rank]
+                self.send_h = [torch.empty(max(n * pre[N], 1), dtype=torch.int32, device="cuda")
+                               for _, n in mine]
+                self.in_lists, self.out_lists = [], []
+                for h, (_, n) in enumerate(mine):
+                    ins, o = [], 0
+                    for (db, de) in wr:
+                        ln = n * (pre[de] - pre[db])
+                        ins.append(self.send_h[h][o:o + ln])
+                        o += ln
+                    outs = []
+                    for r in range(self.world):
+                        cb, cn = self.halves[r][h]
+                        outs.append(self.recv[cb * lloc:(cb + cn) * lloc])
+                    self.in_lists.append(ins)
+                    self.out_lists.append(outs)
         else:
+            self.pipeline = False
             self.local_rows = torch.empty((max(self.pad, 1), samples), dtype=torch.int32,
                                           device="cuda")
         self.counts = torch.empty(samples, dtype=torch.int32, device="cuda")
@@ -152,7 +183,26 @@ class DistributedPlan:
         torch, cp = self.torch, self.cp
         e0, n = self.ranges[self.rank]
         t0 = time.perf_counter()
-        if self.mode == "streams":
+        if self.mode == "streams" and self.pipeline:
+            works = []
+            for h, (hb, hn) in enumerate(self.halves[self.rank]):
+                cp._check(self.L.clairplan_generate_streams(self.plan._h, hb, hn,
+                                                            C.c_void_p(self.send_h[h].data_ptr())))
+                works.append(self.dist.all_to_all(self.out_lists[h], self.in_lists[h],
+                                                  group=self.group, async_op=True))
+            t1 = time.perf_counter()
+            for wk in works:
+                wk.wait()
+            torch.cuda.current_stream().synchronize()
+            t2 = time.perf_counter()
+            cp._check(self.L.clairplan_build_from_streams(
+                self.plan._h, C.c_void_p(self.recv.data_ptr()),
+                self.bounds2.ctypes.data_as(C.c_void_p), 2 * self.world))
+            t3 = time.perf_counter()
+            self.timings = {"generate_ms": round((t1 - t0) * 1e3, 3),
+                            "all_to_all_ms": round((t2 - t1) * 1e3, 3),
+                            "build_ms": round((t3 - t2) * 1e3, 3)}
+        elif self.mode == "streams":
             cp._check(self.L.clairplan_generate_streams(self.plan._h, e0, n,
                                                         C.c_void_p(self.send.data_ptr())))
             t1 = time.perf_counter()
