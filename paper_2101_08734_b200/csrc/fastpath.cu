@@ -372,24 +372,30 @@ __global__ void __launch_bounds__(kThreads) seg_allfit_kernel(
                 tot += __popc(bal);
             }
         }
-        // publish, look back within the worker's chain of chunks
+        // publish, then a warp-wide look-back over the worker's chain of chunks: lane j reads
+        // chunk x-1-j, the window stops at the nearest inclusive prefix (the worker's first
+        // chunk is always inclusive)
         unsigned long long prefix = 0;
-        if (lane == 0) {
-            const uint64_t first_x = (uint64_t)wl * E * C;
-            if (x == first_x) {
-                atomicExch(status + x, kStInc | tot);
-            } else {
-                atomicExch(status + x, kStAgg | tot);
-                for (uint64_t j = x - 1;; --j) {
-                    unsigned long long v;
+        const uint64_t first_x = (uint64_t)wl * E * C;
+        if (lane == 0) atomicExch(status + x, (x == first_x ? kStInc : kStAgg) | tot);
+        if (x != first_x) {
+            for (uint64_t j0 = x - 1;; j0 -= 32) {
+                const bool valid = j0 >= first_x + lane;  // j0 - lane >= first_x
+                unsigned long long v = 0;
+                if (valid) {
                     do {
-                        v = *reinterpret_cast<volatile unsigned long long*>(status + j);
+                        v = *reinterpret_cast<volatile unsigned long long*>(status + (j0 - lane));
                     } while (v == 0);
-                    prefix += v & kStMask;
-                    if ((v & kStInc) || j == first_x) break;
                 }
-                atomicExch(status + x, kStInc | (prefix + tot));
+                const uint32_t incm = __ballot_sync(0xffffffffu, valid && (v & kStInc));
+                const uint32_t upto = incm ? (uint32_t)(__ffs(incm) - 1) : 31u;
+                unsigned long long add = (valid && lane <= upto) ? (v & kStMask) : 0ull;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) add += __shfl_xor_sync(0xffffffffu, add, o);
+                prefix += add;
+                if (incm) break;
             }
+            if (lane == 0) atomicExch(status + x, kStInc | (prefix + tot));
         }
         prefix = __shfl_sync(0xffffffffu, prefix, 0);
         // pass B: block records and the class-1 list
@@ -689,7 +695,7 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 template <int NP>
-__global__ void __launch_bounds__(kThreads) holder_tile_kernel(
+__global__ void __launch_bounds__(kThreads, 5) holder_tile_kernel(
     Part part, const uint32_t* __restrict__ inv, const uint16_t* __restrict__ rank16, uint32_t MB,
     const uint32_t* __restrict__ rec, uint32_t np_rt, uint32_t J, uint32_t Rp,
     const uint32_t* __restrict__ cbase, const uint64_t* __restrict__ pair_off,
