@@ -332,7 +332,8 @@ __global__ void __launch_bounds__(kThreads) seg_allfit_kernel(
     Part part, const uint32_t* __restrict__ stream, const uint16_t* __restrict__ info,
     const uint32_t* __restrict__ cpos, uint32_t MB, uint32_t C,
     unsigned long long* __restrict__ status, uint32_t* __restrict__ ticket,
-    uint32_t* __restrict__ rec, uint32_t* __restrict__ class_list) {
+    uint32_t* __restrict__ rec, uint32_t* __restrict__ class_list, const uint32_t* __restrict__ gate) {
+    if (gate && *gate == 0) return;  // speculative launch, the all-fit test failed
     const uint32_t E = part.E, nloc = part.wend - part.wbegin;
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t nch = (uint64_t)nloc * E * C;
@@ -428,7 +429,8 @@ __global__ void __launch_bounds__(kThreads) seg_allfit_kernel(
 // offset, lists (w, j > 1) empty; class bases 0 (records hold worker-local indices)
 __global__ void allfit_meta_kernel(Part part, uint32_t J, const uint32_t* __restrict__ wcnt,
                                    uint64_t* __restrict__ clen, uint64_t* __restrict__ cstart,
-                                   uint32_t* __restrict__ cbase) {
+                                   uint32_t* __restrict__ cbase, const uint32_t* __restrict__ gate) {
+    if (gate && *gate == 0) return;
     const uint32_t nloc = part.wend - part.wbegin;
     for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x <= nloc * J; x += gridDim.x * blockDim.x) {
         if (x == nloc * J) {
@@ -445,18 +447,40 @@ __global__ void allfit_meta_kernel(Part part, uint32_t J, const uint32_t* __rest
 
 void launch_seg_allfit(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info,
                        const uint32_t* cpos, uint32_t MB, uint32_t C, unsigned long long* status,
-                       uint32_t* ticket, uint32_t* rec, uint32_t* class_list) {
+                       uint32_t* ticket, uint32_t* rec, uint32_t* class_list, const uint32_t* gate) {
     const uint64_t nch = (uint64_t)(part.wend - part.wbegin) * part.E * C;
     cudaMemsetAsync(status, 0, nch * 8, s);
     cudaMemsetAsync(ticket, 0, 4, s);
     seg_allfit_kernel<<<grid_for(nch * 32, kThreads, 148u * 8u), kThreads, 0, s>>>(
-        part, stream, info, cpos, MB, C, status, ticket, rec, class_list);
+        part, stream, info, cpos, MB, C, status, ticket, rec, class_list, gate);
 }
 
 void launch_allfit_meta(cudaStream_t s, const Part& part, uint32_t J, const uint32_t* wcnt,
-                        uint64_t* clen, uint64_t* cstart, uint32_t* cbase) {
+                        uint64_t* clen, uint64_t* cstart, uint32_t* cbase, const uint32_t* gate) {
     allfit_meta_kernel<<<grid_for((uint64_t)(part.wend - part.wbegin) * J + 1, kThreads), kThreads, 0, s>>>(
-        part, J, wcnt, clen, cstart, cbase);
+        part, J, wcnt, clen, cstart, cbase, gate);
+}
+
+// the whole-worker fit test of allfit_decide (plan.cu) on the device: *ok stays nonzero only
+// when no size was negative and every worker's candidates fit class 1
+__global__ void allfit_decide_kernel(uint32_t nloc, const unsigned long long* __restrict__ wsum,
+                                     const uint32_t* __restrict__ wcnt, double C, uint32_t* ok) {
+    for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w <= nloc; w += gridDim.x * blockDim.x) {
+        if (w == nloc) {
+            if (wcnt[nloc]) atomicAnd(ok, 0u);  // the negative-size flag
+            continue;
+        }
+        if (wcnt[w] == 0) continue;
+        const double sw = (double)wsum[w] * 0x1.0p-20;
+        const double tol = ((double)wcnt[w] + 1024.0) * fmax(C, sw) * 0x1.0p-48;
+        if (!(C - sw > tol)) atomicAnd(ok, 0u);
+    }
+}
+
+void launch_allfit_decide(cudaStream_t s, uint32_t nloc, const unsigned long long* wsum,
+                          const uint32_t* wcnt, double C, uint32_t* ok) {
+    cudaMemsetAsync(ok, 0xFF, 4, s);
+    allfit_decide_kernel<<<grid_for((uint64_t)nloc + 1, kThreads), kThreads, 0, s>>>(nloc, wsum, wcnt, C, ok);
 }
 
 // ---------------------------------------------------------------------------- K4c
@@ -699,7 +723,8 @@ __global__ void __launch_bounds__(kThreads, 5) holder_tile_kernel(
     Part part, const uint32_t* __restrict__ inv, const uint16_t* __restrict__ rank16, uint32_t MB,
     const uint32_t* __restrict__ rec, uint32_t np_rt, uint32_t J, uint32_t Rp,
     const uint32_t* __restrict__ cbase, const uint64_t* __restrict__ pair_off,
-    uint32_t* __restrict__ holders) {
+    uint32_t* __restrict__ holders, const uint32_t* __restrict__ gate) {
+    if (gate && *gate == 0) return;  // speculative all-fit launch, the test failed
     extern __shared__ uint32_t sm[];
     const uint32_t E = part.E, F = part.F;
     const uint32_t np = NP > 0 ? (uint32_t)NP : np_rt;
@@ -1056,7 +1081,7 @@ void launch_class_lens(cudaStream_t s, uint32_t nloc, uint32_t E, uint32_t MB, u
 void launch_holder_tile(cudaStream_t s, const Part& part, const uint32_t* inv, const uint16_t* rank16,
                         uint32_t MB, const uint32_t* rec, uint32_t np, uint32_t J, uint32_t Rp,
                         const uint32_t* cbase, const uint64_t* pair_off, uint32_t* holders,
-                        bool allfit) {
+                        bool allfit, const uint32_t* gate) {
     const size_t smem = (size_t)part.E * 33 * 4 + (size_t)part.E * 33 * 2 + 16;
     const uint64_t tiles = ((uint64_t)part.F + 31) / 32;
     const unsigned grid = grid_for(tiles, 1, 148u * 16u);
@@ -1065,7 +1090,7 @@ void launch_holder_tile(cudaStream_t s, const Part& part, const uint32_t* inv, c
         cudaFuncSetAttribute(holder_tile_kernel<NPV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                              (int)smem);                                                         \
         holder_tile_kernel<NPV><<<grid, kThreads, smem, s>>>(part, inv, rank16, MB, rec, np, J, Rp, \
-                                                             cbase, pair_off, holders);          \
+                                                             cbase, pair_off, holders, gate);    \
     } while (0)
     if (allfit) HT_LAUNCH(-1);
     else if (np == 1) HT_LAUNCH(1);

@@ -122,7 +122,8 @@ void launch_holder_sparse(cudaStream_t s, const Part& part, uint64_t n, const ui
                           const uint32_t* stream, const uint32_t* csr, const uint16_t* erank,
                           uint32_t MB, const uint32_t* rec, uint32_t np, uint32_t J, uint32_t Rp,
                           const uint32_t* cbase, const uint64_t* pair_off, uint32_t* holders,
-                          bool allfit);
+                          bool allfit,
+                          const uint32_t* gate = nullptr);
 void launch_stream_inv(cudaStream_t s, const Part& part, const uint32_t* stream, uint32_t* inv);
 void launch_perm_scatter(cudaStream_t s, const Part& part, const uint32_t* perms, uint32_t* inv,
                          uint32_t* stream);
@@ -191,9 +192,13 @@ void launch_seg_hist(cudaStream_t s, const Part& part, const uint32_t* stream, c
 constexpr uint32_t kAllfitChunk = 1024;
 void launch_seg_allfit(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info,
                        const uint32_t* cpos, uint32_t MB, uint32_t C, unsigned long long* status,
-                       uint32_t* ticket, uint32_t* rec, uint32_t* class_list);
+                       uint32_t* ticket, uint32_t* rec, uint32_t* class_list,
+                       const uint32_t* gate = nullptr);
 void launch_allfit_meta(cudaStream_t s, const Part& part, uint32_t J, const uint32_t* wcnt,
-                        uint64_t* clen, uint64_t* cstart, uint32_t* cbase);
+                        uint64_t* clen, uint64_t* cstart, uint32_t* cbase,
+                        const uint32_t* gate = nullptr);
+void launch_allfit_decide(cudaStream_t s, uint32_t nloc, const unsigned long long* wsum,
+                          const uint32_t* wcnt, double C, uint32_t* ok);
 void launch_seg_write2(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info, const uint32_t* cpos,
                        const double* sizes, const uint64_t* seg_off, const uint64_t* sorted_base,
                        uint32_t MB, uint32_t* dest, double* sorted_size, uint32_t* blkmask,
@@ -214,6 +219,6 @@ void launch_class_lens(cudaStream_t s, uint32_t nloc, uint32_t E, uint32_t MB, u
 void launch_holder_tile(cudaStream_t s, const Part& part, const uint32_t* inv, const uint16_t* rank16,
                         uint32_t MB, const uint32_t* rec, uint32_t np, uint32_t J, uint32_t Rp,
                         const uint32_t* cbase, const uint64_t* pair_off, uint32_t* holders,
-                        bool allfit);
+                        bool allfit, const uint32_t* gate = nullptr);
 
 }  // namespace clairplan

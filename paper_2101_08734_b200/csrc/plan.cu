@@ -639,49 +639,6 @@ int no_classes_v2(clairplan_plan* p) {
     return 0;
 }
 
-// All-fit path (every worker's candidates provably fit class 1, fit_check_kernel): the tier
-// order cannot change the outcome of pack_first_fit, so it is not materialised; the block
-// records and class-1 lists come straight from the streams (seg_first), then K8.
-int assign_allfit_v2(clairplan_plan* p) {
-    cudaStream_t s = p->stream;
-    const Part& part = p->part;
-    const uint32_t E = part.E, nloc = p->nloc, J = p->cfg.num_classes;
-    uint32_t np = 0;
-    while ((1u << np) <= J) ++np;
-    const uint32_t Rp = ((np + J) + 3) & ~3u;
-    const uint32_t C = (uint32_t)((part.epoch_len(part.wbegin) + kAllfitChunk - 1) / kAllfitChunk);
-    bool ok = true;
-    uint32_t* centries = need<uint32_t>(p->class_entries, p->A, ok);  // lists at stream offsets
-    uint32_t* rec = need<uint32_t>(p->planes, (uint64_t)std::max<uint32_t>(Rp, 4) * p->v2_nblk, ok);
-    uint32_t* cbase = need<uint32_t>(p->cbase, (uint64_t)nloc * J, ok);
-    uint64_t* clen = need<uint64_t>(p->class_len, (uint64_t)nloc * J, ok);
-    uint64_t* cstart = need<uint64_t>(p->class_start, (uint64_t)nloc * J + 1, ok);
-    unsigned long long* status = need<unsigned long long>(p->chstatus, (uint64_t)nloc * E * C, ok);
-    uint32_t* ticket = need<uint32_t>(p->counters, 4, ok);
-    if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed (class lists)");
-    launch_seg_allfit(s, part, p->stream_buf.get<uint32_t>(), info_src(p),
-                      p->sparse ? p->cpos.get<uint32_t>() : nullptr, p->v2_mb, C, status, ticket,
-                      rec, centries);
-    launch_allfit_meta(s, part, J, p->wcnt.get<uint32_t>(), clen, cstart, cbase);
-    p->launches += 4;
-    p->cl_contig = false;
-    p->mark(6);
-    return holders_v2(p);
-}
-
-// Whole-worker fit test on the host from the sample pass's per-worker sums: every worker's
-// candidates fit class 1 whatever the order (bound as in firstfit.cu ff_prefix_kernel).
-// sum[w] = sum of ceil(size * 2^20) over worker w's candidates (an upper bound).
-bool allfit_decide(double C, const std::vector<unsigned long long>& sum,
-                   const std::vector<uint32_t>& cnt) {
-    for (size_t w = 0; w < sum.size(); ++w) {
-        if (cnt[w] == 0) continue;
-        const double sw = (double)sum[w] * 0x1.0p-20;
-        const double tol = ((double)cnt[w] + 1024.0) * std::max(C, sw) * 0x1.0p-48;
-        if (!(C - sw > tol)) return false;
-    }
-    return true;
-}
 
 // K4c: every candidate's first-order index -> tier position (dest), the sizes in tier order,
 // the block first-masks; per-worker candidate ranges (wbeg / wlen).
@@ -711,6 +668,68 @@ int tier_order_v2(clairplan_plan* p) {
     p->launches += 2;
     p->tier_ready = true;
     return 0;
+}
+
+// Speculative all-fit pipeline: launched before the host knows the fit test's outcome (it is
+// computed on the device into *gate); every kernel exits at once when the test failed, and the
+// host then runs the tier path.  Buffers are sized by A >= D (D is not known yet).
+int spec_allfit_launch(clairplan_plan* p, const uint32_t* gate) {
+    cudaStream_t s = p->stream;
+    const Part& part = p->part;
+    const uint32_t E = part.E, nloc = p->nloc, J = p->cfg.num_classes;
+    uint32_t np = 0;
+    while ((1u << np) <= J) ++np;
+    const uint32_t Rp = ((np + J) + 3) & ~3u;
+    const uint32_t C = (uint32_t)((part.epoch_len(part.wbegin) + kAllfitChunk - 1) / kAllfitChunk);
+    bool ok = true;
+    uint32_t* centries = need<uint32_t>(p->class_entries, p->A, ok);
+    uint32_t* rec = need<uint32_t>(p->planes, (uint64_t)std::max<uint32_t>(Rp, 4) * p->v2_nblk, ok);
+    uint32_t* cbase = need<uint32_t>(p->cbase, (uint64_t)nloc * J, ok);
+    uint64_t* clen = need<uint64_t>(p->class_len, (uint64_t)nloc * J, ok);
+    uint64_t* cstart = need<uint64_t>(p->class_start, (uint64_t)nloc * J + 1, ok);
+    unsigned long long* status = need<unsigned long long>(p->chstatus, (uint64_t)nloc * E * C, ok);
+    uint32_t* ticket = need<uint32_t>(p->counters, 4, ok);
+    uint32_t* htmp = need<uint32_t>(p->holders_tmp, 3 * std::max<uint64_t>(p->A, 1), ok);
+    if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed (all-fit)");
+    p->mark(3);
+    p->mark(4);
+    p->mark(5);
+    launch_seg_allfit(s, part, p->stream_buf.get<uint32_t>(), info_src(p),
+                      p->sparse ? p->cpos.get<uint32_t>() : nullptr, p->v2_mb, C, status, ticket,
+                      rec, centries, gate);
+    launch_allfit_meta(s, part, J, p->wcnt.get<uint32_t>(), clen, cstart, cbase, gate);
+    p->mark(6);
+    p->mark(7);
+    const uint64_t* poff = p->pair_off.get<uint64_t>();
+    if (p->sparse)
+        launch_holder_sparse(s, part, p->A, p->soff.get<uint64_t>(), p->stream_buf.get<uint32_t>(),
+                             p->csr.get<uint32_t>(), p->erank.get<uint16_t>(), p->v2_mb, rec, np, J,
+                             Rp, cbase, poff, htmp, true, gate);
+    else
+        launch_holder_tile(s, part, p->inv.get<uint32_t>(), p->rank16.get<uint16_t>(), p->v2_mb, rec,
+                           np, J, Rp, cbase, poff, htmp, true, gate);
+    p->launches += 6;
+    return 0;
+}
+
+// host state of a finished all-fit build: class list (w, 1) at the worker's stream offset with
+// its candidate count, (w, j > 1) empty; every pair is a holder record
+void finish_allfit(clairplan_plan* p, const std::vector<uint32_t>& wcnt_h) {
+    const uint32_t nloc = p->nloc, J = p->cfg.num_classes;
+    p->class_start_h.assign((size_t)nloc * (J + 1), 0);
+    p->class_len_h.assign((size_t)nloc * (J + 1), 0);
+    for (uint32_t w = 0; w < nloc; ++w) {
+        const uint64_t a = p->part.stream_offset(p->part.wbegin + w);
+        for (uint32_t j = 0; j < J; ++j) {
+            p->class_start_h[(size_t)w * (J + 1) + j] = j == 0 ? a : a + wcnt_h[w];
+            p->class_len_h[(size_t)w * (J + 1) + j] = j == 0 ? wcnt_h[w] : 0;
+        }
+    }
+    p->H = p->D;
+    p->holder_off_dev = p->pair_off.get<uint64_t>();
+    p->holders_dev = p->holders_tmp.get<uint32_t>();
+    p->cl_contig = false;
+    p->allfit = true;
 }
 
 int build_seed_path_v2(clairplan_plan* p, const uint32_t* ext_perms,
@@ -829,35 +848,65 @@ int build_seed_path_v2(clairplan_plan* p, const uint32_t* ext_perms,
         }
         exclusive_scan(s, pcount, F, poff, p->ws);
         p->mark(2);
+        // speculative all-fit pipeline (decided on the device, checked at the one sync below)
+        uint32_t* gate = nullptr;
+        if (sums) {
+            gate = need<uint32_t>(p->allfit_gate, 1, ok);
+            if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed");
+            launch_allfit_decide(s, nloc, wsum, wcnt, p->caps[0], gate);
+            p->v2_mb = MB;
+            p->v2_nblk = nblk;
+            if (int rc = spec_allfit_launch(p, gate)) return rc;
+        }
         std::vector<uint32_t> flags(E);
         uint64_t D = 0;
-        std::vector<unsigned long long> hsum(sums ? nloc : 0);
-        std::vector<uint32_t> hcnt(sums ? nloc + 1 : 0);
+        uint32_t gate_h = 0;
+        std::vector<uint32_t> hcnt(sums ? nloc : 0);
         CK(cudaMemcpyAsync(&D, poff + F, 8, cudaMemcpyDeviceToHost, s));
         if (sums) {
-            CK(cudaMemcpyAsync(hsum.data(), wsum, (size_t)nloc * 8, cudaMemcpyDeviceToHost, s));
-            CK(cudaMemcpyAsync(hcnt.data(), wcnt, (size_t)nloc * 4 + 4, cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(hcnt.data(), wcnt, (size_t)nloc * 4, cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(&gate_h, gate, 4, cudaMemcpyDeviceToHost, s));
         }
         CK(cudaMemcpyAsync(flags.data(), p->rej_flag.get<uint32_t>(), E * 4, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         bool any = false;
         if (int rc = resolve_rejections(p, flags, &any)) return rc;
         if (any) continue;
-        // all-fit test (host); otherwise K4b: per-segment count histograms -> first-order and
-        // tier-order bases
-        bool allfit = false;
-        if (sums && hcnt[nloc] == 0) {
-            hcnt.resize(nloc);
-            allfit = allfit_decide(p->caps[0], hsum, hcnt);
+        if (D >= 0xFFFFFFFFull)
+            return fail(CLAIRPLAN_EOVERFLOW, "more than 2^32-1 (worker, sample) pairs in one handle; "
+                                             "shard the workers over several handles");
+        const bool allfit = sums && gate_h != 0;
+        if (allfit) {  // the speculative pipeline produced the plan
+            p->D = D;
+            p->v2_mb = MB;
+            p->v2_nblk = nblk;
+            p->tier_ready = false;
+            p->hist_ready = false;
+            finish_allfit(p, hcnt);
+            p->launches += 10;
+            p->mark(clairplan_plan::kStages);
+            CK(cudaEventRecord(p->ev1, s));
+            CK(cudaEventSynchronize(p->ev1));
+            CK(cudaGetLastError());
+            if (p->ws.overflow) return fail(CLAIRPLAN_ENOMEM, "internal workspace overflow");
+            float ms = 0;
+            CK(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
+            p->device_ms = ms;
+            for (int i = 0; i < clairplan_plan::kStages; ++i) {
+                float t = 0;
+                if (p->sev[i] && p->sev[i + 1]) cudaEventElapsedTime(&t, p->sev[i], p->sev[i + 1]);
+                p->stage_ms[i] = t;
+            }
+            p->v2 = true;
+            p->built = true;
+            return 0;
         }
-        p->hist_ready = false;
-        if (!allfit) {
-            if (red_hist) launch_segcnt(s, nloc, E, seghist, segcnt);
-            else launch_seg_hist(s, part, stream_buf, info_src(p), p->sparse ? p->cpos.get<uint32_t>() : nullptr, seghist, segcnt);
-            exclusive_scan(s, seghist, NEE, sbase, p->ws);
-            exclusive_scan(s, segcnt, (uint64_t)nloc * E, segoff, p->ws);
-            p->hist_ready = true;
-        }
+        // tier path. K4b: per-segment count histograms -> first-order and tier-order bases
+        if (red_hist) launch_segcnt(s, nloc, E, seghist, segcnt);
+        else launch_seg_hist(s, part, stream_buf, info_src(p), p->sparse ? p->cpos.get<uint32_t>() : nullptr, seghist, segcnt);
+        exclusive_scan(s, seghist, NEE, sbase, p->ws);
+        exclusive_scan(s, segcnt, (uint64_t)nloc * E, segoff, p->ws);
+        p->hist_ready = true;
         p->mark(3);
         p->launches += 10;
         p->D = D;
@@ -867,18 +916,11 @@ int build_seed_path_v2(clairplan_plan* p, const uint32_t* ext_perms,
         p->v2_mb = MB;
         p->v2_nblk = nblk;
         p->tier_ready = false;
-        if (allfit) {
-            p->mark(4);
-            p->mark(5);
-            p->allfit = true;
-            if (int rc = assign_allfit_v2(p)) return rc;
-        } else {
-            p->allfit = false;
-            if (int rc = tier_order_v2(p)) return rc;
-            p->mark(4);
-            p->mark(5);
-            if (int rc = assign_v2(p)) return rc;
-        }
+        p->allfit = false;
+        if (int rc = tier_order_v2(p)) return rc;
+        p->mark(4);
+        p->mark(5);
+        if (int rc = assign_v2(p)) return rc;
         p->mark(clairplan_plan::kStages);
         CK(cudaEventRecord(p->ev1, s));
         CK(cudaEventSynchronize(p->ev1));

@@ -118,7 +118,7 @@ struct clairplan_plan {
     DevBuf wsbuf;
     DevBuf cand_w, dfirst, dcounts;  // explicit-stream (generic) path
     DevBuf inv, info16, rank16, cbase, seghist, sorted_base, blkmask, blkbase, planes, ccount, cpre, hard;
-    DevBuf wsum, wcnt, chstatus;     // all-fit: per-worker size sums / counts, chunk look-back
+    DevBuf wsum, wcnt, chstatus, allfit_gate;  // all-fit: worker sums / counts, look-back, decision
     bool cl_contig = true;           // class lists back to back (tier path) or at stream offsets
     DevBuf koff, sp_cur, csr, cpos, soff, einfo, erank;  // sparse sample-major passes (sharded)
     bool sparse = false;             // last build used the sparse passes
