@@ -83,22 +83,40 @@ __device__ __forceinline__ uint32_t blk_exscan(uint32_t* a, uint32_t n, uint32_t
     return carry;
 }
 
+// Exact draw with the rejection-table shift and the unseen-rejection report (rare path).
+__device__ __noinline__ uint32_t fy_draw_exact(uint64_t key, uint32_t e, uint32_t F, uint32_t i,
+                                               const uint32_t* st, const uint32_t* cu, uint32_t n,
+                                               uint32_t* flag) {
+    uint32_t extra;
+    const uint32_t j = fy_draw(key, e, F, i, n ? rej_shift(st, cu, n, i) : 0, &extra);
+    if (extra && flag) {
+        bool known = false;
+        for (uint32_t t = 0; t < n; ++t) known |= (st[t] == i);
+        if (!known) atomicMax(flag, i + 1);
+    }
+    return j;
+}
+
 struct FyRej {
     const uint32_t* st;
     const uint32_t* cu;
     uint32_t n;
     __device__ __forceinline__ FyRej(const RejTable& rt, uint32_t er)
         : st(rt.step + (size_t)er * rt.cap), cu(rt.cum + (size_t)er * rt.cap), n(rt.count[er]) {}
+    // Epochs without recorded rejections (all but ~1e-13 of them): the first draw at position
+    // (e << 34) + F - 1 - i, Lemire's product for a 32-bit bound in two 32x32->64 multiplies.
+    // Only when the low word of x * (i + 1) is below i + 1 can the draw be a rejection
+    // (threshold 2^64 mod (i+1) < i+1, rng.hpp:55-60): that case takes the exact path.
     __device__ __forceinline__ uint32_t draw(uint64_t key, uint32_t e, uint32_t F, uint32_t i,
                                              uint32_t* flag) const {
-        uint32_t extra;
-        const uint32_t j = fy_draw(key, e, F, i, n ? rej_shift(st, cu, n, i) : 0, &extra);
-        if (extra && flag) {
-            bool known = false;
-            for (uint32_t t = 0; t < n; ++t) known |= (st[t] == i);
-            if (!known) atomicMax(flag, i + 1);
+        if (n == 0) {
+            const uint64_t x = mix64(key + ((((uint64_t)e) << kEpochShift) + (uint64_t)(F - i)) * kGolden);
+            const uint32_t b = i + 1;
+            const uint64_t a = (uint64_t)(uint32_t)x * b;
+            const uint64_t h = (uint64_t)(uint32_t)(x >> 32) * b + (a >> 32);
+            if (!((uint32_t)h == 0 && (uint32_t)a < b)) return (uint32_t)(h >> 32);
         }
-        return j;
+        return fy_draw_exact(key, e, F, i, st, cu, n, flag);
     }
 };
 
