@@ -441,6 +441,122 @@ __global__ void __launch_bounds__(kThreads) fyb_emit_kernel(uint64_t key, Part p
     }
 }
 
+// ---- fyb_emitq: per warp chunk, chase from a work list ---------------------------------
+// fyb_emit's warps wait for the longest of their 64 chains on every iteration (q-chase loads
+// are dependent L2 round trips; chain lengths have a long tail).  Here a warp takes a chunk of
+// kEmitL * 32 steps: all succ loads of the chunk are issued at once, the draws of the last
+// writers are computed, the chunk's chains go to a shared work list and every lane runs
+// chains from it, two at a time, until the list is empty, then the chunk's values are written
+// back: stream and permutation rows coalesced, inv scattered.  Config 2: 1.20 vs 1.27 ms
+// (ncu), 5.85 vs 5.92 ms per plan; CLAIRPLAN_EMITQ=0 selects fyb_emit.
+constexpr uint32_t kEmitL = 16;
+
+template <int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) fyb_emitq_kernel(uint64_t key, Part part, uint32_t e0,
+                                                             RejTable rt,
+                                                             const uint32_t* __restrict__ succ,
+                                                             const uint32_t* __restrict__ q,
+                                                             uint32_t* __restrict__ inv,
+                                                             uint32_t* __restrict__ stream,
+                                                             uint32_t* __restrict__ perm_out,
+                                                             bool inv_all) {
+    constexpr uint32_t CH = kEmitL * 32;
+    __shared__ uint32_t sbuf[kThreads / 32][CH];
+    __shared__ uint16_t slist[kThreads / 32][CH];
+    const uint32_t slot = blockIdx.y, e = e0 + slot, F = part.F;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const FyRej rj(rt, e - rt.e_base);
+    const uint32_t* sc = succ + (size_t)slot * F;
+    const uint32_t* qq = q + (size_t)slot * F;
+    uint32_t* buf = sbuf[warp];
+    uint16_t* lst = slist[warp];
+    const uint32_t nchunk = (F + CH - 1) / CH;
+    const uint32_t nwarp = gridDim.x * (blockDim.x >> 5);
+    for (uint32_t c = blockIdx.x * (blockDim.x >> 5) + warp; c < nchunk; c += nwarp) {
+        const uint32_t cb = c * CH;
+        uint32_t sv[kEmitL];
+#pragma unroll
+        for (uint32_t t = 0; t < kEmitL; ++t) {
+            const uint32_t i = cb + t * 32 + lane;
+            sv[t] = i < F ? (i ? __ldcs(sc + i) : 0u) : 0u;
+        }
+        uint32_t np = 0;
+#pragma unroll
+        for (uint32_t t = 0; t < kEmitL; ++t) {
+            const uint32_t i = cb + t * 32 + lane;
+            const bool chase = i < F && sv[t] != kNone;
+            uint32_t v = sv[t];
+            if (i < F && !chase) v = rj.draw(key, e, F, i, nullptr);  // last writer of its target
+            buf[t * 32 + lane] = v;
+            const uint32_t bal = __ballot_sync(0xffffffffu, chase);
+            if (chase) lst[np + __popc(bal & lanemask_lt())] = (uint16_t)(t * 32 + lane);
+            np += __popc(bal);
+        }
+        __syncwarp();
+        // two chains in flight per lane; entries lane, lane + 32, ... taken in order
+        uint32_t nj = lane;
+        uint32_t idx0 = 0, cur0 = 0, idx1 = 0, cur1 = 0;
+        bool a0 = nj < np;
+        if (a0) {
+            idx0 = lst[nj];
+            cur0 = buf[idx0];
+        }
+        nj += 32;
+        bool a1 = nj < np;
+        if (a1) {
+            idx1 = lst[nj];
+            cur1 = buf[idx1];
+        }
+        nj += 32;
+        while (__any_sync(0xffffffffu, a0 || a1)) {
+            const uint32_t q0 = a0 ? qq[cur0] : 0u;
+            const uint32_t q1 = a1 ? qq[cur1] : 0u;
+            if (a0) {
+                if (q0 == kNone) {
+                    buf[idx0] = cur0;
+                    a0 = nj < np;
+                    if (a0) {
+                        idx0 = lst[nj];
+                        cur0 = buf[idx0];
+                        nj += 32;
+                    }
+                } else {
+                    cur0 = q0;
+                }
+            }
+            if (a1) {
+                if (q1 == kNone) {
+                    buf[idx1] = cur1;
+                    a1 = nj < np;
+                    if (a1) {
+                        idx1 = lst[nj];
+                        cur1 = buf[idx1];
+                        nj += 32;
+                    }
+                } else {
+                    cur1 = q1;
+                }
+            }
+        }
+        __syncwarp();
+#pragma unroll 4
+        for (uint32_t t = 0; t < kEmitL; ++t) {
+            const uint32_t i = cb + t * 32 + lane;
+            if (i >= F) break;
+            const uint32_t v = buf[t * 32 + lane];
+            if (perm_out) perm_out[(size_t)slot * F + i] = v;
+            if (inv && (inv_all || sv[t] != kNone)) inv[(size_t)e * F + v] = i;
+            if (stream && i < part.P) {
+                uint32_t w;
+                uint64_t spos;
+                part.locate(i, e, w, spos);
+                if (w >= part.wbegin && w < part.wend) stream[part.stream_offset(w) + spos] = v;
+            }
+        }
+        __syncwarp();
+    }
+}
+
 // ---- launchers --------------------------------------------------------------------------
 size_t fyb_block_smem(const FyGeom& g) {
     return (size_t)4 * ((1u << g.lgTB) + 2 * g.NT + 1 + g.cap) + 4 * (size_t)g.cap;
@@ -500,7 +616,22 @@ void launch_fyb(cudaStream_t s, uint64_t key, const Part& part, uint32_t e0, uin
         const char* v = getenv("CLAIRPLAN_EMIT_U");  // A/B (2 measured best for config 2)
         return v ? atoi(v) : 2;
     }();
-    if (u == 8) {
+    static const bool emitq = [] {
+        const char* v = getenv("CLAIRPLAN_EMITQ");  // A/B: 0 = fyb_emit (per-thread chains)
+        return !(v && v[0] == '0');
+    }();
+    if (emitq) {
+        const uint32_t nchunk = (F + kEmitL * 32 - 1) / (kEmitL * 32);
+        dim3 gq(std::max<uint32_t>(1, std::min<uint32_t>((nchunk + 7) / 8, 148u * 8u)), ne);
+        static const int minb = [] {
+            const char* v = getenv("CLAIRPLAN_EMITQ_MINB");  // A/B (5: 48 registers, spills)
+            return v ? atoi(v) : 4;
+        }();
+        if (minb == 5)
+            fyb_emitq_kernel<5><<<gq, kThreads, 0, s>>>(key, part, e0, rt, succ, q, inv, stream, perm_out, inv_all);
+        else
+            fyb_emitq_kernel<4><<<gq, kThreads, 0, s>>>(key, part, e0, rt, succ, q, inv, stream, perm_out, inv_all);
+    } else if (u == 8) {
         dim3 g8(grid_for(F, kThreads * 8, 148u * 16u), ne);
         fyb_emit_kernel<8><<<g8, kThreads, 0, s>>>(key, part, e0, rt, succ, q, inv, stream, perm_out, inv_all);
     } else if (u == 2) {
