@@ -951,13 +951,12 @@ __global__ void __launch_bounds__(kThreads) sample_tile_kernel(Part part, const 
             const uint32_t word = lane < W ? bm[lane] : 0u;
             const uint32_t c = __popc(word);
             uint32_t inc = c;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
+            for (uint32_t d = 1; d < W; d <<= 1) {  // lanes >= W hold 0: log2(W) steps suffice
                 const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
-                if (lane >= (uint32_t)d) inc += o;
+                if (lane >= d) inc += o;
             }
             const uint32_t pre = inc - c;
-            const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
+            const uint32_t total = __shfl_sync(0xffffffffu, inc, W - 1);
             if (live && lane == 0) pair_count[k0 + s] = total;
             unsigned long long sz = 0;
             if (ws.sum && live) {
