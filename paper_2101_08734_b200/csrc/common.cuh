@@ -1,5 +1,6 @@
 // Shared device/host helpers for the clairplan kernels (sm_100a).
 #pragma once
+#include <cstdlib>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -234,6 +235,12 @@ __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
+}
+
+// CTAs-per-SM grid factor with an environment override (A/B sweeps of grid sizing)
+inline unsigned env_uint(const char* name, unsigned def) {
+    const char* v = getenv(name);
+    return v ? (unsigned)atoi(v) : def;
 }
 
 inline unsigned grid_for(uint64_t n, unsigned per_block, unsigned cap = 148u * 64u) {

@@ -451,7 +451,8 @@ void launch_seg_allfit(cudaStream_t s, const Part& part, const uint32_t* stream,
     const uint64_t nch = (uint64_t)(part.wend - part.wbegin) * part.E * C;
     cudaMemsetAsync(status, 0, nch * 8, s);
     cudaMemsetAsync(ticket, 0, 4, s);
-    seg_allfit_kernel<<<grid_for(nch * 32, kThreads, 148u * 8u), kThreads, 0, s>>>(
+    static const unsigned gm = env_uint("CLAIRPLAN_GRID_ALLFIT", 8);
+    seg_allfit_kernel<<<grid_for(nch * 32, kThreads, 148u * gm), kThreads, 0, s>>>(
         part, stream, info, cpos, MB, C, status, ticket, rec, class_list, gate);
 }
 
@@ -718,7 +719,7 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-template <int NP>
+template <int NP, int TU = 4>  // TU: tile rows in flight per thread (8 spills: slower)
 __global__ void __launch_bounds__(kThreads, 5) holder_tile_kernel(
     Part part, const uint32_t* __restrict__ inv, const uint16_t* __restrict__ rank16, uint32_t MB,
     const uint32_t* __restrict__ rec, uint32_t np_rt, uint32_t J, uint32_t Rp,
@@ -733,7 +734,6 @@ __global__ void __launch_bounds__(kThreads, 5) holder_tile_kernel(
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
     for (uint64_t k0 = (uint64_t)blockIdx.x * 32; k0 < F; k0 += (uint64_t)gridDim.x * 32) {
         __syncthreads();
-        constexpr int TU = 4;  // rows in flight per thread
         for (uint32_t i0 = threadIdx.x; i0 < E * 32; i0 += TU * blockDim.x) {
             uint32_t iv[TU];
             uint16_t rv[TU];
@@ -1083,7 +1083,12 @@ void launch_holder_tile(cudaStream_t s, const Part& part, const uint32_t* inv, c
                         bool allfit, const uint32_t* gate) {
     const size_t smem = (size_t)part.E * 33 * 4 + (size_t)part.E * 33 * 2 + 16;
     const uint64_t tiles = ((uint64_t)part.F + 31) / 32;
-    const unsigned grid = grid_for(tiles, 1, 148u * 16u);
+    static const int gmul = [] {
+        // A/B: CTAs per SM in the grid (config 2: 10 -> 1.088, 16 -> 1.116, 5 -> 1.097 ms)
+        const char* v = getenv("CLAIRPLAN_HOLDER_GRID");
+        return v ? atoi(v) : 10;
+    }();
+    const unsigned grid = grid_for(tiles, 1, 148u * (unsigned)gmul);
 #define HT_LAUNCH(NPV)                                                                           \
     do {                                                                                         \
         cudaFuncSetAttribute(holder_tile_kernel<NPV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
@@ -1122,7 +1127,8 @@ void launch_sample_tile(cudaStream_t s, const Part& part, const uint32_t* inv, u
                                      (kThreads / 32) * (2 * W * 32 + W) + 2) +
                         (ws.sum ? (size_t)W * 32 * 12 : 0);  // clo, chi, ccnt
     const uint64_t tiles = ((uint64_t)part.F + 31) / 32;
-    const unsigned grid = grid_for(tiles, 1, 148u * 8u);
+    static const unsigned gm = env_uint("CLAIRPLAN_GRID_SAMPLE", 16);
+    const unsigned grid = grid_for(tiles, 1, 148u * gm);
 #define ST_LAUNCH(RV)                                                                             \
     do {                                                                                          \
         cudaFuncSetAttribute(sample_tile_kernel<RV>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
