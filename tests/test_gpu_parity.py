@@ -428,3 +428,60 @@ def test_build_export_matches_separate_exports(cp, ref):
         assert np.array_equal(ho, want_off.astype(np.uint64))
         assert np.array_equal(hh[:3 * st["holders"]], want_hold.reshape(-1))
         p.close()
+
+
+@pytest.mark.parametrize("F,N,b,E,dl,caps", [
+    (20_011, 9, 3, 7, False, None),
+    (262_144, 64, 16, 10, True, None),
+    (262_144, 64, 16, 10, True, [50.0, 1e9]),   # tier path (capacity-limited first fit)
+    (1_281_167, 256, 32, 9, True, None),
+])
+@pytest.mark.parametrize("dense", ["0", "1"])
+def test_sharded_build_from_streams(cp, monkeypatch, F, N, b, E, dl, caps, dense):
+    """One rank's share of the multi-GPU build on one GPU: a worker-range
+    handle fed its workers' streams of every epoch (what the all-to-all delivers, one source)
+    through clairplan_generate_streams / clairplan_build_from_streams, with the sparse (CSR)
+    or dense sample-major passes forced.  Its streams, class lists and holder records must
+    equal the full single-GPU plan's restricted to those workers (the full plan is checked
+    against the reference by the tests above)."""
+    import ctypes as C
+    import torch
+    monkeypatch.setenv("CLAIRPLAN_DENSE", dense)
+    sizes = cp.generate_sizes(F, 0.1077, 0.1, None, 1)
+    part = cp.PartitionSpec(N, b * N, E, dl)
+    caps = caps or [120.0 * F / 1e4, 900.0 * F / 1e4]
+    full = cp.Plan(42, F, part, caps, sizes).build()
+    st_full = full.streams_flat()
+    offs_full, hold_full = full.holders()
+    cl_full = full.class_lists()
+    samp = np.repeat(np.arange(F), np.diff(offs_full.astype(np.int64)))
+    L = cp.lib()
+    L.clairplan_generate_streams.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p]
+    L.clairplan_build_from_streams.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32]
+    L.clairplan_epoch_prefix.argtypes = [C.c_void_p, C.c_uint32, C.POINTER(C.c_uint64)]
+    for wb, we in [(0, N // 2), (N // 2, N), (N // 3, N // 3 + max(1, N // 5))]:
+        sh = cp.Plan(42, F, part, caps, sizes, worker_range=(wb, we))
+        allst = torch.empty(len(st_full), dtype=torch.int32, device="cuda")
+        cp._check(L.clairplan_generate_streams(sh._h, 0, E, C.c_void_p(allst.data_ptr())))
+        pre = []
+        for w in (wb, we):
+            v = C.c_uint64()
+            cp._check(L.clairplan_epoch_prefix(sh._h, w, C.byref(v)))
+            pre.append(int(v.value))
+        recv = allst[pre[0] * E:pre[1] * E]
+        bounds = np.array([0, E], np.uint32)
+        cp._check(L.clairplan_build_from_streams(sh._h, C.c_void_p(recv.data_ptr()),
+                                                 bounds.ctypes.data_as(C.c_void_p), 1))
+        torch.cuda.synchronize()
+        lo = L.clairplan_stream_offset(full._h, wb)
+        hi = L.clairplan_stream_offset(full._h, we)
+        assert np.array_equal(sh.streams_flat(), st_full[lo:hi]), (wb, we)
+        cl = sh.class_lists()
+        assert all(np.array_equal(x, y) for a, c in zip(cl_full[wb:we], cl) for x, y in zip(a, c))
+        offs, hold = sh.holders()
+        m = (hold_full[:, 0] >= wb) & (hold_full[:, 0] < we)
+        assert np.array_equal(hold, hold_full[m]), (wb, we)
+        assert np.array_equal(np.diff(offs.astype(np.int64)), np.bincount(samp[m], minlength=F))
+        sh.close()
+        del allst
+    full.close()
