@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(kThreads) csr_scatter_kernel(const uint32_t* _
 // warp per sample, lanes over its entries (R rounds of 32, entries kept in registers); per-warp
 // shared tables indexed by local worker (nloc <= 32 W)
 template <int R>
-__global__ void __launch_bounds__(kThreads, 6) sparse_sample_kernel(
+__global__ void __launch_bounds__(kThreads, 5) sparse_sample_kernel(
     uint32_t F, uint32_t nloc, uint32_t W, const uint64_t* __restrict__ soff,
     const uint64_t* __restrict__ koff, const uint32_t* __restrict__ csr,
     uint32_t* __restrict__ pair_count, uint16_t* __restrict__ einfo, uint16_t* __restrict__ erank,
@@ -111,9 +111,21 @@ __global__ void __launch_bounds__(kThreads, 6) sparse_sample_kernel(
     }
     if (lane < W) bm[lane] = 0;
     __syncthreads();
-    for (uint32_t k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < F;
-         k += (gridDim.x * blockDim.x) >> 5) {
-        const uint64_t a = koff[k], b = koff[k + 1];
+    const uint32_t kstride = (gridDim.x * blockDim.x) >> 5;
+    uint32_t k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    uint64_t an = 0, bn = 0;  // the next sample's CSR range, loaded one iteration ahead
+    if (k < F) {
+        an = koff[k];
+        bn = koff[k + 1];
+    }
+    for (; k < F; k += kstride) {
+        const uint64_t a = an, b = bn;
+        if (k + kstride < F) {
+            an = koff[k + kstride];
+            bn = koff[k + kstride + 1];
+        }
+        // the sample's size, issued early (used after the rounds)
+        const double szv = (ws.sum && b > a) ? __ldg(ws.sizes + k) : 0.0;
         uint32_t sv[R], xv[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
@@ -139,18 +151,18 @@ __global__ void __launch_bounds__(kThreads, 6) sparse_sample_kernel(
         } else {
             const uint32_t c = __popc(w0) + __popc(w1);
             uint32_t inc = c;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t nl = two ? (W + 1) / 2 : W;  // lanes holding words
+            for (uint32_t d = 1; d < nl; d <<= 1) {
                 const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
-                if (lane >= (uint32_t)d) inc += o;
+                if (lane >= d) inc += o;
             }
             pre = inc - c;
-            total = __shfl_sync(0xffffffffu, inc, 31);
+            total = __shfl_sync(0xffffffffu, inc, nl - 1);
         }
         if (lane == 0) pair_count[k] = total;
         unsigned long long sz = 0;
         if (ws.sum && b > a) {
-            const double v = __ldg(ws.sizes + k);
+            const double v = szv;
             if (!(v >= 0.0 && v < 0x1.0p40)) {
                 if (lane == 0) atomicOr(ws.neg, 1u);  // negative, NaN or huge: no all-fit
             } else {
@@ -322,7 +334,10 @@ void launch_sparse_sample(cudaStream_t s, const Part& part, const uint64_t* soff
     const uint32_t nloc = part.wend - part.wbegin, W = (nloc + 31) / 32;
     const size_t smem = ((size_t)(kThreads / 32) * (2 * W * 32 + W) + 2) * 4 +
                         (ws.sum ? (size_t)W * 32 * 12 : 0);
-    const unsigned grid = grid_for((uint64_t)part.F * 32, kThreads, 148u * 8u);
+    // 5 CTAs per SM (48 registers, no spills), two waves (4-way config-2 shard: 1.73 vs
+    // 1.84 ms per build with 6 per SM in a 1.33-wave grid)
+    static const unsigned gm = env_uint("CLAIRPLAN_GRID_SPARSE", 10);
+    const unsigned grid = grid_for((uint64_t)part.F * 32, kThreads, 148u * gm);
     const FastDiv uni = uniform_len(part);
 #define SS_LAUNCH(RV)                                                                              \
     do {                                                                                           \
