@@ -174,6 +174,18 @@ int clairplan_build_from_streams(clairplan_t plan, const uint32_t* d_recv,
 /* Per-sample number of holder records of the handle's workers, d_out[F] (device): the
  * input of the cross-GPU holder-offset merge (all-gather + exclusive scan over ranks). */
 int clairplan_holder_counts(clairplan_t plan, uint32_t* d_out);
+/* Overlap of that merge with the build's tail (no reference counterpart: the reference is a
+ * single process).  During the next builds, as soon as the per-sample pair counts exist,
+ * they are copied into d_counts[F] (device), `stream` (a cudaStream_t, e.g. the caller's
+ * collective stream) is made to wait for the copy and fn(user) runs on the calling thread —
+ * once per build, on every rank at the same point — to enqueue the all-gather.  fn = NULL
+ * removes the hook. */
+int clairplan_set_counts_hook(clairplan_t plan, uint32_t* d_counts, void* stream,
+                              void (*fn)(void*), void* user);
+/* 1 if the last build's hooked counts are its holder counts (all-fit path: every pair is a
+ * holder; no rejection rerun after the hook), else 0: merge again from
+ * clairplan_holder_counts. */
+int clairplan_counts_hook_valid(clairplan_t plan);
 
 /* Host-side input generator: DatasetModel::generate (perfmodel.cpp:68-99), bit-identical
  * with the reference built with the same glibc (no FMA contraction).  Not timed. */

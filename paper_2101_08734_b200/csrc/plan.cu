@@ -748,6 +748,8 @@ int build_seed_path_v2(clairplan_plan* p, const uint32_t* ext_perms,
     const bool sparse = ext_streams && (dense_env ? dense_env[0] == '0' && sparse_path_fits(part)
                                                   : sparse_path_ok(part, p->A));
     uint32_t* stream_buf = need<uint32_t>(p->stream_buf, p->A, ok);
+    p->hook_fired = false;
+    bool hook_called = false;  // at most once per build: every rank calls its collective once
     // the dense [E][F] sample-major arrays (not needed by the sparse passes)
     uint32_t* inv = sparse ? nullptr : need<uint32_t>(p->inv, EF, ok);
     const uint64_t EFp = (uint64_t)E * part.Fp;  // pitched u16 rows
@@ -848,6 +850,17 @@ int build_seed_path_v2(clairplan_plan* p, const uint32_t* ext_perms,
         }
         exclusive_scan(s, pcount, F, poff, p->ws);
         p->mark(2);
+        if (p->hook_fn && !hook_called) {
+            CK(cudaMemcpyAsync(p->hook_counts, pcount, (size_t)F * 4, cudaMemcpyDeviceToDevice, s));
+            if (!p->hook_ev) CK(cudaEventCreateWithFlags(&p->hook_ev, cudaEventDisableTiming));
+            CK(cudaEventRecord(p->hook_ev, s));
+            CK(cudaStreamWaitEvent(p->hook_stream, p->hook_ev, 0));
+            p->hook_fn(p->hook_user);
+            hook_called = true;
+            p->hook_fired = true;
+        } else {
+            p->hook_fired = false;  // a rejection rerun: the hooked counts are stale
+        }
         // speculative all-fit pipeline (decided on the device, checked at the one sync below)
         uint32_t* gate = nullptr;
         if (sums) {
@@ -1357,6 +1370,22 @@ int clairplan_build_from_perms(clairplan_t p, const uint32_t* d_perms) {
     p->built = false;
     p->v2 = false;
     return build_seed_path_v2(p, d_perms);
+}
+
+int clairplan_set_counts_hook(clairplan_t p, uint32_t* d_counts, void* stream,
+                              void (*fn)(void*), void* user) {
+    if (!p) return fail(CLAIRPLAN_EINVAL, "null plan");
+    if (fn && !d_counts) return fail(CLAIRPLAN_EINVAL, "counts hook needs a device buffer");
+    p->hook_counts = d_counts;
+    p->hook_stream = (cudaStream_t)stream;
+    p->hook_fn = fn;
+    p->hook_user = user;
+    p->hook_fired = false;
+    return 0;
+}
+
+int clairplan_counts_hook_valid(clairplan_t p) {
+    return (p && p->built && p->hook_fired && p->allfit && p->H == p->D) ? 1 : 0;
 }
 
 int clairplan_holder_counts(clairplan_t p, uint32_t* d_out) {

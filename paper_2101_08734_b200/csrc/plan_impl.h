@@ -139,7 +139,18 @@ struct clairplan_plan {
     cudaStream_t xstream = nullptr;   // build_export: stream of the overlapped output copy
     cudaEvent_t xev = nullptr;
     uint32_t* x_streams = nullptr;     // build_export: host stream buffer of the running build
+    // counts hook (multi-GPU holder-offset merge overlapped with the build's tail): once the
+    // per-sample pair counts exist, they are copied to hook_counts, hook_stream waits for them
+    // and hook_fn runs on the host (it enqueues the all-gather); valid if the build then took
+    // the all-fit path (holder counts = pair counts) without a rejection rerun
+    void* hook_counts = nullptr;
+    cudaStream_t hook_stream = nullptr;
+    void (*hook_fn)(void*) = nullptr;
+    void* hook_user = nullptr;
+    cudaEvent_t hook_ev = nullptr;
+    bool hook_fired = false;
     ~clairplan_plan() {
+        if (hook_ev) cudaEventDestroy(hook_ev);
         if (xstream) cudaStreamDestroy(xstream);
         if (xev) cudaEventDestroy(xev);
         if (stream) cudaStreamDestroy(stream);

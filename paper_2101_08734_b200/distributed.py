@@ -24,6 +24,7 @@ records with their global CSR positions.
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import numpy as np
 
@@ -174,14 +175,37 @@ class DistributedPlan:
             self.local_rows = torch.empty((max(self.pad, 1), samples), dtype=torch.int32,
                                           device="cuda")
         self.counts = torch.empty(samples, dtype=torch.int32, device="cuda")
+        self.allc = torch.empty((self.world, samples), dtype=torch.int32, device="cuda")
+        # holder-offset merge overlapped with the build's tail (streams mode, NCCL): the
+        # library calls _on_counts once the pair counts exist; its all-gather runs while the
+        # all-fit kernels finish.  Valid when every rank's build took the all-fit path.
+        self._spec = None
+        self._hook = None
+        L.clairplan_set_counts_hook.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                                C.c_void_p]
+        L.clairplan_counts_hook_valid.argtypes = [C.c_void_p]
+        if mode == "streams" and dist.get_backend(group) == "nccl" and \
+                os.environ.get("CLAIRPLAN_MERGE_OVERLAP", "1") != "0":
+            self._hook = C.CFUNCTYPE(None, C.c_void_p)(self._on_counts)
+            cp._check(L.clairplan_set_counts_hook(
+                self.plan._h, C.c_void_p(self.counts.data_ptr()),
+                C.c_void_p(torch.cuda.current_stream().cuda_stream),
+                C.cast(self._hook, C.c_void_p), None))
         self.timings = {}
         self.global_offsets = None
         self.rank_starts = None
+
+    def _on_counts(self, _user):
+        # runs inside the library's build call (same thread); the stream already waits for the
+        # counts copy
+        self.dist.all_gather_into_tensor(self.allc, self.counts, group=self.group)
+        self._spec = rank_offsets_from_counts(self.allc, self.rank)
 
     def build(self):
         import time
         torch, cp = self.torch, self.cp
         e0, n = self.ranges[self.rank]
+        self._spec = None
         t0 = time.perf_counter()
         if self.mode == "streams" and self.pipeline:
             works = []
@@ -231,10 +255,22 @@ class DistributedPlan:
                                                         C.c_void_p(perms.data_ptr())))
             del perms
         t4 = time.perf_counter()
-        cp._check(self.L.clairplan_holder_counts(self.plan._h, C.c_void_p(self.counts.data_ptr())))
-        allc = torch.empty((self.world, self.samples), dtype=torch.int32, device="cuda")
-        self.dist.all_gather_into_tensor(allc, self.counts, group=self.group)
-        self.global_offsets, self.rank_starts = rank_offsets_from_counts(allc, self.rank)
+        merged = False
+        if self._hook is not None:
+            # the overlapped merge holds only if every rank's hooked counts are its holder counts
+            ok = torch.tensor([1 if (self._spec is not None and
+                                     self.L.clairplan_counts_hook_valid(self.plan._h)) else 0],
+                              dtype=torch.int32, device="cuda")
+            self.dist.all_reduce(ok, op=self.dist.ReduceOp.MIN, group=self.group)
+            if int(ok.item()) == 1:
+                self.global_offsets, self.rank_starts = self._spec
+                merged = True
+        if not merged:
+            cp._check(self.L.clairplan_holder_counts(self.plan._h,
+                                                     C.c_void_p(self.counts.data_ptr())))
+            self.dist.all_gather_into_tensor(self.allc, self.counts, group=self.group)
+            self.global_offsets, self.rank_starts = rank_offsets_from_counts(self.allc, self.rank)
+        self.merge_overlapped = merged
         if self.mode == "streams":
             torch.cuda.current_stream().synchronize()
             self.timings["merge_ms"] = round((time.perf_counter() - t4) * 1e3, 3)
