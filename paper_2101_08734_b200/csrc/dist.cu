@@ -82,7 +82,8 @@ void launch_stream_relayout(cudaStream_t s, const Part& part, const EpochSplit& 
     stream_relayout_kernel<<<grid, kThreads, 0, s>>>(part, es, recv, stream);
 }
 
-void launch_stream_inv(cudaStream_t s, const Part& part, const uint32_t* stream, uint32_t* inv) {
+void launch_stream_inv(cudaStream_t s, const Part& part, const uint32_t* stream, uint32_t* inv,
+                       uint32_t skip_lo, uint32_t skip_hi) {
     // epoch batches of ~40 MB of inv rows: the none-fill and the scatter of a batch meet in L2
     const uint32_t F = part.F, E = part.E;
     // local positions per full batch / in the tail batch
@@ -92,12 +93,19 @@ void launch_stream_inv(cudaStream_t s, const Part& part, const uint32_t* stream,
                                                 (part.wbegin * part.tbase + std::min<uint64_t>(part.wbegin, part.textra)))
                                    : 0u;
     const uint32_t eb = std::max<uint32_t>(1, (uint32_t)((40ull << 20) / ((uint64_t)F * 4)));
-    for (uint32_t e0 = 0; e0 < E; e0 += eb) {
-        const uint32_t e1 = std::min(E, e0 + eb);
+    // epochs [skip_lo, skip_hi) already hold their whole inverse rows (the rank's own epochs,
+    // written by clairplan_generate_streams): rebuilt are the others only
+    for (uint32_t e0 = 0; e0 < E;) {
+        if (e0 >= skip_lo && e0 < skip_hi) {
+            e0 = skip_hi;
+            continue;
+        }
+        const uint32_t e1 = std::min(std::min(E, e0 + eb), e0 < skip_lo ? skip_lo : E);
         cudaMemsetAsync(inv + (size_t)e0 * F, 0xFF, (size_t)(e1 - e0) * F * 4, s);
         const uint64_t n = ((uint64_t)part.full * lfb + ltb) * (e1 - e0);
         stream_inv_kernel<<<grid_for(n, kThreads, 148u * 16u), kThreads, 0, s>>>(
             part, e0, e1, lfb, FastDiv(lfb ? lfb : 1), ltb, stream, inv);
+        e0 = e1;
     }
 }
 

@@ -124,7 +124,8 @@ void launch_holder_sparse(cudaStream_t s, const Part& part, uint64_t n, const ui
                           const uint32_t* cbase, const uint64_t* pair_off, uint32_t* holders,
                           bool allfit,
                           const uint32_t* gate = nullptr);
-void launch_stream_inv(cudaStream_t s, const Part& part, const uint32_t* stream, uint32_t* inv);
+void launch_stream_inv(cudaStream_t s, const Part& part, const uint32_t* stream, uint32_t* inv,
+                       uint32_t skip_lo = 0, uint32_t skip_hi = 0);
 void launch_perm_scatter(cudaStream_t s, const Part& part, const uint32_t* perms, uint32_t* inv,
                          uint32_t* stream);
 

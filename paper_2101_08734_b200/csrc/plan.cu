@@ -732,6 +732,12 @@ void finish_allfit(clairplan_plan* p, const std::vector<uint32_t>& wcnt_h) {
     p->allfit = true;
 }
 
+// sharded build from received streams: sparse (CSR) or dense sample-major passes
+static bool sharded_sparse(clairplan_plan* p) {
+    const char* dense_env = getenv("CLAIRPLAN_DENSE");  // "1": dense, "0": sparse, unset: cost model
+    return dense_env ? dense_env[0] == '0' && sparse_path_fits(p->part) : sparse_path_ok(p->part, p->A);
+}
+
 int build_seed_path_v2(clairplan_plan* p, const uint32_t* ext_perms,
                        const uint32_t* ext_streams = nullptr, const EpochSplit* es = nullptr) {
     cudaStream_t s = p->stream;
@@ -744,9 +750,7 @@ int build_seed_path_v2(clairplan_plan* p, const uint32_t* ext_perms,
     const uint64_t EF = (uint64_t)E * F, NEE = (uint64_t)nloc * E * E;
     bool ok = true;
     // sparse sample-major passes (sharded handle fed by the all-to-all; CLAIRPLAN_DENSE=1: A/B)
-    const char* dense_env = getenv("CLAIRPLAN_DENSE");  // "1": dense, "0": sparse, unset: cost model
-    const bool sparse = ext_streams && (dense_env ? dense_env[0] == '0' && sparse_path_fits(part)
-                                                  : sparse_path_ok(part, p->A));
+    const bool sparse = ext_streams && sharded_sparse(p);
     uint32_t* stream_buf = need<uint32_t>(p->stream_buf, p->A, ok);
     p->hook_fired = false;
     bool hook_called = false;  // at most once per build: every rank calls its collective once
@@ -799,7 +803,7 @@ int build_seed_path_v2(clairplan_plan* p, const uint32_t* ext_perms,
             launch_stream_relayout(s, part, *es, ext_streams, stream_buf);
             ++p->launches;
             if (!sparse) {
-                launch_stream_inv(s, part, stream_buf, inv);  // none-fills inv batch by batch
+                launch_stream_inv(s, part, stream_buf, inv, p->inv_own_lo, p->inv_own_hi);
                 ++p->launches;
             }
         } else if (ext_perms) {
@@ -1323,10 +1327,20 @@ int clairplan_generate_streams(clairplan_t p, uint32_t epoch_begin, uint32_t epo
     Part sp = make_part(pp.F, pp.N, pp.B, epoch_count, pp.drop_last != 0, 0, pp.N);
     sp.ebase = epoch_begin;
     if (int rc = alloc_rej(p, p->part.E)) return rc;
+    // a dense sharded build follows: the shuffle writes this range's whole inverse rows into
+    // the handle's inv (CLAIRPLAN_OWN_INV=0 disables, A/B)
+    p->inv_own_lo = p->inv_own_hi = 0;
+    uint32_t* own_inv = nullptr;
+    static const bool own_ok = env_uint("CLAIRPLAN_OWN_INV", 1) != 0;
+    if (own_ok && v2_ok(p) && !sharded_sparse(p)) {
+        bool ok = true;
+        own_inv = need<uint32_t>(p->inv, (uint64_t)pp.E * pp.F, ok);
+        if (!ok) own_inv = nullptr;
+    }
     for (int attempt = 0; attempt < 2; ++attempt) {
         p->launches = 0;
         CK(cudaEventRecord(p->ev0, p->stream));
-        if (int rc = enqueue_perms(p, d_out, nullptr, nullptr, epoch_begin, epoch_count, &sp)) return rc;
+        if (int rc = enqueue_perms(p, d_out, own_inv, nullptr, epoch_begin, epoch_count, &sp)) return rc;
         std::vector<uint32_t> flags(p->part.E);
         CK(cudaMemcpyAsync(flags.data(), p->rej_flag.get<uint32_t>(), flags.size() * 4,
                            cudaMemcpyDeviceToHost, p->stream));
@@ -1338,6 +1352,10 @@ int clairplan_generate_streams(clairplan_t p, uint32_t epoch_begin, uint32_t epo
             float ms = 0;
             CK(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
             p->gen_ms = ms;
+            if (own_inv) {
+                p->inv_own_lo = epoch_begin;
+                p->inv_own_hi = epoch_begin + epoch_count;
+            }
             return 0;
         }
     }
@@ -1360,7 +1378,9 @@ int clairplan_build_from_streams(clairplan_t p, const uint32_t* d_recv,
     if (!v2_ok(p)) return fail(CLAIRPLAN_EINVAL, "configuration not supported by the sharded path");
     p->built = false;
     p->v2 = false;
-    return build_seed_path_v2(p, nullptr, d_recv, &es);
+    const int rc = build_seed_path_v2(p, nullptr, d_recv, &es);
+    p->inv_own_lo = p->inv_own_hi = 0;  // the rows are the build's now (reassign, later builds)
+    return rc;
 }
 
 int clairplan_build_from_perms(clairplan_t p, const uint32_t* d_perms) {

@@ -149,6 +149,9 @@ struct clairplan_plan {
     void* hook_user = nullptr;
     cudaEvent_t hook_ev = nullptr;
     bool hook_fired = false;
+    // epochs whose whole inverse rows clairplan_generate_streams left in inv (dense sharded
+    // build: not rebuilt from the received streams); [0, 0) = none
+    uint32_t inv_own_lo = 0, inv_own_hi = 0;
     ~clairplan_plan() {
         if (hook_ev) cudaEventDestroy(hook_ev);
         if (xstream) cudaStreamDestroy(xstream);
