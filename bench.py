@@ -236,7 +236,8 @@ def run_ours(args, cfg):
     part = cp.PartitionSpec(N, cfg["b"] * N, cfg["E"], True)
     if world > 1:
         from paper_2101_08734_b200.distributed import DistributedPlan
-        dplan = DistributedPlan(SEED, cfg["F"], part, list(CAPS), sizes)
+        dplan = DistributedPlan(SEED, cfg["F"], part, list(CAPS), sizes,
+                                mode=os.environ.get("CLAIRPLAN_DIST_MODE", "p2p"))
         plan = dplan.plan
 
         def build():

@@ -171,6 +171,23 @@ int clairplan_epoch_prefix(clairplan_t plan, uint32_t worker, uint64_t* entries)
  * [local worker][epoch][t], blocks in rank order.  epoch_bounds[nsrc+1] is host memory. */
 int clairplan_build_from_streams(clairplan_t plan, const uint32_t* d_recv,
                                  const uint32_t* epoch_bounds, uint32_t nsrc);
+/* Fused exchange (multi-GPU on one node, CUDA IPC peer memory over NVLink/NVSwitch): the
+ * epoch-range shuffle writes every stream entry straight into the receive buffer of the rank
+ * owning its worker, replacing generate_streams + the all-to-all.  Rank d (workers
+ * [worker_bounds[d], worker_bounds[d+1])) receives entry idx of this rank's epoch-range
+ * stream layout at ((uint32_t*)dst_base[d])[idx + dst_delta[d]], i.e. the receive layout of
+ * clairplan_build_from_streams.  The caller orders the ranks (a barrier after this call,
+ * before the owners build; receive buffers not reused while an owner still reads them).
+ * Bucketed shuffle only (clairplan_p2p_supported). */
+int clairplan_generate_streams_p2p(clairplan_t plan, uint32_t epoch_begin, uint32_t epoch_count,
+                                   const uint64_t* dst_base, const int64_t* dst_delta,
+                                   const uint32_t* worker_bounds, uint32_t nranks);
+int clairplan_p2p_supported(clairplan_t plan);
+/* Receive buffer i (< 4) of the handle's local entries (allocated on first use, freed with the
+ * handle) and its CUDA IPC handle (64 bytes, may be NULL); peers open it with
+ * clairplan_open_peer_buffer (closed with the handle). */
+int clairplan_recv_buffer(clairplan_t plan, uint32_t i, void** d_ptr, void* ipc_handle);
+int clairplan_open_peer_buffer(clairplan_t plan, const void* ipc_handle, void** d_ptr);
 /* Per-sample number of holder records of the handle's workers, d_out[F] (device): the
  * input of the cross-GPU holder-offset merge (all-gather + exclusive scan over ranks). */
 int clairplan_holder_counts(clairplan_t plan, uint32_t* d_out);

@@ -79,10 +79,21 @@ struct FyGeom {
     uint32_t lgTB = 0, lgTS = 0, NB = 0, NT = 0, cap = 0;
 };
 bool fy_geometry(uint32_t F, FyGeom& g);
+// Multi-GPU fused exchange: the shuffle writes every stream entry straight into the receive
+// buffer of the rank owning its worker (CUDA IPC peer memory over NVLink) instead of a local
+// send buffer + all-to-all.  Entry idx of the local epoch-range stream layout goes to
+// base[d][idx + delta[d]] for the rank d with wb[d] <= worker < wb[d+1].
+constexpr uint32_t kMaxPeers = 16;
+struct StreamDst {
+    uint32_t G = 0;  // 0: the local stream buffer
+    uint32_t wb[kMaxPeers + 1] = {};
+    uint32_t* base[kMaxPeers] = {};
+    long long delta[kMaxPeers] = {};
+};
 void launch_fyb(cudaStream_t s, uint64_t key, const Part& part, uint32_t e0, uint32_t ne,
                 const FyGeom& g, const RejTable& rt, uint32_t* rej_flag, uint32_t* bucket,
                 uint32_t* lst, uint32_t* pool, uint32_t* pool_used, uint32_t* succ, uint32_t* q,
-                uint32_t* inv, uint32_t* stream, uint32_t* perm_out);
+                uint32_t* inv, uint32_t* stream, uint32_t* perm_out, const StreamDst* dst = nullptr);
 
 void launch_fy_table(cudaStream_t s, uint64_t key, uint32_t F, uint32_t e0, uint32_t ne,
                      uint4* tbl, uint32_t* ovh, uint32_t* ovn, const RejTable& rt,

@@ -459,7 +459,7 @@ __global__ void __launch_bounds__(kThreads, MINB) fyb_emitq_kernel(uint64_t key,
                                                              uint32_t* __restrict__ inv,
                                                              uint32_t* __restrict__ stream,
                                                              uint32_t* __restrict__ perm_out,
-                                                             bool inv_all) {
+                                                             bool inv_all, const StreamDst dst) {
     constexpr uint32_t CH = kEmitL * 32;
     __shared__ uint32_t sbuf[kThreads / 32][CH];
     __shared__ uint16_t slist[kThreads / 32][CH];
@@ -546,11 +546,20 @@ __global__ void __launch_bounds__(kThreads, MINB) fyb_emitq_kernel(uint64_t key,
             const uint32_t v = buf[t * 32 + lane];
             if (perm_out) perm_out[(size_t)slot * F + i] = v;
             if (inv && (inv_all || sv[t] != kNone)) inv[(size_t)e * F + v] = i;
-            if (stream && i < part.P) {
+            if ((stream || dst.G) && i < part.P) {
                 uint32_t w;
                 uint64_t spos;
                 part.locate(i, e, w, spos);
-                if (w >= part.wbegin && w < part.wend) stream[part.stream_offset(w) + spos] = v;
+                if (w >= part.wbegin && w < part.wend) {
+                    const uint64_t idx = part.stream_offset(w) + spos;
+                    if (dst.G == 0) {
+                        stream[idx] = v;
+                    } else {  // the owner's receive buffer (peer memory)
+                        uint32_t d = 0;
+                        while (d + 1 < dst.G && dst.wb[d + 1] <= w) ++d;
+                        dst.base[d][(long long)idx + dst.delta[d]] = v;
+                    }
+                }
             }
         }
         __syncwarp();
@@ -575,8 +584,9 @@ void launch_tile(cudaStream_t s, uint64_t key, uint32_t F, uint32_t e0, uint32_t
 void launch_fyb(cudaStream_t s, uint64_t key, const Part& part, uint32_t e0, uint32_t ne,
                 const FyGeom& g, const RejTable& rt, uint32_t* rej_flag, uint32_t* bucket,
                 uint32_t* lst, uint32_t* pool, uint32_t* pool_used, uint32_t* succ, uint32_t* q,
-                uint32_t* inv, uint32_t* stream, uint32_t* perm_out) {
+                uint32_t* inv, uint32_t* stream, uint32_t* perm_out, const StreamDst* dst) {
     const uint32_t F = part.F;
+    const StreamDst dloc = dst ? *dst : StreamDst{};
     if (g.lgTS == 13) launch_tile<(1 << 13) / kTileThreads>(s, key, F, e0, ne, g, rt, rej_flag, bucket, lst);
     else if (g.lgTS == 14) launch_tile<(1 << 14) / kTileThreads>(s, key, F, e0, ne, g, rt, rej_flag, bucket, lst);
     else launch_tile<0>(s, key, F, e0, ne, g, rt, rej_flag, bucket, lst);
@@ -620,7 +630,7 @@ void launch_fyb(cudaStream_t s, uint64_t key, const Part& part, uint32_t e0, uin
         const char* v = getenv("CLAIRPLAN_EMITQ");  // A/B: 0 = fyb_emit (per-thread chains)
         return !(v && v[0] == '0');
     }();
-    if (emitq) {
+    if (emitq || dloc.G) {  // (the peer-memory stream writes exist in fyb_emitq only)
         const uint32_t nchunk = (F + kEmitL * 32 - 1) / (kEmitL * 32);
         dim3 gq(std::max<uint32_t>(1, std::min<uint32_t>((nchunk + 7) / 8, 148u * 8u)), ne);
         static const int minb = [] {
@@ -628,9 +638,9 @@ void launch_fyb(cudaStream_t s, uint64_t key, const Part& part, uint32_t e0, uin
             return v ? atoi(v) : 4;
         }();
         if (minb == 5)
-            fyb_emitq_kernel<5><<<gq, kThreads, 0, s>>>(key, part, e0, rt, succ, q, inv, stream, perm_out, inv_all);
+            fyb_emitq_kernel<5><<<gq, kThreads, 0, s>>>(key, part, e0, rt, succ, q, inv, stream, perm_out, inv_all, dloc);
         else
-            fyb_emitq_kernel<4><<<gq, kThreads, 0, s>>>(key, part, e0, rt, succ, q, inv, stream, perm_out, inv_all);
+            fyb_emitq_kernel<4><<<gq, kThreads, 0, s>>>(key, part, e0, rt, succ, q, inv, stream, perm_out, inv_all, dloc);
     } else if (u == 8) {
         dim3 g8(grid_for(F, kThreads * 8, 148u * 16u), ne);
         fyb_emit_kernel<8><<<g8, kThreads, 0, s>>>(key, part, e0, rt, succ, q, inv, stream, perm_out, inv_all);

@@ -10,6 +10,7 @@
 //   K7    radix pass on class digit      -> prefetch-ordered class lists
 //   K8    holder_scatter (+ compaction)  -> holder CSR
 #include <stdlib.h>
+#include <cstring>
 
 #include "plan_impl.h"
 
@@ -44,7 +45,8 @@ RejTable rej_table(clairplan_plan* p) {
 // Enqueues the permutations of epochs [e_first, e_first + e_count): stream + inverse (or plain
 // permutations).  `spart` (optional) replaces the handle's stream geometry.
 int enqueue_perms(clairplan_plan* p, uint32_t* stream_out, uint32_t* inv_out, uint32_t* perm_out,
-                  uint32_t e_first, uint32_t e_count, const Part* spart = nullptr) {
+                  uint32_t e_first, uint32_t e_count, const Part* spart = nullptr,
+                  const StreamDst* dst = nullptr) {
     const Part& part = spart ? *spart : p->part;  // stream geometry (epoch-range streams)
     const uint32_t F = part.F;
     bool ok = true;
@@ -66,12 +68,13 @@ int enqueue_perms(clairplan_plan* p, uint32_t* stream_out, uint32_t* inv_out, ui
             const uint32_t ne = std::min(EB, e_first + e_count - e0);
             launch_fyb(p->stream, p->key, part, e0, ne, g, rt, p->rej_flag.get<uint32_t>(),
                        bucket, lst, pool, pool_used, succ, q, inv_out, stream_out,
-                       perm_out ? perm_out + (size_t)(e0 - e_first) * F : nullptr);
+                       perm_out ? perm_out + (size_t)(e0 - e_first) * F : nullptr, dst);
             p->launches += 3;
         }
         CK(cudaGetLastError());
         return 0;
     }
+    if (dst && dst->G) return fail(CLAIRPLAN_EINVAL, "peer-memory stream writes need the bucketed shuffle");
     if (mode == "table") {  // slot-table resolution (perm.cu)
         const uint32_t EB = epochs_per_batch(F, e_count, 32);
         uint4* tbl = need<uint4>(p->fytbl, (uint64_t)EB * F, ok);
@@ -1314,11 +1317,11 @@ int clairplan_epoch_prefix(clairplan_t p, uint32_t worker, uint64_t* entries) {
     return 0;
 }
 
-int clairplan_generate_streams(clairplan_t p, uint32_t epoch_begin, uint32_t epoch_count,
-                               uint32_t* d_out) {
+static int generate_streams_impl(clairplan_plan* p, uint32_t epoch_begin, uint32_t epoch_count,
+                                 uint32_t* d_out, const StreamDst* dst) {
     if (!p || p->generic) return fail(CLAIRPLAN_EINVAL, "invalid plan");
     if (epoch_count == 0) return 0;
-    if (!d_out) return fail(CLAIRPLAN_EINVAL, "null output");
+    if (!d_out && !(dst && dst->G)) return fail(CLAIRPLAN_EINVAL, "null output");
     if (epoch_begin + epoch_count > p->part.E) return fail(CLAIRPLAN_EINVAL, "epoch range outside plan");
     CK(cudaSetDevice(p->device));
     const Part& pp = p->part;
@@ -1340,7 +1343,7 @@ int clairplan_generate_streams(clairplan_t p, uint32_t epoch_begin, uint32_t epo
     for (int attempt = 0; attempt < 2; ++attempt) {
         p->launches = 0;
         CK(cudaEventRecord(p->ev0, p->stream));
-        if (int rc = enqueue_perms(p, d_out, own_inv, nullptr, epoch_begin, epoch_count, &sp)) return rc;
+        if (int rc = enqueue_perms(p, d_out, own_inv, nullptr, epoch_begin, epoch_count, &sp, dst)) return rc;
         std::vector<uint32_t> flags(p->part.E);
         CK(cudaMemcpyAsync(flags.data(), p->rej_flag.get<uint32_t>(), flags.size() * 4,
                            cudaMemcpyDeviceToHost, p->stream));
@@ -1360,6 +1363,70 @@ int clairplan_generate_streams(clairplan_t p, uint32_t epoch_begin, uint32_t epo
         }
     }
     return fail(CLAIRPLAN_ECUDA, "rejection tables did not converge");
+}
+
+int clairplan_generate_streams(clairplan_t p, uint32_t epoch_begin, uint32_t epoch_count,
+                               uint32_t* d_out) {
+    return generate_streams_impl(p, epoch_begin, epoch_count, d_out, nullptr);
+}
+
+int clairplan_generate_streams_p2p(clairplan_t p, uint32_t epoch_begin, uint32_t epoch_count,
+                                   const uint64_t* dst_base, const int64_t* dst_delta,
+                                   const uint32_t* worker_bounds, uint32_t nranks) {
+    if (!p || !dst_base || !dst_delta || !worker_bounds) return fail(CLAIRPLAN_EINVAL, "invalid argument");
+    if (nranks < 1 || nranks > kMaxPeers) return fail(CLAIRPLAN_EINVAL, "1..16 ranks supported");
+    if (worker_bounds[0] != 0 || worker_bounds[nranks] != p->part.N)
+        return fail(CLAIRPLAN_EINVAL, "worker bounds must cover [0, workers)");
+    StreamDst d{};
+    d.G = nranks;
+    for (uint32_t r = 0; r <= nranks; ++r) d.wb[r] = worker_bounds[r];
+    for (uint32_t r = 0; r < nranks; ++r) {
+        if (!dst_base[r]) return fail(CLAIRPLAN_EINVAL, "null destination buffer");
+        d.base[r] = reinterpret_cast<uint32_t*>(dst_base[r]);
+        d.delta[r] = (long long)dst_delta[r];
+    }
+    FyGeom g;
+    if (!fy_geometry(p->part.F, g)) return fail(CLAIRPLAN_EINVAL, "peer-memory stream writes need the bucketed shuffle");
+    return generate_streams_impl(p, epoch_begin, epoch_count, nullptr, &d);
+}
+
+int clairplan_p2p_supported(clairplan_t p) {
+    FyGeom g;
+    const char* m = getenv("CLAIRPLAN_FY");
+    return (p && !p->generic && fy_geometry(p->part.F, g) && !(m && std::string(m) != "bucket")) ? 1 : 0;
+}
+
+int clairplan_recv_buffer(clairplan_t p, uint32_t i, void** d_ptr, void* ipc_handle) {
+    if (!p || !d_ptr || i >= 4) return fail(CLAIRPLAN_EINVAL, "invalid argument");
+    CK(cudaSetDevice(p->device));
+    if (p->recvbufs.size() <= i) p->recvbufs.resize(i + 1, nullptr);
+    if (!p->recvbufs[i]) {
+        void* b = nullptr;
+        if (cudaMalloc(&b, std::max<uint64_t>(p->A, 1) * 4) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(CLAIRPLAN_ENOMEM, "receive buffer allocation failed");
+        }
+        p->recvbufs[i] = b;
+    }
+    *d_ptr = p->recvbufs[i];
+    if (ipc_handle) {
+        cudaIpcMemHandle_t h;
+        CK(cudaIpcGetMemHandle(&h, p->recvbufs[i]));
+        memcpy(ipc_handle, &h, sizeof(h));
+    }
+    return 0;
+}
+
+int clairplan_open_peer_buffer(clairplan_t p, const void* ipc_handle, void** d_ptr) {
+    if (!p || !ipc_handle || !d_ptr) return fail(CLAIRPLAN_EINVAL, "invalid argument");
+    CK(cudaSetDevice(p->device));
+    cudaIpcMemHandle_t h;
+    memcpy(&h, ipc_handle, sizeof(h));
+    void* ptr = nullptr;
+    CK(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    p->peerbufs.push_back(ptr);
+    *d_ptr = ptr;
+    return 0;
 }
 
 int clairplan_build_from_streams(clairplan_t p, const uint32_t* d_recv,

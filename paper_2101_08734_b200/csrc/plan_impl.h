@@ -152,7 +152,12 @@ struct clairplan_plan {
     // epochs whose whole inverse rows clairplan_generate_streams left in inv (dense sharded
     // build: not rebuilt from the received streams); [0, 0) = none
     uint32_t inv_own_lo = 0, inv_own_hi = 0;
+    std::vector<void*> recvbufs;   // multi-GPU fused exchange: this rank's receive buffers
+    std::vector<void*> peerbufs;   // opened peers' receive buffers (CUDA IPC)
     ~clairplan_plan() {
+        for (void* b : peerbufs) cudaIpcCloseMemHandle(b);
+        for (void* b : recvbufs)
+            if (b) cudaFree(b);
         if (hook_ev) cudaEventDestroy(hook_ev);
         if (xstream) cudaStreamDestroy(xstream);
         if (xev) cudaEventDestroy(xev);

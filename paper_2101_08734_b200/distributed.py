@@ -105,7 +105,7 @@ class DistributedPlan:
     mode "perms": permutation rows all-gathered to every rank (the earlier scheme, kept for
     A/B measurements)."""
 
-    def __init__(self, seed, samples, part, capacities_mb, sizes_mb, group=None, mode="streams",
+    def __init__(self, seed, samples, part, capacities_mb, sizes_mb, group=None, mode="p2p",
                  pipeline=False):
         import torch
         import torch.distributed as dist
@@ -130,6 +130,10 @@ class DistributedPlan:
         L.clairplan_epoch_prefix.argtypes = [C.c_void_p, C.c_uint32, C.POINTER(C.c_uint64)]
         self.L = L
         N = part.num_workers
+        self.p2p = False
+        if mode == "p2p":  # fused exchange through peer memory, else the all-to-all
+            mode = self.mode = "streams"
+            self.p2p = dist.get_backend(group) == "nccl" and bool(L.clairplan_p2p_supported(self.plan._h))
         if mode == "streams":
             pre = []
             for w in range(N + 1):
@@ -138,10 +142,13 @@ class DistributedPlan:
                 pre.append(int(v.value))
             wr = [worker_range(N, r, self.world) for r in range(self.world)]
             self.send_splits, self.recv_splits = stream_splits(pre, self.ranges, wr, self.rank)
-            self.pipeline = pipeline and dist.get_backend(group) == "nccl"
-            self.send = None if self.pipeline else torch.empty(max(sum(self.send_splits), 1),
-                                                               dtype=torch.int32, device="cuda")
-            self.recv = torch.empty(max(sum(self.recv_splits), 1), dtype=torch.int32, device="cuda")
+            if self.p2p:
+                self._setup_p2p(pre, wr)
+            self.pipeline = pipeline and dist.get_backend(group) == "nccl" and not self.p2p
+            self.send = None if (self.pipeline or self.p2p) else torch.empty(
+                max(sum(self.send_splits), 1), dtype=torch.int32, device="cuda")
+            self.recv = None if self.p2p else torch.empty(max(sum(self.recv_splits), 1),
+                                                          dtype=torch.int32, device="cuda")
             self.bounds = np.array([b for b, _ in self.ranges] + [part.epochs], np.uint32)
             # pipelined variant (NCCL): every rank's epochs in two halves, the first half's
             # all-to-all overlapping the second half's shuffle (measured at 4 ranks: generate +
@@ -195,6 +202,40 @@ class DistributedPlan:
         self.global_offsets = None
         self.rank_starts = None
 
+    def _setup_p2p(self, pre, wr):
+        """Two receive buffers per rank (alternating builds), their CUDA IPC handles exchanged
+        once; every rank's shuffle then writes each stream entry into its owner's buffer."""
+        torch, L, cp = self.torch, self.L, self.cp
+        L.clairplan_recv_buffer.argtypes = [C.c_void_p, C.c_uint32, C.POINTER(C.c_void_p), C.c_void_p]
+        L.clairplan_open_peer_buffer.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]
+        L.clairplan_generate_streams_p2p.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p,
+                                                     C.c_void_p, C.c_void_p, C.c_uint32]
+        own, handles = [], []
+        for i in range(2):
+            ptr, hb = C.c_void_p(), (C.c_char * 64)()
+            cp._check(L.clairplan_recv_buffer(self.plan._h, i, C.byref(ptr), hb))
+            own.append(ptr.value)
+            handles.append(bytes(hb))
+        allh = [None] * self.world
+        self.dist.all_gather_object(allh, handles, group=self.group)
+        self.dst_ptrs = [np.zeros(self.world, np.uint64) for _ in range(2)]
+        for r in range(self.world):
+            for i in range(2):
+                if r == self.rank:
+                    self.dst_ptrs[i][r] = own[i]
+                else:
+                    hb = (C.c_char * 64).from_buffer_copy(allh[r][i])
+                    ptr = C.c_void_p()
+                    cp._check(L.clairplan_open_peer_buffer(self.plan._h, hb, C.byref(ptr)))
+                    self.dst_ptrs[i][r] = ptr.value
+        self.own_recv = own
+        e0, ne = self.ranges[self.rank]
+        # rank d's buffer holds, from this rank, [d's worker w][my epoch e][Le(w)] at e0 * lloc(d)
+        self.deltas = np.array([e0 * (pre[we] - pre[wb]) - ne * pre[wb] for wb, we in wr], np.int64)
+        self.wbounds = np.array([wb for wb, _ in wr] + [self.part.num_workers], np.uint32)
+        self.iter = 0
+        self.flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+
     def _on_counts(self, _user):
         # runs inside the library's build call (same thread); the stream already waits for the
         # counts copy
@@ -222,6 +263,26 @@ class DistributedPlan:
             cp._check(self.L.clairplan_build_from_streams(
                 self.plan._h, C.c_void_p(self.recv.data_ptr()),
                 self.bounds2.ctypes.data_as(C.c_void_p), 2 * self.world))
+            t3 = time.perf_counter()
+            self.timings = {"generate_ms": round((t1 - t0) * 1e3, 3),
+                            "all_to_all_ms": round((t2 - t1) * 1e3, 3),
+                            "build_ms": round((t3 - t2) * 1e3, 3)}
+        elif self.mode == "streams" and self.p2p:
+            i = self.iter & 1
+            self.iter += 1
+            cp._check(self.L.clairplan_generate_streams_p2p(
+                self.plan._h, e0, n, self.dst_ptrs[i].ctypes.data_as(C.c_void_p),
+                self.deltas.ctypes.data_as(C.c_void_p), self.wbounds.ctypes.data_as(C.c_void_p),
+                self.world))
+            t1 = time.perf_counter()
+            # every rank's shuffle has finished writing into the peers' buffers (the library
+            # synchronised its stream): one small all-reduce orders them before the builds
+            self.dist.all_reduce(self.flag, group=self.group)
+            torch.cuda.current_stream().synchronize()
+            t2 = time.perf_counter()
+            cp._check(self.L.clairplan_build_from_streams(
+                self.plan._h, C.c_void_p(self.own_recv[i]),
+                self.bounds.ctypes.data_as(C.c_void_p), self.world))
             t3 = time.perf_counter()
             self.timings = {"generate_ms": round((t1 - t0) * 1e3, 3),
                             "all_to_all_ms": round((t2 - t1) * 1e3, 3),

@@ -27,15 +27,24 @@ def main():
              (1_281_167, 256, 32, 9, True, "sparse", None), (20_011, 9, 3, 7, False, "sparse", None),
              (262_144, 64, 16, 10, True, "sparse", [50.0, 1e9]), (30_000, 5, 7, 3, False, "sparse", None),
              (1_281_167, 256, 32, 9, True, "perms", None), (20_000, 7, 5, 13, True, "perms", None),
-             (20_011, 9, 3, 7, False, "pipelined", None), (1_281_167, 256, 32, 9, True, "pipelined", None)]
+             (20_011, 9, 3, 7, False, "pipelined", None), (1_281_167, 256, 32, 9, True, "pipelined", None),
+             (1_281_167, 256, 32, 9, True, "p2p", None), (20_011, 9, 3, 7, False, "p2p", None),
+             (262_144, 64, 16, 10, True, "p2p", [50.0, 1e9]), (20_000, 7, 5, 13, True, "p2p2", None),
+             (1_281_167, 256, 32, 9, True, "p2p2", None)]
     for (F, N, b, E, dl, mode, caps) in cases:
         sizes = cp.generate_sizes(F, 0.1077, 0.1, None, 1)
         part = cp.PartitionSpec(N, b * N, E, dl)
         caps = caps or [120.0 * F / 1e4, 900.0 * F / 1e4]
         if mode in ("dense", "sparse"):  # streams mode, forced sample-major pass flavour
             os.environ["CLAIRPLAN_DENSE"] = "1" if mode == "dense" else "0"
-        dp = DistributedPlan(42, F, part, caps, sizes, mode="perms" if mode == "perms" else "streams",
+        dmode = "perms" if mode == "perms" else "p2p" if mode.startswith("p2p") else "streams"
+        dp = DistributedPlan(42, F, part, caps, sizes, mode=dmode,
                              pipeline=(mode == "pipelined")).build()
+        if mode == "p2p2":  # second build: the other receive buffer
+            dp.build()
+        if mode.startswith("p2p") and not dp.p2p:
+            print(f"rank {rank}: p2p mode not taken", flush=True)
+            ok = False
         os.environ.pop("CLAIRPLAN_DENSE", None)
         full = cp.Plan(42, F, part, caps, sizes, device=torch.cuda.current_device()).build()
         wb, we = dp.wrange
