@@ -133,7 +133,8 @@ class DistributedPlan:
         self.p2p = False
         if mode == "p2p":  # fused exchange through peer memory, else the all-to-all
             mode = self.mode = "streams"
-            self.p2p = dist.get_backend(group) == "nccl" and bool(L.clairplan_p2p_supported(self.plan._h))
+            self.p2p = (dist.get_backend(group) == "nccl" and self.world <= 16 and
+                        bool(L.clairplan_p2p_supported(self.plan._h)))
         if mode == "streams":
             pre = []
             for w in range(N + 1):
@@ -143,7 +144,7 @@ class DistributedPlan:
             wr = [worker_range(N, r, self.world) for r in range(self.world)]
             self.send_splits, self.recv_splits = stream_splits(pre, self.ranges, wr, self.rank)
             if self.p2p:
-                self._setup_p2p(pre, wr)
+                self.p2p = self._setup_p2p(pre, wr)
             self.pipeline = pipeline and dist.get_backend(group) == "nccl" and not self.p2p
             self.send = None if (self.pipeline or self.p2p) else torch.empty(
                 max(sum(self.send_splits), 1), dtype=torch.int32, device="cuda")
@@ -204,30 +205,44 @@ class DistributedPlan:
 
     def _setup_p2p(self, pre, wr):
         """Two receive buffers per rank (alternating builds), their CUDA IPC handles exchanged
-        once; every rank's shuffle then writes each stream entry into its owner's buffer."""
+        once; every rank's shuffle then writes each stream entry into its owner's buffer.
+        Collective and all-or-nothing: returns False on every rank (all-to-all fallback) if
+        any rank could not allocate, export or open a buffer."""
         torch, L, cp = self.torch, self.L, self.cp
         L.clairplan_recv_buffer.argtypes = [C.c_void_p, C.c_uint32, C.POINTER(C.c_void_p), C.c_void_p]
         L.clairplan_open_peer_buffer.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]
         L.clairplan_generate_streams_p2p.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p,
                                                      C.c_void_p, C.c_void_p, C.c_uint32]
         own, handles = [], []
-        for i in range(2):
-            ptr, hb = C.c_void_p(), (C.c_char * 64)()
-            cp._check(L.clairplan_recv_buffer(self.plan._h, i, C.byref(ptr), hb))
-            own.append(ptr.value)
-            handles.append(bytes(hb))
+        try:
+            for i in range(2):
+                ptr, hb = C.c_void_p(), (C.c_char * 64)()
+                cp._check(L.clairplan_recv_buffer(self.plan._h, i, C.byref(ptr), hb))
+                own.append(ptr.value)
+                handles.append(bytes(hb))
+        except Exception:
+            handles = None
         allh = [None] * self.world
         self.dist.all_gather_object(allh, handles, group=self.group)
+        ok = all(h is not None for h in allh)
         self.dst_ptrs = [np.zeros(self.world, np.uint64) for _ in range(2)]
-        for r in range(self.world):
-            for i in range(2):
-                if r == self.rank:
-                    self.dst_ptrs[i][r] = own[i]
-                else:
-                    hb = (C.c_char * 64).from_buffer_copy(allh[r][i])
-                    ptr = C.c_void_p()
-                    cp._check(L.clairplan_open_peer_buffer(self.plan._h, hb, C.byref(ptr)))
-                    self.dst_ptrs[i][r] = ptr.value
+        if ok:
+            try:
+                for r in range(self.world):
+                    for i in range(2):
+                        if r == self.rank:
+                            self.dst_ptrs[i][r] = own[i]
+                        else:
+                            hb = (C.c_char * 64).from_buffer_copy(allh[r][i])
+                            ptr = C.c_void_p()
+                            cp._check(L.clairplan_open_peer_buffer(self.plan._h, hb, C.byref(ptr)))
+                            self.dst_ptrs[i][r] = ptr.value
+            except Exception:
+                ok = False
+        flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device="cuda")
+        self.dist.all_reduce(flag, op=self.dist.ReduceOp.MIN, group=self.group)
+        if int(flag.item()) == 0:
+            return False
         self.own_recv = own
         e0, ne = self.ranges[self.rank]
         # rank d's buffer holds, from this rank, [d's worker w][my epoch e][Le(w)] at e0 * lloc(d)
@@ -235,6 +250,7 @@ class DistributedPlan:
         self.wbounds = np.array([wb for wb, _ in wr] + [self.part.num_workers], np.uint32)
         self.iter = 0
         self.flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+        return True
 
     def _on_counts(self, _user):
         # runs inside the library's build call (same thread); the stream already waits for the
