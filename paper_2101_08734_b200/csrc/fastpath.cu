@@ -360,7 +360,9 @@ __global__ void __launch_bounds__(kThreads) seg_allfit_kernel(
 #pragma unroll
             for (int u = 0; u < kSU; ++u) {
                 const uint64_t t = t0 + 32 * u + lane;
-                k[u] = t < t_hi ? __ldcs(stream + g0 + t) : kNone;
+                // kept in L2 for pass B (an evict-first load here made pass B re-read the
+                // chunk from DRAM: +0.42 GB per config-2 plan)
+                k[u] = t < t_hi ? stream[g0 + t] : kNone;
             }
 #pragma unroll
             for (int u = 0; u < kSU; ++u)
@@ -407,7 +409,7 @@ __global__ void __launch_bounds__(kThreads) seg_allfit_kernel(
 #pragma unroll
             for (int u = 0; u < kSU; ++u) {
                 const uint64_t t = t0 + 32 * u + lane;
-                k[u] = t < t_hi ? stream[g0 + t] : kNone;
+                k[u] = t < t_hi ? __ldcs(stream + g0 + t) : kNone;  // last use
             }
 #pragma unroll
             for (int u = 0; u < kSU; ++u) {
