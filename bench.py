@@ -3,19 +3,24 @@
 
 A step = one full plan build (seed -> every epoch's permutation -> per-worker access
 streams -> (count, first-access) per (worker, sample) -> tier assignment -> prefetch orders
--> holder CSR) of the ImageNet-1k-shape, 90-epoch, 256-worker configuration
-(BASELINE.json configs[1]).  `value` = sample accesses per second of the device-resident
-build (sizes already in HBM), timed with the library's CUDA events on its stream; `e2e` is
-the same plan through the C ABI with host buffers (sizes H2D, every output D2H) inside the
-timed region.
+-> holder CSR).  Default workload: the ImageNet-22k shape, 14,197,122 samples, 90 epochs,
+1024 workers, per-worker batch 32 (BASELINE.json configs[3], the north-star shape and the
+largest configuration that builds on one B200; `--config N` selects another).  `value` =
+sample accesses per second of the device-resident build (sizes already in HBM), timed with
+the library's CUDA events on its stream; `e2e` is the same plan through the C ABI with host
+buffers (sizes H2D, every output D2H) inside the timed region.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C]
 
 Multi-GPU (torchrun, one rank per GPU, paper_2101_08734_b200/distributed.py): every rank
-draws the permutations of its epoch range, the rows are all-gathered over NVLink (NCCL), every
-rank builds the plan of its contiguous worker range and the holder-CSR offsets are merged with
-an NCCL all-gather of the per-sample holder counts; time = max over ranks (strong scaling: the
-same configuration at every N).
+generates the streams of its epoch range, the stream slices move to the ranks owning their
+workers over NVLink, every rank builds the plan of its contiguous worker range and the holder
+CSR offsets are merged with an NCCL all-gather of the per-sample holder counts; time = max
+over ranks (strong scaling: the same configuration at every N).
+
+The reference arm (`--impl reference`) and the `cpu_baseline` leg run the reference's own
+C++ functions (oracle/_ref) on all host threads over a bounded sample of the same workload
+(see cpu_reference_sample).
 """
 import argparse
 import json
@@ -162,16 +167,52 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm), "source": "nvidia-smi"}
 
 
-def cpu_reference_plan(cfg, sizes, threads):
-    """The reference's own functions (oracle/_ref, per-worker harness on all host threads);
-    only this leg and --impl reference execute anything under oracle/."""
+def cpu_reference_sample(cfg, sizes, threads):
+    """The reference's own functions (oracle/_ref, per-worker harness on all host threads) on a
+    bounded sample of the workload: every epoch's permutation and every worker's stream (the
+    whole of those phases), then the assignment + build_index of an evenly spaced worker
+    subset (all workers when N <= 2 * threads).  The assignment phase is linear in the
+    workers, so the full-plan time is estimated as perms + streams + (assign + index) * N / S.
+    Only this leg and --impl reference execute anything under oracle/."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     from _oracle import Ref
     ref = Ref()
+    N = cfg["N"]
+    S = N if N <= 2 * threads else 2 * threads
+    subset = np.unique(np.linspace(0, N - 1, S).round().astype(np.uint32))
+    S = len(subset)
     t0 = time.perf_counter()
-    ref.plan(SEED, cfg["F"], cfg["N"], cfg["b"] * cfg["N"], cfg["E"], True, list(CAPS), sizes,
-             mode=1, threads=threads)
-    return time.perf_counter() - t0
+    ph = ref.time_subset(SEED, cfg["F"], N, cfg["b"] * N, cfg["E"], True, list(CAPS), sizes,
+                         subset, threads)
+    wall = time.perf_counter() - t0
+    est = (ph[0] + ph[1] + (ph[2] + ph[3]) * N / S) / 1e3
+    return {"est_s": est, "wall_s": wall, "subset": S, "phases_ms": [round(x, 1) for x in ph]}
+
+
+def cpu_baseline_entry(cfg, smp, threads):
+    A = accesses_of(cfg)
+    exact = smp["subset"] == cfg["N"]
+    how = ("full plan" if exact else
+           f"{smp['subset']} of {cfg['N']} workers assigned, full-plan time = perms + streams + "
+           f"(assign + build_index) x {cfg['N']}/{smp['subset']}")
+    return {"value": A / smp["est_s"], "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": f"{cfg['name']}: reference epoch_permutation for all {cfg['E']} epochs, "
+                      f"every worker's stream, access_frequencies + nopfs_assign_caches + "
+                      f"build_index per worker on {threads} host threads ({how}); "
+                      f"phases ms {smp['phases_ms']}, sample wall {smp['wall_s']:.2f} s, "
+                      f"estimated plan {smp['est_s']:.2f} s"}
+
+
+def config_dict(cfg, world):
+    """The `config` of both arms (identical for the same workload and N)."""
+    return {"workload": cfg["name"], "samples": cfg["F"], "workers": cfg["N"],
+            "per_worker_batch": cfg["b"], "epochs": cfg["E"], "seed": SEED,
+            "capacities_mb": list(CAPS), "drop_last": True,
+            "l2": "256 MB flush before every timed step (device arm)",
+            "sharding": ("single GPU" if world == 1 else
+                         f"epochs sharded over {world} GPUs for the permutations and stream "
+                         "cutting, streams exchanged over NVLink, worker ranges for the rest, "
+                         "holder offsets merged by NCCL all-gather")}
 
 
 def run_reference(args, cfg):
@@ -179,26 +220,26 @@ def run_reference(args, cfg):
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    from paper_2101_08734_b200 import clairplan as cp
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from _oracle import Ref  # sizes from the reference's own DatasetModel::generate
     mu, sd, tot = cfg["sizes"]
-    sizes = cp.generate_sizes(cfg["F"], mu, sd, tot, 1)
+    sizes = Ref().generate_sizes(cfg["F"], mu, sd, tot, 1)
     for _ in range(args.warmup):
-        cpu_reference_plan(cfg, sizes, threads)
-    times = [cpu_reference_plan(cfg, sizes, threads) for _ in range(args.steps)]
-    A = accesses_of(cfg)
-    t = statistics.mean(times)
-    v = A / t
+        cpu_reference_sample(cfg, sizes, threads)
+    smps = [cpu_reference_sample(cfg, sizes, threads) for _ in range(args.steps)]
+    smp = dict(smps[-1])
+    smp["est_s"] = statistics.mean(x["est_s"] for x in smps)
+    smp["wall_s"] = statistics.mean(x["wall_s"] for x in smps)
+    cpu = cpu_baseline_entry(cfg, smp, threads)
+    v = cpu["value"]
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": smp["est_s"] * 1e3,
+        "sample_wall_ms_per_step": smp["wall_s"] * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic (seed-generated, BASELINE config shapes)",
-        "config": {"workload": cfg["name"], "samples": cfg["F"], "workers": cfg["N"],
-                   "per_worker_batch": cfg["b"], "epochs": cfg["E"], "seed": SEED},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
-                         "sample": f"full {cfg['name']} plan via the reference's epoch_permutation"
-                                   "/access_frequencies/nopfs_assign_caches/build_index "
-                                   "(per-worker decomposition on all host threads)"},
+        "config": config_dict(cfg, world),
+        "cpu_baseline": cpu,
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
 
@@ -318,13 +359,9 @@ def run_ours(args, cfg):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
         try:
-            threads = os.cpu_count() or 1
-            t = cpu_reference_plan(cfg, sizes, threads)
-            cpu = {"value": accesses_of(cfg) / t, "unit": UNIT, "cores": threads,
-                   "kind": "reference",
-                   "sample": f"one full {cfg['name']} plan (reference functions, per-worker "
-                             f"decomposition on {threads} host threads), {t:.2f} s"}
+            cpu = cpu_baseline_entry(cfg, cpu_reference_sample(cfg, sizes, threads), threads)
         except Exception as ex:  # no oracle/_ref on this box
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                    "sample": f"unavailable: {ex}"}
@@ -348,15 +385,7 @@ def run_ours(args, cfg):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "u32", "data": "synthetic (seed-generated, BASELINE config shapes)",
-            "config": {"workload": cfg["name"], "samples": cfg["F"], "workers": N,
-                       "per_worker_batch": cfg["b"], "epochs": cfg["E"], "seed": SEED,
-                       "capacities_mb": list(CAPS), "drop_last": True,
-                       "l2": "256 MB flush before every timed step",
-                       "sharding": ("single GPU" if world == 1 else
-                                    f"epochs sharded over {world} GPUs for the permutations "
-                                    "and stream cutting, one NCCL all-to-all of the stream "
-                                    "slices, worker ranges for the rest, holder offsets "
-                                    "merged by NCCL all-gather")},
+            "config": config_dict(cfg, world),
             "plan_latency_ms": ms_step,
             "wall_ms_per_step": t_wall * 1e3 / args.steps,
             "accesses": int(A_all), "pairs": int(D_all),
@@ -420,7 +449,7 @@ def e2e_measure(cp, plan, build, sizes, cfg, args, world, A_all):
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
-    n = max(1, min(args.steps, 5))
+    n = max(1, args.steps)
     t = time.perf_counter()
     for _ in range(n):
         step()
@@ -446,7 +475,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--config", type=int, default=4, choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()

@@ -17,6 +17,7 @@
 //                        anonymous namespace, so restated here).  tests/ check mode 1 ==
 //                        mode 0 before it is trusted for large configs / the baseline.
 #include <atomic>
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -36,6 +37,15 @@ using namespace clairsim;
 namespace {
 
 thread_local std::string g_err;
+// wall-clock phases of the last ref_plan_build_subset on this thread (ms): permutations,
+// stream cutting, per-worker assignment, build_index (the CPU-baseline sample extrapolates
+// the assignment phase of a worker subset to all workers)
+thread_local double g_phase_ms[4] = {0, 0, 0, 0};
+
+double now_ms() {
+    return std::chrono::duration<double, std::milli>(
+               std::chrono::steady_clock::now().time_since_epoch()).count();
+}
 
 struct RefPlan {
     uint32_t F = 0;
@@ -92,6 +102,10 @@ void flatten_holders(RefPlan& p) {
 extern "C" {
 
 const char* ref_last_error() { return g_err.c_str(); }
+
+void ref_last_phase_ms(double* out) {
+    for (int i = 0; i < 4; ++i) out[i] = g_phase_ms[i];
+}
 
 // CounterRng stream values (rng.hpp:36-47).
 int ref_rng_stream(uint64_t seed, uint64_t tag, uint64_t start, uint64_t n, uint64_t* out) {
@@ -198,10 +212,13 @@ void* ref_plan_build_subset(uint64_t seed, uint32_t F, uint32_t N, uint32_t B, u
         PartitionSpec part{N, B, E, drop_last != 0};
         const DatasetModel dataset = DatasetModel::from_sizes(std::vector<double>(sizes, sizes + F));
         part.validate(F);
+        double t0 = now_ms();
         std::vector<std::vector<uint32_t>> perms(E);
         parallel_for(E, threads, [&](uint64_t e) {
             perms[e] = epoch_permutation(Seed{seed}, static_cast<uint32_t>(e), F);
         });
+        double t1 = now_ms();
+        g_phase_ms[0] = t1 - t0;
         const uint64_t full = F / B;
         const uint64_t tail = part.drop_last ? 0 : F % B;
         const uint64_t nb = full + (tail > 0 ? 1 : 0);
@@ -222,6 +239,8 @@ void* ref_plan_build_subset(uint64_t seed, uint32_t F, uint32_t N, uint32_t B, u
                 st.epoch_offsets.push_back(st.entries.size());
             }
         });
+        t0 = now_ms();
+        g_phase_ms[1] = t0 - t1;
         perms.clear();
         perms.shrink_to_fit();
         p->assign.class_lists.assign(N, std::vector<std::vector<uint32_t>>(J));
@@ -236,7 +255,10 @@ void* ref_plan_build_subset(uint64_t seed, uint32_t F, uint32_t N, uint32_t B, u
             auto one = nopfs_assign_caches({freq}, cfg1, dataset, {st});
             if (J > 0) p->assign.class_lists[w] = std::move(one.class_lists[0]);
         });
+        t1 = now_ms();
+        g_phase_ms[2] = t1 - t0;
         p->assign.build_index(F);
+        g_phase_ms[3] = now_ms() - t1;
         flatten_holders(*p);
         return p.release();
     } catch (const std::exception& e) {

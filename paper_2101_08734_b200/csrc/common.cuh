@@ -117,7 +117,7 @@ struct Part {
     uint64_t off0;                   // stream_offset(wbegin)
     uint32_t ebase;                  // first epoch held in the stream (epoch-range streams)
     uint32_t pow2, lgB, lgBase;      // B and base powers of two, no remainder, no tail: shifts
-    uint32_t Fp;                     // row pitch of the u16 [E][F] arrays (info, rank): F to 8
+    uint32_t Fp;                     // row pitch of the [E][F] u8/u16 arrays (info, rank): F to 16
     FastDiv dB, dFull1, dFull0, dTail1, dTail0;  // B, base+1, base, tbase+1, tbase
 
     __host__ __device__ uint64_t len(uint32_t w) const { return base + (w < extra ? 1 : 0); }
@@ -216,7 +216,7 @@ inline Part make_part(uint32_t F, uint32_t N, uint32_t B, uint32_t E, bool drop_
     };
     p.lgB = lg(B);
     p.lgBase = lg(p.base);
-    p.Fp = (F + 7u) & ~7u;
+    p.Fp = (F + 15u) & ~15u;
     p.pow2 = (p.extra == 0 && p.tail == 0 && p.base >= 1 && (1ull << p.lgB) == B &&
               (1ull << p.lgBase) == p.base) ? 1u : 0u;
     return p;
@@ -241,6 +241,19 @@ __device__ __forceinline__ T warp_sum(T v) {
 inline unsigned env_uint(const char* name, unsigned def) {
     const char* v = getenv(name);
     return v ? (unsigned)atoi(v) : def;
+}
+
+// Grid of a grid-stride kernel whose work order matters (epoch-major passes): never more CTAs
+// than can be resident at once, so every CTA walks the work in lockstep with the others.
+template <typename K>
+inline unsigned resident_grid(K kernel, int threads, size_t smem, unsigned per_sm_cap) {
+    int dev = 0, nsm = 148, nb = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, threads, smem);
+    if (nb < 1) nb = 1;
+    if ((unsigned)nb > per_sm_cap) nb = (int)per_sm_cap;
+    return (unsigned)(nb * nsm);
 }
 
 inline unsigned grid_for(uint64_t n, unsigned per_block, unsigned cap = 148u * 64u) {

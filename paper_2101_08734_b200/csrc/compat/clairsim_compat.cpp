@@ -193,7 +193,8 @@ CacheAssignment nopfs_assign_caches(const std::vector<FrequencyTable>& freqs,
         const uint32_t* dh = nullptr;
         uint64_t H = 0;
         check(clairplan_device_holders(h, &dho, &dh, &H));
-        if (H > 0xFFFFFFFFull) throw std::overflow_error("holder count exceeds the u32 CSR");
+        if (H > 0xFFFFFFFFull)
+            throw std::overflow_error("EOVERFLOW: holder count exceeds the u32 holder_offsets");
         std::vector<uint64_t> ho(F + 1);
         std::vector<uint32_t> hv(3 * H);
         check(clairplan_export_holders(h, ho.data(), hv.data(), H));
@@ -224,6 +225,11 @@ void CacheAssignment::build_index(uint64_t samples) {
         for (uint32_t j = 0; j < J; ++j)
             std::copy(class_lists[w][j].begin(), class_lists[w][j].end(),
                       flat.begin() + off[static_cast<size_t>(w) * J + j]);
+    // the reference's u32 holder_offsets (policies.hpp:59) cannot hold 2^32 or more holders:
+    // refuse (EOVERFLOW) instead of truncating; clairplan_build_index keeps u64 offsets
+    if (flat.size() > 0xFFFFFFFFull)
+        throw std::overflow_error("EOVERFLOW: " + std::to_string(flat.size()) +
+                                  " holders exceed the u32 holder_offsets of CacheAssignment");
     std::vector<uint64_t> ho(samples + 1);
     std::vector<uint32_t> hv(3 * flat.size() + 3);
     check(clairplan_build_index(N, J, samples, flat.data(), off.data(), ho.data(), hv.data(),

@@ -244,8 +244,9 @@ constexpr int kSU = 4;
 // With `sizes`: also the sum and minimum of the sizes of the segment's first accesses
 // (segsum/segmin), the input of the whole-worker fit test (fit_check_kernel).
 // seghist[(wl*E + (E - c))*E + e] = first accesses with count c in segment (w, e)
+template <typename IT>
 __global__ void __launch_bounds__(kThreads) seg_hist_kernel(Part part, const uint32_t* __restrict__ stream,
-                                                             const uint16_t* __restrict__ info,
+                                                             const IT* __restrict__ info,
                                                              const uint32_t* __restrict__ cpos,
                                                              uint32_t* __restrict__ seghist,
                                                              uint32_t* __restrict__ segcnt) {
@@ -262,7 +263,7 @@ __global__ void __launch_bounds__(kThreads) seg_hist_kernel(Part part, const uin
         __syncwarp();
         const uint64_t Le = part.epoch_len(w);
         const uint64_t g0 = part.stream_offset(w) + (uint64_t)e * Le;
-        const uint16_t* row = info + (size_t)e * part.Fp;
+        const IT* row = info + (size_t)e * part.Fp;
         uint32_t tot = 0;
         for (uint64_t t0 = 0; t0 < Le; t0 += 32 * kSU) {
             uint32_t k[kSU], c[kSU];
@@ -328,8 +329,9 @@ void launch_segcnt(cudaStream_t s, uint32_t nloc, uint32_t E, const uint32_t* se
 //              worker's stream offset.
 constexpr unsigned long long kStAgg = 1ull << 62, kStInc = 2ull << 62, kStMask = (1ull << 62) - 1;
 
+template <typename IT>
 __global__ void __launch_bounds__(kThreads) seg_allfit_kernel(
-    Part part, const uint32_t* __restrict__ stream, const uint16_t* __restrict__ info,
+    Part part, const uint32_t* __restrict__ stream, const IT* __restrict__ info,
     const uint32_t* __restrict__ cpos, uint32_t MB, uint32_t C,
     unsigned long long* __restrict__ status, uint32_t* __restrict__ ticket,
     uint32_t* __restrict__ rec, uint32_t* __restrict__ class_list, const uint32_t* __restrict__ gate) {
@@ -351,7 +353,7 @@ __global__ void __launch_bounds__(kThreads) seg_allfit_kernel(
         const uint64_t t_hi = t_lo + kAllfitChunk < Le ? t_lo + kAllfitChunk : Le;
         const uint64_t sw = part.stream_offset(w);
         const uint64_t g0 = sw + (uint64_t)e * Le;
-        const uint16_t* row = info + (size_t)e * part.Fp;
+        const IT* row = info + (size_t)e * part.Fp;
         const uint64_t x = ((uint64_t)wl * E + e) * C + ci;  // worker-major chunk index
         // pass A: first-access ballots, lane b keeps block b's
         uint32_t mymask = 0, tot = 0;
@@ -447,15 +449,20 @@ __global__ void allfit_meta_kernel(Part part, uint32_t J, const uint32_t* __rest
     }
 }
 
-void launch_seg_allfit(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info,
-                       const uint32_t* cpos, uint32_t MB, uint32_t C, unsigned long long* status,
-                       uint32_t* ticket, uint32_t* rec, uint32_t* class_list, const uint32_t* gate) {
+void launch_seg_allfit(cudaStream_t s, const Part& part, const uint32_t* stream, const void* info,
+                       bool info8, const uint32_t* cpos, uint32_t MB, uint32_t C,
+                       unsigned long long* status, uint32_t* ticket, uint32_t* rec,
+                       uint32_t* class_list, const uint32_t* gate) {
     const uint64_t nch = (uint64_t)(part.wend - part.wbegin) * part.E * C;
     cudaMemsetAsync(status, 0, nch * 8, s);
     cudaMemsetAsync(ticket, 0, 4, s);
-    static const unsigned gm = env_uint("CLAIRPLAN_GRID_ALLFIT", 8);
-    seg_allfit_kernel<<<grid_for(nch * 32, kThreads, 148u * gm), kThreads, 0, s>>>(
-        part, stream, info, cpos, MB, C, status, ticket, rec, class_list, gate);
+    const unsigned grid = grid_for(nch * 32, kThreads, 148u * 8u);
+    if (info8)
+        seg_allfit_kernel<uint8_t><<<grid, kThreads, 0, s>>>(
+            part, stream, static_cast<const uint8_t*>(info), cpos, MB, C, status, ticket, rec, class_list, gate);
+    else
+        seg_allfit_kernel<uint16_t><<<grid, kThreads, 0, s>>>(
+            part, stream, static_cast<const uint16_t*>(info), cpos, MB, C, status, ticket, rec, class_list, gate);
 }
 
 void launch_allfit_meta(cudaStream_t s, const Part& part, uint32_t J, const uint32_t* wcnt,
@@ -487,8 +494,9 @@ void launch_allfit_decide(cudaStream_t s, uint32_t nloc, const unsigned long lon
 }
 
 // ---------------------------------------------------------------------------- K4c
+template <typename IT>
 __global__ void __launch_bounds__(kThreads) seg_write_kernel2(
-    Part part, const uint32_t* __restrict__ stream, const uint16_t* __restrict__ info, const uint32_t* __restrict__ cpos,
+    Part part, const uint32_t* __restrict__ stream, const IT* __restrict__ info, const uint32_t* __restrict__ cpos,
     const double* __restrict__ sizes, const uint64_t* __restrict__ seg_off,
     const uint64_t* __restrict__ sorted_base, uint32_t MB, uint32_t* __restrict__ dest,
     double* __restrict__ sorted_size, uint32_t* __restrict__ blkmask,
@@ -506,7 +514,7 @@ __global__ void __launch_bounds__(kThreads) seg_write_kernel2(
         __syncwarp();
         const uint64_t Le = part.epoch_len(w);
         const uint64_t g0 = part.stream_offset(w) + (uint64_t)e * Le;
-        const uint16_t* row = info + (size_t)e * part.Fp;
+        const IT* row = info + (size_t)e * part.Fp;
         const uint64_t fbase = seg_off[(uint64_t)wl * E + e];
         const uint64_t* sbase = sorted_base + (uint64_t)wl * E * E + e;  // + (E-c)*E
         const uint64_t blk0 = ((uint64_t)wl * E + e) * MB;
@@ -876,9 +884,9 @@ __device__ __forceinline__ void st_issue(const uint32_t* inv, uint32_t E, uint32
     cp_async_commit();
 }
 
-template <int R>
+template <int R, typename IT>
 __global__ void __launch_bounds__(kThreads) sample_tile_kernel(Part part, const uint32_t* __restrict__ inv,
-                                                               uint16_t* __restrict__ info,
+                                                               IT* __restrict__ info,
                                                                uint16_t* __restrict__ rank16,
                                                                uint32_t* __restrict__ pair_count,
                                                                uint32_t W,
@@ -889,8 +897,9 @@ __global__ void __launch_bounds__(kThreads) sample_tile_kernel(Part part, const 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
     const uint32_t nloc = part.wend - part.wbegin;
     uint32_t* tin[2] = {sm, sm + E * kStInv};
-    uint16_t* oinfo = reinterpret_cast<uint16_t*>(sm + 2 * E * kStInv);  // [E][34]
-    uint16_t* orank = oinfo + E * kStOut;                                 // [E][34]
+    uint16_t* orank = reinterpret_cast<uint16_t*>(sm + 2 * E * kStInv);  // [E][34]
+    IT* oinfo = reinterpret_cast<IT*>(orank + E * kStOut);                 // [E][kSI]
+    constexpr uint32_t kSI = sizeof(IT) == 1 ? 36 : kStOut;  // row stride: 4-B aligned rows
     uint32_t* tabs = sm + 2 * E * kStInv + E * kStOut;                    // per warp
     uint32_t* fe = tabs + warp * (2 * W * 32 + W);  // [nloc] first epoch
     uint32_t* cnt = fe + W * 32;                     // [nloc] count
@@ -977,9 +986,10 @@ __global__ void __launch_bounds__(kThreads) sample_tile_kernel(Part part, const 
                 const uint32_t pw = __shfl_sync(0xffffffffu, pre, xw);
                 const uint32_t ww = __shfl_sync(0xffffffffu, word, xw);
                 if (e < E) {
-                    uint16_t ci = 0, rk = 0xFFFFu;
+                    IT ci = 0;
+                    uint16_t rk = 0xFFFFu;
                     if (x != kNone && fe[x] == e) {
-                        ci = (uint16_t)cnt[x];
+                        ci = (IT)cnt[x];
                         rk = (uint16_t)(pw + __popc(ww & ((1u << (x & 31)) - 1u)));
                         if (seghist) atomicAdd(&seghist[((uint64_t)x * E + (E - ci)) * E + e], 1u);
                         if (ws.sum) {
@@ -987,7 +997,7 @@ __global__ void __launch_bounds__(kThreads) sample_tile_kernel(Part part, const 
                             atomicAdd(&ccnt[x], 1u);
                         }
                     }
-                    oinfo[e * kStOut + s] = ci;
+                    oinfo[e * kSI + s] = ci;
                     orank[e * kStOut + s] = rk;
                 }
             }
@@ -1004,24 +1014,28 @@ __global__ void __launch_bounds__(kThreads) sample_tile_kernel(Part part, const 
             __syncwarp();
         }
         __syncthreads();
-        // coalesced write-back of the info / rank rows: 16-B stores of 8 samples (the rows
-        // are pitched to Fp, a multiple of 8 samples), scalar for a partial last tile
+        // coalesced write-back of the info / rank rows: 16-B stores of 16 / 8 samples (the
+        // rows are pitched to Fp, a multiple of 16 samples), scalar for a partial last tile
         const uint32_t n = (uint32_t)(F - k0 < 32 ? F - k0 : 32);
         if (n == 32) {
+            constexpr uint32_t IQ = 16 / sizeof(IT);  // samples per 16-B info store
             for (uint32_t idx = threadIdx.x; idx < E * 4; idx += blockDim.x) {
                 const uint32_t e = idx >> 2, q = (idx & 3) * 8;
-                const uint32_t* si = reinterpret_cast<const uint32_t*>(oinfo + e * kStOut + q);
                 const uint32_t* sr = reinterpret_cast<const uint32_t*>(orank + e * kStOut + q);
-                __stcs(reinterpret_cast<uint4*>(info + (size_t)e * part.Fp + k0 + q),
-                       make_uint4(si[0], si[1], si[2], si[3]));
                 __stcs(reinterpret_cast<uint4*>(rank16 + (size_t)e * part.Fp + k0 + q),
                        make_uint4(sr[0], sr[1], sr[2], sr[3]));
+            }
+            for (uint32_t idx = threadIdx.x; idx < E * (32 / IQ); idx += blockDim.x) {
+                const uint32_t e = idx / (32 / IQ), q = (idx % (32 / IQ)) * IQ;
+                const uint32_t* si = reinterpret_cast<const uint32_t*>(oinfo + e * kSI + q);
+                __stcs(reinterpret_cast<uint4*>(info + (size_t)e * part.Fp + k0 + q),
+                       make_uint4(si[0], si[1], si[2], si[3]));
             }
         } else {
             for (uint32_t idx = threadIdx.x; idx < E * 32; idx += blockDim.x) {
                 const uint32_t e = idx >> 5, l = idx & 31;
                 if (l < n) {
-                    __stcs(info + (size_t)e * part.Fp + k0 + l, oinfo[e * kStOut + l]);
+                    __stcs(info + (size_t)e * part.Fp + k0 + l, oinfo[e * kSI + l]);
                     __stcs(rank16 + (size_t)e * part.Fp + k0 + l, orank[e * kStOut + l]);
                 }
             }
@@ -1120,7 +1134,7 @@ bool tile_path_ok(const Part& part) {
     return (part.wend - part.wbegin) <= kTileWorkers && part.E <= 128;
 }
 
-void launch_sample_tile(cudaStream_t s, const Part& part, const uint32_t* inv, uint16_t* info,
+void launch_sample_tile(cudaStream_t s, const Part& part, const uint32_t* inv, void* info, bool info8,
                         uint16_t* rank16, uint32_t* pair_count, uint32_t* seghist,
                         const WorkerSums& ws) {
     const uint32_t nloc = part.wend - part.wbegin;
@@ -1133,10 +1147,17 @@ void launch_sample_tile(cudaStream_t s, const Part& part, const uint32_t* inv, u
     const unsigned grid = grid_for(tiles, 1, 148u * gm);
 #define ST_LAUNCH(RV)                                                                             \
     do {                                                                                          \
-        cudaFuncSetAttribute(sample_tile_kernel<RV>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
-                             (int)smem);                                                          \
-        sample_tile_kernel<RV><<<grid, kThreads, smem, s>>>(part, inv, info, rank16, pair_count,  \
-                                                            W, seghist, ws);                      \
+        if (info8) {                                                                              \
+            cudaFuncSetAttribute(sample_tile_kernel<RV, uint8_t>,                                 \
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);         \
+            sample_tile_kernel<RV, uint8_t><<<grid, kThreads, smem, s>>>(                         \
+                part, inv, static_cast<uint8_t*>(info), rank16, pair_count, W, seghist, ws);      \
+        } else {                                                                                  \
+            cudaFuncSetAttribute(sample_tile_kernel<RV, uint16_t>,                                \
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);         \
+            sample_tile_kernel<RV, uint16_t><<<grid, kThreads, smem, s>>>(                        \
+                part, inv, static_cast<uint16_t*>(info), rank16, pair_count, W, seghist, ws);     \
+        }                                                                                         \
     } while (0)
     const uint32_t R = (part.E + 31) / 32;
     if (R == 1) ST_LAUNCH(1);
@@ -1160,13 +1181,20 @@ void launch_sample_hash(cudaStream_t s, const Part& part, const uint32_t* inv, u
         part, inv, info, rank16, pair_count, list, nlist, hs, W, seghist);
 }
 
-void launch_seg_hist(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info,
-                     const uint32_t* cpos, uint32_t* seghist, uint32_t* segcnt) {
+void launch_seg_hist(cudaStream_t s, const Part& part, const uint32_t* stream, const void* info,
+                     bool info8, const uint32_t* cpos, uint32_t* seghist, uint32_t* segcnt) {
     const uint64_t nseg = (uint64_t)(part.wend - part.wbegin) * part.E;
     const size_t smem = (size_t)(kThreads / 32) * part.E * 4;
-    cudaFuncSetAttribute(seg_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    seg_hist_kernel<<<grid_for(nseg * 32, kThreads, 148u * 64u), kThreads, smem, s>>>(
-        part, stream, info, cpos, seghist, segcnt);
+    const unsigned grid = grid_for(nseg * 32, kThreads, 148u * 64u);
+    if (info8) {
+        cudaFuncSetAttribute(seg_hist_kernel<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        seg_hist_kernel<uint8_t><<<grid, kThreads, smem, s>>>(part, stream, static_cast<const uint8_t*>(info),
+                                                              cpos, seghist, segcnt);
+    } else {
+        cudaFuncSetAttribute(seg_hist_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        seg_hist_kernel<uint16_t><<<grid, kThreads, smem, s>>>(part, stream, static_cast<const uint16_t*>(info),
+                                                               cpos, seghist, segcnt);
+    }
 }
 
 
@@ -1176,8 +1204,8 @@ void launch_seg_write2(cudaStream_t s, const Part& part, const uint32_t* stream,
                        uint32_t* blkbase) {
     const uint64_t nseg = (uint64_t)(part.wend - part.wbegin) * part.E;
     const size_t smem = (size_t)(kThreads / 32) * part.E * 4;
-    cudaFuncSetAttribute(seg_write_kernel2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    seg_write_kernel2<<<grid_for(nseg * 32, kThreads, 148u * 64u), kThreads, smem, s>>>(
+    cudaFuncSetAttribute(seg_write_kernel2<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    seg_write_kernel2<uint16_t><<<grid_for(nseg * 32, kThreads, 148u * 64u), kThreads, smem, s>>>(
         part, stream, info, cpos, sizes, seg_off, sorted_base, MB, dest, sorted_size, blkmask, blkbase);
 }
 

@@ -134,8 +134,13 @@ __global__ void __launch_bounds__(kThreads) ff_stats_kernel(TileMap tm,
         for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
             const double v = p[i];
             s += v;
-            mn = fmin(mn, v);
-            mx = fmax(mx, v);
+            if (v >= 0.0 && v < INFINITY) {
+                mn = fmin(mn, v);
+                mx = fmax(mx, v);
+            } else {  // negative / NaN / inf: no fast path may touch this chunk (see below)
+                mn = -INFINITY;
+                mx = INFINITY;
+            }
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -303,15 +308,19 @@ __global__ void ff_resolve_kernel(TileMap tm, const uint64_t* __restrict__ seg_b
                 const uint64_t i = off + s0 + lane;
                 const bool valid = s0 + lane < n;
                 const double s = valid ? base[i] : 0.0;
+                // the monoid and the skip assume finite non-negative sizes; any other value
+                // (policies.cpp:47 `s <= remaining` never takes a NaN and always a negative
+                // size) sends the sub-chunk through the exact chain
+                const bool odd = __any_sync(0xffffffffu, valid && !(s >= 0.0 && s < INFINITY));
                 const double smin = warp_min(valid ? s : INFINITY);
                 uint8_t flag = 0;
-                if (r < smin) {
+                if (!odd && r < smin) {
                     if (valid) flags[i] = 0;
                     continue;
                 }
                 const double smax = warp_max(valid ? s : 0.0);
                 bool done = false;
-                if (r > 0) {
+                if (!odd && r > 0) {
                     const int kk = binade(r);
                     if (kk > -1000 && ldexp(1.0, kk) >= smax) {
                         Mono m = valid ? mono_elem(s, kk) : mono_id();

@@ -191,7 +191,7 @@ bool lane_path_ok(const Part& part);
 void launch_sample_lanes(cudaStream_t s, const Part& part, const uint32_t* inv, uint16_t* info,
                          uint16_t* rank16, uint32_t* pair_count, uint32_t* seghist);
 bool tile_path_ok(const Part& part);
-void launch_sample_tile(cudaStream_t s, const Part& part, const uint32_t* inv, uint16_t* info,
+void launch_sample_tile(cudaStream_t s, const Part& part, const uint32_t* inv, void* info, bool info8,
                         uint16_t* rank16, uint32_t* pair_count, uint32_t* seghist,
                         const WorkerSums& ws);
 void launch_sample_hash(cudaStream_t s, const Part& part, const uint32_t* inv, uint16_t* info,
@@ -199,13 +199,13 @@ void launch_sample_hash(cudaStream_t s, const Part& part, const uint32_t* inv, u
                         const uint32_t* nlist, uint64_t max_items, uint32_t* seghist);
 void launch_segcnt(cudaStream_t s, uint32_t nloc, uint32_t E, const uint32_t* seghist,
                    uint32_t* segcnt);
-void launch_seg_hist(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info,
-                     const uint32_t* cpos, uint32_t* seghist, uint32_t* segcnt);
+void launch_seg_hist(cudaStream_t s, const Part& part, const uint32_t* stream, const void* info,
+                     bool info8, const uint32_t* cpos, uint32_t* seghist, uint32_t* segcnt);
 constexpr uint32_t kAllfitChunk = 1024;
-void launch_seg_allfit(cudaStream_t s, const Part& part, const uint32_t* stream, const uint16_t* info,
-                       const uint32_t* cpos, uint32_t MB, uint32_t C, unsigned long long* status,
-                       uint32_t* ticket, uint32_t* rec, uint32_t* class_list,
-                       const uint32_t* gate = nullptr);
+void launch_seg_allfit(cudaStream_t s, const Part& part, const uint32_t* stream, const void* info,
+                       bool info8, const uint32_t* cpos, uint32_t MB, uint32_t C,
+                       unsigned long long* status, uint32_t* ticket, uint32_t* rec,
+                       uint32_t* class_list, const uint32_t* gate = nullptr);
 void launch_allfit_meta(cudaStream_t s, const Part& part, uint32_t J, const uint32_t* wcnt,
                         uint64_t* clen, uint64_t* cstart, uint32_t* cbase,
                         const uint32_t* gate = nullptr);
@@ -215,6 +215,18 @@ void launch_seg_write2(cudaStream_t s, const Part& part, const uint32_t* stream,
                        const double* sizes, const uint64_t* seg_off, const uint64_t* sorted_base,
                        uint32_t MB, uint32_t* dest, double* sorted_size, uint32_t* blkmask,
                        uint32_t* blkbase);
+// tier.cu (dense tier path)
+void launch_seg_write3(cudaStream_t s, const Part& part, const uint32_t* stream, const void* info,
+                       bool info8, const uint64_t* seg_off, const uint64_t* sorted_base, uint32_t MB,
+                       uint32_t* dest, uint32_t* sorted_k, uint32_t* blkmask, uint32_t* blkbase);
+void launch_gather_sorted_sizes(cudaStream_t s, const uint32_t* sorted_k, const double* sizes,
+                                uint64_t n, double* out);
+void launch_fill_class(cudaStream_t s, uint8_t* cls, uint64_t n, uint8_t j);
+void launch_hp_fill(cudaStream_t s, const Part& part, const uint32_t* inv, const uint16_t* rank16,
+                    uint32_t MB, const uint32_t* rec, uint32_t np, uint32_t J, uint32_t Rp,
+                    const uint32_t* cbase, uint32_t* hp);
+void launch_holder_hp(cudaStream_t s, const Part& part, const uint32_t* inv, const uint16_t* rank16,
+                      const uint32_t* hp, const uint64_t* pair_off, uint32_t* holders);
 void launch_blk_codes(cudaStream_t s, const Part& part, uint32_t MB, const uint32_t* blkmask,
                       const uint32_t* blkbase, const uint32_t* dest, const uint8_t* cls_sorted,
                       uint32_t np, uint32_t J, uint32_t Rp, uint32_t* rec, uint32_t* ccount,

@@ -439,6 +439,21 @@ bool v2_ok(const clairplan_plan* p) {
            (uint64_t)p->nloc * part.E * part.E <= (1ull << 28);
 }
 
+// The whole-worker fit test of the all-fit path (allfit_decide_kernel) against capacity C,
+// on the per-worker sums of the last seed build: sizes non-negative and every worker's total
+// below C by more than any summation / chain rounding.  Then `s <= remaining` holds at every
+// step of the chain of any subset of a worker's candidates in any order.
+bool class_takes_all(const clairplan_plan* p, double C) {
+    if (!p->sums_ok || p->wcnt_h.size() != (size_t)p->nloc + 1 || p->wcnt_h[p->nloc]) return false;
+    for (uint32_t w = 0; w < p->nloc; ++w) {
+        if (p->wcnt_h[w] == 0) continue;
+        const double sw = (double)p->wsum_h[w] * 0x1.0p-20;
+        const double tol = ((double)p->wcnt_h[w] + 1024.0) * std::max(C, sw) * 0x1.0p-48;
+        if (!(C - sw > tol)) return false;
+    }
+    return true;
+}
+
 // First fit of the tier-ordered sizes, class by class (pack_first_fit, policies.cpp:40-55);
 // cls[s] = class of tier-ordered element s (0 = not cached).
 int first_fit_classes(clairplan_plan* p, const double* ssize, uint8_t* cls) {
@@ -460,6 +475,13 @@ int first_fit_classes(clairplan_plan* p, const double* ssize, uint8_t* cls) {
     uint64_t remaining = D, prev_total = D;
     for (uint32_t j = 1; j <= J; ++j) {
         if (remaining == 0) break;
+        if (j > 1 && class_takes_all(p, p->caps[j - 1])) {
+            // every worker's whole candidate set fits class j: its first-fit chain over the
+            // rejects of classes < j takes all of them (policies.cpp:40-55, any order)
+            launch_fill_class(s, cls, D, (uint8_t)j);
+            ++p->launches;
+            break;
+        }
         uint8_t* taken = cls;
         if (j > 1) {
             // rejects of the previous class, still in tier order, packed for this class
@@ -506,12 +528,24 @@ int first_fit_classes(clairplan_plan* p, const double* ssize, uint8_t* cls) {
 
 // (count at first access) source of the segment passes: info[e][k] (dense sample pass) or
 // einfo[csr slot] with cpos[stream index] = csr slot (sparse sample pass of a sharded handle)
-inline const uint16_t* info_src(clairplan_plan* p) {
-    return p->sparse ? p->einfo.get<uint16_t>() : p->info16.get<uint16_t>();
+inline const void* info_src(clairplan_plan* p) {
+    return p->sparse ? p->einfo.get<uint16_t>() : p->info16.get<void>();
 }
 
 int holders_v2(clairplan_plan* p);
 int no_classes_v2(clairplan_plan* p);
+
+// holder records from the [E][F] class/position rows (tier.cu): dense sample-major arrays,
+// classes and list positions fit 4 + 28 bits
+bool hp_path_ok(const clairplan_plan* p) {
+    const Part& part = p->part;
+    uint64_t lmax = 0;
+    for (uint32_t w : {part.wbegin, part.wend - 1}) lmax = std::max<uint64_t>(lmax, part.E * part.epoch_len(w));
+    // (hp_fill + holder_hp measured 26.7 + 11.1 ms against holder_tile's 30 ms at the
+    // ImageNet-22k shape: latency-bound record gathers; off until that pass is faster)
+    static const bool on = env_uint("CLAIRPLAN_HP_PATH", 0) != 0;
+    return on && !p->sparse && !p->allfit && p->cfg.num_classes <= 15 && lmax < (1ull << 28);
+}
 
 // K6-K8 of the v2 path on the cached tier-ordered sizes / block masks: first fit, block class
 // records, class lists, holder CSR.  Also the whole of clairplan_reassign.
@@ -552,6 +586,14 @@ int assign_v2(clairplan_plan* p) {
         launch_class_lens(s, nloc, E, MB, J, cpre, nblk, clen);
         exclusive_scan(s, clen, (uint64_t)nloc * J, cstart, p->ws);
         launch_class_write(s, part, MB, stream_buf, rec, np, J, Rp, cbase, cstart, centries, nblk);
+        p->hp_path = hp_path_ok(p);
+        if (p->hp_path) {
+            uint32_t* hp = need<uint32_t>(p->hpos, (uint64_t)E * part.Fp, ok);
+            if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed (holder positions)");
+            launch_hp_fill(s, part, p->inv.get<uint32_t>(), p->rank16.get<uint16_t>(), MB, rec, np, J, Rp,
+                           cbase, hp);
+            ++p->launches;
+        }
         p->launches += 4 + 3 * J + 3;
         p->cl_contig = true;
         return holders_v2(p);
@@ -590,6 +632,8 @@ int holders_v2(clairplan_plan* p) {
             launch_holder_sparse(s, part, p->A, p->soff.get<uint64_t>(), p->stream_buf.get<uint32_t>(),
                                  p->csr.get<uint32_t>(), p->erank.get<uint16_t>(), MB, rec, np, J, Rp,
                                  cbase, poff, htmp, p->allfit);
+        else if (p->hp_path && !p->allfit)
+            launch_holder_hp(s, part, inv, rank16, p->hpos.get<uint32_t>(), poff, htmp);
         else
             launch_holder_tile(s, part, inv, rank16, MB, rec, np, J, Rp, cbase, poff, htmp, p->allfit);
         ++p->launches;
@@ -657,16 +701,26 @@ int tier_order_v2(clairplan_plan* p) {
     const uint64_t* segoff = p->seg_off.get<uint64_t>();
     if (!p->hist_ready) {  // all-fit build: the count histograms were not needed then
         const uint64_t NEE = (uint64_t)nloc * E * E;
-        launch_seg_hist(s, part, p->stream_buf.get<uint32_t>(), info_src(p), p->sparse ? p->cpos.get<uint32_t>() : nullptr,
+        launch_seg_hist(s, part, p->stream_buf.get<uint32_t>(), info_src(p), p->info8, p->sparse ? p->cpos.get<uint32_t>() : nullptr,
                         p->seghist.get<uint32_t>(), p->segcnt.get<uint32_t>());
         exclusive_scan(s, p->seghist.get<uint32_t>(), NEE, p->sorted_base.get<uint64_t>(), p->ws);
         exclusive_scan(s, p->segcnt.get<uint32_t>(), (uint64_t)nloc * E, p->seg_off.get<uint64_t>(), p->ws);
         p->launches += 4;
         p->hist_ready = true;
     }
-    launch_seg_write2(s, part, p->stream_buf.get<uint32_t>(), info_src(p), p->sparse ? p->cpos.get<uint32_t>() : nullptr,
-                      p->sizes.get<double>(), segoff, p->sorted_base.get<uint64_t>(), p->v2_mb, dest,
-                      ssize, p->blkmask.get<uint32_t>(), p->blkbase.get<uint32_t>());
+    if (p->sparse) {
+        launch_seg_write2(s, part, p->stream_buf.get<uint32_t>(), p->einfo.get<uint16_t>(), p->cpos.get<uint32_t>(),
+                          p->sizes.get<double>(), segoff, p->sorted_base.get<uint64_t>(), p->v2_mb, dest,
+                          ssize, p->blkmask.get<uint32_t>(), p->blkbase.get<uint32_t>());
+    } else {  // epoch-major segment CTAs, then the size gather on its own (tier.cu)
+        uint32_t* sk = need<uint32_t>(p->sorted_k, D, ok);
+        if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed (tier order)");
+        launch_seg_write3(s, part, p->stream_buf.get<uint32_t>(), info_src(p), p->info8, segoff,
+                          p->sorted_base.get<uint64_t>(), p->v2_mb, dest, sk,
+                          p->blkmask.get<uint32_t>(), p->blkbase.get<uint32_t>());
+        launch_gather_sorted_sizes(s, sk, p->sizes.get<double>(), D, ssize);
+        ++p->launches;
+    }
     launch_worker_segments(s, segoff, nloc, E, p->wbeg.get<uint64_t>(), p->wlen.get<uint64_t>());
     p->launches += 2;
     p->tier_ready = true;
@@ -694,14 +748,16 @@ int spec_allfit_launch(clairplan_plan* p, const uint32_t* gate) {
     uint32_t* ticket = need<uint32_t>(p->counters, 4, ok);
     uint32_t* htmp = need<uint32_t>(p->holders_tmp, 3 * std::max<uint64_t>(p->A, 1), ok);
     if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed (all-fit)");
+    // stage labels: the one segment pass writes the class lists (stage 6), the first fit is
+    // decided by the whole-worker test (no tier order, no first-fit chain)
     p->mark(3);
     p->mark(4);
     p->mark(5);
-    launch_seg_allfit(s, part, p->stream_buf.get<uint32_t>(), info_src(p),
+    p->mark(6);
+    launch_seg_allfit(s, part, p->stream_buf.get<uint32_t>(), info_src(p), p->info8,
                       p->sparse ? p->cpos.get<uint32_t>() : nullptr, p->v2_mb, C, status, ticket,
                       rec, centries, gate);
     launch_allfit_meta(s, part, J, p->wcnt.get<uint32_t>(), clen, cstart, cbase, gate);
-    p->mark(6);
     p->mark(7);
     const uint64_t* poff = p->pair_off.get<uint64_t>();
     if (p->sparse)
@@ -760,7 +816,12 @@ int build_seed_path_v2(clairplan_plan* p, const uint32_t* ext_perms,
     // the dense [E][F] sample-major arrays (not needed by the sparse passes)
     uint32_t* inv = sparse ? nullptr : need<uint32_t>(p->inv, EF, ok);
     const uint64_t EFp = (uint64_t)E * part.Fp;  // pitched u16 rows
-    uint16_t* info = sparse ? nullptr : need<uint16_t>(p->info16, EFp, ok);
+    // info rows are u8 when every count fits (E <= 255) and the tile sample pass writes them:
+    // half the L2 footprint of the gathers from the segment passes
+    static const bool lanes_only = getenv("CLAIRPLAN_SAMPLE_LANES") != nullptr;  // A/B
+    const bool tile_pass = !sparse && tile_path_ok(part) && !lanes_only;
+    p->info8 = tile_pass && E <= 255;
+    void* info = sparse ? nullptr : need<uint8_t>(p->info16, EFp * (p->info8 ? 1 : 2), ok);
     uint16_t* rank16 = sparse ? nullptr : need<uint16_t>(p->rank16, EFp, ok);
     uint32_t* pcount = need<uint32_t>(p->pair_count, F, ok);
     uint64_t* poff = need<uint64_t>(p->pair_off, (uint64_t)F + 1, ok);
@@ -772,7 +833,6 @@ int build_seed_path_v2(clairplan_plan* p, const uint32_t* ext_perms,
     uint64_t* wlen = need<uint64_t>(p->wlen, nloc, ok);
     uint32_t* bmask = need<uint32_t>(p->blkmask, nblk, ok);
     uint32_t* bbase = need<uint32_t>(p->blkbase, nblk, ok);
-    uint32_t* hard = need<uint32_t>(p->hard, (uint64_t)F + 1, ok);
     unsigned long long* wsum = need<unsigned long long>(p->wsum, nloc, ok);
     uint32_t* wcnt = need<uint32_t>(p->wcnt, (uint64_t)nloc + 1, ok);  // + the negative-size flag
     uint32_t* wneg = wcnt + nloc;
@@ -793,7 +853,6 @@ int build_seed_path_v2(clairplan_plan* p, const uint32_t* ext_perms,
     if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed (streams / histograms)");
     if (int rc = ensure_ws(p, std::max<uint64_t>(p->A, std::max<uint64_t>(NEE, F)), nloc)) return rc;
     if (int rc = alloc_rej(p, E)) return rc;
-    (void)hard;
     const bool lanes = lane_path_ok(part);
 
     for (int attempt = 0; attempt < 2; ++attempt) {
@@ -830,7 +889,6 @@ int build_seed_path_v2(clairplan_plan* p, const uint32_t* ext_perms,
         const bool red_hist = F >= (1u << 22) && !sparse;
         uint32_t* hist_out = red_hist ? seghist : nullptr;
         if (red_hist) CK(cudaMemsetAsync(seghist, 0, NEE * 4, s));
-        static const bool lanes_only = getenv("CLAIRPLAN_SAMPLE_LANES") != nullptr;  // A/B
         // per-worker candidate size sums for the whole-worker fit test (all-fit path)
         const bool no_allfit = getenv("CLAIRPLAN_NO_ALLFIT") != nullptr;
         const bool sums = J > 0 && !no_allfit && (sparse || (tile_path_ok(part) && !lanes_only));
@@ -849,11 +907,11 @@ int build_seed_path_v2(clairplan_plan* p, const uint32_t* ext_perms,
             launch_sparse_sample(s, part, sp_soff, sp_koff, sp_csr, pcount, sp_einfo, sp_erank, wsm);
             p->launches += 7;
         } else if (tile_path_ok(part) && !lanes_only) {
-            launch_sample_tile(s, part, inv, info, rank16, pcount, hist_out, wsm);
+            launch_sample_tile(s, part, inv, info, p->info8, rank16, pcount, hist_out, wsm);
         } else if (lanes) {
-            launch_sample_lanes(s, part, inv, info, rank16, pcount, hist_out);
+            launch_sample_lanes(s, part, inv, static_cast<uint16_t*>(info), rank16, pcount, hist_out);
         } else {
-            launch_sample_hash(s, part, inv, info, rank16, pcount, nullptr, nullptr, F, hist_out);
+            launch_sample_hash(s, part, inv, static_cast<uint16_t*>(info), rank16, pcount, nullptr, nullptr, F, hist_out);
         }
         exclusive_scan(s, pcount, F, poff, p->ws);
         p->mark(2);
@@ -886,7 +944,12 @@ int build_seed_path_v2(clairplan_plan* p, const uint32_t* ext_perms,
         if (sums) {
             CK(cudaMemcpyAsync(hcnt.data(), wcnt, (size_t)nloc * 4, cudaMemcpyDeviceToHost, s));
             CK(cudaMemcpyAsync(&gate_h, gate, 4, cudaMemcpyDeviceToHost, s));
+            p->wsum_h.resize(nloc);
+            p->wcnt_h.resize((size_t)nloc + 1);
+            CK(cudaMemcpyAsync(p->wsum_h.data(), wsum, (size_t)nloc * 8, cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(p->wcnt_h.data(), wcnt, ((size_t)nloc + 1) * 4, cudaMemcpyDeviceToHost, s));
         }
+        p->sums_ok = sums;
         CK(cudaMemcpyAsync(flags.data(), p->rej_flag.get<uint32_t>(), E * 4, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         bool any = false;
@@ -923,7 +986,7 @@ int build_seed_path_v2(clairplan_plan* p, const uint32_t* ext_perms,
         }
         // tier path. K4b: per-segment count histograms -> first-order and tier-order bases
         if (red_hist) launch_segcnt(s, nloc, E, seghist, segcnt);
-        else launch_seg_hist(s, part, stream_buf, info_src(p), p->sparse ? p->cpos.get<uint32_t>() : nullptr, seghist, segcnt);
+        else launch_seg_hist(s, part, stream_buf, info_src(p), p->info8, p->sparse ? p->cpos.get<uint32_t>() : nullptr, seghist, segcnt);
         exclusive_scan(s, seghist, NEE, sbase, p->ws);
         exclusive_scan(s, segcnt, (uint64_t)nloc * E, segoff, p->ws);
         p->hist_ready = true;
@@ -1068,11 +1131,29 @@ int clairplan_build_export(clairplan_t p, const double* host_sizes, uint32_t* st
         cudaStreamSynchronize(p->xstream);
         return rc;
     }
+    // output capacities are checked before any further copy is issued; an error after the
+    // build waits for the stream copy already in flight on xstream (the caller may free or
+    // reuse its buffers as soon as this returns)
+    uint64_t cl_need = 0;
+    for (uint32_t w = 0; w < p->nloc; ++w)
+        for (uint32_t j = 0; j < p->cfg.num_classes; ++j)
+            cl_need += p->class_len_h[(size_t)w * (p->cfg.num_classes + 1) + j];
+    if (cl_cap < cl_need || holders_cap < p->H || (cl_need && !class_lists_out) ||
+        (p->H && !holders_out)) {
+        cudaStreamSynchronize(p->xstream);
+        cudaStreamSynchronize(p->stream);
+        return fail(CLAIRPLAN_ERANGE, cl_cap < cl_need || holders_cap < p->H
+                                          ? "output buffer too small"
+                                          : "null output buffer");
+    }
     if (!copied)
         CK(cudaMemcpyAsync(streams_out, p->stream_buf.get<uint32_t>(), p->A * 4, cudaMemcpyDeviceToHost,
                            p->stream));
-    if (int rc2 = clairplan_export_class_lists_async(p, class_lists_out, cl_cap)) return rc2;
-    if (holders_cap < p->H) return fail(CLAIRPLAN_ERANGE, "holder buffer too small");
+    if (int rc2 = clairplan_export_class_lists_async(p, class_lists_out, cl_cap)) {
+        cudaStreamSynchronize(p->xstream);
+        cudaStreamSynchronize(p->stream);
+        return rc2;
+    }
     CK(cudaMemcpyAsync(offsets_out, p->holder_off_dev, ((uint64_t)p->part.F + 1) * 8,
                        cudaMemcpyDeviceToHost, p->stream));
     if (p->H) CK(cudaMemcpyAsync(holders_out, p->holders_dev, p->H * 12, cudaMemcpyDeviceToHost, p->stream));

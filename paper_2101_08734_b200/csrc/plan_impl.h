@@ -117,10 +117,20 @@ struct clairplan_plan {
     DevBuf head, next, q, scratch, counters, rej_flag, rej_step, rej_cum, rej_count;
     DevBuf wsbuf;
     DevBuf cand_w, dfirst, dcounts;  // explicit-stream (generic) path
-    DevBuf inv, info16, rank16, cbase, seghist, sorted_base, blkmask, blkbase, planes, ccount, cpre, hard;
+    DevBuf inv, info16, rank16, cbase, seghist, sorted_base, blkmask, blkbase, planes, ccount, cpre;
     DevBuf wsum, wcnt, chstatus, allfit_gate;  // all-fit: worker sums / counts, look-back, decision
     bool cl_contig = true;           // class lists back to back (tier path) or at stream offsets
     DevBuf koff, sp_cur, csr, cpos, soff, einfo, erank;  // sparse sample-major passes (sharded)
+    DevBuf sorted_k;                 // tier path: sample id of every tier position (seg_write3)
+    DevBuf hpos;                     // tier path: [E][Fp] class << 28 | class-list position (hp_fill)
+    bool hp_path = false;            // last assignment wrote hpos (holder_hp replaces holder_tile)
+    bool info8 = false;              // info rows of the last dense build are u8 (else u16)
+    // whole-worker candidate size sums of the last seed build (sample pass; all-fit test) on
+    // the host: a class whose capacity holds every worker's total takes all its remaining
+    // candidates (first_fit_classes)
+    std::vector<unsigned long long> wsum_h;
+    std::vector<uint32_t> wcnt_h;
+    bool sums_ok = false;
     bool sparse = false;             // last build used the sparse passes
     bool allfit = false;             // last build took the all-fit path (no tier order)
     bool tier_ready = false;         // dest / sorted_size / block masks hold the tier order

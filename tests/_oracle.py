@@ -166,6 +166,7 @@ class Ref:
         L.ref_plan_build_subset.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
                                             C.c_uint32, C.c_int, C.c_uint32, f64p, f64p, C.c_int,
                                             u32p, C.c_uint32]
+        L.ref_last_phase_ms.argtypes = [f64p]
         L.ref_plan_build_subset_lowmem.restype = C.c_void_p
         L.ref_plan_build_subset_lowmem.argtypes = L.ref_plan_build_subset.argtypes
         L.ref_assign_from_streams.restype = C.c_void_p
@@ -272,6 +273,23 @@ class Ref:
         if not h:
             raise ValueError(self.err())
         return self._collect(h, N, len(caps), F)
+
+    def time_subset(self, seed, F, N, B, E, drop_last, caps, sizes, workers, threads):
+        """Builds the per-worker reference plan of a worker subset (every permutation, every
+        worker's stream, the subset's assignment, build_index) without copying it out; returns
+        the wall-clock phases in ms: permutations, streams, assignment, build_index."""
+        caps = np.ascontiguousarray(caps, np.float64)
+        sizes = np.ascontiguousarray(sizes, np.float64)
+        ws = np.ascontiguousarray(workers, np.uint32)
+        h = self.L.ref_plan_build_subset(seed, F, N, B, E, int(drop_last), len(caps),
+                                         _ptr(caps, f64p), _ptr(sizes, f64p), threads,
+                                         _ptr(ws, u32p), len(ws))
+        if not h:
+            raise ValueError(self.err())
+        ph = np.zeros(4, np.float64)
+        self.L.ref_last_phase_ms(_ptr(ph, f64p))
+        self.L.ref_plan_free(h)
+        return ph
 
     def plan_subset_lowmem(self, seed, F, N, B, E, drop_last, caps, sizes, workers, threads):
         """Worker-subset plan that never holds all permutations (config 5)."""
