@@ -319,6 +319,29 @@ def test_cpp_compat_suite():
     assert "0 failures" in r.stdout
 
 
+@pytest.mark.parametrize("preset", [("imagenet1k", "0.01", "4"), ("cosmoflow", "0.02", "3"),
+                                    ("imagenet22k", "0.001", "3")])
+def test_reference_simulator_over_the_dropin(preset):
+    """The reference's own build_policy(Nopfs) + simulate (policies.cpp:446-456,
+    simulator.cpp:393-399), compiled unmodified into oracle/_ref/libclairsim_sim.so, with
+    libclairsim_b200.so linked ahead of it (tests/cpp/Makefile): every planner call, also
+    the ones made inside the reference library, resolves to the drop-in; streams, cache
+    assignment, holder CSR and the simulation result digest equal the all-CPU build's."""
+    import subprocess
+    exe = {n: os.path.join(HERE, "cpp", n) for n in ("refsim_cpu", "refsim_b200")}
+    if not all(os.path.exists(x) for x in exe.values()):
+        pytest.skip("refsim drivers not built (need the reference sources at build time)")
+    out = {}
+    for n, x in exe.items():
+        r = subprocess.run([x, *preset], capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stdout + r.stderr
+        out[n] = r.stdout.splitlines()
+    assert "nopfs_assign_caches=libclairsim_b200.so" in out["refsim_b200"][0]
+    assert "build_access_streams=libclairsim_b200.so" in out["refsim_b200"][0]
+    assert "nopfs_assign_caches=libclairsim_sim.so" in out["refsim_cpu"][0]
+    assert out["refsim_cpu"][1:] == out["refsim_b200"][1:], (out["refsim_cpu"], out["refsim_b200"])
+
+
 def test_rejection_kat_device(cp):
     """Epochs whose shuffle hits a Lemire rejection (found with tools/find_rejection, digests
     from the reference): the device path resolves them bit-exactly."""
@@ -365,38 +388,105 @@ def test_build_from_perms_matches_build(cp, ref):
         b.close()
 
 
-def test_config4_imagenet22k_against_reference_worker_subset(cp, ref):
-    """Config 4 (ImageNet-22k shape, 90 epochs, 1024 workers): every stream bit-exact with the
-    reference; class lists and holder CSR bit-exact for a worker subset (the reference's own
-    per-worker functions; the CSR restricted to a worker subset is a subsequence of the full
-    CSR because build_index orders holders by worker)."""
+def test_config4_imagenet22k_full_plan_against_reference(cp, ref):
+    """Config 4 (ImageNet-22k shape, 90 epochs, 1024 workers; the north-star shape) in full:
+    every stream, every worker's class lists (prefetch orders) and the whole holder CSR equal
+    the reference's own per-worker plan (epoch_permutation, access_frequencies,
+    nopfs_assign_caches per worker on all host threads, then the reference's build_index;
+    policies.cpp:144-166, checked equal to the verbatim composition in test_oracle.py)."""
     F, N, b, E = 14_197_122, 1024, 32, 90
     caps = [120_000.0, 900_000.0]
     sizes = ref.generate_sizes(F, 0.1077, 0.2, 1_500_000.0, 1)
-    subset = np.array([0, 1, 2, 255, 511, 512, 777, 1022, 1023], np.uint32)
-    a = ref.plan_subset(42, F, N, b * N, E, True, caps, sizes, subset, os.cpu_count() or 8)
     p = cp.Plan(42, F, cp.PartitionSpec(N, b * N, E, True), caps, sizes).build()
     st = p.stats()
-    assert st["accesses"] == 1_276_968_960
+    assert st["accesses"] == 1_276_968_960 and st["path"] == "tier"
     flat = p.streams_flat()
+    cl = p.class_lists()
+    offs, hold = p.holders()
+    p.close()
+    a = ref.plan(42, F, N, b * N, E, True, caps, sizes, mode=1, threads=os.cpu_count() or 8)
     o = 0
     for w in range(N):
         n = len(a.streams[w])
         assert np.array_equal(flat[o:o + n], a.streams[w]), w
         o += n
+    assert o == len(flat)
     del flat
-    cl = p.class_lists()
-    for w in subset:
+    for w in range(N):
         for j in range(2):
             assert np.array_equal(cl[w][j], a.class_lists[w][j]), (w, j)
-    offs, hold = p.holders()
-    p.close()
-    keep = np.isin(hold[:, 0], subset)
-    owner = np.repeat(np.arange(F, dtype=np.int64), np.diff(offs.astype(np.int64)))
-    sub_offs = np.zeros(F + 1, np.int64)
-    sub_offs[1:] = np.cumsum(np.bincount(owner[keep], minlength=F))
-    assert np.array_equal(sub_offs, a.holder_offsets.astype(np.int64))
-    assert np.array_equal(hold[keep], a.holders)
+    del cl
+    assert st["pairs"] == int(sum(len(x) for lists in a.class_lists for x in lists))
+    assert np.array_equal(offs.astype(np.uint64), a.holder_offsets.astype(np.uint64))
+    assert np.array_equal(hold, a.holders)
+
+
+def test_config5_worker_subset_against_reference(cp, ref):
+    """Config 5 (100 M samples, 100 epochs, 8192 workers): a full plan needs the
+    sharded build (2^32 or more accesses); here the worker ranges [0, 512) and [7680, 8192)
+    are built on one GPU and 64 workers inside them (both ends and both range edges included)
+    are compared with the reference's own functions: streams, class lists and the
+    subset-restricted holder CSR (a subsequence of the full CSR: holders are worker-ordered).
+    The reference side never holds the 100 permutations together (epoch by epoch)."""
+    F, E, N, b, R = 100_000_000, 100, 8192, 32, 512
+    caps = [120_000.0, 900_000.0]
+    sizes = ref.generate_sizes(F, 0.1077, 0.1, None, 1)
+    rng = np.random.default_rng(5)
+    subset = {0, 1, 2, R - 1, N - R, N - R + 1, N - 2, N - 1}
+    while len(subset) < 64:
+        subset.add(int(rng.integers(0, R)) if len(subset) % 2 else int(rng.integers(N - R, N)))
+    subset = np.array(sorted(subset), np.uint32)
+    a = ref.plan_subset_lowmem(42, F, N, b * N, E, True, caps, sizes, subset, os.cpu_count() or 8)
+    roffs = a.holder_offsets.astype(np.int64)
+    rowner = np.repeat(np.arange(F, dtype=np.int64), np.diff(roffs))
+    for wr in ((0, R), (N - R, N)):
+        sub = subset[(subset >= wr[0]) & (subset < wr[1])]
+        p = cp.Plan(42, F, cp.PartitionSpec(N, b * N, E, True), caps, sizes, worker_range=wr).build()
+        for w in sub:
+            assert np.array_equal(p.stream(int(w)), a.streams[w]), w
+        cl = p.class_lists()
+        for w in sub:
+            for j in range(2):
+                assert np.array_equal(cl[int(w) - wr[0]][j], a.class_lists[w][j]), (w, j)
+        offs, hold = p.holders()
+        p.close()
+        keep = np.isin(hold[:, 0], sub)
+        owner = np.repeat(np.arange(F, dtype=np.int64), np.diff(offs.astype(np.int64)))
+        rkeep = np.isin(a.holders[:, 0], sub)
+        assert np.array_equal(owner[keep], rowner[rkeep]), wr
+        assert np.array_equal(hold[keep], a.holders[rkeep]), wr
+
+
+def test_concurrent_handles_from_host_threads(cp, ref):
+    """The sweep pool calls the planner from several host threads at once
+    (simulator.cpp:471-480 -> policies.cpp:454): four threads build four different plans on
+    their own handles concurrently (ctypes releases the GIL); each equals the reference."""
+    import threading
+    cases = [(42, 20_000, 8, 256, 12, True, [150.0, 400.0]),
+             (7, 30_011, 12, 120, 9, False, [60.0, 900.0]),
+             (11, 25_000, 16, 512, 7, True, [1e6, 1e6]),
+             (3, 40_000, 5, 100, 10, True, [20.0, 80.0, 300.0])]
+    sizes = [ref.generate_sizes(c[1], 0.1077, 0.2, None, 1 + i) for i, c in enumerate(cases)]
+    out = [None] * len(cases)
+    errs = []
+
+    def run(i):
+        try:
+            seed, F, N, B, E, dl, caps = cases[i]
+            for _ in range(3):  # several builds per handle, interleaved with the other threads
+                out[i] = device_plan(cp, seed, F, N, B, E, dl, caps, sizes[i])
+        except Exception as ex:  # noqa: BLE001 - reported below
+            errs.append((i, ex))
+
+    ts = [threading.Thread(target=run, args=(i,)) for i in range(len(cases))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
+    for i, (seed, F, N, B, E, dl, caps) in enumerate(cases):
+        want = ref.plan(seed, F, N, B, E, dl, caps, sizes[i])
+        assert plans_equal(want, out[i]) is None, i
 
 
 def test_build_export_matches_separate_exports(cp, ref):
@@ -437,7 +527,7 @@ def test_build_export_matches_separate_exports(cp, ref):
     (1_281_167, 256, 32, 9, True, None),
 ])
 @pytest.mark.parametrize("dense", ["0", "1"])
-def test_sharded_build_from_streams(cp, monkeypatch, F, N, b, E, dl, caps, dense):
+def test_sharded_build_from_streams(cp, ref, monkeypatch, F, N, b, E, dl, caps, dense):
     """One rank's share of the multi-GPU build on one GPU: a worker-range
     handle fed its workers' streams of every epoch (what the all-to-all delivers, one source)
     through clairplan_generate_streams / clairplan_build_from_streams, with the sparse (CSR)
@@ -454,6 +544,12 @@ def test_sharded_build_from_streams(cp, monkeypatch, F, N, b, E, dl, caps, dense
     st_full = full.streams_flat()
     offs_full, hold_full = full.holders()
     cl_full = full.class_lists()
+    # the full plan the shards are compared with is itself the reference's (policies.cpp:144-166)
+    want = ref.plan(42, F, N, b * N, E, dl, caps, sizes, mode=1, threads=os.cpu_count() or 8)
+    assert np.array_equal(st_full, np.concatenate(want.streams))
+    assert all(np.array_equal(x, y) for a, c in zip(want.class_lists, cl_full) for x, y in zip(a, c))
+    assert np.array_equal(offs_full.astype(np.uint64), want.holder_offsets.astype(np.uint64))
+    assert np.array_equal(hold_full, want.holders)
     samp = np.repeat(np.arange(F), np.diff(offs_full.astype(np.int64)))
     L = cp.lib()
     L.clairplan_generate_streams.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p]
