@@ -117,10 +117,15 @@ struct FFChunks {
     uint8_t* segfit;  // per segment: provably everything fits (skip the exact chain)
 };
 
+// GATHER: the sizes are gathered here (sz[i] = src[idx[i]], the tier order's sample ids) and
+// written for the later passes, instead of by a separate gather pass over the same chunks
+template <bool GATHER>
 __global__ void __launch_bounds__(kThreads) ff_stats_kernel(TileMap tm,
                                                              const uint64_t* __restrict__ seg_begin,
                                                              const uint64_t* __restrict__ seg_len,
-                                                             const double* __restrict__ sz,
+                                                             double* __restrict__ sz,
+                                                             const uint32_t* __restrict__ idx,
+                                                             const double* __restrict__ src,
                                                              FFChunks ch) {
     __shared__ double ssum[kThreads / 32], smin[kThreads / 32], smax[kThreads / 32];
     for (uint64_t t = blockIdx.x; t < tm.max_tiles; t += gridDim.x) {
@@ -129,10 +134,16 @@ __global__ void __launch_bounds__(kThreads) ff_stats_kernel(TileMap tm,
         const uint64_t off = (t - tm.tile_base[seg]) * (uint64_t)tm.tile;
         const uint64_t L = seg_len[seg];
         const uint64_t n = L - off < tm.tile ? L - off : tm.tile;
-        const double* p = sz + seg_begin[seg] + off;
+        double* p = sz + seg_begin[seg] + off;
         double s = 0, mn = INFINITY, mx = 0;
         for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-            const double v = p[i];
+            double v;
+            if constexpr (GATHER) {
+                v = __ldg(src + __ldcs(idx + seg_begin[seg] + off + i));
+                p[i] = v;
+            } else {
+                v = p[i];
+            }
             s += v;
             if (v >= 0.0 && v < INFINITY) {
                 mn = fmin(mn, v);
@@ -372,7 +383,8 @@ __global__ void __launch_bounds__(kThreads) ff_expand_kernel(TileMap tm,
 // capacity C (same capacity for every worker, SystemConfig is shared).
 void first_fit_pass(cudaStream_t s, const uint64_t* seg_begin, const uint64_t* seg_len,
                     uint32_t nseg, uint64_t total, const double* sz, double C, uint8_t* taken,
-                    Workspace& ws, unsigned long long* taken_count) {
+                    Workspace& ws, unsigned long long* taken_count, const uint32_t* gather_idx,
+                    const double* gather_src) {
     TileMap tm;
     build_tilemap(s, seg_len, nseg, total, kChunk, tm, ws);
     FFChunks ch;
@@ -388,7 +400,12 @@ void first_fit_pass(cudaStream_t s, const uint64_t* seg_begin, const uint64_t* s
     ch.status = ws.scratch<uint8_t>(m);
     ch.segfit = ws.scratch<uint8_t>(nseg + 1);
     const unsigned g = grid_for(m, 1, 148u * 64u);
-    ff_stats_kernel<<<g, kThreads, 0, s>>>(tm, seg_begin, seg_len, sz, ch);
+    if (gather_idx)
+        ff_stats_kernel<true><<<g, kThreads, 0, s>>>(tm, seg_begin, seg_len, const_cast<double*>(sz),
+                                                     gather_idx, gather_src, ch);
+    else
+        ff_stats_kernel<false><<<g, kThreads, 0, s>>>(tm, seg_begin, seg_len, const_cast<double*>(sz),
+                                                      nullptr, nullptr, ch);
     ff_prefix_kernel<<<grid_for((uint64_t)nseg * 32, kThreads), kThreads, 0, s>>>(tm, seg_len, C, ch);
     ff_agg_kernel<<<g, kThreads, 0, s>>>(tm, seg_begin, seg_len, sz, C, ch);
     ff_resolve_kernel<<<grid_for((uint64_t)nseg * 32, 128), 128, 0, s>>>(tm, seg_begin, seg_len,

@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <stddef.h>
 #include <stdint.h>
+#include <vector>
 
 #include "common.cuh"
 
@@ -95,6 +96,29 @@ void launch_fyb(cudaStream_t s, uint64_t key, const Part& part, uint32_t e0, uin
                 uint32_t* lst, uint32_t* pool, uint32_t* pool_used, uint32_t* succ, uint32_t* q,
                 uint32_t* inv, uint32_t* stream, uint32_t* perm_out, const StreamDst* dst = nullptr);
 
+// contiguous-bucket Fisher-Yates resolution for large F (perm_fyc.cu)
+struct FycHost {
+    uint32_t F = 0, NB = 0, lgW = 0, pack = 0;
+    uint64_t rtotal = 0;
+    std::vector<uint32_t> bstart, cap, cell;  // block starts [NB+1], capacities, target cells
+    std::vector<uint64_t> roff;               // region offsets [NB+1]
+};
+struct FycDev {
+    uint32_t NB = 0, lgW = 0, pack = 0;
+    uint64_t rtotal = 0;
+    const uint32_t* bstart = nullptr;
+    const uint32_t* cell = nullptr;
+    const uint32_t* roff = nullptr;
+    const uint32_t* cap = nullptr;
+};
+bool fyc_plan(uint32_t F, FycHost& h);
+uint32_t fyc_epochs_per_batch(uint32_t F, uint32_t E);
+void launch_fyc(cudaStream_t s, uint64_t key, const Part& part, uint32_t e0, uint32_t ne,
+                const FycDev& g, const RejTable& rt, uint32_t* rej_flag, uint32_t* region,
+                uint32_t* cursor, uint32_t* tsucc, uint32_t* q, uint32_t* inv, uint32_t* stream,
+                uint32_t* perm_out, const StreamDst* dst);
+constexpr uint32_t kRejOverflow = 0x80000000u;  // rej_flag bit: a fyc block region overflowed
+
 void launch_fy_table(cudaStream_t s, uint64_t key, uint32_t F, uint32_t e0, uint32_t ne,
                      uint4* tbl, uint32_t* ovh, uint32_t* ovn, const RejTable& rt,
                      uint32_t* rej_flag);
@@ -155,7 +179,8 @@ void launch_worker_segments(cudaStream_t s, const uint64_t* seg_off, uint32_t nl
 
 void first_fit_pass(cudaStream_t s, const uint64_t* seg_begin, const uint64_t* seg_len,
                     uint32_t nseg, uint64_t total, const double* sz, double C, uint8_t* taken,
-                    Workspace& ws, unsigned long long* taken_count = nullptr);
+                    Workspace& ws, unsigned long long* taken_count = nullptr,
+                    const uint32_t* gather_idx = nullptr, const double* gather_src = nullptr);
 
 void compact_rejects(cudaStream_t s, const uint64_t* seg_begin, const uint64_t* seg_len,
                      uint32_t nseg, uint64_t total, const uint8_t* taken, const uint32_t* seq_idx,

@@ -42,6 +42,46 @@ RejTable rej_table(clairplan_plan* p) {
     return rt;
 }
 
+// Geometry of the contiguous-bucket shuffle for F (computed once per handle, uploaded once).
+bool fyc_ready(clairplan_plan* p, uint32_t F, FycDev& g) {
+    if (p->fyc_off) return false;
+    FycHost& h = p->fych;
+    if (h.F != F) {
+        if (!fyc_plan(F, h)) {
+            h.F = 0;
+            return false;
+        }
+        const uint64_t nb = h.NB + 1, nc = h.cell.size();
+        if (!p->fyc_geo.ensure((3 * nb + nc) * 4)) {
+            h.F = 0;
+            return false;
+        }
+        std::vector<uint32_t> buf;
+        buf.reserve(3 * nb + nc);
+        buf.insert(buf.end(), h.bstart.begin(), h.bstart.end());
+        buf.insert(buf.end(), h.cap.begin(), h.cap.end());
+        buf.push_back(0);
+        for (uint64_t x : h.roff) buf.push_back((uint32_t)x);
+        buf.insert(buf.end(), h.cell.begin(), h.cell.end());
+        if (cudaMemcpy(p->fyc_geo.p, buf.data(), buf.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) {
+            cudaGetLastError();
+            h.F = 0;
+            return false;
+        }
+    }
+    const uint32_t* d = p->fyc_geo.get<uint32_t>();
+    const uint64_t nb = h.NB + 1;
+    g.NB = h.NB;
+    g.lgW = h.lgW;
+    g.pack = h.pack;
+    g.rtotal = h.rtotal;
+    g.bstart = d;
+    g.cap = d + nb;
+    g.roff = d + 2 * nb;
+    g.cell = d + 3 * nb;
+    return true;
+}
+
 // Enqueues the permutations of epochs [e_first, e_first + e_count): stream + inverse (or plain
 // permutations).  `spart` (optional) replaces the handle's stream geometry.
 int enqueue_perms(clairplan_plan* p, uint32_t* stream_out, uint32_t* inv_out, uint32_t* perm_out,
@@ -51,11 +91,29 @@ int enqueue_perms(clairplan_plan* p, uint32_t* stream_out, uint32_t* inv_out, ui
     const uint32_t F = part.F;
     bool ok = true;
     const RejTable rt = rej_table(p);
-    static const char* mode_env = getenv("CLAIRPLAN_FY");  // "lists" / "table" (A/B only)
-    const std::string mode = mode_env ? mode_env : "bucket";
+    static const char* mode_env = getenv("CLAIRPLAN_FY");  // "fyc" / "bucket" / "lists" / "table" (A/B)
+    const std::string mode = mode_env ? mode_env : "fyc";
     static const bool fy_out_mode = getenv("CLAIRPLAN_FY_OUT") != nullptr;
+    FycDev fg;
+    if (mode == "fyc" && fyc_ready(p, F, fg)) {  // contiguous target-block buckets
+        const uint32_t EB = fyc_epochs_per_batch(F, e_count);
+        uint32_t* region = need<uint32_t>(p->fyc_region, (uint64_t)EB * fg.rtotal, ok);
+        uint32_t* cursor = need<uint32_t>(p->fyc_cursor, (uint64_t)EB * fg.NB, ok);
+        uint32_t* tsucc = need<uint32_t>(p->next, (uint64_t)EB * F, ok);
+        uint32_t* q = need<uint32_t>(p->q, (uint64_t)EB * F, ok);
+        if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed (permutation workspace)");
+        for (uint32_t e0 = e_first; e0 < e_first + e_count; e0 += EB) {
+            const uint32_t ne = std::min(EB, e_first + e_count - e0);
+            launch_fyc(p->stream, p->key, part, e0, ne, fg, rt, p->rej_flag.get<uint32_t>(), region,
+                       cursor, tsucc, q, inv_out, stream_out,
+                       perm_out ? perm_out + (size_t)(e0 - e_first) * F : nullptr, dst);
+            p->launches += 4;
+        }
+        CK(cudaGetLastError());
+        return 0;
+    }
     FyGeom g;
-    if (mode == "bucket" && fy_geometry(F, g)) {  // shared-memory bucketed resolution
+    if ((mode == "fyc" || mode == "bucket") && fy_geometry(F, g)) {  // shared-memory bucketed resolution
         const uint32_t EB = epochs_per_batch(F, e_count, 32);
         uint32_t* bucket = need<uint32_t>(p->fybucket, (uint64_t)EB * F, ok);
         uint32_t* lst = need<uint32_t>(p->fylst, (uint64_t)EB * g.NT * (g.NB + 1), ok);
@@ -138,6 +196,14 @@ int resolve_rejections(clairplan_plan* p, const std::vector<uint32_t>& flags, bo
     for (uint32_t er = 0; er < flags.size(); ++er) {
         const uint32_t e = er + p->rej_ebase;
         uint32_t flag = flags[er];
+        if (flag & kRejOverflow) {
+            // a contiguous-bucket region overflowed (mean + 10 sigma exceeded): rerun the
+            // shuffle on the linked-list path; its own detection finds any rejection again
+            p->fyc_off = true;
+            *any = true;
+            CK(cudaMemsetAsync(p->rej_flag.get<uint32_t>() + er, 0, sizeof(uint32_t), p->stream));
+            continue;
+        }
         while (flag) {
             *any = true;
             const uint32_t i = flag - 1;
@@ -358,7 +424,7 @@ int build_seed_path(clairplan_plan* p) {
     if (sample_pass_config(part, &hs, &nw, &warps, &smem))
         return fail(CLAIRPLAN_EINVAL, "epochs/workers too large for the device histogram");
 
-    for (int attempt = 0; attempt < 2; ++attempt) {
+    for (int attempt = 0; attempt < 3; ++attempt) {
         p->launches = 0;
         CK(cudaEventRecord(p->ev0, s));
         p->mark(0);
@@ -506,7 +572,11 @@ int first_fit_classes(clairplan_plan* p, const double* ssize, uint8_t* cls) {
         CK(cudaMemsetAsync(cnt, 0, 8, s));
         const size_t m = ws.mark();
         const uint64_t total = (j == 1) ? D : remaining;
-        first_fit_pass(s, sb, sl, nloc, total, seq_sz, p->caps[j - 1], taken, ws, cnt);
+        const bool gather = j == 1 && p->ssize_pending;  // tier-order sizes not written yet
+        first_fit_pass(s, sb, sl, nloc, total, seq_sz, p->caps[j - 1], taken, ws, cnt,
+                       gather ? p->sorted_k.get<uint32_t>() : nullptr,
+                       gather ? p->sizes.get<double>() : nullptr);
+        if (gather) p->ssize_pending = false;
         ws.release(m);
         p->launches += 6;
         if (j > 1) {
@@ -718,8 +788,7 @@ int tier_order_v2(clairplan_plan* p) {
         launch_seg_write3(s, part, p->stream_buf.get<uint32_t>(), info_src(p), p->info8, segoff,
                           p->sorted_base.get<uint64_t>(), p->v2_mb, dest, sk,
                           p->blkmask.get<uint32_t>(), p->blkbase.get<uint32_t>());
-        launch_gather_sorted_sizes(s, sk, p->sizes.get<double>(), D, ssize);
-        ++p->launches;
+        p->ssize_pending = true;  // gathered by class 1's first-fit statistics pass
     }
     launch_worker_segments(s, segoff, nloc, E, p->wbeg.get<uint64_t>(), p->wlen.get<uint64_t>());
     p->launches += 2;
@@ -855,7 +924,7 @@ int build_seed_path_v2(clairplan_plan* p, const uint32_t* ext_perms,
     if (int rc = alloc_rej(p, E)) return rc;
     const bool lanes = lane_path_ok(part);
 
-    for (int attempt = 0; attempt < 2; ++attempt) {
+    for (int attempt = 0; attempt < 3; ++attempt) {
         p->launches = 0;
         p->ws.used = 0;
         CK(cudaEventRecord(p->ev0, s));
@@ -1331,7 +1400,7 @@ int clairplan_epoch_permutation(uint64_t seed, uint32_t epoch, uint32_t samples,
     if (int rc = alloc_rej(&p, 1)) return rc;
     DevBuf perm;
     if (!perm.ensure((size_t)samples * 4)) return fail(CLAIRPLAN_ENOMEM, "device allocation failed");
-    for (int attempt = 0; attempt < 2; ++attempt) {
+    for (int attempt = 0; attempt < 3; ++attempt) {
         if (int rc = enqueue_perms(&p, nullptr, nullptr, perm.get<uint32_t>(), epoch, 1)) return rc;
         std::vector<uint32_t> flags(1, 0);
         CK(cudaMemcpyAsync(&flags[0], p.rej_flag.get<uint32_t>(), 4,
@@ -1377,7 +1446,7 @@ int clairplan_generate_perms(clairplan_t p, uint32_t epoch_begin, uint32_t epoch
     if (epoch_begin + epoch_count > p->part.E) return fail(CLAIRPLAN_EINVAL, "epoch range outside plan");
     CK(cudaSetDevice(p->device));
     if (int rc = alloc_rej(p, p->part.E)) return rc;
-    for (int attempt = 0; attempt < 2; ++attempt) {
+    for (int attempt = 0; attempt < 3; ++attempt) {
         p->launches = 0;
         if (int rc = enqueue_perms(p, nullptr, nullptr, d_out, epoch_begin, epoch_count)) return rc;
         std::vector<uint32_t> flags(p->part.E);
@@ -1421,7 +1490,7 @@ static int generate_streams_impl(clairplan_plan* p, uint32_t epoch_begin, uint32
         own_inv = need<uint32_t>(p->inv, (uint64_t)pp.E * pp.F, ok);
         if (!ok) own_inv = nullptr;
     }
-    for (int attempt = 0; attempt < 2; ++attempt) {
+    for (int attempt = 0; attempt < 3; ++attempt) {
         p->launches = 0;
         CK(cudaEventRecord(p->ev0, p->stream));
         if (int rc = enqueue_perms(p, d_out, own_inv, nullptr, epoch_begin, epoch_count, &sp, dst)) return rc;
@@ -1467,14 +1536,20 @@ int clairplan_generate_streams_p2p(clairplan_t p, uint32_t epoch_begin, uint32_t
         d.delta[r] = (long long)dst_delta[r];
     }
     FyGeom g;
-    if (!fy_geometry(p->part.F, g)) return fail(CLAIRPLAN_EINVAL, "peer-memory stream writes need the bucketed shuffle");
+    FycDev fg;
+    if (!fyc_ready(p, p->part.F, fg) && !fy_geometry(p->part.F, g))
+        return fail(CLAIRPLAN_EINVAL, "peer-memory stream writes need the bucketed shuffle");
     return generate_streams_impl(p, epoch_begin, epoch_count, nullptr, &d);
 }
 
 int clairplan_p2p_supported(clairplan_t p) {
     FyGeom g;
+    FycDev fg;
     const char* m = getenv("CLAIRPLAN_FY");
-    return (p && !p->generic && fy_geometry(p->part.F, g) && !(m && std::string(m) != "bucket")) ? 1 : 0;
+    const std::string mode = m ? m : "fyc";
+    if (!p || p->generic) return 0;
+    if (mode == "fyc" && fyc_ready(p, p->part.F, fg)) return 1;
+    return ((mode == "fyc" || mode == "bucket") && fy_geometry(p->part.F, g)) ? 1 : 0;
 }
 
 int clairplan_recv_buffer(clairplan_t p, uint32_t i, void** d_ptr, void* ipc_handle) {

@@ -121,7 +121,13 @@ struct clairplan_plan {
     DevBuf wsum, wcnt, chstatus, allfit_gate;  // all-fit: worker sums / counts, look-back, decision
     bool cl_contig = true;           // class lists back to back (tier path) or at stream offsets
     DevBuf koff, sp_cur, csr, cpos, soff, einfo, erank;  // sparse sample-major passes (sharded)
+    // contiguous-bucket shuffle (perm_fyc.cu): host geometry of the handle's F, its device
+    // copy (block starts, capacities, target cells, region offsets), bucket regions, cursors
+    FycHost fych;
+    DevBuf fyc_geo, fyc_region, fyc_cursor;
+    bool fyc_off = false;            // a block region overflowed once: linked-list path
     DevBuf sorted_k;                 // tier path: sample id of every tier position (seg_write3)
+    bool ssize_pending = false;      // sorted_size not yet gathered (class 1's ff_stats does it)
     DevBuf hpos;                     // tier path: [E][Fp] class << 28 | class-list position (hp_fill)
     bool hp_path = false;            // last assignment wrote hpos (holder_hp replaces holder_tile)
     bool info8 = false;              // info rows of the last dense build are u8 (else u16)
