@@ -435,7 +435,8 @@ __global__ void __launch_bounds__(kThreads, 4) fyc_emit_kernel(Part part, uint32
 
 // ---- launcher ----------------------------------------------------------------------------
 uint32_t fyc_epochs_per_batch(uint32_t F, uint32_t E) {
-    uint64_t eb = (40ull << 20) / F;  // ~40 M steps per launch (several waves of CTAs)
+    static const uint64_t steps = (uint64_t)env_uint("CLAIRPLAN_FYC_MSTEPS", 256) << 20;  // A/B
+    uint64_t eb = steps / F;  // ~256 M steps per launch: launch tails dominate (config 4: 40 M 50.7, 200 M 49.0 ms)
     if (eb < 1) eb = 1;
     if (eb > E) eb = E;
     if (eb > 128) eb = 128;
