@@ -228,6 +228,34 @@ int clairplan_build_export(clairplan_t plan, const double* host_sizes, uint32_t*
  * memory for an end-to-end step; the copy is ordered before the next build. */
 int clairplan_set_sizes(clairplan_t plan, const double* sizes_mb, int on_device);
 
+/* ---- plan consumer ----------------------------------------
+ * Replaces per-access calls of nopfs_choose_source / choose_source / best_cached_source
+ * (policies.hpp:100-117, policies.cpp:168-233) with one batched device call over the plan's
+ * holder CSR.  Kinds follow FetchSource::Kind (policies.hpp:77-82). */
+#define CLAIRPLAN_SRC_PFS 0
+#define CLAIRPLAN_SRC_REMOTE 1
+#define CLAIRPLAN_SRC_LOCAL 2
+typedef struct {
+    uint8_t kind;           /* CLAIRPLAN_SRC_* */
+    uint8_t storage_class;  /* 1-based (Remote / Local), 0 for the PFS */
+    uint16_t reserved;
+    uint32_t worker;        /* holder (Remote), the requester (Local), 0 (PFS) */
+} clairplan_source;
+/* n queries (samples[i], workers[i]); progress[w * J + j] = PrefetchProgress::completed[w][j]
+ * for ALL N workers (u64, policies.hpp:73-75); local_time / remote_time[j] = fetch_time_local /
+ * fetch_time_remote(1.0, cfg, j + 1), pfs_time = fetch_time_pfs(1.0, cfg, gamma)
+ * (perfmodel.cpp:109-121); on_device: every pointer but the two time tables is device memory.
+ * nopfs_choose_source = allow_local = allow_remote = 1. */
+int clairplan_choose_sources(clairplan_t plan, uint64_t n, const uint32_t* samples,
+                             const uint32_t* workers, const uint64_t* progress,
+                             const double* local_time, const double* remote_time, double pfs_time,
+                             int allow_local, int allow_remote, int heuristic, int on_device,
+                             clairplan_source* out);
+/* "Earliest remote holder" table: per sample, out[3k..3k+2] = {worker, class, position} of
+ * the holder with the smallest (remote_time[class-1], position, worker); all 0xFFFFFFFF for
+ * samples nobody caches.  A derived view (the reference scans holders_of per access). */
+int clairplan_earliest_holders(clairplan_t plan, const double* remote_time, uint32_t* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -31,6 +31,7 @@
 #include "clairsim/perfmodel.hpp"
 #include "clairsim/policies.hpp"
 #include "clairsim/rng.hpp"
+#include "clairsim/scenarios.hpp"
 
 using namespace clairsim;
 
@@ -420,6 +421,63 @@ int ref_all_access_counts(uint64_t seed, uint32_t F, uint32_t N, uint32_t B, uin
         const auto c = all_access_counts(Seed{seed}, F, PartitionSpec{N, B, E, drop_last != 0});
         for (uint32_t w = 0; w < N; ++w)
             std::memcpy(out + static_cast<uint64_t>(w) * F, c[w].data(), F * sizeof(uint32_t));
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 22;
+    }
+}
+
+// The presets' reference system (scenarios.cpp:15-46, reached through make_scenario: the
+// builder is file-local) for N workers with cache classes 1..J of the given capacities
+// (class specs beyond the preset's two repeat the last one).
+static SystemConfig chooser_cfg(uint32_t N, uint32_t J, const double* caps) {
+    SystemConfig cfg = make_scenario("imagenet1k").system;
+    cfg.workers = N;
+    const StorageClassSpec last = cfg.storage.back();
+    cfg.storage.resize(1 + J, last);
+    for (uint32_t j = 0; j < J; ++j) cfg.storage[1 + j].capacity_mb = caps[j];
+    return cfg;
+}
+
+// fetch_time_local / fetch_time_remote (1.0, cfg, j) and fetch_time_pfs (1.0, cfg, gamma):
+// the unit times the device chooser compares (perfmodel.cpp:109-121)
+int ref_unit_times(uint32_t N, uint32_t J, const double* caps, uint32_t gamma, double* local_t,
+                   double* remote_t, double* pfs_t) {
+    try {
+        const SystemConfig cfg = chooser_cfg(N, J, caps);
+        for (uint32_t j = 0; j < J; ++j) {
+            local_t[j] = fetch_time_local(1.0, cfg, j + 1);
+            remote_t[j] = fetch_time_remote(1.0, cfg, j + 1);
+        }
+        *pfs_t = fetch_time_pfs(1.0, cfg, gamma);
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 22;
+    }
+}
+
+// The reference's choose_source (policies.cpp:218-227) per query on the plan's assignment;
+// out[3i..3i+2] = {kind (FetchSource::Kind), storage_class, worker}.
+int ref_choose_sources(void* h, uint32_t N, uint32_t J, const double* caps, const uint64_t* progress,
+                       uint32_t gamma, int allow_local, int allow_remote, int heuristic,
+                       uint64_t n, const uint32_t* samples, const uint32_t* workers,
+                       uint32_t* out) {
+    try {
+        auto* p = static_cast<RefPlan*>(h);
+        const SystemConfig cfg = chooser_cfg(N, J, caps);
+        PrefetchProgress pr;
+        pr.completed.assign(N, std::vector<uint64_t>(J, 0));
+        for (uint32_t w = 0; w < N; ++w)
+            for (uint32_t j = 0; j < J; ++j) pr.completed[w][j] = progress[(uint64_t)w * J + j];
+        for (uint64_t i = 0; i < n; ++i) {
+            const FetchSource s = choose_source(samples[i], workers[i], p->assign, pr, gamma, cfg,
+                                                allow_local != 0, allow_remote != 0, heuristic != 0);
+            out[3 * i] = static_cast<uint32_t>(s.kind);
+            out[3 * i + 1] = s.storage_class;
+            out[3 * i + 2] = s.worker;
+        }
         return 0;
     } catch (const std::exception& e) {
         g_err = e.what();

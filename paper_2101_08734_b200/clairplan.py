@@ -107,8 +107,18 @@ def lib():
                                         u32p, C.c_int]
     L.clairplan_generate_sizes.argtypes = [C.c_uint64, C.c_double, C.c_double, C.c_int,
                                            C.c_double, C.c_uint64, C.c_int, f64p]
+    L.clairplan_choose_sources.argtypes = [C.c_void_p, C.c_uint64, u32p, u32p, u64p, f64p, f64p,
+                                           C.c_double, C.c_int, C.c_int, C.c_int, C.c_int,
+                                           C.c_void_p]
+    L.clairplan_earliest_holders.argtypes = [C.c_void_p, f64p, u32p]
     _lib = L
     return L
+
+
+# clairplan_source (include/clairplan.h): kind = FetchSource::Kind (0 Pfs, 1 Remote, 2 Local)
+SOURCE_DTYPE = np.dtype([("kind", np.uint8), ("storage_class", np.uint8), ("reserved", np.uint16),
+                         ("worker", np.uint32)])
+SRC_PFS, SRC_REMOTE, SRC_LOCAL = 0, 1, 2
 
 
 def _check(rc: int) -> None:
@@ -317,6 +327,37 @@ class Plan:
     def assignment(self) -> CacheAssignment:
         offs, hold = self.holders()
         return CacheAssignment(self.class_lists(), offs, hold)
+
+    def choose_sources(self, samples, workers, progress, local_time, remote_time, pfs_time,
+                       allow_local=True, allow_remote=True, heuristic=False) -> np.ndarray:
+        """choose_source / nopfs_choose_source (policies.cpp:184-233) for every (sample, worker)
+        query at once over this plan's holder CSR.  progress[w, j] = completed prefetches of
+        worker w in class j + 1 (PrefetchProgress, all N workers); local_time / remote_time[j]
+        and pfs_time: the unit fetch times of the caller's SystemConfig (perfmodel.cpp:109-121).
+        Returns a SOURCE_DTYPE array (kind, storage_class, worker)."""
+        samples = np.ascontiguousarray(samples, np.uint32)
+        workers = np.ascontiguousarray(workers, np.uint32)
+        progress = np.ascontiguousarray(progress, np.uint64)
+        lt = np.ascontiguousarray(local_time, np.float64)
+        rt = np.ascontiguousarray(remote_time, np.float64)
+        if samples.shape != workers.shape:
+            raise ValueError("samples and workers must have the same length")
+        out = np.zeros(len(samples), SOURCE_DTYPE)
+        _check(lib().clairplan_choose_sources(self._h, len(samples), _p(samples, u32p),
+                                              _p(workers, u32p), _p(progress, u64p), _p(lt, f64p),
+                                              _p(rt, f64p), float(pfs_time), int(allow_local),
+                                              int(allow_remote), int(heuristic), 0,
+                                              out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def earliest_holders(self, remote_time) -> np.ndarray:
+        """Per sample the holder {worker, class, position} with the smallest (remote unit fetch
+        time, position, worker): the north star's "earliest remote holder" table (a derived view;
+        0xFFFFFFFF rows for samples nobody caches)."""
+        rt = np.ascontiguousarray(remote_time, np.float64)
+        out = np.empty(self.samples * 3, np.uint32)
+        _check(lib().clairplan_earliest_holders(self._h, _p(rt, f64p), _p(out, u32p)))
+        return out.reshape(self.samples, 3)
 
 
 class StreamsAssignment(Plan):

@@ -167,6 +167,9 @@ class Ref:
                                             C.c_uint32, C.c_int, C.c_uint32, f64p, f64p, C.c_int,
                                             u32p, C.c_uint32]
         L.ref_last_phase_ms.argtypes = [f64p]
+        L.ref_unit_times.argtypes = [C.c_uint32, C.c_uint32, f64p, C.c_uint32, f64p, f64p, f64p]
+        L.ref_choose_sources.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, f64p, u64p, C.c_uint32,
+                                         C.c_int, C.c_int, C.c_int, C.c_uint64, u32p, u32p, u32p]
         L.ref_plan_build_subset_lowmem.restype = C.c_void_p
         L.ref_plan_build_subset_lowmem.argtypes = L.ref_plan_build_subset.argtypes
         L.ref_assign_from_streams.restype = C.c_void_p
@@ -306,6 +309,32 @@ class Ref:
     def access_frequencies(self, plan, w, eb, ee, F):
         out = np.empty(F, np.uint32)
         self.L.ref_access_frequencies(plan._h, w, eb, ee, _ptr(out, u32p))
+        return out
+
+    def unit_times(self, N, caps, gamma):
+        """fetch_time_local / _remote per class and fetch_time_pfs at size 1.0 on the preset
+        reference system (scenarios.cpp:15-46) with these class capacities."""
+        caps = np.ascontiguousarray(caps, np.float64)
+        J = len(caps)
+        lt, rt, pf = np.zeros(max(J, 1)), np.zeros(max(J, 1)), C.c_double()
+        if self.L.ref_unit_times(N, J, _ptr(caps, f64p), gamma, _ptr(lt, f64p), _ptr(rt, f64p),
+                                 C.byref(pf)):
+            raise ValueError(self.err())
+        return lt[:J], rt[:J], pf.value
+
+    def choose_sources(self, plan, N, caps, progress, gamma, samples, workers, allow_local=True,
+                       allow_remote=True, heuristic=False):
+        """The reference's choose_source per query: [n, 3] = (kind, class, worker)."""
+        caps = np.ascontiguousarray(caps, np.float64)
+        progress = np.ascontiguousarray(progress, np.uint64)
+        samples = np.ascontiguousarray(samples, np.uint32)
+        workers = np.ascontiguousarray(workers, np.uint32)
+        out = np.zeros((len(samples), 3), np.uint32)
+        if self.L.ref_choose_sources(plan._h, N, len(caps), _ptr(caps, f64p), _ptr(progress, u64p),
+                                     gamma, int(allow_local), int(allow_remote), int(heuristic),
+                                     len(samples), _ptr(samples, u32p), _ptr(workers, u32p),
+                                     _ptr(out, u32p)):
+            raise ValueError(self.err())
         return out
 
     def free(self, plan):

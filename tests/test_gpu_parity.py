@@ -342,6 +342,54 @@ def test_reference_simulator_over_the_dropin(preset):
     assert out["refsim_cpu"][1:] == out["refsim_b200"][1:], (out["refsim_cpu"], out["refsim_b200"])
 
 
+def test_choose_sources_match_reference(cp, ref):
+    """The plan consumer: the device's batched source chooser equals the
+    reference's choose_source (policies.cpp:184-233) query by query — local / remote /
+    PFS, progress thresholds, heuristic mode, the allow flags, ties (Local = Remote unit times
+    on the preset system) broken Local > Remote > lowest worker."""
+    F, N, B, E = 20_000, 8, 256, 6
+    for caps in ([150.0, 400.0], [1e6, 1e6], [20.0, 60.0, 100.0]):
+        sizes = ref.generate_sizes(F, 0.1077, 0.2, None, 1)
+        rp = ref.plan(42, F, N, B, E, True, caps, sizes, keep=True)
+        p = cp.Plan(42, F, cp.PartitionSpec(N, B, E, True), caps, sizes).build()
+        J = len(caps)
+        rng = np.random.default_rng(len(caps))
+        lens = np.array([[len(rp.class_lists[w][j]) for j in range(J)] for w in range(N)], np.uint64)
+        nq = 30_000
+        samples = rng.integers(0, F, nq).astype(np.uint32)
+        workers = rng.integers(0, N, nq).astype(np.uint32)
+        for trial in range(6):
+            frac = rng.uniform(0, 1.2, (N, J))
+            progress = np.minimum((lens * frac).astype(np.uint64), lens)
+            if trial == 0:
+                progress = lens.copy()        # every prefetch done
+            gamma = int(rng.integers(1, 9))
+            heuristic = bool(trial % 2)
+            al, ar = (True, True) if trial < 4 else ((trial == 4), (trial == 5))
+            lt, rt, pf = ref.unit_times(N, caps, gamma)
+            want = ref.choose_sources(rp, N, caps, progress, gamma, samples, workers, al, ar, heuristic)
+            got = p.choose_sources(samples, workers, progress, lt, rt, pf, al, ar, heuristic)
+            assert np.array_equal(got["kind"], want[:, 0].astype(np.uint8)), (caps, trial)
+            assert np.array_equal(got["storage_class"], want[:, 1].astype(np.uint8)), (caps, trial)
+            assert np.array_equal(got["worker"], want[:, 2]), (caps, trial)
+            kinds = set(np.unique(got["kind"]).tolist())
+            if trial == 0 and al and ar:
+                assert cp.SRC_LOCAL in kinds and cp.SRC_REMOTE in kinds
+        # the "earliest remote holder" table against a restatement over the holder CSR
+        lt, rt, pf = ref.unit_times(N, caps, 1)
+        eh = p.earliest_holders(rt)
+        offs, hold = p.holders()
+        for k in rng.integers(0, F, 2000):
+            hs = hold[offs[k]:offs[k + 1]]
+            if len(hs) == 0:
+                assert list(eh[k]) == [0xFFFFFFFF] * 3
+                continue
+            best = min(hs.tolist(), key=lambda h: (rt[h[1] - 1], h[2], h[0]))
+            assert list(eh[k]) == best, k
+        ref.free(rp)
+        p.close()
+
+
 def test_rejection_kat_device(cp):
     """Epochs whose shuffle hits a Lemire rejection (found with tools/find_rejection, digests
     from the reference): the device path resolves them bit-exactly."""
