@@ -256,6 +256,19 @@ int clairplan_choose_sources(clairplan_t plan, uint64_t n, const uint32_t* sampl
  * samples nobody caches.  A derived view (the reference scans holders_of per access). */
 int clairplan_earliest_holders(clairplan_t plan, const double* remote_time, uint32_t* out);
 
+/* ---- analysis reuse: counts stay on the device ------------------------
+ * FrequencyHistogram of one worker's counts on a built plan: buckets[c] = samples the worker
+ * accesses exactly c times (c > max_count lands in buckets[max_count]); analysis.hpp:33-41. */
+int clairplan_count_histogram(clairplan_t plan, uint32_t worker, uint32_t max_count,
+                              uint64_t* buckets);
+/* monte_carlo_histogram (analysis.cpp:84-96): worker 0 of the B = N, drop_last = false
+ * partition; buckets[0..epochs]. */
+int clairplan_monte_carlo_histogram(uint64_t seed, uint32_t workers, uint32_t epochs,
+                                    uint32_t samples, uint64_t* buckets, int device);
+/* Per sample the largest / smallest access count over all workers (the inputs of the Lemma-1
+ * property suite, acceptance.cpp:98-158), from the device counts. */
+int clairplan_count_extremes(const clairplan_config* cfg, uint32_t* hi, uint32_t* lo);
+
 #ifdef __cplusplus
 }
 #endif

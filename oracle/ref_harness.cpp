@@ -28,6 +28,7 @@
 #include <vector>
 
 #include "clairsim/access.hpp"
+#include "clairsim/analysis.hpp"
 #include "clairsim/perfmodel.hpp"
 #include "clairsim/policies.hpp"
 #include "clairsim/rng.hpp"
@@ -478,6 +479,41 @@ int ref_choose_sources(void* h, uint32_t N, uint32_t J, const double* caps, cons
             out[3 * i + 1] = s.storage_class;
             out[3 * i + 2] = s.worker;
         }
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 22;
+    }
+}
+
+// analysis.cpp:84-96 and the C1 / C2 acceptance quantities (acceptance.cpp:76-158)
+int ref_monte_carlo_histogram(uint64_t seed, uint32_t N, uint32_t E, uint32_t F, uint64_t* out) {
+    try {
+        const FrequencyHistogram h = monte_carlo_histogram(Seed{seed}, N, E, F);
+        for (size_t c = 0; c < h.buckets.size(); ++c) out[c] = h.buckets[c];
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 22;
+    }
+}
+
+double ref_expected_hot_samples(uint32_t N, uint32_t E, uint64_t F, double delta) {
+    return expected_hot_samples(AccessDistributionParams{N, E, F, delta});
+}
+
+uint32_t ref_hot_count_threshold(uint32_t N, uint32_t E, double delta) {
+    return hot_count_threshold(N, E, delta);
+}
+
+// {high_threshold, counterpart_low_bound, low_threshold, counterpart_high_bound}
+int ref_lemma1_bounds(uint32_t N, uint32_t E, double delta, int64_t* out) {
+    try {
+        const Lemma1Bounds b = lemma1_bounds(N, E, delta);
+        out[0] = b.high_threshold;
+        out[1] = b.counterpart_low_bound;
+        out[2] = b.low_threshold;
+        out[3] = b.counterpart_high_bound;
         return 0;
     } catch (const std::exception& e) {
         g_err = e.what();

@@ -111,6 +111,10 @@ def lib():
                                            C.c_double, C.c_int, C.c_int, C.c_int, C.c_int,
                                            C.c_void_p]
     L.clairplan_earliest_holders.argtypes = [C.c_void_p, f64p, u32p]
+    L.clairplan_count_histogram.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, u64p]
+    L.clairplan_monte_carlo_histogram.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
+                                                  u64p, C.c_int]
+    L.clairplan_count_extremes.argtypes = [C.POINTER(_Config), u32p, u32p]
     _lib = L
     return L
 
@@ -350,6 +354,12 @@ class Plan:
                                               out.ctypes.data_as(C.c_void_p)))
         return out
 
+    def count_histogram(self, worker: int, max_count: int) -> np.ndarray:
+        """FrequencyHistogram of `worker`'s access counts, computed on the device."""
+        out = np.zeros(max_count + 1, np.uint64)
+        _check(lib().clairplan_count_histogram(self._h, worker, max_count, _p(out, u64p)))
+        return out
+
     def earliest_holders(self, remote_time) -> np.ndarray:
         """Per sample the holder {worker, class, position} with the smallest (remote unit fetch
         time, position, worker): the north star's "earliest remote holder" table (a derived view;
@@ -474,6 +484,24 @@ def nopfs_assign_caches(freqs, capacities_mb, sizes_mb, streams, device: int = 0
     a = plan.assignment()
     plan.close()
     return a
+
+
+def monte_carlo_histogram(seed: int, workers: int, epochs: int, samples: int,
+                          device: int = 0) -> np.ndarray:
+    """analysis.cpp:84-96 on the device: worker 0's count histogram (B = N, drop_last=false)."""
+    out = np.zeros(epochs + 1, np.uint64)
+    _check(lib().clairplan_monte_carlo_histogram(seed, workers, epochs, samples, _p(out, u64p), device))
+    return out
+
+
+def count_extremes(seed: int, samples: int, part: PartitionSpec, device: int = 0):
+    """Per sample (largest, smallest) access count over all workers, from device counts
+    (the Lemma-1 property suite's inputs, acceptance.cpp:98-158)."""
+    cfg = _cfg_only(seed, samples, part, device)
+    hi = np.empty(samples, np.uint32)
+    lo = np.empty(samples, np.uint32)
+    _check(lib().clairplan_count_extremes(C.byref(cfg), _p(hi, u32p), _p(lo, u32p)))
+    return hi, lo
 
 
 def generate_sizes(samples: int, mean_mb: float, sigma_mb: float, total_mb=None, seed: int = 1,

@@ -167,6 +167,12 @@ class Ref:
                                             C.c_uint32, C.c_int, C.c_uint32, f64p, f64p, C.c_int,
                                             u32p, C.c_uint32]
         L.ref_last_phase_ms.argtypes = [f64p]
+        L.ref_monte_carlo_histogram.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, u64p]
+        L.ref_expected_hot_samples.restype = C.c_double
+        L.ref_expected_hot_samples.argtypes = [C.c_uint32, C.c_uint32, C.c_uint64, C.c_double]
+        L.ref_hot_count_threshold.restype = C.c_uint32
+        L.ref_hot_count_threshold.argtypes = [C.c_uint32, C.c_uint32, C.c_double]
+        L.ref_lemma1_bounds.argtypes = [C.c_uint32, C.c_uint32, C.c_double, C.POINTER(C.c_int64)]
         L.ref_unit_times.argtypes = [C.c_uint32, C.c_uint32, f64p, C.c_uint32, f64p, f64p, f64p]
         L.ref_choose_sources.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, f64p, u64p, C.c_uint32,
                                          C.c_int, C.c_int, C.c_int, C.c_uint64, u32p, u32p, u32p]
@@ -310,6 +316,24 @@ class Ref:
         out = np.empty(F, np.uint32)
         self.L.ref_access_frequencies(plan._h, w, eb, ee, _ptr(out, u32p))
         return out
+
+    def monte_carlo_histogram(self, seed, N, E, F):
+        out = np.zeros(E + 1, np.uint64)
+        if self.L.ref_monte_carlo_histogram(seed, N, E, F, _ptr(out, u64p)):
+            raise ValueError(self.err())
+        return out
+
+    def expected_hot_samples(self, N, E, F, delta):
+        return self.L.ref_expected_hot_samples(N, E, F, delta)
+
+    def hot_count_threshold(self, N, E, delta):
+        return self.L.ref_hot_count_threshold(N, E, delta)
+
+    def lemma1_bounds(self, N, E, delta):
+        out = (C.c_int64 * 4)()
+        if self.L.ref_lemma1_bounds(N, E, delta, out):
+            raise ValueError(self.err())
+        return tuple(int(x) for x in out)
 
     def unit_times(self, N, caps, gamma):
         """fetch_time_local / _remote per class and fetch_time_pfs at size 1.0 on the preset

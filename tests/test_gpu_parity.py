@@ -390,6 +390,49 @@ def test_choose_sources_match_reference(cp, ref):
         p.close()
 
 
+def test_analysis_reuse_monte_carlo_c1(cp, ref):
+    """Acceptance C1 (acceptance.cpp:76-93) on device counts: monte_carlo_histogram
+    (analysis.cpp:84-96) equals the reference's bucket for bucket, and its hot count lies
+    within 5% of the analytic expectation (expected_hot_samples, ~31,635)."""
+    N, E, F, delta = 16, 90, 1_281_167, 0.8
+    got = cp.monte_carlo_histogram(1, N, E, F)
+    want = ref.monte_carlo_histogram(1, N, E, F)
+    assert np.array_equal(got, want)
+    assert int(got.sum()) == F
+    expected = ref.expected_hot_samples(N, E, F, delta)
+    assert abs(expected - 31634.685810763236) < 1e-6
+    hot = int(got[ref.hot_count_threshold(N, E, delta):].sum())
+    assert abs(hot - expected) / expected < 0.05
+    for seed, N, E, F in ((3, 4, 10, 5000), (7, 16, 100, 20_011)):
+        assert np.array_equal(cp.monte_carlo_histogram(seed, N, E, F),
+                              ref.monte_carlo_histogram(seed, N, E, F))
+
+
+def test_analysis_reuse_lemma1_c2(cp, ref):
+    """Acceptance C2 (acceptance.cpp:98-158): the Lemma-1 counterpart bounds over 50 seeds,
+    N in {2, 4, 16}, E in {4, 10, 90}, F in {1e3, 1e4}, evaluated from device per-sample count
+    extremes (after removing one worker holding the maximum, the others' minimum is the
+    minimum, and symmetrically); extremes equal the reference's all_access_counts reductions."""
+    checked = 0
+    for N in (2, 4, 16):
+        for E in (4, 10, 90):
+            for F in (1000, 10000):
+                part = cp.PartitionSpec(N, N, E, False)
+                for seed in range(50):
+                    hi, lo = cp.count_extremes(seed, F, part)
+                    if seed % 17 == 0:
+                        allc = ref.all_access_counts(seed, F, N, N, E, False)
+                        assert np.array_equal(hi, allc.max(axis=0)) and np.array_equal(lo, allc.min(axis=0))
+                    for delta in (0.2, 0.4, 0.6, 0.8, 1.0):
+                        if delta > N - 1:
+                            continue
+                        hth, clow, lth, chigh = ref.lemma1_bounds(N, E, delta)
+                        assert not np.any((hi >= hth) & (lo > clow)), (N, E, F, seed, delta)
+                        assert not np.any((lo.astype(np.int64) <= lth) & (hi < chigh)), (N, E, F, seed, delta)
+                        checked += F
+    assert checked > 0
+
+
 def test_rejection_kat_device(cp):
     """Epochs whose shuffle hits a Lemire rejection (found with tools/find_rejection, digests
     from the reference): the device path resolves them bit-exactly."""
