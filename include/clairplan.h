@@ -269,6 +269,30 @@ int clairplan_monte_carlo_histogram(uint64_t seed, uint32_t workers, uint32_t ep
  * property suite, acceptance.cpp:98-158), from the device counts. */
 int clairplan_count_extremes(const clairplan_config* cfg, uint32_t* hi, uint32_t* lo);
 
+/* ---- plan wire format -------------------------------------------------
+ * A versioned binary image of one handle's plan for files and for distribution (the paper's
+ * middleware all-gathers the access information at setup; the reference
+ * has no serialization).  Sections follow the header at the recorded offsets (16-B aligned):
+ * capacities f64[J], streams u32[A], class bounds u64[2 * nloc * J] ({offset, length} into
+ * the class-list section, worker-major), class lists u32[class_entries], holder offsets
+ * u64[F + 1], holders u32[3 * holders].  checksum[s] = sum_i mix64((s << 56) + i * golden)
+ * ^ word_i (mod 2^64) over the 32-bit words of section s (0 caps .. 5 holders). */
+#define CLAIRPLAN_WIRE_VERSION 1
+typedef struct {
+    char magic[8];              /* "CLPLAN\0\1" */
+    uint32_t version, header_bytes;
+    uint64_t seed;
+    uint32_t samples, num_workers, global_batch, epochs;
+    uint32_t drop_last, num_classes, worker_begin, worker_end;
+    uint64_t accesses, class_entries, holders;
+    uint64_t off_caps, off_streams, off_class_bounds, off_class_lists, off_holder_offsets,
+        off_holders, total_bytes;
+    uint64_t checksum[6];
+    uint8_t reserved[256 - 8 - 8 - 8 - 32 - 24 - 56 - 48];
+} clairplan_wire_header;
+int clairplan_wire_size(clairplan_t plan, uint64_t* bytes);
+int clairplan_wire_write(clairplan_t plan, void* out, uint64_t cap);
+
 #ifdef __cplusplus
 }
 #endif

@@ -111,6 +111,8 @@ def lib():
                                            C.c_double, C.c_int, C.c_int, C.c_int, C.c_int,
                                            C.c_void_p]
     L.clairplan_earliest_holders.argtypes = [C.c_void_p, f64p, u32p]
+    L.clairplan_wire_size.argtypes = [C.c_void_p, u64p]
+    L.clairplan_wire_write.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64]
     L.clairplan_count_histogram.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, u64p]
     L.clairplan_monte_carlo_histogram.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
                                                   u64p, C.c_int]
@@ -352,6 +354,14 @@ class Plan:
                                               _p(rt, f64p), float(pfs_time), int(allow_local),
                                               int(allow_remote), int(heuristic), 0,
                                               out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def wire(self) -> np.ndarray:
+        """The plan as a versioned binary image (include/clairplan.h, wire.py parses it)."""
+        n = C.c_uint64()
+        _check(lib().clairplan_wire_size(self._h, C.byref(n)))
+        out = np.empty(n.value, np.uint8)
+        _check(lib().clairplan_wire_write(self._h, out.ctypes.data_as(C.c_void_p), n.value))
         return out
 
     def count_histogram(self, worker: int, max_count: int) -> np.ndarray:

@@ -433,6 +433,37 @@ def test_analysis_reuse_lemma1_c2(cp, ref):
     assert checked > 0
 
 
+def test_wire_image_round_trip_and_shard_merge(cp, ref):
+    """Plan wire format: the device writer's image parses with every section
+    checksum verified and equals the plan's exports and the reference; images of three
+    worker-range handles merged on the host equal the single-handle plan."""
+    from paper_2101_08734_b200 import wire
+    F, N, B, E = 30_000, 12, 240, 9
+    for caps in ([20.0, 60.0], [1e6, 1e6]):
+        sizes = ref.generate_sizes(F, 0.1077, 0.2, None, 1)
+        p = cp.Plan(5, F, cp.PartitionSpec(N, B, E, True), caps, sizes).build()
+        img = wire.parse(p.wire())
+        want = ref.plan(5, F, N, B, E, True, caps, sizes)
+        assert np.array_equal(img["streams"], np.concatenate(want.streams))
+        assert all(np.array_equal(x, y) for a, b in zip(wire.class_lists(img), want.class_lists)
+                   for x, y in zip(a, b))
+        assert np.array_equal(img["holder_offsets"], want.holder_offsets.astype(np.uint64))
+        assert np.array_equal(img["holders"], want.holders)
+        assert list(img["capacities"]) == caps
+        p.close()
+        shards = []
+        for wr in ((0, 5), (5, 6), (6, 12)):
+            q = cp.Plan(5, F, cp.PartitionSpec(N, B, E, True), caps, sizes, worker_range=wr).build()
+            shards.append(wire.parse(q.wire()))
+            q.close()
+        m = wire.merge_shards(shards[::-1])
+        assert np.array_equal(m["streams"], img["streams"])
+        assert np.array_equal(m["holder_offsets"], img["holder_offsets"])
+        assert np.array_equal(m["holders"], img["holders"])
+        assert all(np.array_equal(x, y) for a, b in zip(m["class_lists"], wire.class_lists(img))
+                   for x, y in zip(a, b))
+
+
 def test_rejection_kat_device(cp):
     """Epochs whose shuffle hits a Lemire rejection (found with tools/find_rejection, digests
     from the reference): the device path resolves them bit-exactly."""
