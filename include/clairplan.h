@@ -191,6 +191,12 @@ int clairplan_open_peer_buffer(clairplan_t plan, const void* ipc_handle, void** 
 /* Per-sample number of holder records of the handle's workers, d_out[F] (device): the
  * input of the cross-GPU holder-offset merge (all-gather + exclusive scan over ranks). */
 int clairplan_holder_counts(clairplan_t plan, uint32_t* d_out);
+/* Holder-offset merge of a worker-sharded plan on `stream` (0: the legacy default stream): d_allc =
+ * [world][F] per-rank per-sample holder counts (the all-gather of clairplan_holder_counts),
+ * d_glob[F + 1] = global CSR offsets, d_starts[F] = where this rank's records of each sample
+ * start (ranks own ascending worker ranges: build_index's order, policies.cpp:124-142). */
+int clairplan_merge_holder_counts(clairplan_t plan, const uint32_t* d_allc, uint32_t world,
+                                  uint32_t rank, int64_t* d_glob, int64_t* d_starts, void* stream);
 /* Overlap of that merge with the build's tail (no reference counterpart: the reference is a
  * single process).  During the next builds, as soon as the per-sample pair counts exist,
  * they are copied into d_counts[F] (device), `stream` (a cudaStream_t, e.g. the caller's
@@ -292,6 +298,15 @@ typedef struct {
 } clairplan_wire_header;
 int clairplan_wire_size(clairplan_t plan, uint64_t* bytes);
 int clairplan_wire_write(clairplan_t plan, void* out, uint64_t cap);
+/* Section checksums of the image this handle contributes to a merged (all-shard) image,
+ * computed on the device without any copy: the streams start at word stream_base of the
+ * merged streams section, the class lists at entry list_base, and the holder records at the
+ * global CSR positions d_holder_starts[k] + local rank (device u64[F]; null: the handle's own
+ * CSR, whose offsets are then summed too).  out[1] streams, out[3] class lists, out[4] holder
+ * offsets (own CSR only), out[5] holders; out[0], out[2] are 0.  Summing the shards' values
+ * (mod 2^64) gives the merged image's checksums: a scale-free cross-check of sharded builds. */
+int clairplan_wire_checksums(clairplan_t plan, uint64_t stream_base, uint64_t list_base,
+                             const uint64_t* d_holder_starts, uint64_t* out);
 
 #ifdef __cplusplus
 }

@@ -110,3 +110,66 @@ void launch_stream_inv(cudaStream_t s, const Part& part, const uint32_t* stream,
 }
 
 }  // namespace clairplan
+
+// ---- holder-offset merge of a worker-sharded plan (DESIGN §6 step 4) -------------------
+// allc[r][k] = holder records of sample k on rank r; the global CSR offset of k is the
+// exclusive scan of the per-sample totals, and rank `rank`'s records of k start after those
+// of ranks < rank (contiguous ascending worker ranges: build_index's worker order,
+// policies.cpp:124-142).
+namespace clairplan {
+
+__global__ void merge_counts_kernel(const uint32_t* __restrict__ allc, uint32_t world, uint32_t rank,
+                                    uint32_t F, uint32_t* __restrict__ tot, uint32_t* __restrict__ before) {
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < F; k += gridDim.x * blockDim.x) {
+        uint32_t t = 0, b = 0;
+        for (uint32_t r = 0; r < world; ++r) {
+            const uint32_t c = allc[(uint64_t)r * F + k];
+            t += c;
+            b += r < rank ? c : 0u;
+        }
+        tot[k] = t;
+        before[k] = b;
+    }
+}
+
+__global__ void merge_starts_kernel(const uint64_t* __restrict__ glob, const uint32_t* __restrict__ before,
+                                    uint32_t F, uint64_t* __restrict__ starts) {
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < F; k += gridDim.x * blockDim.x)
+        starts[k] = glob[k] + before[k];
+}
+
+}  // namespace clairplan
+
+#include "plan_impl.h"
+
+extern "C" int clairplan_merge_holder_counts(clairplan_t p, const uint32_t* d_allc, uint32_t world,
+                                             uint32_t rank, int64_t* d_glob, int64_t* d_starts,
+                                             void* stream) {
+    if (!p || !d_allc || !d_glob || !d_starts) return fail(CLAIRPLAN_EINVAL, "null argument");
+    if (world < 1 || rank >= world) return fail(CLAIRPLAN_EINVAL, "invalid rank");
+    CK(cudaSetDevice(p->device));
+    const uint32_t F = p->part.F;
+    // the caller's stream as given: 0 is the legacy default stream (torch's default stream,
+    // where the all-gather of the counts ran), not "the handle's stream"
+    cudaStream_t s = (cudaStream_t)stream;
+    // own scratch: this may run while the handle's build is still in flight on p->stream
+    // scan scratch: two (tiles + 1) u64 arrays per level, 256-B rounded (generous: a scratch
+    // request that does not fit would hand the scan kernels a null pointer)
+    const uint64_t nb = (uint64_t)F / 256 + 64;
+    if (!p->merge_buf.ensure((uint64_t)F * 8 + 4 * nb * 8 + (64u << 10)))
+        return fail(CLAIRPLAN_ENOMEM, "device allocation failed (holder merge)");
+    uint32_t* tot = p->merge_buf.get<uint32_t>();
+    uint32_t* before = tot + F;
+    Workspace ws;
+    ws.base = reinterpret_cast<char*>(p->merge_buf.get<uint32_t>() + 2 * (uint64_t)F);
+    ws.base = reinterpret_cast<char*>(((uintptr_t)ws.base + 255) & ~(uintptr_t)255);
+    ws.cap = p->merge_buf.bytes - (ws.base - p->merge_buf.get<char>());
+    merge_counts_kernel<<<grid_for(F, kThreads), kThreads, 0, s>>>(d_allc, world, rank, F, tot, before);
+    exclusive_scan(s, tot, F, reinterpret_cast<uint64_t*>(d_glob), ws);
+    merge_starts_kernel<<<grid_for(F, kThreads), kThreads, 0, s>>>(reinterpret_cast<uint64_t*>(d_glob),
+                                                                   before, F,
+                                                                   reinterpret_cast<uint64_t*>(d_starts));
+    CK(cudaGetLastError());
+    if (ws.overflow) return fail(CLAIRPLAN_ENOMEM, "internal workspace overflow (holder merge)");
+    return 0;
+}

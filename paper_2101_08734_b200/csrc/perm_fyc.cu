@@ -23,6 +23,7 @@
 // Large F (lg F + lg W > 32): bucket entries hold the step only and fyc_block redraws j_i;
 // otherwise (step << lgW) | target-in-block.
 #include <cmath>
+#include <cstdio>
 #include <vector>
 
 #include "internal.h"
@@ -253,12 +254,15 @@ __global__ void __launch_bounds__(kFycPT) fyc_block_kernel(uint64_t key, uint32_
                                                            const uint32_t* __restrict__ cursor,
                                                            uint32_t* __restrict__ tsucc,
                                                            uint32_t* __restrict__ q,
-                                                           uint32_t* __restrict__ inv) {
+                                                           uint32_t* __restrict__ inv, int check) {
     extern __shared__ uint32_t sm[];
     __shared__ uint32_t wsum[kFycPT / 32];
     const uint32_t b = blockIdx.x, slot = blockIdx.y, e = e0 + slot;
     const uint32_t y0 = __ldg(g.bstart + b), W = __ldg(g.bstart + b + 1) - y0;
     const uint32_t n = min(cursor[(size_t)slot * g.NB + b], __ldg(g.cap + b));
+    if (check && threadIdx.x == 0 && cursor[(size_t)slot * g.NB + b] > __ldg(g.cap + b))
+        printf("fyc_block: block %u of epoch %u overflows (%u > cap %u)\n", b, e,
+               cursor[(size_t)slot * g.NB + b], __ldg(g.cap + b));
     uint32_t* off = sm;               // [W + 1] counts -> offsets
     uint32_t* S = sm + kFycW + 1;     // [n] writers grouped by target
     const uint32_t* reg = region + (size_t)slot * g.rtotal + __ldg(g.roff + b);
@@ -285,6 +289,10 @@ __global__ void __launch_bounds__(kFycPT) fyc_block_kernel(uint64_t key, uint32_
             iv[k] >>= g.lgW;
         } else {
             jl = fyc_draw(key, e, F, iv[k], st, cu, nrej, nullptr) - y0;
+        }
+        if (check && (jl >= W || iv[k] >= F)) {
+            printf("fyc_block: entry out of range b=%u e=%u i=%u jl=%u W=%u\n", b, e, iv[k], jl, W);
+            continue;
         }
         jr[k] = jl | (atomicAdd(&off[jl], 1u) << 16);  // jl < 8192, rank < 7168
     }
@@ -330,7 +338,8 @@ __global__ void __launch_bounds__(kThreads, 4) fyc_emit_kernel(Part part, uint32
                                                                uint32_t* __restrict__ inv,
                                                                uint32_t* __restrict__ stream,
                                                                uint32_t* __restrict__ perm_out,
-                                                               const StreamDst dst) {
+                                                               const StreamDst dst, int check,
+                                                               uint32_t* __restrict__ err) {
     constexpr uint32_t CH = kFycEmitL * 32;
     __shared__ uint32_t sbuf[kThreads / 32][CH];
     __shared__ uint16_t slist[kThreads / 32][CH];
@@ -376,6 +385,13 @@ __global__ void __launch_bounds__(kThreads, 4) fyc_emit_kernel(Part part, uint32
         }
         nj += 32;
         while (__any_sync(0xffffffffu, a0 || a1)) {
+            if (check && ((a0 && cur0 >= F) || (a1 && cur1 >= F))) {
+                printf("fyc_emit: chase index out of range e=%u chunk=%u cur0=%u cur1=%u F=%u\n", e, c,
+                       a0 ? cur0 : 0u, a1 ? cur1 : 0u, F);
+                atomicOr(err, 1u);
+                a0 = a1 = false;
+                break;
+            }
             const uint32_t q0 = a0 ? qq[cur0] : 0u;
             const uint32_t q1 = a1 ? qq[cur1] : 0u;
             if (a0) {
@@ -411,6 +427,11 @@ __global__ void __launch_bounds__(kThreads, 4) fyc_emit_kernel(Part part, uint32
             const uint32_t i = cb + t * 32 + lane;
             if (i >= F) break;
             const uint32_t v = buf[t * 32 + lane];
+            if (check && v >= F) {
+                printf("fyc_emit: output out of range e=%u i=%u v=%u sv=%x\n", e, i, v, sv[t]);
+                atomicOr(err, 2u);
+                continue;
+            }
             if (perm_out) perm_out[(size_t)slot * F + i] = v;
             if (inv && !(sv[t] & kTag)) inv[(size_t)e * F + v] = i;  // chase roots only
             if ((stream || dst.G) && i < part.P) {
@@ -448,6 +469,7 @@ void launch_fyc(cudaStream_t s, uint64_t key, const Part& part, uint32_t e0, uin
                 uint32_t* cursor, uint32_t* tsucc, uint32_t* q, uint32_t* inv, uint32_t* stream,
                 uint32_t* perm_out, const StreamDst* dst) {
     const uint32_t F = part.F;
+    static const int check = (int)env_uint("CLAIRPLAN_FYC_CHECK", 0);  // debug bounds checks
     cudaMemsetAsync(cursor, 0, (size_t)ne * g.NB * 4, s);
     const uint32_t TS = g.pack ? kFycTS : 2 * kFycTS;
     const uint32_t NT = (F + TS - 1) / TS;
@@ -458,18 +480,19 @@ void launch_fyc(cudaStream_t s, uint64_t key, const Part& part, uint32_t e0, uin
         cudaFuncSetAttribute(fyc_block_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_block);
         fyc_part_kernel<true><<<dim3(NT, ne), kFycPT, sm_part, s>>>(key, F, e0, g, rt, rej_flag, region, cursor);
         fyc_block_kernel<true><<<dim3(g.NB, ne), kFycPT, sm_block, s>>>(key, F, e0, g, rt, region, cursor,
-                                                                        tsucc, q, inv);
+                                                                        tsucc, q, inv, check);
     } else {
         cudaFuncSetAttribute(fyc_part_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_part);
         cudaFuncSetAttribute(fyc_block_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_block);
         fyc_part_kernel<false><<<dim3(NT, ne), kFycPT, sm_part, s>>>(key, F, e0, g, rt, rej_flag, region, cursor);
         fyc_block_kernel<false><<<dim3(g.NB, ne), kFycPT, sm_block, s>>>(key, F, e0, g, rt, region, cursor,
-                                                                         tsucc, q, inv);
+                                                                         tsucc, q, inv, check);
     }
     const StreamDst dloc = dst ? *dst : StreamDst{};
     const uint32_t nchunk = (F + kFycEmitL * 32 - 1) / (kFycEmitL * 32);
     dim3 gq(std::max<uint32_t>(1, std::min<uint32_t>((nchunk + 7) / 8, 148u * 8u)), ne);
-    fyc_emit_kernel<<<gq, kThreads, 0, s>>>(part, e0, tsucc, q, inv, stream, perm_out, dloc);
+    fyc_emit_kernel<<<gq, kThreads, 0, s>>>(part, e0, tsucc, q, inv, stream, perm_out, dloc, check,
+                                            rej_flag + (e0 - rt.e_base));
 }
 
 }  // namespace clairplan

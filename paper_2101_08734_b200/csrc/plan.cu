@@ -63,7 +63,11 @@ bool fyc_ready(clairplan_plan* p, uint32_t F, FycDev& g) {
         buf.push_back(0);
         for (uint64_t x : h.roff) buf.push_back((uint32_t)x);
         buf.insert(buf.end(), h.cell.begin(), h.cell.end());
-        if (cudaMemcpy(p->fyc_geo.p, buf.data(), buf.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) {
+        // stream-ordered with the shuffle kernels (a plain cudaMemcpy from pageable memory may
+        // return before its DMA lands, and the handle's stream does not wait for the legacy
+        // stream); pageable source: the call returns once the buffer is staged
+        if (cudaMemcpyAsync(p->fyc_geo.p, buf.data(), buf.size() * 4, cudaMemcpyHostToDevice,
+                            p->stream) != cudaSuccess) {
             cudaGetLastError();
             h.F = 0;
             return false;
@@ -1150,8 +1154,11 @@ int clairplan_create(const clairplan_config* c, clairplan_t* out) {
     }
     cudaError_t e = cudaSuccess;
     if (c->sizes_mb)
-        e = cudaMemcpy(p->sizes.get<double>(), c->sizes_mb, (size_t)c->samples * 8,
-                       c->sizes_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice);
+        // on the handle's (non-blocking) stream: every kernel reading the sizes runs there
+        e = cudaMemcpyAsync(p->sizes.get<double>(), c->sizes_mb, (size_t)c->samples * 8,
+                            c->sizes_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                            p->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(p->stream);  // the caller may free sizes_mb
     if (e != cudaSuccess) {
         delete p;
         return fail(CLAIRPLAN_ECUDA, std::string("sizes upload: ") + cudaGetErrorString(e));

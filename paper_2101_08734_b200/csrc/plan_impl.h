@@ -126,6 +126,7 @@ struct clairplan_plan {
     FycHost fych;
     DevBuf fyc_geo, fyc_region, fyc_cursor;
     bool fyc_off = false;            // a block region overflowed once: linked-list path
+    DevBuf merge_buf;                // clairplan_merge_holder_counts scratch (own: may overlap a build)
     DevBuf sorted_k;                 // tier path: sample id of every tier position (seg_write3)
     bool ssize_pending = false;      // sorted_size not yet gathered (class 1's ff_stats does it)
     DevBuf hpos;                     // tier path: [E][Fp] class << 28 | class-list position (hp_fill)

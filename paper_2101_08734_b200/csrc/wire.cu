@@ -29,6 +29,33 @@ __global__ void wire_sum_kernel(const uint32_t* __restrict__ w, uint64_t n, uint
     if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
 }
 
+// holder records of a shard summed at their positions in the merged (all-shard) CSR:
+// record r of sample k sits at starts[k] + (r - own_offset[k])
+__global__ void wire_holder_sum_kernel(const uint32_t* __restrict__ hold, const uint64_t* __restrict__ hoff,
+                                       const uint64_t* __restrict__ starts, uint32_t F, uint64_t key,
+                                       unsigned long long* __restrict__ out) {
+    unsigned long long acc = 0;
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < F; k += gridDim.x * blockDim.x) {
+        const uint64_t a = hoff[k], b = hoff[k + 1], g = starts[k];
+        for (uint64_t r = a; r < b; ++r)
+            for (uint32_t c = 0; c < 3; ++c)
+                acc += mix64(key + (3 * (g + r - a) + c) * kGolden) ^ (uint64_t)hold[3 * r + c];
+    }
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
+}
+
+// a section of `words` 32-bit words starting at word position `base` of the merged section
+__global__ void wire_sum_at_kernel(const uint32_t* __restrict__ w, uint64_t n, uint64_t base,
+                                   uint64_t key, unsigned long long* __restrict__ out) {
+    unsigned long long acc = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        acc += mix64(key + (base + i) * kGolden) ^ (uint64_t)w[i];
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
+}
+
 static uint64_t align16(uint64_t x) { return (x + 15) & ~15ull; }
 
 struct WireLayout {
@@ -144,6 +171,49 @@ int clairplan_wire_write(clairplan_t p, void* out, uint64_t cap) {
     h.checksum[4] = hs[4];
     h.checksum[5] = hs[5];
     memcpy(o, &h, sizeof(h));
+    return 0;
+}
+
+int clairplan_wire_checksums(clairplan_t p, uint64_t stream_base, uint64_t list_base,
+                             const uint64_t* d_holder_starts, uint64_t* out) {
+    if (!p || !p->built || p->generic) return fail(CLAIRPLAN_EINVAL, "plan not built");
+    if (!out) return fail(CLAIRPLAN_EINVAL, "null argument");
+    CK(cudaSetDevice(p->device));
+    cudaStream_t s = p->stream;
+    const uint32_t J = p->cfg.num_classes, F = p->part.F;
+    DevBuf sums;
+    if (!sums.ensure(8 * 6)) return fail(CLAIRPLAN_ENOMEM, "device allocation failed");
+    CK(cudaMemsetAsync(sums.p, 0, 8 * 6, s));
+    unsigned long long* ds = sums.get<unsigned long long>();
+    if (p->A)
+        wire_sum_at_kernel<<<grid_for(p->A, kThreads, 148u * 8u), kThreads, 0, s>>>(
+            p->stream_buf.get<uint32_t>(), p->A, stream_base, 1ull << 56, ds + 1);
+    // class lists: (w, j) lists back to back, worker-major, from the list start of the shard
+    uint64_t o = list_base;
+    for (uint32_t w = 0; w < p->nloc; ++w)
+        for (uint32_t j = 0; j < J; ++j) {
+            const uint64_t n = p->class_len_h[(size_t)w * (J + 1) + j];
+            const uint64_t st = p->class_start_h[(size_t)w * (J + 1) + j];
+            if (n)
+                wire_sum_at_kernel<<<grid_for(n, kThreads, 148u * 8u), kThreads, 0, s>>>(
+                    p->class_entries.get<uint32_t>() + st, n, o, 3ull << 56, ds + 3);
+            o += n;
+        }
+    if (!d_holder_starts) {
+        wire_sum_kernel<<<grid_for(2 * ((uint64_t)F + 1), kThreads, 148u * 8u), kThreads, 0, s>>>(
+            reinterpret_cast<const uint32_t*>(p->holder_off_dev), 2 * ((uint64_t)F + 1), 4ull << 56, ds + 4);
+        if (p->H)
+            wire_sum_kernel<<<grid_for(3 * p->H, kThreads, 148u * 8u), kThreads, 0, s>>>(
+                p->holders_dev, 3 * p->H, 5ull << 56, ds + 5);
+    } else if (p->H) {
+        wire_holder_sum_kernel<<<grid_for(F, kThreads, 148u * 8u), kThreads, 0, s>>>(
+            p->holders_dev, p->holder_off_dev, d_holder_starts, F, 5ull << 56, ds + 5);
+    }
+    CK(cudaGetLastError());
+    unsigned long long hs[6] = {};
+    CK(cudaMemcpyAsync(hs, ds, sizeof(hs), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (int i = 0; i < 6; ++i) out[i] = hs[i];
     return 0;
 }
 

@@ -128,6 +128,8 @@ class DistributedPlan:
         L.clairplan_generate_streams.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p]
         L.clairplan_build_from_streams.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32]
         L.clairplan_epoch_prefix.argtypes = [C.c_void_p, C.c_uint32, C.POINTER(C.c_uint64)]
+        L.clairplan_merge_holder_counts.argtypes = [C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32,
+                                                    C.c_void_p, C.c_void_p, C.c_void_p]
         self.L = L
         N = part.num_workers
         self.p2p = False
@@ -252,11 +254,23 @@ class DistributedPlan:
         self.flag = torch.zeros(1, dtype=torch.int32, device="cuda")
         return True
 
+    def _merge(self):
+        """Global CSR offsets + this rank's starts from the gathered counts: one library call
+        (merge kernel + scan) on torch's current stream, after the all-gather."""
+        torch = self.torch
+        glob = torch.empty(self.samples + 1, dtype=torch.int64, device="cuda")
+        starts = torch.empty(self.samples, dtype=torch.int64, device="cuda")
+        self.cp._check(self.L.clairplan_merge_holder_counts(
+            self.plan._h, C.c_void_p(self.allc.data_ptr()), self.world, self.rank,
+            C.c_void_p(glob.data_ptr()), C.c_void_p(starts.data_ptr()),
+            C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+        return glob, starts
+
     def _on_counts(self, _user):
         # runs inside the library's build call (same thread); the stream already waits for the
         # counts copy
         self.dist.all_gather_into_tensor(self.allc, self.counts, group=self.group)
-        self._spec = rank_offsets_from_counts(self.allc, self.rank)
+        self._spec = self._merge()
 
     def build(self):
         import time
@@ -346,7 +360,7 @@ class DistributedPlan:
             cp._check(self.L.clairplan_holder_counts(self.plan._h,
                                                      C.c_void_p(self.counts.data_ptr())))
             self.dist.all_gather_into_tensor(self.allc, self.counts, group=self.group)
-            self.global_offsets, self.rank_starts = rank_offsets_from_counts(self.allc, self.rank)
+            self.global_offsets, self.rank_starts = self._merge()
         self.merge_overlapped = merged
         if self.mode == "streams":
             torch.cuda.current_stream().synchronize()

@@ -464,6 +464,36 @@ def test_wire_image_round_trip_and_shard_merge(cp, ref):
                    for x, y in zip(a, b))
 
 
+def test_merge_holder_counts_kernel(cp, ref):
+    """The sharded plan's holder-offset merge (clairplan_merge_holder_counts) against its
+    definition: global offsets = exclusive scan of the per-sample totals, rank r's starts =
+    offsets + the counts of ranks < r."""
+    import ctypes as C
+    import torch
+    L = cp.lib()
+    L.clairplan_merge_holder_counts.argtypes = [C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32,
+                                                C.c_void_p, C.c_void_p, C.c_void_p]
+    rng = np.random.default_rng(4)
+    for F, world in ((40_000, 4), (1_281_167, 8), (5, 3), (262_144, 2)):
+        sizes = ref.generate_sizes(F, 0.1, 0.1, None, 1)
+        p = cp.Plan(1, F, cp.PartitionSpec(2, 2, 1, True), [1.0], sizes)
+        allc = rng.integers(0, 90, (world, F)).astype(np.int32)
+        d_allc = torch.from_numpy(allc).cuda()
+        tot = allc.astype(np.int64).sum(axis=0)
+        want_glob = np.concatenate([[0], np.cumsum(tot)])
+        for r in range(world):
+            glob = torch.empty(F + 1, dtype=torch.int64, device="cuda")
+            starts = torch.empty(F, dtype=torch.int64, device="cuda")
+            cp._check(L.clairplan_merge_holder_counts(p._h, C.c_void_p(d_allc.data_ptr()), world, r,
+                                                      C.c_void_p(glob.data_ptr()),
+                                                      C.c_void_p(starts.data_ptr()), None))
+            torch.cuda.synchronize()
+            p_ = p  # the handle's stream was used: wait for it through a library sync
+            assert np.array_equal(glob.cpu().numpy(), want_glob), (F, world, r)
+            assert np.array_equal(starts.cpu().numpy(), want_glob[:-1] + allc[:r].astype(np.int64).sum(axis=0)), (F, r)
+        p.close()
+
+
 def test_rejection_kat_device(cp):
     """Epochs whose shuffle hits a Lemire rejection (found with tools/find_rejection, digests
     from the reference): the device path resolves them bit-exactly."""
