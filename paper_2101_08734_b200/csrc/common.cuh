@@ -237,11 +237,22 @@ __device__ __forceinline__ T warp_sum(T v) {
     return v;
 }
 
-// CTAs-per-SM grid factor with an environment override (A/B sweeps of grid sizing)
-inline unsigned env_uint(const char* name, unsigned def) {
+// A/B tuning knobs: read from the environment only in debug builds (make AB_KNOBS=1 defines
+// CLAIRPLAN_AB_KNOBS); release builds always use the measured defaults.
+inline unsigned ab_knob(const char* name, unsigned def) {
+#ifdef CLAIRPLAN_AB_KNOBS
     const char* v = getenv(name);
     return v ? (unsigned)atoi(v) : def;
+#else
+    (void)name;
+    return def;
+#endif
 }
+inline bool ab_flag(const char* name) { return ab_knob(name, 0) != 0; }
+
+// Path selections the parity suite forces to cover every pipeline (documented in DESIGN.md
+// §2): CLAIRPLAN_NO_ALLFIT, CLAIRPLAN_FORCE_V1, CLAIRPLAN_DENSE, CLAIRPLAN_FY_LISTS.
+inline const char* path_switch(const char* name) { return getenv(name); }
 
 // Grid of a grid-stride kernel whose work order matters (epoch-major passes): never more CTAs
 // than can be resident at once, so every CTA walks the work in lockstep with the others.

@@ -1099,11 +1099,8 @@ void launch_holder_tile(cudaStream_t s, const Part& part, const uint32_t* inv, c
                         bool allfit, const uint32_t* gate) {
     const size_t smem = (size_t)part.E * 33 * 4 + (size_t)part.E * 33 * 2 + 16;
     const uint64_t tiles = ((uint64_t)part.F + 31) / 32;
-    static const int gmul = [] {
-        // A/B: CTAs per SM in the grid (config 2: 10 -> 1.088, 16 -> 1.116, 5 -> 1.097 ms)
-        const char* v = getenv("CLAIRPLAN_HOLDER_GRID");
-        return v ? atoi(v) : 10;
-    }();
+    // CTAs per SM in the grid (config 2: 10 -> 1.088, 16 -> 1.116, 5 -> 1.097 ms)
+    static const int gmul = (int)ab_knob("CLAIRPLAN_HOLDER_GRID", 10);
     const unsigned grid = grid_for(tiles, 1, 148u * (unsigned)gmul);
 #define HT_LAUNCH(NPV)                                                                           \
     do {                                                                                         \
@@ -1143,7 +1140,7 @@ void launch_sample_tile(cudaStream_t s, const Part& part, const uint32_t* inv, v
                                      (kThreads / 32) * (2 * W * 32 + W) + 2) +
                         (ws.sum ? (size_t)W * 32 * 12 : 0);  // clo, chi, ccnt
     const uint64_t tiles = ((uint64_t)part.F + 31) / 32;
-    static const unsigned gm = env_uint("CLAIRPLAN_GRID_SAMPLE", 16);
+    static const unsigned gm = ab_knob("CLAIRPLAN_GRID_SAMPLE", 16);
     const unsigned grid = grid_for(tiles, 1, 148u * gm);
 #define ST_LAUNCH(RV)                                                                             \
     do {                                                                                          \

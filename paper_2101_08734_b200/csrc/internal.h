@@ -75,11 +75,6 @@ constexpr uint32_t kRadixTile = 2048;
 void launch_fy_link(cudaStream_t s, uint64_t key, uint32_t F, uint32_t e0, uint32_t ne,
                     uint32_t* head, uint32_t* next, const RejTable& rt, uint32_t* rej_flag,
                     bool detect_only, uint32_t i_limit);
-// bucketed Fisher-Yates resolution (perm_bucket.cu)
-struct FyGeom {
-    uint32_t lgTB = 0, lgTS = 0, NB = 0, NT = 0, cap = 0;
-};
-bool fy_geometry(uint32_t F, FyGeom& g);
 // Multi-GPU fused exchange: the shuffle writes every stream entry straight into the receive
 // buffer of the rank owning its worker (CUDA IPC peer memory over NVLink) instead of a local
 // send buffer + all-to-all.  Entry idx of the local epoch-range stream layout goes to
@@ -91,11 +86,6 @@ struct StreamDst {
     uint32_t* base[kMaxPeers] = {};
     long long delta[kMaxPeers] = {};
 };
-void launch_fyb(cudaStream_t s, uint64_t key, const Part& part, uint32_t e0, uint32_t ne,
-                const FyGeom& g, const RejTable& rt, uint32_t* rej_flag, uint32_t* bucket,
-                uint32_t* lst, uint32_t* pool, uint32_t* pool_used, uint32_t* succ, uint32_t* q,
-                uint32_t* inv, uint32_t* stream, uint32_t* perm_out, const StreamDst* dst = nullptr);
-
 // contiguous-bucket Fisher-Yates resolution for large F (perm_fyc.cu)
 struct FycHost {
     uint32_t F = 0, NB = 0, lgW = 0, pack = 0;
@@ -119,16 +109,6 @@ void launch_fyc(cudaStream_t s, uint64_t key, const Part& part, uint32_t e0, uin
                 uint32_t* perm_out, const StreamDst* dst);
 constexpr uint32_t kRejOverflow = 0x80000000u;  // rej_flag bit: a fyc block region overflowed
 
-void launch_fy_table(cudaStream_t s, uint64_t key, uint32_t F, uint32_t e0, uint32_t ne,
-                     uint4* tbl, uint32_t* ovh, uint32_t* ovn, const RejTable& rt,
-                     uint32_t* rej_flag);
-void launch_fy_qmin(cudaStream_t s, uint32_t F, uint32_t ne, const uint4* tbl, const uint32_t* ovh,
-                    const uint32_t* ovn, uint32_t* q);
-void launch_fy_out(cudaStream_t s, const Part& part, uint32_t e0, uint32_t ne, uint4* tbl,
-                   uint32_t* ovh, const uint32_t* ovn, const uint32_t* q, uint32_t* inv,
-                   uint32_t* stream, uint32_t* perm_out);
-void launch_fy_succ(cudaStream_t s, uint32_t F, uint32_t ne, uint4* tbl, uint32_t* ovh,
-                    const uint32_t* ovn, uint32_t* succ, uint32_t* q);
 void launch_fy_group(cudaStream_t s, uint32_t F, uint32_t ne, const uint32_t* head,
                      uint32_t* next, uint32_t* q, uint32_t* scratch, uint32_t scratch_cap,
                      uint32_t* scratch_used, uint32_t* err);

@@ -1,5 +1,6 @@
-// K1-K3: bit-exact parallel Fisher-Yates (rng.cpp:15-24, access.cpp:52-57) fused with the
-// partition into per-worker streams (access.cpp:14-39, 59-78).
+// K1-K3, linked-list resolution: the fallback of perm_fyc.cu (a bucket region overflow, or
+// a geometry that does not apply).  Bit-exact parallel Fisher-Yates (rng.cpp:15-24,
+// access.cpp:52-57) fused with the partition into per-worker streams (access.cpp:14-39, 59-78).
 //
 // The sequential shuffle "for i = F-1 .. 1: swap(a[i], a[j_i])" is resolved without
 // executing the swaps in order.  Group the steps by target: writers of y are the steps
@@ -273,345 +274,6 @@ void launch_perm_scatter(cudaStream_t s, const Part& part, const uint32_t* perms
     perm_scatter_kernel<<<grid, kThreads, 0, s>>>(part, perms, inv, stream);
 }
 
-// ---- slot-table variant (default) ------------------------------------------------------
-// Same resolution, no linked-list walks on the common path:
-//   fy_table : draw j_i; c = atomicAdd(T[j].cnt); writers 0..2 go into the 16-byte entry of
-//              target j, later ones onto a per-target overflow list (ovh/ovn, ~1/8 of draws)
-//   fy_qmin  : per target (streaming), q[y] = smallest writer != y
-//   fy_out   : per target, sorted writers w_1 < ... < w_m:  out[w_m] = y and
-//              out[w_t] = V(w_{t+1}) (chase through q), plus out[0] = V(0); writes the
-//              worker-stream slot, inv and the permutation row, then empties the entry (so
-//              the table needs no clearing between batches).
-constexpr uint32_t kLongList = 64;  // sorted in local memory beyond 3 writers
-
-__global__ void __launch_bounds__(kThreads) fy_table_kernel(uint64_t key, uint32_t F, uint32_t e0,
-                                                             uint4* __restrict__ tbl,
-                                                             uint32_t* __restrict__ ovh,
-                                                             uint32_t* __restrict__ ovn,
-                                                             RejTable rt,
-                                                             uint32_t* __restrict__ rej_flag) {
-    const uint32_t slot = blockIdx.y;
-    const uint32_t e = e0 + slot;
-    uint32_t* T = reinterpret_cast<uint32_t*>(tbl + (size_t)slot * F);
-    uint32_t* oh = ovh + (size_t)slot * F;
-    uint32_t* on = ovn + (size_t)slot * F;
-    const uint32_t er = e - rt.e_base;
-    const uint32_t n = rt.count[er];
-    const uint32_t* st = rt.step + (size_t)er * rt.cap;
-    const uint32_t* cu = rt.cum + (size_t)er * rt.cap;
-    constexpr int U = 4;
-    const uint32_t stride = gridDim.x * blockDim.x;
-    for (uint32_t i0 = 1 + blockIdx.x * blockDim.x + threadIdx.x; i0 < F; i0 += U * stride) {
-        uint32_t j[U], c[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const uint32_t i = i0 + u * stride;
-            j[u] = kNone;
-            if (i < F) {
-                const uint32_t shift = n ? rej_shift(st, cu, n, i) : 0;
-                uint32_t extra;
-                j[u] = fy_draw(key, e, F, i, shift, &extra);
-                if (extra) {
-                    bool known = false;
-                    for (uint32_t t = 0; t < n; ++t) known |= (st[t] == i);
-                    if (!known) atomicMax(&rej_flag[er], i + 1);
-                }
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-            if (j[u] != kNone) c[u] = atomicAdd(&T[4 * (size_t)j[u]], 1u);
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            if (j[u] == kNone) continue;
-            const uint32_t i = i0 + u * stride;
-            if (c[u] < 3) T[4 * (size_t)j[u] + 1 + c[u]] = i;
-            else on[i] = atomicExch(&oh[j[u]], i);
-        }
-    }
-}
-
-__global__ void __launch_bounds__(kThreads) fy_qmin_kernel(uint32_t F, const uint4* __restrict__ tbl,
-                                                            const uint32_t* __restrict__ ovh,
-                                                            const uint32_t* __restrict__ ovn,
-                                                            uint32_t* __restrict__ q) {
-    const uint32_t slot = blockIdx.y;
-    const uint4* T = tbl + (size_t)slot * F;
-    const uint32_t* oh = ovh + (size_t)slot * F;
-    const uint32_t* on = ovn + (size_t)slot * F;
-    uint32_t* qq = q + (size_t)slot * F;
-    constexpr int U = 4;
-    const uint32_t stride = gridDim.x * blockDim.x;
-    for (uint32_t y0 = blockIdx.x * blockDim.x + threadIdx.x; y0 < F; y0 += U * stride) {
-        uint4 t[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const uint32_t y = y0 + u * stride;
-            t[u] = y < F ? T[y] : make_uint4(0, 0, 0, 0);
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const uint32_t y = y0 + u * stride;
-            if (y >= F) break;
-            const uint32_t m = t[u].x;
-            uint32_t qv = kNone;
-            if (m > 0 && t[u].y != y) qv = t[u].y;
-            if (m > 1 && t[u].z != y) qv = min(qv, t[u].z);
-            if (m > 2 && t[u].w != y) qv = min(qv, t[u].w);
-            if (m > 3)
-                for (uint32_t c = oh[y]; c != kNone; c = on[c])
-                    if (c != y) qv = min(qv, c);
-            qq[y] = qv;
-        }
-    }
-}
-
-// Per target: q[y] = smallest writer != y and the ascending writer chain succ[w_t] = w_{t+1}
-// (succ[w_m] = none) for fy_emit; empties the entry.  Replaces fy_qmin + fy_out.
-__device__ __noinline__ void fy_succ_long(uint32_t y, uint4 t, uint32_t* oh, const uint32_t* on,
-                                          uint32_t* sc, uint32_t* qq) {
-    const uint32_t h0 = oh[y];
-    oh[y] = kNone;
-    uint32_t buf[kLongList];
-    buf[0] = t.y;
-    buf[1] = t.z;
-    buf[2] = t.w;
-    uint32_t n = 3;
-    for (uint32_t c = h0; c != kNone && n <= kLongList; c = on[c]) {
-        if (n < kLongList) buf[n] = c;
-        ++n;
-    }
-    if (n <= kLongList) {
-        for (uint32_t a = 1; a < n; ++a) {
-            const uint32_t v = buf[a];
-            int b = (int)a - 1;
-            while (b >= 0 && buf[b] > v) {
-                buf[b + 1] = buf[b];
-                --b;
-            }
-            buf[b + 1] = v;
-        }
-        qq[y] = buf[0] == y ? buf[1] : buf[0];
-        for (uint32_t a = 0; a + 1 < n; ++a) sc[buf[a]] = buf[a + 1];
-        sc[buf[n - 1]] = kNone;
-        return;
-    }
-    // selection walk in place (never seen: more than kLongList writers of one target)
-    uint32_t cur = min(min(t.y, t.z), t.w);
-    for (uint32_t c = h0; c != kNone; c = on[c]) cur = min(cur, c);
-    qq[y] = kNone;
-    for (;;) {
-        uint32_t nx = kNone;
-        if (t.y > cur) nx = min(nx, t.y);
-        if (t.z > cur) nx = min(nx, t.z);
-        if (t.w > cur) nx = min(nx, t.w);
-        for (uint32_t c = h0; c != kNone; c = on[c])
-            if (c > cur) nx = min(nx, c);
-        if (cur != y && qq[y] == kNone) qq[y] = cur;
-        sc[cur] = nx;
-        if (nx == kNone) break;
-        cur = nx;
-    }
-}
-
-__global__ void __launch_bounds__(kThreads) fy_succ_kernel(uint32_t F, uint4* __restrict__ tbl,
-                                                            uint32_t* __restrict__ ovh,
-                                                            const uint32_t* __restrict__ ovn,
-                                                            uint32_t* __restrict__ succ,
-                                                            uint32_t* __restrict__ q) {
-    const uint32_t slot = blockIdx.y;
-    uint4* T = tbl + (size_t)slot * F;
-    uint32_t* oh = ovh + (size_t)slot * F;
-    const uint32_t* on = ovn + (size_t)slot * F;
-    uint32_t* sc = succ + (size_t)slot * F;
-    uint32_t* qq = q + (size_t)slot * F;
-    constexpr int U = 4;
-    const uint32_t stride = gridDim.x * blockDim.x;
-    for (uint32_t y0 = blockIdx.x * blockDim.x + threadIdx.x; y0 < F; y0 += U * stride) {
-        uint4 t[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const uint32_t y = y0 + u * stride;
-            t[u] = y < F ? T[y] : make_uint4(0, 0, 0, 0);
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const uint32_t y = y0 + u * stride;
-            if (y >= F) break;
-            const uint32_t m = t[u].x;
-            if (m == 0) {
-                qq[y] = kNone;
-                continue;
-            }
-            T[y] = make_uint4(0, 0, 0, 0);
-            if (m > 3) {
-                fy_succ_long(y, t[u], oh, on, sc, qq);
-                continue;
-            }
-            uint32_t a = t[u].y, b = m >= 2 ? t[u].z : kNone, c = m == 3 ? t[u].w : kNone;
-            const uint32_t lo = min(a, b), hi = max(a, b);
-            a = min(lo, c);
-            b = max(lo, min(hi, c));
-            c = max(hi, c);
-            qq[y] = a == y ? b : a;
-            sc[a] = b;
-            if (b != kNone) sc[b] = c;
-            if (c != kNone) sc[c] = kNone;
-        }
-    }
-}
-
-struct FyOut {
-    Part part;
-    uint32_t e, slot, F;
-    uint32_t* inv;
-    uint32_t* stream;
-    uint32_t* perm_out;
-    __device__ __forceinline__ void emit(uint32_t w, uint32_t v) const {
-        if (perm_out) perm_out[(size_t)slot * F + w] = v;
-        if (inv) inv[(size_t)e * F + v] = w;
-        if (stream && w < part.P) {
-            uint32_t wk;
-            uint64_t spos;
-            part.locate(w, e, wk, spos);
-            if (wk >= part.wbegin && wk < part.wend) stream[part.stream_offset(wk) + spos] = v;
-        }
-    }
-};
-
-__device__ __forceinline__ uint32_t chase(const uint32_t* qq, uint32_t x) {
-    for (uint32_t nq = qq[x]; nq != kNone; nq = qq[x]) x = nq;
-    return x;
-}
-
-__device__ __forceinline__ uint32_t next_writer(uint4 t, const uint32_t* oh, const uint32_t* on,
-                                                uint32_t y, uint32_t prev, bool first) {
-    uint32_t best = kNone;
-    const uint32_t w3[3] = {t.y, t.z, t.w};
-    for (int a = 0; a < 3; ++a)
-        if ((first || w3[a] > prev) && w3[a] < best) best = w3[a];
-    for (uint32_t c = oh[y]; c != kNone; c = on[c])
-        if ((first || c > prev) && c < best) best = c;
-    return best;
-}
-
-// One target with more than 3 writers: collect, sort, emit (rare; lists stay short — the
-// expected length at target y is ~ln(F/y); beyond kLongList an in-place selection walk).
-__device__ __noinline__ void fy_out_long(const FyOut& o, uint32_t y, uint4 t, uint32_t* oh,
-                                         const uint32_t* on, const uint32_t* qq) {
-    uint32_t buf[kLongList];
-    buf[0] = t.y;
-    buf[1] = t.z;
-    buf[2] = t.w;
-    uint32_t n = 3;
-    for (uint32_t c = oh[y]; c != kNone && n <= kLongList; c = on[c]) {
-        if (n < kLongList) buf[n] = c;
-        ++n;
-    }
-    if (n <= kLongList) {
-        for (uint32_t a = 1; a < n; ++a) {
-            const uint32_t v = buf[a];
-            int b = (int)a - 1;
-            while (b >= 0 && buf[b] > v) {
-                buf[b + 1] = buf[b];
-                --b;
-            }
-            buf[b + 1] = v;
-        }
-        for (uint32_t a = 0; a + 1 < n; ++a) o.emit(buf[a], chase(qq, buf[a + 1]));
-        o.emit(buf[n - 1], y);
-    } else {
-        uint32_t cur = next_writer(t, oh, on, y, 0, true);
-        for (;;) {
-            const uint32_t nx = next_writer(t, oh, on, y, cur, false);
-            if (nx == kNone) break;
-            o.emit(cur, chase(qq, nx));
-            cur = nx;
-        }
-        o.emit(cur, y);
-    }
-    oh[y] = kNone;
-}
-
-__global__ void __launch_bounds__(kThreads) fy_out_kernel(Part part, uint32_t e0, uint4* __restrict__ tbl,
-                                                           uint32_t* __restrict__ ovh,
-                                                           const uint32_t* __restrict__ ovn,
-                                                           const uint32_t* __restrict__ q,
-                                                           uint32_t* __restrict__ inv,
-                                                           uint32_t* __restrict__ stream,
-                                                           uint32_t* __restrict__ perm_out) {
-    const uint32_t slot = blockIdx.y;
-    const uint32_t F = part.F;
-    FyOut o{part, e0 + slot, slot, F, inv, stream, perm_out};
-    uint4* T = tbl + (size_t)slot * F;
-    uint32_t* oh = ovh + (size_t)slot * F;
-    const uint32_t* on = ovn + (size_t)slot * F;
-    const uint32_t* qq = q + (size_t)slot * F;
-    constexpr int U = 4;
-    const uint32_t stride = gridDim.x * blockDim.x;
-    for (uint32_t y0 = blockIdx.x * blockDim.x + threadIdx.x; y0 < F; y0 += U * stride) {
-        uint4 t[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const uint32_t y = y0 + u * stride;
-            t[u] = y < F ? T[y] : make_uint4(0, 0, 0, 0);
-        }
-        // up to two chases per target (3 writers), all advanced together
-        uint32_t cur[2 * U], from[2 * U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const uint32_t y = y0 + u * stride;
-            const uint32_t m = t[u].x;
-            cur[2 * u] = cur[2 * u + 1] = kNone;
-            if (m >= 2 && m <= 3) {
-                uint32_t a = t[u].y, b = t[u].z, c = m == 3 ? t[u].w : kNone;
-                uint32_t lo = min(a, b), hi = max(a, b);
-                // sorted a <= b <= c
-                a = min(lo, c);
-                const uint32_t mid = max(lo, min(hi, c));
-                c = max(hi, c);
-                b = mid;
-                if (m == 2) {  // (a, b): out[a] = V(b), out[b] = y
-                    from[2 * u] = a;
-                    cur[2 * u] = b;
-                    o.emit(b, y);
-                } else {       // (a, b, c): out[a] = V(b), out[b] = V(c), out[c] = y
-                    from[2 * u] = a;
-                    cur[2 * u] = b;
-                    from[2 * u + 1] = b;
-                    cur[2 * u + 1] = c;
-                    o.emit(c, y);
-                }
-            } else if (m == 1) {
-                o.emit(t[u].y, y);
-            }
-        }
-        uint32_t live = 0;
-#pragma unroll
-        for (int k = 0; k < 2 * U; ++k) live |= (cur[k] != kNone ? 1u : 0u) << k;
-        while (live) {
-#pragma unroll
-            for (int k = 0; k < 2 * U; ++k) {
-                if (!((live >> k) & 1u)) continue;
-                const uint32_t nq = qq[cur[k]];
-                if (nq == kNone) live &= ~(1u << k);
-                else cur[k] = nq;
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < 2 * U; ++k)
-            if (cur[k] != kNone) o.emit(from[k], cur[k]);
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const uint32_t y = y0 + u * stride;
-            if (y >= F) break;
-            if (t[u].x > 3) fy_out_long(o, y, t[u], oh, on, qq);
-            if (t[u].x) T[y] = make_uint4(0, 0, 0, 0);
-            if (y == 0) o.emit(0, chase(qq, 0));
-        }
-    }
-}
-
 // ---- host launchers ------------------------------------------------------------------
 void launch_fy_link(cudaStream_t s, uint64_t key, uint32_t F, uint32_t e0, uint32_t ne,
                     uint32_t* head, uint32_t* next, const RejTable& rt, uint32_t* rej_flag,
@@ -627,32 +289,6 @@ void launch_fy_group(cudaStream_t s, uint32_t F, uint32_t ne, const uint32_t* he
     dim3 grid(grid_for(F, kThreads * 4, 148u * 16u), ne);
     fy_group_kernel<<<grid, kThreads, 0, s>>>(F, head, next, q, scratch, scratch_cap,
                                               scratch_used, err);
-}
-
-void launch_fy_table(cudaStream_t s, uint64_t key, uint32_t F, uint32_t e0, uint32_t ne,
-                     uint4* tbl, uint32_t* ovh, uint32_t* ovn, const RejTable& rt,
-                     uint32_t* rej_flag) {
-    dim3 grid(grid_for(F, kThreads * 4, 148u * 16u), ne);
-    fy_table_kernel<<<grid, kThreads, 0, s>>>(key, F, e0, tbl, ovh, ovn, rt, rej_flag);
-}
-
-void launch_fy_qmin(cudaStream_t s, uint32_t F, uint32_t ne, const uint4* tbl, const uint32_t* ovh,
-                    const uint32_t* ovn, uint32_t* q) {
-    dim3 grid(grid_for(F, kThreads * 4, 148u * 16u), ne);
-    fy_qmin_kernel<<<grid, kThreads, 0, s>>>(F, tbl, ovh, ovn, q);
-}
-
-void launch_fy_out(cudaStream_t s, const Part& part, uint32_t e0, uint32_t ne, uint4* tbl,
-                   uint32_t* ovh, const uint32_t* ovn, const uint32_t* q, uint32_t* inv,
-                   uint32_t* stream, uint32_t* perm_out) {
-    dim3 grid(grid_for(part.F, kThreads * 4, 148u * 16u), ne);
-    fy_out_kernel<<<grid, kThreads, 0, s>>>(part, e0, tbl, ovh, ovn, q, inv, stream, perm_out);
-}
-
-void launch_fy_succ(cudaStream_t s, uint32_t F, uint32_t ne, uint4* tbl, uint32_t* ovh,
-                    const uint32_t* ovn, uint32_t* succ, uint32_t* q) {
-    dim3 grid(grid_for(F, kThreads * 4, 148u * 16u), ne);
-    fy_succ_kernel<<<grid, kThreads, 0, s>>>(F, tbl, ovh, ovn, succ, q);
 }
 
 void launch_fy_emit(cudaStream_t s, uint64_t key, const Part& part, uint32_t e0, uint32_t ne,

@@ -1,6 +1,6 @@
 // K1-K3 for large F: Fisher-Yates resolution with contiguous target-block buckets ("fyc").
 //
-// Same resolution as perm.cu / perm_bucket.cu (rng.cpp:15-24, access.cpp:52-57): with the
+// Same resolution as perm.cu (rng.cpp:15-24, access.cpp:52-57): with the
 // writers of target y sorted, w_1 < ... < w_m,
 //   q(y) = smallest writer != y,   succ(w_k) = w_{k+1},   V(x) = V(q(x)) or x,
 //   out[i] = V(succ(i)), or j_i for the last writer of its target,   out[0] = V(0).
@@ -123,7 +123,7 @@ __device__ __forceinline__ uint32_t fyc_block_of(const FycDev& g, uint32_t y) {
     return b;
 }
 
-// exact draw with the rejection-table shift (perm_bucket.cu's FyRej, restated: per epoch)
+// exact draw with the rejection-table shift
 __device__ __noinline__ uint32_t fyc_draw_exact(uint64_t key, uint32_t e, uint32_t F, uint32_t i,
                                                 const uint32_t* st, const uint32_t* cu, uint32_t n,
                                                 uint32_t* flag) {
@@ -456,7 +456,7 @@ __global__ void __launch_bounds__(kThreads, 4) fyc_emit_kernel(Part part, uint32
 
 // ---- launcher ----------------------------------------------------------------------------
 uint32_t fyc_epochs_per_batch(uint32_t F, uint32_t E) {
-    static const uint64_t steps = (uint64_t)env_uint("CLAIRPLAN_FYC_MSTEPS", 256) << 20;  // A/B
+    static const uint64_t steps = (uint64_t)ab_knob("CLAIRPLAN_FYC_MSTEPS", 256) << 20;  // A/B
     uint64_t eb = steps / F;  // ~256 M steps per launch: launch tails dominate (config 4: 40 M 50.7, 200 M 49.0 ms)
     if (eb < 1) eb = 1;
     if (eb > E) eb = E;
@@ -469,7 +469,7 @@ void launch_fyc(cudaStream_t s, uint64_t key, const Part& part, uint32_t e0, uin
                 uint32_t* cursor, uint32_t* tsucc, uint32_t* q, uint32_t* inv, uint32_t* stream,
                 uint32_t* perm_out, const StreamDst* dst) {
     const uint32_t F = part.F;
-    static const int check = (int)env_uint("CLAIRPLAN_FYC_CHECK", 0);  // debug bounds checks
+    static const int check = (int)ab_knob("CLAIRPLAN_FYC_CHECK", 0);  // debug bounds checks
     cudaMemsetAsync(cursor, 0, (size_t)ne * g.NB * 4, s);
     const uint32_t TS = g.pack ? kFycTS : 2 * kFycTS;
     const uint32_t NT = (F + TS - 1) / TS;

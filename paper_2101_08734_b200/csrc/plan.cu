@@ -24,7 +24,7 @@ namespace clairplan {
 uint32_t epochs_per_batch(uint32_t F, uint32_t E, uint32_t bytes_per_target) {
     const uint64_t per = (uint64_t)F * bytes_per_target;
     uint64_t budget = 4096ull << 20;  // B200: 180 GB HBM; whole-run batches fill the GPU
-    if (const char* env = getenv("CLAIRPLAN_PERM_BUDGET_MB")) budget = strtoull(env, nullptr, 10) << 20;
+    budget = (uint64_t)ab_knob("CLAIRPLAN_PERM_BUDGET_MB", 4096) << 20;
     uint64_t eb = budget / (per ? per : 1);
     if (eb < 1) eb = 1;
     if (eb > E) eb = E;
@@ -95,11 +95,11 @@ int enqueue_perms(clairplan_plan* p, uint32_t* stream_out, uint32_t* inv_out, ui
     const uint32_t F = part.F;
     bool ok = true;
     const RejTable rt = rej_table(p);
-    static const char* mode_env = getenv("CLAIRPLAN_FY");  // "fyc" / "bucket" / "lists" / "table" (A/B)
-    const std::string mode = mode_env ? mode_env : "fyc";
-    static const bool fy_out_mode = getenv("CLAIRPLAN_FY_OUT") != nullptr;
+    // contiguous-bucket resolution; the linked-list one (perm.cu) after a bucket overflow or
+    // where the geometry does not apply (CLAIRPLAN_FY_LISTS forces it: parity coverage)
+    const bool lists = path_switch("CLAIRPLAN_FY_LISTS") != nullptr;
     FycDev fg;
-    if (mode == "fyc" && fyc_ready(p, F, fg)) {  // contiguous target-block buckets
+    if (!lists && fyc_ready(p, F, fg)) {  // contiguous target-block buckets
         const uint32_t EB = fyc_epochs_per_batch(F, e_count);
         uint32_t* region = need<uint32_t>(p->fyc_region, (uint64_t)EB * fg.rtotal, ok);
         uint32_t* cursor = need<uint32_t>(p->fyc_cursor, (uint64_t)EB * fg.NB, ok);
@@ -116,59 +116,7 @@ int enqueue_perms(clairplan_plan* p, uint32_t* stream_out, uint32_t* inv_out, ui
         CK(cudaGetLastError());
         return 0;
     }
-    FyGeom g;
-    if ((mode == "fyc" || mode == "bucket") && fy_geometry(F, g)) {  // shared-memory bucketed resolution
-        const uint32_t EB = epochs_per_batch(F, e_count, 32);
-        uint32_t* bucket = need<uint32_t>(p->fybucket, (uint64_t)EB * F, ok);
-        uint32_t* lst = need<uint32_t>(p->fylst, (uint64_t)EB * g.NT * (g.NB + 1), ok);
-        uint32_t* pool = need<uint32_t>(p->fypool, (uint64_t)EB * 4 * F, ok);
-        uint32_t* pool_used = need<uint32_t>(p->fypool_used, EB, ok);
-        uint32_t* succ = need<uint32_t>(p->next, (uint64_t)EB * F, ok);
-        uint32_t* q = need<uint32_t>(p->q, (uint64_t)EB * F, ok);
-        if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed (permutation workspace)");
-        for (uint32_t e0 = e_first; e0 < e_first + e_count; e0 += EB) {
-            const uint32_t ne = std::min(EB, e_first + e_count - e0);
-            launch_fyb(p->stream, p->key, part, e0, ne, g, rt, p->rej_flag.get<uint32_t>(),
-                       bucket, lst, pool, pool_used, succ, q, inv_out, stream_out,
-                       perm_out ? perm_out + (size_t)(e0 - e_first) * F : nullptr, dst);
-            p->launches += 3;
-        }
-        CK(cudaGetLastError());
-        return 0;
-    }
     if (dst && dst->G) return fail(CLAIRPLAN_EINVAL, "peer-memory stream writes need the bucketed shuffle");
-    if (mode == "table") {  // slot-table resolution (perm.cu)
-        const uint32_t EB = epochs_per_batch(F, e_count, 32);
-        uint4* tbl = need<uint4>(p->fytbl, (uint64_t)EB * F, ok);
-        uint32_t* ovh = need<uint32_t>(p->fyovh, (uint64_t)EB * F, ok);
-        uint32_t* ovn = need<uint32_t>(p->fyovn, (uint64_t)EB * F, ok);
-        uint32_t* q = need<uint32_t>(p->q, (uint64_t)EB * F, ok);
-        uint32_t* succ = need<uint32_t>(p->next, (uint64_t)EB * F, ok);
-        if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed (permutation workspace)");
-        if (p->fy_clean != p->fytbl.p) {
-            CK(cudaMemsetAsync(tbl, 0, p->fytbl.bytes, p->stream));
-            CK(cudaMemsetAsync(ovh, 0xFF, p->fyovh.bytes, p->stream));
-        }
-        p->fy_clean = nullptr;
-        for (uint32_t e0 = e_first; e0 < e_first + e_count; e0 += EB) {
-            const uint32_t ne = std::min(EB, e_first + e_count - e0);
-            launch_fy_table(p->stream, p->key, F, e0, ne, tbl, ovh, ovn, rt,
-                            p->rej_flag.get<uint32_t>());
-            if (fy_out_mode) {
-                launch_fy_qmin(p->stream, F, ne, tbl, ovh, ovn, q);
-                launch_fy_out(p->stream, part, e0, ne, tbl, ovh, ovn, q, inv_out, stream_out,
-                              perm_out ? perm_out + (size_t)(e0 - e_first) * F : nullptr);
-            } else {
-                launch_fy_succ(p->stream, F, ne, tbl, ovh, ovn, succ, q);
-                launch_fy_emit(p->stream, p->key, part, e0, ne, succ, q, rt, inv_out, stream_out,
-                               perm_out ? perm_out + (size_t)(e0 - e_first) * F : nullptr);
-            }
-            p->launches += 3;
-        }
-        CK(cudaGetLastError());
-        p->fy_clean = p->fytbl.p;  // fy_out empties every entry it used
-        return 0;
-    }
     const uint32_t EB = epochs_per_batch(F, e_count, 12);
     uint32_t* head = need<uint32_t>(p->head, (uint64_t)EB * F, ok);
     uint32_t* next = need<uint32_t>(p->next, (uint64_t)EB * F, ok);
@@ -180,13 +128,19 @@ int enqueue_perms(clairplan_plan* p, uint32_t* stream_out, uint32_t* inv_out, ui
     for (uint32_t e0 = e_first; e0 < e_first + e_count; e0 += EB) {
         const uint32_t ne = std::min(EB, e_first + e_count - e0);
         CK(cudaMemsetAsync(head, 0xFF, (size_t)ne * F * sizeof(uint32_t), p->stream));
-        CK(cudaMemsetAsync(counters, 0, sizeof(uint32_t), p->stream));
+        CK(cudaMemsetAsync(counters, 0, 2 * sizeof(uint32_t), p->stream));  // cursor + overflow
         launch_fy_link(p->stream, p->key, F, e0, ne, head, next, rt, p->rej_flag.get<uint32_t>(),
                        false, F);
         launch_fy_group(p->stream, F, ne, head, next, q, scratch, scap, counters, counters + 1);
         launch_fy_emit(p->stream, p->key, part, e0, ne, next, q, rt, inv_out, stream_out,
                        perm_out ? perm_out + (size_t)(e0 - e_first) * F : nullptr);
         p->launches += 3;
+        // fy_group's long-list scratch overflowed (never seen: lists at target y are ~ln(F/y)
+        // long): its targets were not linked, so refuse rather than return a wrong plan
+        uint32_t ovf = 0;
+        CK(cudaMemcpyAsync(&ovf, counters + 1, sizeof(uint32_t), cudaMemcpyDeviceToHost, p->stream));
+        CK(cudaStreamSynchronize(p->stream));
+        if (ovf) return fail(CLAIRPLAN_ENOMEM, "linked-list shuffle: long-list scratch overflow");
     }
     CK(cudaGetLastError());
     return 0;
@@ -617,7 +571,7 @@ bool hp_path_ok(const clairplan_plan* p) {
     for (uint32_t w : {part.wbegin, part.wend - 1}) lmax = std::max<uint64_t>(lmax, part.E * part.epoch_len(w));
     // (hp_fill + holder_hp measured 26.7 + 11.1 ms against holder_tile's 30 ms at the
     // ImageNet-22k shape: latency-bound record gathers; off until that pass is faster)
-    static const bool on = env_uint("CLAIRPLAN_HP_PATH", 0) != 0;
+    static const bool on = ab_flag("CLAIRPLAN_HP_PATH");
     return on && !p->sparse && !p->allfit && p->cfg.num_classes <= 15 && lmax < (1ull << 28);
 }
 
@@ -866,7 +820,7 @@ void finish_allfit(clairplan_plan* p, const std::vector<uint32_t>& wcnt_h) {
 
 // sharded build from received streams: sparse (CSR) or dense sample-major passes
 static bool sharded_sparse(clairplan_plan* p) {
-    const char* dense_env = getenv("CLAIRPLAN_DENSE");  // "1": dense, "0": sparse, unset: cost model
+    const char* dense_env = path_switch("CLAIRPLAN_DENSE");  // "1": dense, "0": sparse, unset: cost model
     return dense_env ? dense_env[0] == '0' && sparse_path_fits(p->part) : sparse_path_ok(p->part, p->A);
 }
 
@@ -891,7 +845,7 @@ int build_seed_path_v2(clairplan_plan* p, const uint32_t* ext_perms,
     const uint64_t EFp = (uint64_t)E * part.Fp;  // pitched u16 rows
     // info rows are u8 when every count fits (E <= 255) and the tile sample pass writes them:
     // half the L2 footprint of the gathers from the segment passes
-    static const bool lanes_only = getenv("CLAIRPLAN_SAMPLE_LANES") != nullptr;  // A/B
+    static const bool lanes_only = ab_flag("CLAIRPLAN_SAMPLE_LANES");  // A/B
     const bool tile_pass = !sparse && tile_path_ok(part) && !lanes_only;
     p->info8 = tile_pass && E <= 255;
     void* info = sparse ? nullptr : need<uint8_t>(p->info16, EFp * (p->info8 ? 1 : 2), ok);
@@ -963,7 +917,7 @@ int build_seed_path_v2(clairplan_plan* p, const uint32_t* ext_perms,
         uint32_t* hist_out = red_hist ? seghist : nullptr;
         if (red_hist) CK(cudaMemsetAsync(seghist, 0, NEE * 4, s));
         // per-worker candidate size sums for the whole-worker fit test (all-fit path)
-        const bool no_allfit = getenv("CLAIRPLAN_NO_ALLFIT") != nullptr;
+        const bool no_allfit = path_switch("CLAIRPLAN_NO_ALLFIT") != nullptr;
         const bool sums = J > 0 && !no_allfit && (sparse || (tile_path_ok(part) && !lanes_only));
         WorkerSums wsm;
         if (sums) {
@@ -1180,7 +1134,7 @@ int clairplan_build(clairplan_t p) {
     CK(cudaSetDevice(p->device));
     p->built = false;
     p->v2 = false;
-    const char* force = getenv("CLAIRPLAN_FORCE_V1");
+    const char* force = path_switch("CLAIRPLAN_FORCE_V1");
     if (v2_ok(p) && !(force && force[0] == '1')) return build_seed_path_v2(p, nullptr);
     return build_seed_path(p);
 }
@@ -1491,7 +1445,7 @@ static int generate_streams_impl(clairplan_plan* p, uint32_t epoch_begin, uint32
     // the handle's inv (CLAIRPLAN_OWN_INV=0 disables, A/B)
     p->inv_own_lo = p->inv_own_hi = 0;
     uint32_t* own_inv = nullptr;
-    static const bool own_ok = env_uint("CLAIRPLAN_OWN_INV", 1) != 0;
+    static const bool own_ok = ab_knob("CLAIRPLAN_OWN_INV", 1) != 0;
     if (own_ok && v2_ok(p) && !sharded_sparse(p)) {
         bool ok = true;
         own_inv = need<uint32_t>(p->inv, (uint64_t)pp.E * pp.F, ok);
@@ -1542,21 +1496,15 @@ int clairplan_generate_streams_p2p(clairplan_t p, uint32_t epoch_begin, uint32_t
         d.base[r] = reinterpret_cast<uint32_t*>(dst_base[r]);
         d.delta[r] = (long long)dst_delta[r];
     }
-    FyGeom g;
     FycDev fg;
-    if (!fyc_ready(p, p->part.F, fg) && !fy_geometry(p->part.F, g))
+    if (!fyc_ready(p, p->part.F, fg))
         return fail(CLAIRPLAN_EINVAL, "peer-memory stream writes need the bucketed shuffle");
     return generate_streams_impl(p, epoch_begin, epoch_count, nullptr, &d);
 }
 
 int clairplan_p2p_supported(clairplan_t p) {
-    FyGeom g;
     FycDev fg;
-    const char* m = getenv("CLAIRPLAN_FY");
-    const std::string mode = m ? m : "fyc";
-    if (!p || p->generic) return 0;
-    if (mode == "fyc" && fyc_ready(p, p->part.F, fg)) return 1;
-    return ((mode == "fyc" || mode == "bucket") && fy_geometry(p->part.F, g)) ? 1 : 0;
+    return (p && !p->generic && !path_switch("CLAIRPLAN_FY_LISTS") && fyc_ready(p, p->part.F, fg)) ? 1 : 0;
 }
 
 int clairplan_recv_buffer(clairplan_t p, uint32_t i, void** d_ptr, void* ipc_handle) {

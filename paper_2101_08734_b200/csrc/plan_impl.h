@@ -112,8 +112,6 @@ struct clairplan_plan {
     DevBuf cand_k, cand_info, cand_cls, order, sorted_size;
     DevBuf keys, vals, okeys, ovals, taken, seqsz, dest;
     DevBuf class_entries, class_start, class_len, holders, holders_tmp, hcount, hoff;
-    DevBuf fytbl, fyovh, fyovn, fybucket, fylst, fypool, fypool_used;
-    const void* fy_clean = nullptr;  // fytbl/fyovh hold their empty state
     DevBuf head, next, q, scratch, counters, rej_flag, rej_step, rej_cum, rej_count;
     DevBuf wsbuf;
     DevBuf cand_w, dfirst, dcounts;  // explicit-stream (generic) path
@@ -187,8 +185,7 @@ struct clairplan_plan {
     void mark(int i) {
         if (sev[i]) cudaEventRecord(sev[i], stream);
         static const bool dbg = [] {
-            const char* e = getenv("CLAIRPLAN_DEBUG_SYNC");
-            return e && e[0] == '1';
+            return ab_flag("CLAIRPLAN_DEBUG_SYNC");
         }();
         if (dbg) {
             const cudaError_t err = cudaStreamSynchronize(stream);

@@ -307,7 +307,7 @@ void launch_sparse_csr(cudaStream_t s, const Part& part, const uint32_t* stream,
 }
 
 uint64_t csr_windows(uint64_t n) {
-    if (const char* v = getenv("CLAIRPLAN_CSR_WINDOWS")) return std::max(1, atoi(v));  // A/B
+    if (const unsigned v = ab_knob("CLAIRPLAN_CSR_WINDOWS", 0)) return std::max(1u, v);  // A/B
     const uint64_t w = std::max<uint64_t>(1, (n * 4 + (64ull << 20) - 1) / (64ull << 20));
     return w <= 16 ? w : 1;  // a CSR of many L2 sizes: one pass (the writes miss L2 anyway)
 }
@@ -336,7 +336,7 @@ void launch_sparse_sample(cudaStream_t s, const Part& part, const uint64_t* soff
                         (ws.sum ? (size_t)W * 32 * 12 : 0);
     // 5 CTAs per SM (48 registers, no spills), two waves (4-way config-2 shard: 1.73 vs
     // 1.84 ms per build with 6 per SM in a 1.33-wave grid)
-    static const unsigned gm = env_uint("CLAIRPLAN_GRID_SPARSE", 10);
+    static const unsigned gm = ab_knob("CLAIRPLAN_GRID_SPARSE", 10);
     const unsigned grid = grid_for((uint64_t)part.F * 32, kThreads, 148u * gm);
     const FastDiv uni = uniform_len(part);
 #define SS_LAUNCH(RV)                                                                              \

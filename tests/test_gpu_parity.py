@@ -112,6 +112,21 @@ def test_plan_v1_pipeline_matches_reference(cp, ref, case, monkeypatch):
     assert plans_equal(a, b) is None
 
 
+@pytest.mark.parametrize("case", CASES[:5] + [CASES[11]])
+def test_linked_list_shuffle_fallback(cp, ref, case, monkeypatch):
+    """The linked-list shuffle (perm.cu), the fallback after a bucket-region overflow of the
+    contiguous-bucket shuffle (perm_fyc.cu), forced: plans and permutations equal the
+    reference's."""
+    monkeypatch.setenv("CLAIRPLAN_FY_LISTS", "1")
+    seed, F, N, B, E, dl, caps, (mu, sd) = case
+    sizes = ref.generate_sizes(F, mu, sd, None, 1)
+    a = ref.plan(seed, F, N, B, E, dl, caps, sizes)
+    b = device_plan(cp, seed, F, N, B, E, dl, caps, sizes)
+    assert plans_equal(a, b) is None
+    for F2, e in ((1_281_167, 3), (14_197_122, 1), (7, 0)):
+        assert np.array_equal(cp.epoch_permutation(42, e, F2), ref.epoch_permutation(42, e, F2))
+
+
 def test_plan_random_configs(cp, ref):
     rng = np.random.default_rng(9)
     for _ in range(25):
