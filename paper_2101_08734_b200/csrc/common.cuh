@@ -222,6 +222,17 @@ inline Part make_part(uint32_t F, uint32_t N, uint32_t B, uint32_t E, bool drop_
     return p;
 }
 
+// Block records (class bit-planes + class prefix counts per 32-entry block of a (worker, epoch)
+// segment) are stored EPOCH-major: one epoch's records of all the handle's workers are
+// contiguous (7 MB at the ImageNet-22k shape), so the sample-major passes that gather them one
+// epoch at a time stay inside a few 2-MB pages (a per-epoch record set spread worker-major over
+// 638 MB gathered 4.5x slower: TLB reach, tools/probe/spread_probe.cu).  The scans over blocks
+// (class prefix counts) keep the worker-major block order blk = (wl * E + e) * MB + b.
+__host__ __device__ __forceinline__ uint64_t rec_index(uint32_t wl, uint32_t e, uint32_t nloc,
+                                                       uint32_t MB, uint32_t b) {
+    return ((uint64_t)e * nloc + wl) * MB + b;
+}
+
 // ---- small device utilities --------------------------------------------------------------
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
 __device__ __forceinline__ uint32_t lanemask_lt() {

@@ -405,7 +405,7 @@ __global__ void __launch_bounds__(kThreads) seg_allfit_kernel(
         prefix = __shfl_sync(0xffffffffu, prefix, 0);
         // pass B: block records and the class-1 list
         uint64_t run = prefix;
-        const uint64_t blk0 = ((uint64_t)wl * E + e) * MB;
+        const uint64_t blk0 = rec_index(wl, e, nloc, MB, 0);
         for (uint64_t t0 = t_lo; t0 < t_hi; t0 += 32 * kSU) {
             uint32_t k[kSU];
 #pragma unroll
@@ -586,6 +586,7 @@ __global__ void __launch_bounds__(kThreads) blk_codes_kernel(
         const uint32_t wl = (uint32_t)(seg / E);
         const uint32_t nb = (uint32_t)((part.epoch_len(part.wbegin + wl) + 31) >> 5);
         const uint64_t blk0 = seg * MB;
+        const uint64_t rec0 = rec_index(wl, (uint32_t)(seg - (uint64_t)wl * E), nloc, MB, 0);
         for (uint32_t b0 = 0; b0 < MB; b0 += kBU) {
             uint32_t m[kBU], c[kBU], d[kBU], cls[kBU];
 #pragma unroll
@@ -616,19 +617,23 @@ __global__ void __launch_bounds__(kThreads) blk_codes_kernel(
                     const uint32_t bj = __ballot_sync(0xffffffffu, cls[u] == j);
                     if (lane == j - 1) ccount[(uint64_t)(j - 1) * nblk + blk] = __popc(bj);
                 }
-                if (lane < np) rec[blk * Rp + lane] = word;
+                if (lane < np) rec[(rec0 + bi) * Rp + lane] = word;
             }
         }
     }
 }
 
 __global__ void rec_fill_kernel(const uint64_t* __restrict__ cpre, uint64_t nblk, uint32_t np,
-                                uint32_t J, uint32_t Rp, uint32_t* __restrict__ rec) {
+                                uint32_t J, uint32_t Rp, uint32_t* __restrict__ rec, uint32_t nloc,
+                                uint32_t E, uint32_t MB) {
     for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < nblk * J;
          x += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t blk = x / J;
+        const uint64_t blk = x / J;  // worker-major block order of the prefix scan
         const uint32_t j = (uint32_t)(x % J);
-        rec[blk * Rp + np + j] = (uint32_t)cpre[(uint64_t)j * (nblk + 1) + blk];
+        const uint64_t seg = blk / MB;
+        const uint32_t wl = (uint32_t)(seg / E), e = (uint32_t)(seg - (uint64_t)wl * E);
+        rec[rec_index(wl, e, nloc, MB, (uint32_t)(blk - seg * MB)) * Rp + np + j] =
+            (uint32_t)cpre[(uint64_t)j * (nblk + 1) + blk];
     }
 }
 
@@ -657,7 +662,7 @@ __global__ void __launch_bounds__(kThreads) class_write_kernel(
         const uint32_t w = part.wbegin + wl;
         const uint64_t Le = part.epoch_len(w);
         const uint64_t g0 = part.stream_offset(w) + (uint64_t)e * Le;
-        const uint64_t blk0 = seg * MB;
+        const uint64_t blk0 = rec_index(wl, e, nloc, MB, 0);
         // class bases / list starts of this worker: lanes j < J
         const uint32_t cb = lane < J ? cbase[wl * J + lane] : 0;
         const uint64_t cs = lane < J ? cstart[(uint64_t)wl * J + lane] : 0;
@@ -781,7 +786,7 @@ __global__ void __launch_bounds__(kThreads, 5) holder_tile_kernel(
                         if (rk[r] != 0xFFFFu) {
                             const uint32_t tseg = part.within_epoch(tinv[e * 33 + s], w[r]);
                             const uint32_t wl = w[r] - part.wbegin;
-                            const uint64_t blk = ((uint64_t)wl * E + e) * MB + (tseg >> 5);
+                            const uint64_t blk = rec_index(wl, e, part.wend - part.wbegin, MB, tseg >> 5);
                             bit[r] = tseg & 31;
                             a2[r] = __ldg(reinterpret_cast<const uint2*>(rec) + blk);
                             cb[r] = __ldg(cbase + wl * J);
@@ -811,7 +816,7 @@ __global__ void __launch_bounds__(kThreads, 5) holder_tile_kernel(
                 uint32_t w;
                 const uint32_t tseg = part.within_epoch(tinv[e * 33 + s], w);
                 const uint32_t wl = w - part.wbegin;
-                const uint64_t blk = ((uint64_t)wl * E + e) * MB + (tseg >> 5);
+                const uint64_t blk = rec_index(wl, e, part.wend - part.wbegin, MB, tseg >> 5);
                 const uint32_t bit = tseg & 31;
                 uint32_t cls, pos = 0;
                 if constexpr (NP == -1) {
@@ -1073,7 +1078,8 @@ void launch_blk_codes(cudaStream_t s, const Part& part, uint32_t MB, const uint3
 void launch_rec_fill(cudaStream_t s, const uint64_t* cpre, uint64_t nblk, uint32_t np, uint32_t J,
                      uint32_t Rp, uint32_t* rec, uint32_t nloc, uint32_t E, uint32_t MB,
                      uint32_t* cbase) {
-    rec_fill_kernel<<<grid_for(nblk * J, kThreads), kThreads, 0, s>>>(cpre, nblk, np, J, Rp, rec);
+    rec_fill_kernel<<<grid_for(nblk * J, kThreads), kThreads, 0, s>>>(cpre, nblk, np, J, Rp, rec, nloc, E,
+                                                                     MB);
     class_base_kernel<<<grid_for((uint64_t)nloc * J, kThreads), kThreads, 0, s>>>(cpre, nblk, nloc, E,
                                                                                  MB, J, cbase);
 }

@@ -571,7 +571,7 @@ bool hp_path_ok(const clairplan_plan* p) {
     for (uint32_t w : {part.wbegin, part.wend - 1}) lmax = std::max<uint64_t>(lmax, part.E * part.epoch_len(w));
     // (hp_fill + holder_hp measured 26.7 + 11.1 ms against holder_tile's 30 ms at the
     // ImageNet-22k shape: latency-bound record gathers; off until that pass is faster)
-    static const bool on = ab_flag("CLAIRPLAN_HP_PATH");
+    static const bool on = !ab_flag("CLAIRPLAN_NO_HP_PATH");
     return on && !p->sparse && !p->allfit && p->cfg.num_classes <= 15 && lmax < (1ull << 28);
 }
 

@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(kThreads) holder_sparse_kernel(
     const uint32_t* __restrict__ cbase, const uint64_t* __restrict__ pair_off,
     uint32_t* __restrict__ holders, FastDiv uni, const uint32_t* __restrict__ gate) {
     if (gate && *gate == 0) return;  // speculative all-fit launch, the test failed
-    const uint32_t E = part.E, nloc = part.wend - part.wbegin;
+    const uint32_t nloc = part.wend - part.wbegin;
     const uint32_t np = NP > 0 ? (uint32_t)NP : np_rt;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x) {
@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(kThreads) holder_sparse_kernel(
         const uint32_t rel = (uint32_t)(s - soff[wl]);
         const uint32_t e = rel / Le;
         const uint32_t t = rel - e * Le;
-        const uint64_t blk = ((uint64_t)wl * E + e) * MB + (t >> 5);
+        const uint64_t blk = rec_index(wl, e, nloc, MB, t >> 5);
         const uint32_t bit = t & 31;
         uint32_t cls, pos = 0;
         if constexpr (NP == -1) {

@@ -261,42 +261,46 @@ void launch_fill_class(cudaStream_t s, uint8_t* cls, uint64_t n, uint8_t j) {
 // block records gathered for epoch e (nloc * MB records, 7 MB at the ImageNet-22k shape) stay
 // in L2 while the epoch's rows stream through; inv / rank rows are read and hp rows written
 // coalesced.  The holder pass then needs no gather at all.
-__global__ void __launch_bounds__(kThreads) hp_fill_kernel(Part part, const uint32_t* __restrict__ inv,
+constexpr int kHpU = 8;  // consecutive samples per thread: 8 independent record gathers in flight
+
+__global__ void __launch_bounds__(kThreads, 3) hp_fill_kernel(Part part, const uint32_t* __restrict__ inv,
                                                            const uint16_t* __restrict__ rank16,
                                                            uint32_t MB, const uint32_t* __restrict__ rec,
                                                            uint32_t np, uint32_t J, uint32_t Rp,
                                                            const uint32_t* __restrict__ cbase,
                                                            uint32_t* __restrict__ hp) {
     const uint32_t E = part.E, F = part.F;
-    const uint32_t nq = (F + 3) / 4;  // quads of samples per row
+    const uint32_t nq = (F + kHpU - 1) / kHpU;  // groups of kHpU samples per row
     const uint64_t total = (uint64_t)E * nq;
     for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < total;
          x += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t e = (uint32_t)(x / nq);
-        const uint32_t k0 = (uint32_t)(x - (uint64_t)e * nq) * 4;
-        uint32_t p[4], out[4];
-        uint16_t rk[4];
+        const uint32_t k0 = (uint32_t)(x - (uint64_t)e * nq) * kHpU;
+        // rank row: one 16-B load (rows pitched to Fp, a multiple of 16 samples)
+        const uint4 rv = __ldcs(reinterpret_cast<const uint4*>(rank16 + (size_t)e * part.Fp + k0));
+        const uint32_t rw[4] = {rv.x, rv.y, rv.z, rv.w};
+        uint32_t p[kHpU];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const bool ok = k0 + u < F;
-            rk[u] = ok ? __ldcs(rank16 + (size_t)e * part.Fp + k0 + u) : (uint16_t)0xFFFFu;
-            p[u] = (ok && rk[u] != 0xFFFFu) ? __ldcs(inv + (size_t)e * F + k0 + u) : kNone;
+        for (int u = 0; u < kHpU; ++u) {
+            const uint32_t rk = (rw[u >> 1] >> ((u & 1) * 16)) & 0xFFFFu;
+            p[u] = (k0 + u < F && rk != 0xFFFFu) ? __ldcs(inv + (size_t)e * F + k0 + u) : kNone;
         }
-        uint4 a[4];
-        uint64_t row[4];
-        uint32_t bit[4], wl[4];
+        uint4 a[kHpU];
+        uint64_t row[kHpU];
+        uint32_t bit[kHpU], wl[kHpU];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < kHpU; ++u) {
             if (p[u] == kNone) continue;
             uint32_t w;
             const uint32_t t = part.within_epoch(p[u], w);
             wl[u] = w - part.wbegin;
             bit[u] = t & 31;
-            row[u] = (((uint64_t)wl[u] * E + e) * MB + (t >> 5)) * Rp;
+            row[u] = rec_index(wl[u], e, part.wend - part.wbegin, MB, t >> 5) * Rp;
             a[u] = __ldg(reinterpret_cast<const uint4*>(rec + row[u]));
         }
+        uint32_t out[kHpU];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < kHpU; ++u) {
             out[u] = 0;
             if (p[u] == kNone) continue;
             uint32_t cls = 0, cm = 0xffffffffu;
@@ -317,15 +321,17 @@ __global__ void __launch_bounds__(kThreads) hp_fill_kernel(Part part, const uint
                 out[u] = (cls << 28) | pos;
             }
         }
-        // rows pitched to Fp (a multiple of 16 samples): aligned 16-B stores
-        __stcs(reinterpret_cast<uint4*>(hp + (size_t)e * part.Fp + k0), make_uint4(out[0], out[1], out[2], out[3]));
+        uint4* dst = reinterpret_cast<uint4*>(hp + (size_t)e * part.Fp + k0);
+        __stcs(dst, make_uint4(out[0], out[1], out[2], out[3]));
+        __stcs(dst + 1, make_uint4(out[4], out[5], out[6], out[7]));
     }
 }
 
 void launch_hp_fill(cudaStream_t s, const Part& part, const uint32_t* inv, const uint16_t* rank16,
                     uint32_t MB, const uint32_t* rec, uint32_t np, uint32_t J, uint32_t Rp,
                     const uint32_t* cbase, uint32_t* hp) {
-    const uint64_t total = (uint64_t)part.E * ((part.F + 3) / 4);
+    const uint64_t total = (uint64_t)part.E * ((part.F + kHpU - 1) / kHpU);
+    // resident grid: epochs in lockstep, so one epoch's records stay in L2
     const unsigned grid = std::min<unsigned>(resident_grid(hp_fill_kernel, kThreads, 0, 8),
                                              grid_for(total, kThreads, 148u * 64u));
     hp_fill_kernel<<<grid, kThreads, 0, s>>>(part, inv, rank16, MB, rec, np, J, Rp, cbase, hp);
