@@ -369,14 +369,16 @@ def run_ours(args, cfg):
     hbm, peak_kind = peaks()
     B_alg = 8 * A_all + 32 * D_all + 4 * (cfg["F"] + 1)
     achieved = B_alg / (ms_step / 1e3) / 1e9
-    traffic = None
+    # DRAM bytes per plan of this workload from the committed ncu launch list of the same
+    # build (an ncu capture cannot run inside the timed bench); null when none is committed
+    traffic, traffic_src = None, None
     tpath = os.path.join(ROOT, "profiles", "traffic_latest.json")
-    if os.path.exists(tpath):
+    if os.path.exists(tpath) and world == 1:
         try:
             with open(tpath) as f:
-                tj = json.load(f)
-            if tj.get("workload") == cfg["name"] and world == 1:
-                traffic = tj.get("dram_bytes_per_plan")
+                tw = json.load(f).get("workloads", {}).get(cfg["name"])
+            if tw:
+                traffic, traffic_src = tw["dram_bytes_per_plan"], tw["list"]
         except Exception:
             traffic = None
     if rank == 0:
@@ -391,6 +393,7 @@ def run_ours(args, cfg):
             "accesses": int(A_all), "pairs": int(D_all),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm * world,
                          "unit": "GB/s", "frac": achieved / (hbm * world), "traffic": traffic,
+                         "traffic_source": traffic_src,
                          "kernel": "whole plan pipeline (B_alg = 8A + 32D + 4(F+1) per plan)",
                          "peak_kind": f"{peak_kind} copy bandwidth x {world}",
                          "dominant_stage": dominant_stage(stage_ms, A_loc, hbm)},
