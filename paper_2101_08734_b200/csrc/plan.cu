@@ -983,8 +983,9 @@ int build_seed_path_v2(clairplan_plan* p, const uint32_t* ext_perms,
         if (int rc = resolve_rejections(p, flags, &any)) return rc;
         if (any) continue;
         if (D >= 0xFFFFFFFFull)
-            return fail(CLAIRPLAN_EOVERFLOW, "more than 2^32-1 (worker, sample) pairs in one handle; "
-                                             "shard the workers over several handles");
+            return fail(CLAIRPLAN_EOVERFLOW, "more than 2^32-1 (worker, sample) pairs in one handle (" +
+                                                 std::to_string(D) + " of " + std::to_string(p->A) +
+                                                 " entries); shard the workers over several handles");
         const bool allfit = sums && gate_h != 0;
         if (allfit) {  // the speculative pipeline produced the plan
             p->D = D;

@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(kThreads, 5) sparse_sample_kernel(
         fs[x] = kNone;
         cnt[x] = 0;
     }
-    if (lane < W) bm[lane] = 0;
+    for (uint32_t t = lane; t < W; t += 32) bm[t] = 0;  // W <= 64 words
     __syncthreads();
     const uint32_t kstride = (gridDim.x * blockDim.x) >> 5;
     uint32_t k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(kThreads, 5) sparse_sample_kernel(
                 cnt[xv[r]] = 0;
             }
         }
-        if (lane < W) bm[lane] = 0;
+        for (uint32_t t = lane; t < W; t += 32) bm[t] = 0;  // W <= 64 words
         __syncwarp();
     }
     if (ws.sum) {

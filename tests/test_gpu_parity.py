@@ -692,6 +692,7 @@ def test_build_export_matches_separate_exports(cp, ref):
     (262_144, 64, 16, 10, True, None),
     (262_144, 64, 16, 10, True, [50.0, 1e9]),   # tier path (capacity-limited first fit)
     (1_281_167, 256, 32, 9, True, None),
+    (65_536, 4096, 1, 3, True, None),           # 2048-worker shard: 64 bitmap words per sample
 ])
 @pytest.mark.parametrize("dense", ["0", "1"])
 def test_sharded_build_from_streams(cp, ref, monkeypatch, F, N, b, E, dl, caps, dense):
