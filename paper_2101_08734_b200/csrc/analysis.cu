@@ -70,7 +70,7 @@ int clairplan_count_histogram(clairplan_t p, uint32_t worker, uint32_t max_count
     if (int rc = worker_counts_dev(p, worker, cnt.get<uint32_t>())) return rc;
     CK(cudaMemsetAsync(hb.p, 0, ((size_t)max_count + 1) * 8, p->stream));
     const size_t smem = ((size_t)max_count + 1) * 8;
-    CK(cudaFuncSetAttribute(count_bucket_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(allow_smem(count_bucket_kernel, (int)smem));
     count_bucket_kernel<<<grid_for(p->part.F, kThreads, 148u * 4u), kThreads, smem, p->stream>>>(
         cnt.get<uint32_t>(), p->part.F, max_count, hb.get<unsigned long long>());
     CK(cudaGetLastError());

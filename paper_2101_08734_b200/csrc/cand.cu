@@ -23,7 +23,7 @@ __global__ void __launch_bounds__(kThreads) seg_count_kernel(Part part,
         const uint32_t w = part.wbegin + wl;
         const uint64_t Le = part.epoch_len(w);
         const uint64_t g0 = part.stream_offset(w) + (uint64_t)e * Le;
-        const uint32_t* row = info + (size_t)e * part.F;
+        const uint32_t* row = info + (size_t)e * part.Fp;
         uint32_t c = 0;
         for (uint64_t t = threadIdx.x; t < Le; t += blockDim.x) c += row[stream[g0 + t]] != 0;
         c = warp_sum(c);
@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(kThreads) seg_write_kernel(Part part,
         const uint32_t w = part.wbegin + wl;
         const uint64_t Le = part.epoch_len(w);
         const uint64_t g0 = part.stream_offset(w) + (uint64_t)e * Le;
-        const uint32_t* row = info + (size_t)e * part.F;
+        const uint32_t* row = info + (size_t)e * part.Fp;
         uint64_t out = seg_off[(uint64_t)wl * part.E + e];
         for (uint64_t t0 = 0; t0 < Le; t0 += blockDim.x) {
             const uint64_t t = t0 + threadIdx.x;

@@ -1,5 +1,6 @@
 // Shared device/host helpers for the clairplan kernels (sm_100a).
 #pragma once
+#include <atomic>
 #include <cstdlib>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -231,6 +232,41 @@ inline Part make_part(uint32_t F, uint32_t N, uint32_t B, uint32_t E, bool drop_
 __host__ __device__ __forceinline__ uint64_t rec_index(uint32_t wl, uint32_t e, uint32_t nloc,
                                                        uint32_t MB, uint32_t b) {
     return ((uint64_t)e * nloc + wl) * MB + b;
+}
+
+// Row pitch of the [E][F] per-(epoch, sample) arrays (inverse permutations, info, rank, hp):
+// F rounded up to 16 samples, so every row starts 64-B aligned and the sample-major passes
+// load 32-sample row pieces with 16-B vector loads (tools/probe/tile_probe.cu: 3.67 vs 1.81
+// TB/s for the scalar loads of unaligned rows).
+__host__ __device__ __forceinline__ uint64_t pitch16(uint32_t F) { return (uint64_t)((F + 15u) & ~15u); }
+
+// Dynamic shared memory opt-in.  The attribute is per (function, device), not per launch:
+// handles built concurrently from several host threads must not lower it under each other
+// (thread A sets 20 KB, thread B sets 10 KB, A's 20 KB launch fails with "invalid argument"),
+// so every caller raises it to the device's opt-in maximum; a launch's occupancy follows the
+// bytes it requests, not this limit.
+inline int smem_optin_max() {
+    static std::atomic<int> cache[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::atomic<int>& c = cache[dev & 63];
+    int v = c.load(std::memory_order_relaxed);
+    if (v == 0) {
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess || v <= 0)
+            v = 48 << 10;
+        c.store(v, std::memory_order_relaxed);
+    }
+    return v;
+}
+// (the limit is the opt-in maximum less the kernel's static shared memory: a larger value is
+// rejected with cudaErrorInvalidValue)
+template <typename K>
+inline cudaError_t allow_smem(K* kernel, int /*bytes: checked at launch*/) {
+    cudaFuncAttributes a;
+    cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(kernel));
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(reinterpret_cast<const void*>(kernel), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                smem_optin_max() - (int)a.sharedSizeBytes);
 }
 
 // ---- small device utilities --------------------------------------------------------------

@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(kThreads) stream_inv_kernel(Part part, uint32_
         uint64_t spos;
         part.locate(pos, e, w, spos);
         const uint32_t k = __ldcs(stream + part.stream_offset(w) + spos);
-        inv[(size_t)e * F + k] = pos;
+        inv[(size_t)e * pitch16(F) + k] = pos;
     }
 }
 
@@ -101,7 +101,7 @@ void launch_stream_inv(cudaStream_t s, const Part& part, const uint32_t* stream,
             continue;
         }
         const uint32_t e1 = std::min(std::min(E, e0 + eb), e0 < skip_lo ? skip_lo : E);
-        cudaMemsetAsync(inv + (size_t)e0 * F, 0xFF, (size_t)(e1 - e0) * F * 4, s);
+        cudaMemsetAsync(inv + (size_t)e0 * part.Fp, 0xFF, (size_t)(e1 - e0) * part.Fp * 4, s);
         const uint64_t n = ((uint64_t)part.full * lfb + ltb) * (e1 - e0);
         stream_inv_kernel<<<grid_for(n, kThreads, 148u * 16u), kThreads, 0, s>>>(
             part, e0, e1, lfb, FastDiv(lfb ? lfb : 1), ltb, stream, inv);

@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(128) sample_lanes_kernel(Part part, const uint
             uint32_t pv[kU];
 #pragma unroll
             for (int u = 0; u < kU; ++u)
-                pv[u] = (live && e0 + u < E) ? ld_inv(inv + (size_t)(e0 + u) * F + k) : kNone;
+                pv[u] = (live && e0 + u < E) ? ld_inv(inv + (size_t)(e0 + u) * part.Fp + k) : kNone;
 #pragma unroll
             for (int u = 0; u < kU; ++u) {
                 const uint32_t e = e0 + u;
@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(128) sample_hash_kernel(Part part, const uint3
             const uint32_t e = r * 32 + lane;
             uint32_t w = kNone;
             if (e < E) {
-                const uint32_t p = inv[(size_t)e * F + k];
+                const uint32_t p = inv[(size_t)e * part.Fp + k];
                 if (p < part.P) {
                     const uint32_t ww = part.worker_of(p);
                     if (ww >= part.wbegin && ww < part.wend) w = ww - part.wbegin;
@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(128) sample_hash_kernel(Part part, const uint3
         for (uint32_t r = 0; r * 32 < E; ++r) {
             const uint32_t e = r * 32 + lane;
             if (e >= E) continue;
-            const uint32_t p = inv[(size_t)e * F + k];
+            const uint32_t p = inv[(size_t)e * part.Fp + k];
             uint16_t out = 0, rk = 0xFFFFu;
             if (p < part.P) {
                 const uint32_t ww = part.worker_of(p);
@@ -757,7 +757,7 @@ __global__ void __launch_bounds__(kThreads, 5) holder_tile_kernel(
                 const uint32_t idx = i0 + u * blockDim.x;
                 const uint32_t e = idx >> 5, l = idx & 31;
                 const bool ok = idx < E * 32 && k0 + l < F;
-                iv[u] = ok ? __ldcs(inv + (size_t)e * F + k0 + l) : kNone;
+                iv[u] = ok ? __ldcs(inv + (size_t)e * part.Fp + k0 + l) : kNone;
                 rv[u] = ok ? __ldcs(rank16 + (size_t)e * part.Fp + k0 + l) : (uint16_t)0xFFFFu;
             }
 #pragma unroll
@@ -884,7 +884,7 @@ __device__ __forceinline__ void st_issue(const uint32_t* inv, uint32_t E, uint32
     const uint32_t n = (uint32_t)(F - k0 < 32 ? F - k0 : 32);
     for (uint32_t idx = threadIdx.x; idx < E * 32; idx += blockDim.x) {
         const uint32_t e = idx >> 5, l = idx & 31;
-        if (l < n) cp_async4(tinv + e * kStInv + l, inv + (size_t)e * F + k0 + l);
+        if (l < n) cp_async4(tinv + e * kStInv + l, inv + (size_t)e * pitch16(F) + k0 + l);
     }
     cp_async_commit();
 }
@@ -1110,7 +1110,7 @@ void launch_holder_tile(cudaStream_t s, const Part& part, const uint32_t* inv, c
     const unsigned grid = grid_for(tiles, 1, 148u * (unsigned)gmul);
 #define HT_LAUNCH(NPV)                                                                           \
     do {                                                                                         \
-        cudaFuncSetAttribute(holder_tile_kernel<NPV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+        allow_smem(holder_tile_kernel<NPV>, \
                              (int)smem);                                                         \
         holder_tile_kernel<NPV><<<grid, kThreads, smem, s>>>(part, inv, rank16, MB, rec, np, J, Rp, \
                                                              cbase, pair_off, holders, gate);    \
@@ -1127,7 +1127,7 @@ void launch_sample_lanes(cudaStream_t s, const Part& part, const uint32_t* inv, 
     const uint32_t nloc = part.wend - part.wbegin;
     const uint32_t W = (nloc + 31) / 32;
     const size_t smem = (size_t)4 * (64 * W + 32 * part.E) * 4;
-    cudaFuncSetAttribute(sample_lanes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    allow_smem(sample_lanes_kernel, (int)smem);
     const uint64_t groups = ((uint64_t)part.F + 31) / 32;
     sample_lanes_kernel<<<grid_for(groups, 4, 148u * 8u), 128, smem, s>>>(part, inv, info, rank16,
                                                                          pair_count, W, seghist);
@@ -1151,13 +1151,13 @@ void launch_sample_tile(cudaStream_t s, const Part& part, const uint32_t* inv, v
 #define ST_LAUNCH(RV)                                                                             \
     do {                                                                                          \
         if (info8) {                                                                              \
-            cudaFuncSetAttribute(sample_tile_kernel<RV, uint8_t>,                                 \
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);         \
+            allow_smem(sample_tile_kernel<RV, uint8_t>,                                 \
+                                 (int)smem);         \
             sample_tile_kernel<RV, uint8_t><<<grid, kThreads, smem, s>>>(                         \
                 part, inv, static_cast<uint8_t*>(info), rank16, pair_count, W, seghist, ws);      \
         } else {                                                                                  \
-            cudaFuncSetAttribute(sample_tile_kernel<RV, uint16_t>,                                \
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);         \
+            allow_smem(sample_tile_kernel<RV, uint16_t>,                                \
+                                 (int)smem);         \
             sample_tile_kernel<RV, uint16_t><<<grid, kThreads, smem, s>>>(                        \
                 part, inv, static_cast<uint16_t*>(info), rank16, pair_count, W, seghist, ws);     \
         }                                                                                         \
@@ -1179,7 +1179,7 @@ void launch_sample_hash(cudaStream_t s, const Part& part, const uint32_t* inv, u
     while (hs < 2 * d) hs <<= 1;
     const uint32_t W = (nloc + 31) / 32;
     const size_t smem = (size_t)4 * (2 * hs + 2 * W) * 4;
-    cudaFuncSetAttribute(sample_hash_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    allow_smem(sample_hash_kernel, (int)smem);
     sample_hash_kernel<<<grid_for(max_items, 4, 148u * 16u), 128, smem, s>>>(
         part, inv, info, rank16, pair_count, list, nlist, hs, W, seghist);
 }
@@ -1190,11 +1190,11 @@ void launch_seg_hist(cudaStream_t s, const Part& part, const uint32_t* stream, c
     const size_t smem = (size_t)(kThreads / 32) * part.E * 4;
     const unsigned grid = grid_for(nseg * 32, kThreads, 148u * 64u);
     if (info8) {
-        cudaFuncSetAttribute(seg_hist_kernel<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        allow_smem(seg_hist_kernel<uint8_t>, (int)smem);
         seg_hist_kernel<uint8_t><<<grid, kThreads, smem, s>>>(part, stream, static_cast<const uint8_t*>(info),
                                                               cpos, seghist, segcnt);
     } else {
-        cudaFuncSetAttribute(seg_hist_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        allow_smem(seg_hist_kernel<uint16_t>, (int)smem);
         seg_hist_kernel<uint16_t><<<grid, kThreads, smem, s>>>(part, stream, static_cast<const uint16_t*>(info),
                                                                cpos, seghist, segcnt);
     }
@@ -1207,7 +1207,7 @@ void launch_seg_write2(cudaStream_t s, const Part& part, const uint32_t* stream,
                        uint32_t* blkbase) {
     const uint64_t nseg = (uint64_t)(part.wend - part.wbegin) * part.E;
     const size_t smem = (size_t)(kThreads / 32) * part.E * 4;
-    cudaFuncSetAttribute(seg_write_kernel2<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    allow_smem(seg_write_kernel2<uint16_t>, (int)smem);
     seg_write_kernel2<uint16_t><<<grid_for(nseg * 32, kThreads, 148u * 64u), kThreads, smem, s>>>(
         part, stream, info, cpos, sizes, seg_off, sorted_base, MB, dest, sorted_size, blkmask, blkbase);
 }

@@ -230,6 +230,7 @@ void launch_fill_class(cudaStream_t s, uint8_t* cls, uint64_t n, uint8_t j);
 void launch_hp_fill(cudaStream_t s, const Part& part, const uint32_t* inv, const uint16_t* rank16,
                     uint32_t MB, const uint32_t* rec, uint32_t np, uint32_t J, uint32_t Rp,
                     const uint32_t* cbase, uint32_t* hp);
+bool holder_hp_ok(const Part& part);  // E within one TMA box, tiles within shared memory
 void launch_holder_hp(cudaStream_t s, const Part& part, const uint32_t* inv, const uint16_t* rank16,
                       const uint32_t* hp, const uint64_t* pair_off, uint32_t* holders);
 void launch_blk_codes(cudaStream_t s, const Part& part, uint32_t MB, const uint32_t* blkmask,

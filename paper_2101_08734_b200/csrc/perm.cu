@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(kThreads) fy_emit_kernel(uint64_t key, Part pa
             v = x;
         }
         if (perm_out) perm_out[(size_t)slot * F + i] = v;
-        if (inv) inv[(size_t)e * F + v] = i;
+        if (inv) inv[(size_t)e * pitch16(F) + v] = i;
         if (stream && i < part.P) {
             uint32_t w;
             uint64_t spos;
@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(kThreads) perm_scatter_kernel(Part part, const
     const uint32_t* row = perms + (size_t)e * F;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < F; i += gridDim.x * blockDim.x) {
         const uint32_t v = __ldcs(row + i);
-        inv[(size_t)e * F + v] = i;
+        inv[(size_t)e * pitch16(F) + v] = i;
         if (i < part.P) {
             uint32_t w;
             uint64_t spos;

@@ -304,7 +304,7 @@ __global__ void __launch_bounds__(kFycPT) fyc_block_kernel(uint64_t key, uint32_
     __syncthreads();
     uint32_t* qq = q + (size_t)slot * F;
     uint32_t* ts = tsucc + (size_t)slot * F;
-    uint32_t* irow = inv ? inv + (size_t)e * F : nullptr;
+    uint32_t* irow = inv ? inv + (size_t)e * pitch16(F) : nullptr;
     for (uint32_t t = threadIdx.x; t < W; t += kFycPT) {
         const uint32_t y = y0 + t, beg = off[t], end = off[t + 1];
         if (beg == end) {
@@ -433,7 +433,7 @@ __global__ void __launch_bounds__(kThreads, 4) fyc_emit_kernel(Part part, uint32
                 continue;
             }
             if (perm_out) perm_out[(size_t)slot * F + i] = v;
-            if (inv && !(sv[t] & kTag)) inv[(size_t)e * F + v] = i;  // chase roots only
+            if (inv && !(sv[t] & kTag)) inv[(size_t)e * pitch16(F) + v] = i;  // chase roots only
             if ((stream || dst.G) && i < part.P) {
                 uint32_t w;
                 uint64_t spos;
@@ -476,14 +476,14 @@ void launch_fyc(cudaStream_t s, uint64_t key, const Part& part, uint32_t e0, uin
     const size_t sm_part = (size_t)4 * (g.NB + 1);
     const size_t sm_block = (size_t)4 * (kFycW + 1 + kFycCap);
     if (g.pack) {
-        cudaFuncSetAttribute(fyc_part_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_part);
-        cudaFuncSetAttribute(fyc_block_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_block);
+        allow_smem(fyc_part_kernel<true>, (int)sm_part);
+        allow_smem(fyc_block_kernel<true>, (int)sm_block);
         fyc_part_kernel<true><<<dim3(NT, ne), kFycPT, sm_part, s>>>(key, F, e0, g, rt, rej_flag, region, cursor);
         fyc_block_kernel<true><<<dim3(g.NB, ne), kFycPT, sm_block, s>>>(key, F, e0, g, rt, region, cursor,
                                                                         tsucc, q, inv, check);
     } else {
-        cudaFuncSetAttribute(fyc_part_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_part);
-        cudaFuncSetAttribute(fyc_block_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_block);
+        allow_smem(fyc_part_kernel<false>, (int)sm_part);
+        allow_smem(fyc_block_kernel<false>, (int)sm_block);
         fyc_part_kernel<false><<<dim3(NT, ne), kFycPT, sm_part, s>>>(key, F, e0, g, rt, rej_flag, region, cursor);
         fyc_block_kernel<false><<<dim3(g.NB, ne), kFycPT, sm_block, s>>>(key, F, e0, g, rt, region, cursor,
                                                                          tsucc, q, inv, check);

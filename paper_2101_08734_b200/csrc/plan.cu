@@ -367,7 +367,7 @@ int build_seed_path(clairplan_plan* p) {
     const uint32_t F = part.F, E = part.E, nloc = p->nloc;
     bool ok = true;
     uint32_t* stream_buf = need<uint32_t>(p->stream_buf, p->A, ok);
-    uint32_t* info = need<uint32_t>(p->info, (uint64_t)E * F, ok);
+    uint32_t* info = need<uint32_t>(p->info, (uint64_t)E * part.Fp, ok);  // pitched rows
     uint32_t* pcount = need<uint32_t>(p->pair_count, F, ok);
     uint64_t* poff = need<uint64_t>(p->pair_off, (uint64_t)F + 1, ok);
     uint32_t* segcnt = need<uint32_t>(p->segcnt, (uint64_t)nloc * E, ok);
@@ -569,10 +569,11 @@ bool hp_path_ok(const clairplan_plan* p) {
     const Part& part = p->part;
     uint64_t lmax = 0;
     for (uint32_t w : {part.wbegin, part.wend - 1}) lmax = std::max<uint64_t>(lmax, part.E * part.epoch_len(w));
-    // (hp_fill + holder_hp measured 26.7 + 11.1 ms against holder_tile's 30 ms at the
-    // ImageNet-22k shape: latency-bound record gathers; off until that pass is faster)
+    // (hp_fill + holder_hp: 12.5 + 8.3 ms against holder_tile's 30 ms at the ImageNet-22k
+    // shape, round-2 launch lists; CLAIRPLAN_NO_HP_PATH=1: A/B)
     static const bool on = !ab_flag("CLAIRPLAN_NO_HP_PATH");
-    return on && !p->sparse && !p->allfit && p->cfg.num_classes <= 15 && lmax < (1ull << 28);
+    return on && !p->sparse && !p->allfit && p->cfg.num_classes <= 15 && lmax < (1ull << 28) &&
+           holder_hp_ok(part);
 }
 
 // K6-K8 of the v2 path on the cached tier-ordered sizes / block masks: first fit, block class
@@ -833,7 +834,7 @@ int build_seed_path_v2(clairplan_plan* p, const uint32_t* ext_perms,
     const uint64_t nblk = (uint64_t)nloc * E * MB;
     uint32_t np = 0;
     while ((1u << np) <= J) ++np;  // bits to hold classes 0..J
-    const uint64_t EF = (uint64_t)E * F, NEE = (uint64_t)nloc * E * E;
+    const uint64_t NEE = (uint64_t)nloc * E * E;
     bool ok = true;
     // sparse sample-major passes (sharded handle fed by the all-to-all; CLAIRPLAN_DENSE=1: A/B)
     const bool sparse = ext_streams && sharded_sparse(p);
@@ -841,7 +842,7 @@ int build_seed_path_v2(clairplan_plan* p, const uint32_t* ext_perms,
     p->hook_fired = false;
     bool hook_called = false;  // at most once per build: every rank calls its collective once
     // the dense [E][F] sample-major arrays (not needed by the sparse passes)
-    uint32_t* inv = sparse ? nullptr : need<uint32_t>(p->inv, EF, ok);
+    uint32_t* inv = sparse ? nullptr : need<uint32_t>(p->inv, (uint64_t)E * part.Fp, ok);
     const uint64_t EFp = (uint64_t)E * part.Fp;  // pitched u16 rows
     // info rows are u8 when every count fits (E <= 255) and the tile sample pass writes them:
     // half the L2 footprint of the gathers from the segment passes
@@ -1449,7 +1450,7 @@ static int generate_streams_impl(clairplan_plan* p, uint32_t epoch_begin, uint32
     static const bool own_ok = ab_knob("CLAIRPLAN_OWN_INV", 1) != 0;
     if (own_ok && v2_ok(p) && !sharded_sparse(p)) {
         bool ok = true;
-        own_inv = need<uint32_t>(p->inv, (uint64_t)pp.E * pp.F, ok);
+        own_inv = need<uint32_t>(p->inv, (uint64_t)pp.E * pp.Fp, ok);
         if (!ok) own_inv = nullptr;
     }
     for (int attempt = 0; attempt < 3; ++attempt) {

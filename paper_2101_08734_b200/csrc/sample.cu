@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(kThreads) sample_pass_kernel(Part part,
         __syncthreads();
         for (uint32_t idx = threadIdx.x; idx < E * 32; idx += blockDim.x) {
             const uint32_t e = idx >> 5, l = idx & 31;
-            T[idx] = (k0 + l < F) ? info[(size_t)e * F + k0 + l] : kNone;
+            T[idx] = (k0 + l < F) ? info[(size_t)e * pitch16(F) + k0 + l] : kNone;
         }
         __syncthreads();
         for (uint32_t s = warp; s < 32; s += nwarps) {
@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(kThreads) sample_pass_kernel(Part part,
         __syncthreads();
         for (uint32_t idx = threadIdx.x; idx < E * 32; idx += blockDim.x) {
             const uint32_t e = idx >> 5, l = idx & 31;
-            if (k0 + l < F) info[(size_t)e * F + k0 + l] = T[idx];
+            if (k0 + l < F) info[(size_t)e * pitch16(F) + k0 + l] = T[idx];
         }
     }
 }
@@ -168,7 +168,7 @@ int sample_pass_config(const Part& part, uint32_t* hs, uint32_t* nw_words, uint3
 void launch_sample_pass(cudaStream_t s, const Part& part, uint32_t* info, uint32_t* pair_count,
                         uint32_t hs, uint32_t nw_words, uint32_t warps, size_t smem) {
     // per-device attribute; cheap and idempotent
-    cudaFuncSetAttribute(sample_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    allow_smem(sample_pass_kernel, 
                          200 * 1024);
     const unsigned grid = grid_for(((uint64_t)part.F + 31) / 32, 1, 148u * 8u);
     sample_pass_kernel<<<grid, warps * 32, smem, s>>>(part, info, pair_count, hs, nw_words);

@@ -341,7 +341,7 @@ void launch_sparse_sample(cudaStream_t s, const Part& part, const uint64_t* soff
     const FastDiv uni = uniform_len(part);
 #define SS_LAUNCH(RV)                                                                              \
     do {                                                                                           \
-        cudaFuncSetAttribute(sparse_sample_kernel<RV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+        allow_smem(sparse_sample_kernel<RV>, \
                              (int)smem);                                                           \
         sparse_sample_kernel<RV><<<grid, kThreads, smem, s>>>(part.F, nloc, W, soff, koff, csr,      \
                                                               pair_count, einfo, erank, ws, uni);  \

@@ -174,7 +174,7 @@ static void seg_write3_launch(cudaStream_t s, const Part& part, const uint32_t* 
     // one epoch of segments, so that epoch's info row stays in L2
 #define SW3(ST)                                                                                   \
     do {                                                                                          \
-        cudaFuncSetAttribute(seg_write3_kernel<IT, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+        allow_smem(seg_write3_kernel<IT, ST>, \
                              (int)smem);                                                          \
         const unsigned grid = std::min<unsigned>(                                                 \
             resident_grid(seg_write3_kernel<IT, ST>, kSegWarps * 32, smem, 4), (unsigned)nseg);   \
@@ -279,11 +279,15 @@ __global__ void __launch_bounds__(kThreads, 3) hp_fill_kernel(Part part, const u
         // rank row: one 16-B load (rows pitched to Fp, a multiple of 16 samples)
         const uint4 rv = __ldcs(reinterpret_cast<const uint4*>(rank16 + (size_t)e * part.Fp + k0));
         const uint32_t rw[4] = {rv.x, rv.y, rv.z, rv.w};
+        // inv row: two 16-B loads (same pitch; k0 + kHpU <= Fp)
+        const uint4* iv4 = reinterpret_cast<const uint4*>(inv + (size_t)e * part.Fp + k0);
+        const uint4 i0 = __ldcs(iv4), i1 = __ldcs(iv4 + 1);
+        const uint32_t iw[kHpU] = {i0.x, i0.y, i0.z, i0.w, i1.x, i1.y, i1.z, i1.w};
         uint32_t p[kHpU];
 #pragma unroll
         for (int u = 0; u < kHpU; ++u) {
             const uint32_t rk = (rw[u >> 1] >> ((u & 1) * 16)) & 0xFFFFu;
-            p[u] = (k0 + u < F && rk != 0xFFFFu) ? __ldcs(inv + (size_t)e * F + k0 + u) : kNone;
+            p[u] = (k0 + u < F && rk != 0xFFFFu) ? iw[u] : kNone;
         }
         uint4 a[kHpU];
         uint64_t row[kHpU];
@@ -338,8 +342,8 @@ void launch_hp_fill(cudaStream_t s, const Part& part, const uint32_t* inv, const
 }
 
 // ---------------------------------------------------------------------------- K8
-// CTA = 32 samples: inv / rank / hp rows of the tile into padded shared tiles (coalesced
-// 128-B rows), then a warp per sample, lanes = epochs: every first access (rank != 0xFFFF)
+// CTA = 32 samples: inv / rank / hp rows of the tile into padded shared tiles (16-B / 8-B
+// vector loads of the pitched rows; a TMA-box variant measured slower: DESIGN.md §4), then a warp per sample, lanes = epochs: every first access (rank != 0xFFFF)
 // writes {worker, class, position} at pair_off[k] + rank (build_index order,
 // policies.cpp:124-142).  Class 0 (not cached) records are compacted out afterwards if any.
 template <int TU = 4>
@@ -356,26 +360,33 @@ __global__ void __launch_bounds__(kThreads) holder_hp_kernel(Part part, const ui
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
     for (uint64_t k0 = (uint64_t)blockIdx.x * 32; k0 < F; k0 += (uint64_t)gridDim.x * 32) {
         __syncthreads();
-        for (uint32_t i0 = threadIdx.x; i0 < E * 32; i0 += TU * blockDim.x) {
-            uint32_t iv[TU], hv[TU];
-            uint16_t rv[TU];
+        // thread per (epoch, quad of 4 samples): 16-B inv / hp loads and an 8-B rank load
+        // (rows pitched to Fp: a quad that starts below F lies inside its row)
+        for (uint32_t i0 = threadIdx.x; i0 < E * 8; i0 += TU * blockDim.x) {
+            uint4 iv[TU], hv[TU];
+            uint2 rv[TU];
 #pragma unroll
             for (int u = 0; u < TU; ++u) {
                 const uint32_t idx = i0 + u * blockDim.x;
-                const uint32_t e = idx >> 5, l = idx & 31;
-                const bool ok = idx < E * 32 && k0 + l < F;
-                rv[u] = ok ? __ldcs(rank16 + (size_t)e * part.Fp + k0 + l) : (uint16_t)0xFFFFu;
-                iv[u] = ok ? __ldcs(inv + (size_t)e * F + k0 + l) : kNone;
-                hv[u] = ok ? __ldcs(hp + (size_t)e * part.Fp + k0 + l) : 0u;
+                const uint32_t e = idx >> 3, l = (idx & 7) * 4;
+                const bool ok = idx < E * 8 && k0 + l < F;
+                const size_t o = (size_t)e * part.Fp + k0 + l;
+                rv[u] = ok ? __ldcs(reinterpret_cast<const uint2*>(rank16 + o)) : make_uint2(~0u, ~0u);
+                iv[u] = ok ? __ldcs(reinterpret_cast<const uint4*>(inv + o)) : make_uint4(kNone, kNone, kNone, kNone);
+                hv[u] = ok ? __ldcs(reinterpret_cast<const uint4*>(hp + o)) : make_uint4(0, 0, 0, 0);
             }
 #pragma unroll
             for (int u = 0; u < TU; ++u) {
                 const uint32_t idx = i0 + u * blockDim.x;
-                if (idx < E * 32) {
-                    const uint32_t e = idx >> 5, l = idx & 31;
-                    tinv[e * 33 + l] = iv[u];
-                    thp[e * 33 + l] = hv[u];
-                    trk[e * 33 + l] = rv[u];
+                if (idx < E * 8) {
+                    const uint32_t e = idx >> 3, l = (idx & 7) * 4;
+                    uint32_t* ti = tinv + e * 33 + l;
+                    uint32_t* th = thp + e * 33 + l;
+                    uint16_t* tr = trk + e * 33 + l;
+                    ti[0] = iv[u].x, ti[1] = iv[u].y, ti[2] = iv[u].z, ti[3] = iv[u].w;
+                    th[0] = hv[u].x, th[1] = hv[u].y, th[2] = hv[u].z, th[3] = hv[u].w;
+                    tr[0] = (uint16_t)rv[u].x, tr[1] = (uint16_t)(rv[u].x >> 16);
+                    tr[2] = (uint16_t)rv[u].y, tr[3] = (uint16_t)(rv[u].y >> 16);
                 }
             }
         }
@@ -396,11 +407,15 @@ __global__ void __launch_bounds__(kThreads) holder_hp_kernel(Part part, const ui
     }
 }
 
+bool holder_hp_ok(const Part& part) {  // the padded tiles fit one CTA's shared memory
+    return (size_t)part.E * 33 * 4 * 2 + (size_t)part.E * 33 * 2 + 16 <= (200u << 10);
+}
+
 void launch_holder_hp(cudaStream_t s, const Part& part, const uint32_t* inv, const uint16_t* rank16,
                       const uint32_t* hp, const uint64_t* pair_off, uint32_t* holders) {
     const size_t smem = (size_t)part.E * 33 * 4 * 2 + (size_t)part.E * 33 * 2 + 16;
     const uint64_t tiles = ((uint64_t)part.F + 31) / 32;
-    cudaFuncSetAttribute(holder_hp_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    allow_smem(holder_hp_kernel<4>, (int)smem);
     holder_hp_kernel<4><<<grid_for(tiles, 1, 148u * 8u), kThreads, smem, s>>>(part, inv, rank16, hp,
                                                                               pair_off, holders);
 }
