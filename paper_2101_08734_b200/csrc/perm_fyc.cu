@@ -181,12 +181,19 @@ __global__ void __launch_bounds__(kFycPT) fyc_part_kernel(uint64_t key, uint32_t
             const uint32_t i = i_lo + (k0 + u) * kFycPT + threadIdx.x;
             jj[u] = (i < i_hi && i > 0) ? fyc_draw(key, e, F, i, st, cu, nrej, rej_flag + er) : kNone;
         }
+        // block lookups of the 8 draws issued together: cell, then the first boundary test
+        uint32_t bb[8], nx[8];
+#pragma unroll
+        for (uint32_t u = 0; u < 8; ++u) bb[u] = jj[u] != kNone ? __ldg(g.cell + (jj[u] >> kFycLgCell)) : 0u;
+#pragma unroll
+        for (uint32_t u = 0; u < 8; ++u) nx[u] = __ldg(g.bstart + bb[u] + 1);
 #pragma unroll
         for (uint32_t u = 0; u < 8; ++u) {
             if constexpr (PACK) jv[k0 + u] = jj[u];
             bk[k0 + u] = kNone;
             if (jj[u] != kNone) {
-                const uint32_t b = fyc_block_of(g, jj[u]);
+                uint32_t b = bb[u];
+                for (uint32_t v = nx[u]; v <= jj[u];) v = __ldg(g.bstart + (++b) + 1);
                 const uint32_t r = atomicAdd(&hist[b], 1u);
                 bk[k0 + u] = (b << RB) | r;
                 if constexpr (PACK) jv[k0 + u] = jj[u] - __ldg(g.bstart + b);
@@ -331,6 +338,7 @@ __global__ void __launch_bounds__(kFycPT) fyc_block_kernel(uint64_t key, uint32_
 
 // ---- fyc_emit ----------------------------------------------------------------------------
 constexpr uint32_t kFycEmitL = 16;
+constexpr uint32_t kFycChains = 2;  // chase chains in flight per lane (4: 18.8 vs 18.6 ms, config 4)
 
 __global__ void __launch_bounds__(kThreads, 4) fyc_emit_kernel(Part part, uint32_t e0,
                                                                const uint32_t* __restrict__ tsucc,
@@ -369,55 +377,48 @@ __global__ void __launch_bounds__(kThreads, 4) fyc_emit_kernel(Part part, uint32
             np += __popc(bal);
         }
         __syncwarp();
-        // two chains in flight per lane, taken from the chunk's work list in order
+        // kFycChains chains in flight per lane, taken from the chunk's work list in order
         uint32_t nj = lane;
-        uint32_t idx0 = 0, cur0 = 0, idx1 = 0, cur1 = 0;
-        bool a0 = nj < np;
-        if (a0) {
-            idx0 = lst[nj];
-            cur0 = buf[idx0];
+        uint32_t idx[kFycChains], cur[kFycChains];
+        bool act[kFycChains];
+#pragma unroll
+        for (uint32_t c2 = 0; c2 < kFycChains; ++c2) {
+            act[c2] = nj < np;
+            idx[c2] = act[c2] ? lst[nj] : 0u;
+            cur[c2] = act[c2] ? buf[idx[c2]] : 0u;
+            nj += 32;
         }
-        nj += 32;
-        bool a1 = nj < np;
-        if (a1) {
-            idx1 = lst[nj];
-            cur1 = buf[idx1];
-        }
-        nj += 32;
-        while (__any_sync(0xffffffffu, a0 || a1)) {
-            if (check && ((a0 && cur0 >= F) || (a1 && cur1 >= F))) {
-                printf("fyc_emit: chase index out of range e=%u chunk=%u cur0=%u cur1=%u F=%u\n", e, c,
-                       a0 ? cur0 : 0u, a1 ? cur1 : 0u, F);
-                atomicOr(err, 1u);
-                a0 = a1 = false;
-                break;
-            }
-            const uint32_t q0 = a0 ? qq[cur0] : 0u;
-            const uint32_t q1 = a1 ? qq[cur1] : 0u;
-            if (a0) {
-                if (q0 == kNone) {
-                    buf[idx0] = cur0;
-                    a0 = nj < np;
-                    if (a0) {
-                        idx0 = lst[nj];
-                        cur0 = buf[idx0];
-                        nj += 32;
-                    }
-                } else {
-                    cur0 = q0;
+        for (;;) {
+            bool any = false;
+#pragma unroll
+            for (uint32_t c2 = 0; c2 < kFycChains; ++c2) any |= act[c2];
+            if (!__any_sync(0xffffffffu, any)) break;
+            if (check) {
+                bool bad = false;
+#pragma unroll
+                for (uint32_t c2 = 0; c2 < kFycChains; ++c2) bad |= act[c2] && cur[c2] >= F;
+                if (bad) {
+                    printf("fyc_emit: chase index out of range e=%u chunk=%u F=%u\n", e, c, F);
+                    atomicOr(err, 1u);
+                    break;
                 }
             }
-            if (a1) {
-                if (q1 == kNone) {
-                    buf[idx1] = cur1;
-                    a1 = nj < np;
-                    if (a1) {
-                        idx1 = lst[nj];
-                        cur1 = buf[idx1];
+            uint32_t qv[kFycChains];
+#pragma unroll
+            for (uint32_t c2 = 0; c2 < kFycChains; ++c2) qv[c2] = act[c2] ? qq[cur[c2]] : 0u;
+#pragma unroll
+            for (uint32_t c2 = 0; c2 < kFycChains; ++c2) {
+                if (!act[c2]) continue;
+                if (qv[c2] == kNone) {  // chain ends: V = cur; next chain from the list
+                    buf[idx[c2]] = cur[c2];
+                    act[c2] = nj < np;
+                    if (act[c2]) {
+                        idx[c2] = lst[nj];
+                        cur[c2] = buf[idx[c2]];
                         nj += 32;
                     }
                 } else {
-                    cur1 = q1;
+                    cur[c2] = qv[c2];
                 }
             }
         }
