@@ -289,28 +289,29 @@ __global__ void __launch_bounds__(kThreads, 3) hp_fill_kernel(Part part, const u
             const uint32_t rk = (rw[u >> 1] >> ((u & 1) * 16)) & 0xFFFFu;
             p[u] = (k0 + u < F && rk != 0xFFFFu) ? iw[u] : kNone;
         }
+        // per sample: its record (16 B) and (local worker << 5 | bit in the block) -- the
+        // record row is recomputed in the rare case it is needed again (registers: no spills)
         uint4 a[kHpU];
-        uint64_t row[kHpU];
-        uint32_t bit[kHpU], wl[kHpU];
+        uint32_t wb[kHpU];
 #pragma unroll
         for (int u = 0; u < kHpU; ++u) {
             if (p[u] == kNone) continue;
             uint32_t w;
             const uint32_t t = part.within_epoch(p[u], w);
-            wl[u] = w - part.wbegin;
-            bit[u] = t & 31;
-            row[u] = rec_index(wl[u], e, part.wend - part.wbegin, MB, t >> 5) * Rp;
-            a[u] = __ldg(reinterpret_cast<const uint4*>(rec + row[u]));
+            wb[u] = ((w - part.wbegin) << 5) | (t & 31);
+            a[u] = __ldg(reinterpret_cast<const uint4*>(
+                rec + rec_index(w - part.wbegin, e, part.wend - part.wbegin, MB, t >> 5) * Rp));
         }
         uint32_t out[kHpU];
 #pragma unroll
         for (int u = 0; u < kHpU; ++u) {
             out[u] = 0;
             if (p[u] == kNone) continue;
+            const uint32_t bit = wb[u] & 31, wl = wb[u] >> 5;
             uint32_t cls = 0, cm = 0xffffffffu;
             for (uint32_t q = 0; q < np; ++q) {
                 const uint32_t pl = q == 0 ? a[u].x : q == 1 ? a[u].y : q == 2 ? a[u].z : a[u].w;
-                cls |= ((pl >> bit[u]) & 1u) << q;
+                cls |= ((pl >> bit) & 1u) << q;
             }
             for (uint32_t q = 0; q < np; ++q) {
                 const uint32_t pl = q == 0 ? a[u].x : q == 1 ? a[u].y : q == 2 ? a[u].z : a[u].w;
@@ -318,10 +319,15 @@ __global__ void __launch_bounds__(kThreads, 3) hp_fill_kernel(Part part, const u
             }
             if (cls) {
                 const uint32_t wi = np + cls - 1;
-                const uint32_t prew = wi == 0 ? a[u].x : wi == 1 ? a[u].y : wi == 2 ? a[u].z
-                                    : wi == 3 ? a[u].w : __ldg(rec + row[u] + wi);
-                const uint32_t pos = prew - __ldg(cbase + wl[u] * J + cls - 1) +
-                                     __popc(cm & ((1u << bit[u]) - 1u));
+                uint32_t prew;
+                if (wi < 4) {
+                    prew = wi == 0 ? a[u].x : wi == 1 ? a[u].y : wi == 2 ? a[u].z : a[u].w;
+                } else {
+                    uint32_t w;
+                    const uint32_t t = part.within_epoch(p[u], w);
+                    prew = __ldg(rec + rec_index(wl, e, part.wend - part.wbegin, MB, t >> 5) * Rp + wi);
+                }
+                const uint32_t pos = prew - __ldg(cbase + wl * J + cls - 1) + __popc(cm & ((1u << bit) - 1u));
                 out[u] = (cls << 28) | pos;
             }
         }
@@ -336,6 +342,7 @@ void launch_hp_fill(cudaStream_t s, const Part& part, const uint32_t* inv, const
                     const uint32_t* cbase, uint32_t* hp) {
     const uint64_t total = (uint64_t)part.E * ((part.F + kHpU - 1) / kHpU);
     // resident grid: epochs in lockstep, so one epoch's records stay in L2
+    // (72 registers at 3 CTAs/SM: no spills; 2 CTAs/SM measured the same, 4 spills)
     const unsigned grid = std::min<unsigned>(resident_grid(hp_fill_kernel, kThreads, 0, 8),
                                              grid_for(total, kThreads, 148u * 64u));
     hp_fill_kernel<<<grid, kThreads, 0, s>>>(part, inv, rank16, MB, rec, np, J, Rp, cbase, hp);
