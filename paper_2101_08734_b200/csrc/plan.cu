@@ -914,7 +914,8 @@ int build_seed_path_v2(clairplan_plan* p, const uint32_t* ext_perms,
         // K4a: per-sample (worker, count, first epoch)
         // Large F: the segment histograms are accumulated by the sample pass itself (REDs
         // overlap its latency); small F: a separate warp-per-segment pass is cheaper.
-        const bool red_hist = F >= (1u << 22) && !sparse;
+        static const bool red_ok = ab_knob("CLAIRPLAN_RED_HIST", 1) != 0;  // A/B
+        const bool red_hist = F >= (1u << 22) && !sparse && red_ok;
         uint32_t* hist_out = red_hist ? seghist : nullptr;
         if (red_hist) CK(cudaMemsetAsync(seghist, 0, NEE * 4, s));
         // per-worker candidate size sums for the whole-worker fit test (all-fit path)
