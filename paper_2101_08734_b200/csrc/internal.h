@@ -223,13 +223,14 @@ void launch_seg_write2(cudaStream_t s, const Part& part, const uint32_t* stream,
 // tier.cu (dense tier path)
 void launch_seg_write3(cudaStream_t s, const Part& part, const uint32_t* stream, const void* info,
                        bool info8, const uint64_t* seg_off, const uint64_t* sorted_base, uint32_t MB,
-                       uint32_t* dest, uint32_t* sorted_k, uint32_t* blkmask, uint32_t* blkbase);
+                       uint32_t* dest, uint32_t* sorted_k, uint32_t* blkmask, uint32_t* blkbase,
+                       uint32_t* claim);
 void launch_gather_sorted_sizes(cudaStream_t s, const uint32_t* sorted_k, const double* sizes,
                                 uint64_t n, double* out);
 void launch_fill_class(cudaStream_t s, uint8_t* cls, uint64_t n, uint8_t j);
 void launch_hp_fill(cudaStream_t s, const Part& part, const uint32_t* inv, const uint16_t* rank16,
                     uint32_t MB, const uint32_t* rec, uint32_t np, uint32_t J, uint32_t Rp,
-                    const uint32_t* cbase, uint32_t* hp);
+                    const uint32_t* cbase, uint32_t* hp, uint32_t* claim);
 bool holder_hp_ok(const Part& part);  // E within one TMA box, tiles within shared memory
 void launch_holder_hp(cudaStream_t s, const Part& part, const uint32_t* inv, const uint16_t* rank16,
                       const uint32_t* hp, const uint64_t* pair_off, uint32_t* holders);

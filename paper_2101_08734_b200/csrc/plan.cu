@@ -619,8 +619,10 @@ int assign_v2(clairplan_plan* p) {
         if (p->hp_path) {
             uint32_t* hp = need<uint32_t>(p->hpos, (uint64_t)E * part.Fp, ok);
             if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed (holder positions)");
+            uint32_t* claim = need<uint32_t>(p->sched, 8, ok);
+            if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed (holder positions)");
             launch_hp_fill(s, part, p->inv.get<uint32_t>(), p->rank16.get<uint16_t>(), MB, rec, np, J, Rp,
-                           cbase, hp);
+                           cbase, hp, claim + 1);
             ++p->launches;
         }
         p->launches += 4 + 3 * J + 3;
@@ -744,9 +746,11 @@ int tier_order_v2(clairplan_plan* p) {
     } else {  // epoch-major segment CTAs, then the size gather on its own (tier.cu)
         uint32_t* sk = need<uint32_t>(p->sorted_k, D, ok);
         if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed (tier order)");
+        uint32_t* claim = need<uint32_t>(p->sched, 8, ok);
+        if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed (tier order)");
         launch_seg_write3(s, part, p->stream_buf.get<uint32_t>(), info_src(p), p->info8, segoff,
                           p->sorted_base.get<uint64_t>(), p->v2_mb, dest, sk,
-                          p->blkmask.get<uint32_t>(), p->blkbase.get<uint32_t>());
+                          p->blkmask.get<uint32_t>(), p->blkbase.get<uint32_t>(), claim);
         p->ssize_pending = true;  // gathered by class 1's first-fit statistics pass
     }
     launch_worker_segments(s, segoff, nloc, E, p->wbeg.get<uint64_t>(), p->wlen.get<uint64_t>());

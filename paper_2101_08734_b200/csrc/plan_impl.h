@@ -127,6 +127,7 @@ struct clairplan_plan {
     DevBuf merge_buf;                // clairplan_merge_holder_counts scratch (own: may overlap a build)
     DevBuf sorted_k;                 // tier path: sample id of every tier position (seg_write3)
     bool ssize_pending = false;      // sorted_size not yet gathered (class 1's ff_stats does it)
+    DevBuf sched;                    // in-order work claim counters (seg_write3, hp_fill)
     DevBuf hpos;                     // tier path: [E][Fp] class << 28 | class-list position (hp_fill)
     bool hp_path = false;            // last assignment wrote hpos (holder_hp replaces holder_tile)
     bool info8 = false;              // info rows of the last dense build are u8 (else u16)

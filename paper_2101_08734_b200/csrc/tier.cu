@@ -43,8 +43,9 @@ __global__ void __launch_bounds__(kSegWarps * 32) seg_write3_kernel(
     Part part, const uint32_t* __restrict__ stream, const IT* __restrict__ info,
     const uint64_t* __restrict__ seg_off, const uint64_t* __restrict__ sorted_base, uint32_t MB,
     uint32_t* __restrict__ dest, uint32_t* __restrict__ sorted_k, uint32_t* __restrict__ blkmask,
-    uint32_t* __restrict__ blkbase) {
-    extern __shared__ uint32_t sm[];  // [kSegWarps][E] count histograms -> offsets, [kSegWarps]
+    uint32_t* __restrict__ blkbase, uint32_t* __restrict__ claim) {
+    extern __shared__ uint32_t sm[];
+    __shared__ uint32_t s_seg;  // [kSegWarps][E] count histograms -> offsets, [kSegWarps]
                                       // totals, STAGE: u8 count per segment entry
     const uint32_t E = part.E, nloc = part.wend - part.wbegin;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -54,7 +55,16 @@ __global__ void __launch_bounds__(kSegWarps * 32) seg_write3_kernel(
     uint32_t* sk = sm + kSegWarps * E + kSegWarps;                          // STAGE 2: [Lst]
     IT* sc = reinterpret_cast<IT*>(sk + (STAGE == 2 ? Lst : 0));            // STAGE >= 1: [Lst]
     const uint64_t nseg = (uint64_t)nloc * E;
-    for (uint64_t seg = blockIdx.x; seg < nseg; seg += gridDim.x) {
+    // segments claimed in order from one counter (claim != null): the CTAs in flight stay within
+    // ~one epoch however unevenly they progress (a fixed grid-stride assignment drifts apart
+    // over the 90 epochs and the info rows of several epochs compete for L2)
+    for (uint64_t seg = blockIdx.x;; seg += gridDim.x) {
+        if (claim) {
+            if (threadIdx.x == 0) s_seg = atomicAdd(claim, 1u);
+            __syncthreads();
+            seg = s_seg;
+        }
+        if (seg >= nseg) break;
         const uint32_t e = (uint32_t)(seg / nloc), wl = (uint32_t)(seg - (uint64_t)e * nloc);
         const uint32_t w = part.wbegin + wl;
         const uint64_t Le = part.epoch_len(w);
@@ -162,7 +172,8 @@ __global__ void __launch_bounds__(kSegWarps * 32) seg_write3_kernel(
 template <typename IT>
 static void seg_write3_launch(cudaStream_t s, const Part& part, const uint32_t* stream, const IT* info,
                               const uint64_t* seg_off, const uint64_t* sorted_base, uint32_t MB,
-                              uint32_t* dest, uint32_t* sorted_k, uint32_t* blkmask, uint32_t* blkbase) {
+                              uint32_t* dest, uint32_t* sorted_k, uint32_t* blkmask, uint32_t* blkbase,
+                              uint32_t* claim) {
     const uint64_t nseg = (uint64_t)(part.wend - part.wbegin) * part.E;
     const uint64_t Lmax = (uint64_t)MB * 32;
     const size_t hbytes = (size_t)(kSegWarps * part.E + kSegWarps) * 4;
@@ -179,7 +190,7 @@ static void seg_write3_launch(cudaStream_t s, const Part& part, const uint32_t* 
         const unsigned grid = std::min<unsigned>(                                                 \
             resident_grid(seg_write3_kernel<IT, ST>, kSegWarps * 32, smem, 4), (unsigned)nseg);   \
         seg_write3_kernel<IT, ST><<<grid, kSegWarps * 32, smem, s>>>(                             \
-            part, stream, info, seg_off, sorted_base, MB, dest, sorted_k, blkmask, blkbase);      \
+            part, stream, info, seg_off, sorted_base, MB, dest, sorted_k, blkmask, blkbase, claim); \
     } while (0)
     if (stage == 1) SW3(1);
     else SW3(0);
@@ -188,13 +199,17 @@ static void seg_write3_launch(cudaStream_t s, const Part& part, const uint32_t* 
 
 void launch_seg_write3(cudaStream_t s, const Part& part, const uint32_t* stream, const void* info,
                        bool info8, const uint64_t* seg_off, const uint64_t* sorted_base, uint32_t MB,
-                       uint32_t* dest, uint32_t* sorted_k, uint32_t* blkmask, uint32_t* blkbase) {
+                       uint32_t* dest, uint32_t* sorted_k, uint32_t* blkmask, uint32_t* blkbase,
+                       uint32_t* claim) {
+    static const bool dyn = ab_knob("CLAIRPLAN_DYN", 1) != 0;  // A/B: fixed grid-stride order
+    if (claim && dyn) cudaMemsetAsync(claim, 0, 4, s);
+    if (!dyn) claim = nullptr;
     if (info8)
         seg_write3_launch(s, part, stream, static_cast<const uint8_t*>(info), seg_off, sorted_base, MB,
-                          dest, sorted_k, blkmask, blkbase);
+                          dest, sorted_k, blkmask, blkbase, claim);
     else
         seg_write3_launch(s, part, stream, static_cast<const uint16_t*>(info), seg_off, sorted_base, MB,
-                          dest, sorted_k, blkmask, blkbase);
+                          dest, sorted_k, blkmask, blkbase, claim);
 }
 
 // ---------------------------------------------------------------------------- sizes
@@ -268,12 +283,24 @@ __global__ void __launch_bounds__(kThreads, 3) hp_fill_kernel(Part part, const u
                                                            uint32_t MB, const uint32_t* __restrict__ rec,
                                                            uint32_t np, uint32_t J, uint32_t Rp,
                                                            const uint32_t* __restrict__ cbase,
-                                                           uint32_t* __restrict__ hp) {
+                                                           uint32_t* __restrict__ hp,
+                                                           uint32_t* __restrict__ claim) {
     const uint32_t E = part.E, F = part.F;
     const uint32_t nq = (F + kHpU - 1) / kHpU;  // groups of kHpU samples per row
     const uint64_t total = (uint64_t)E * nq;
-    for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < total;
-         x += (uint64_t)gridDim.x * blockDim.x) {
+    __shared__ uint32_t s_chunk;
+    // chunks of blockDim groups claimed in order (claim != null): the CTAs stay within one
+    // epoch's records; else a fixed grid-stride order
+    for (uint64_t x0 = (uint64_t)blockIdx.x * blockDim.x;; x0 += (uint64_t)gridDim.x * blockDim.x) {
+        if (claim) {
+            __syncthreads();
+            if (threadIdx.x == 0) s_chunk = atomicAdd(claim, 1u);
+            __syncthreads();
+            x0 = (uint64_t)s_chunk * blockDim.x;
+        }
+        if (x0 >= total) break;
+        const uint64_t x = x0 + threadIdx.x;
+        if (x >= total) continue;
         const uint32_t e = (uint32_t)(x / nq);
         const uint32_t k0 = (uint32_t)(x - (uint64_t)e * nq) * kHpU;
         // rank row: one 16-B load (rows pitched to Fp, a multiple of 16 samples)
@@ -339,13 +366,16 @@ __global__ void __launch_bounds__(kThreads, 3) hp_fill_kernel(Part part, const u
 
 void launch_hp_fill(cudaStream_t s, const Part& part, const uint32_t* inv, const uint16_t* rank16,
                     uint32_t MB, const uint32_t* rec, uint32_t np, uint32_t J, uint32_t Rp,
-                    const uint32_t* cbase, uint32_t* hp) {
+                    const uint32_t* cbase, uint32_t* hp, uint32_t* claim) {
     const uint64_t total = (uint64_t)part.E * ((part.F + kHpU - 1) / kHpU);
     // resident grid: epochs in lockstep, so one epoch's records stay in L2
     // (72 registers at 3 CTAs/SM: no spills; 2 CTAs/SM measured the same, 4 spills)
     const unsigned grid = std::min<unsigned>(resident_grid(hp_fill_kernel, kThreads, 0, 8),
                                              grid_for(total, kThreads, 148u * 64u));
-    hp_fill_kernel<<<grid, kThreads, 0, s>>>(part, inv, rank16, MB, rec, np, J, Rp, cbase, hp);
+    static const bool dyn = ab_knob("CLAIRPLAN_DYN", 1) != 0;
+    if (claim && dyn) cudaMemsetAsync(claim, 0, 4, s);
+    hp_fill_kernel<<<grid, kThreads, 0, s>>>(part, inv, rank16, MB, rec, np, J, Rp, cbase, hp,
+                                             dyn ? claim : nullptr);
 }
 
 // ---------------------------------------------------------------------------- K8
