@@ -347,19 +347,37 @@ __global__ void __launch_bounds__(kThreads, 4) fyc_emit_kernel(Part part, uint32
                                                                uint32_t* __restrict__ stream,
                                                                uint32_t* __restrict__ perm_out,
                                                                const StreamDst dst, int check,
-                                                               uint32_t* __restrict__ err) {
+                                                               uint32_t* __restrict__ err,
+                                                               uint32_t* __restrict__ claim, uint32_t ne) {
     constexpr uint32_t CH = kFycEmitL * 32;
     __shared__ uint32_t sbuf[kThreads / 32][CH];
     __shared__ uint16_t slist[kThreads / 32][CH];
-    const uint32_t slot = blockIdx.y, e = e0 + slot, F = part.F;
+    const uint32_t F = part.F;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t* sc = tsucc + (size_t)slot * F;
-    const uint32_t* qq = q + (size_t)slot * F;
     uint32_t* buf = sbuf[warp];
     uint16_t* lst = slist[warp];
     const uint32_t nchunk = (F + CH - 1) / CH;
     const uint32_t nwarp = gridDim.x * (blockDim.x >> 5);
-    for (uint32_t c = blockIdx.x * (blockDim.x >> 5) + warp; c < nchunk; c += nwarp) {
+    // claim != null: (epoch, chunk) pairs claimed in order by each warp from one counter (the
+    // warps in flight stay within ~one epoch's q / inv rows); else blockIdx.y = epoch slot and a
+    // grid-stride walk over its chunks
+    for (uint32_t it = 0;; ++it) {
+        uint32_t slot, c;
+        if (claim) {
+            uint32_t g = 0;
+            if (lane == 0) g = atomicAdd(claim, 1u);
+            g = __shfl_sync(0xffffffffu, g, 0);
+            slot = g / nchunk;
+            c = g - slot * nchunk;
+            if (slot >= ne) break;
+        } else {
+            slot = blockIdx.y;
+            c = blockIdx.x * (blockDim.x >> 5) + warp + it * nwarp;
+            if (c >= nchunk) break;
+        }
+        const uint32_t e = e0 + slot;
+        const uint32_t* sc = tsucc + (size_t)slot * F;
+        const uint32_t* qq = q + (size_t)slot * F;
         const uint32_t cb = c * CH;
         uint32_t sv[kFycEmitL];
 #pragma unroll
@@ -471,7 +489,7 @@ void launch_fyc(cudaStream_t s, uint64_t key, const Part& part, uint32_t e0, uin
                 uint32_t* perm_out, const StreamDst* dst) {
     const uint32_t F = part.F;
     static const int check = (int)ab_knob("CLAIRPLAN_FYC_CHECK", 0);  // debug bounds checks
-    cudaMemsetAsync(cursor, 0, (size_t)ne * g.NB * 4, s);
+    cudaMemsetAsync(cursor, 0, ((size_t)ne * g.NB + 1) * 4, s);  // + fyc_emit's claim counter
     const uint32_t TS = g.pack ? kFycTS : 2 * kFycTS;
     const uint32_t NT = (F + TS - 1) / TS;
     const size_t sm_part = (size_t)4 * (g.NB + 1);
@@ -491,9 +509,16 @@ void launch_fyc(cudaStream_t s, uint64_t key, const Part& part, uint32_t e0, uin
     }
     const StreamDst dloc = dst ? *dst : StreamDst{};
     const uint32_t nchunk = (F + kFycEmitL * 32 - 1) / (kFycEmitL * 32);
-    dim3 gq(std::max<uint32_t>(1, std::min<uint32_t>((nchunk + 7) / 8, 148u * 8u)), ne);
-    fyc_emit_kernel<<<gq, kThreads, 0, s>>>(part, e0, tsucc, q, inv, stream, perm_out, dloc, check,
-                                            rej_flag + (e0 - rt.e_base));
+    static const bool dyn = ab_knob("CLAIRPLAN_DYN", 1) != 0;  // A/B: per-epoch grid-stride walk
+    if (dyn) {
+        const uint32_t gx = std::max<uint32_t>(1, std::min<uint64_t>(((uint64_t)nchunk * ne + 7) / 8, 148u * 4u));
+        fyc_emit_kernel<<<gx, kThreads, 0, s>>>(part, e0, tsucc, q, inv, stream, perm_out, dloc, check,
+                                                rej_flag + (e0 - rt.e_base), cursor + (size_t)ne * g.NB, ne);
+    } else {
+        dim3 gq(std::max<uint32_t>(1, std::min<uint32_t>((nchunk + 7) / 8, 148u * 8u)), ne);
+        fyc_emit_kernel<<<gq, kThreads, 0, s>>>(part, e0, tsucc, q, inv, stream, perm_out, dloc, check,
+                                                rej_flag + (e0 - rt.e_base), nullptr, ne);
+    }
 }
 
 }  // namespace clairplan

@@ -102,7 +102,7 @@ int enqueue_perms(clairplan_plan* p, uint32_t* stream_out, uint32_t* inv_out, ui
     if (!lists && fyc_ready(p, F, fg)) {  // contiguous target-block buckets
         const uint32_t EB = fyc_epochs_per_batch(F, e_count);
         uint32_t* region = need<uint32_t>(p->fyc_region, (uint64_t)EB * fg.rtotal, ok);
-        uint32_t* cursor = need<uint32_t>(p->fyc_cursor, (uint64_t)EB * fg.NB, ok);
+        uint32_t* cursor = need<uint32_t>(p->fyc_cursor, (uint64_t)EB * fg.NB + 1, ok);  // + emit claim
         uint32_t* tsucc = need<uint32_t>(p->next, (uint64_t)EB * F, ok);
         uint32_t* q = need<uint32_t>(p->q, (uint64_t)EB * F, ok);
         if (!ok) return fail(CLAIRPLAN_ENOMEM, "device allocation failed (permutation workspace)");
