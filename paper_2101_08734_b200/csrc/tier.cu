@@ -278,6 +278,7 @@ void launch_fill_class(cudaStream_t s, uint8_t* cls, uint64_t n, uint8_t j) {
 // coalesced.  The holder pass then needs no gather at all.
 constexpr int kHpU = 8;  // consecutive samples per thread: 8 independent record gathers in flight
 
+template <int NP>  // class bit-planes per record (0: runtime np)
 __global__ void __launch_bounds__(kThreads, 3) hp_fill_kernel(Part part, const uint32_t* __restrict__ inv,
                                                            const uint16_t* __restrict__ rank16,
                                                            uint32_t MB, const uint32_t* __restrict__ rec,
@@ -335,17 +336,22 @@ __global__ void __launch_bounds__(kThreads, 3) hp_fill_kernel(Part part, const u
             out[u] = 0;
             if (p[u] == kNone) continue;
             const uint32_t bit = wb[u] & 31, wl = wb[u] >> 5;
+            const uint32_t npv = NP > 0 ? (uint32_t)NP : np;
             uint32_t cls = 0, cm = 0xffffffffu;
-            for (uint32_t q = 0; q < np; ++q) {
+#pragma unroll
+            for (uint32_t q = 0; q < (NP > 0 ? (uint32_t)NP : 4u); ++q) {
+                if (q >= npv) break;
                 const uint32_t pl = q == 0 ? a[u].x : q == 1 ? a[u].y : q == 2 ? a[u].z : a[u].w;
                 cls |= ((pl >> bit) & 1u) << q;
             }
-            for (uint32_t q = 0; q < np; ++q) {
+#pragma unroll
+            for (uint32_t q = 0; q < (NP > 0 ? (uint32_t)NP : 4u); ++q) {
+                if (q >= npv) break;
                 const uint32_t pl = q == 0 ? a[u].x : q == 1 ? a[u].y : q == 2 ? a[u].z : a[u].w;
                 cm &= ((cls >> q) & 1u) ? pl : ~pl;
             }
             if (cls) {
-                const uint32_t wi = np + cls - 1;
+                const uint32_t wi = npv + cls - 1;
                 uint32_t prew;
                 if (wi < 4) {
                     prew = wi == 0 ? a[u].x : wi == 1 ? a[u].y : wi == 2 ? a[u].z : a[u].w;
@@ -370,12 +376,19 @@ void launch_hp_fill(cudaStream_t s, const Part& part, const uint32_t* inv, const
     const uint64_t total = (uint64_t)part.E * ((part.F + kHpU - 1) / kHpU);
     // resident grid: epochs in lockstep, so one epoch's records stay in L2
     // (72 registers at 3 CTAs/SM: no spills; 2 CTAs/SM measured the same, 4 spills)
-    const unsigned grid = std::min<unsigned>(resident_grid(hp_fill_kernel, kThreads, 0, 8),
-                                             grid_for(total, kThreads, 148u * 64u));
     static const bool dyn = ab_knob("CLAIRPLAN_DYN", 1) != 0;
     if (claim && dyn) cudaMemsetAsync(claim, 0, 4, s);
-    hp_fill_kernel<<<grid, kThreads, 0, s>>>(part, inv, rank16, MB, rec, np, J, Rp, cbase, hp,
-                                             dyn ? claim : nullptr);
+#define HPF(NPV)                                                                                   \
+    do {                                                                                           \
+        const unsigned grid = std::min<unsigned>(resident_grid(hp_fill_kernel<NPV>, kThreads, 0, 8), \
+                                                 grid_for(total, kThreads, 148u * 64u));           \
+        hp_fill_kernel<NPV><<<grid, kThreads, 0, s>>>(part, inv, rank16, MB, rec, np, J, Rp, cbase, hp, \
+                                                      dyn ? claim : nullptr);                      \
+    } while (0)
+    if (np == 1) HPF(1);
+    else if (np == 2) HPF(2);
+    else HPF(0);
+#undef HPF
 }
 
 // ---------------------------------------------------------------------------- K8
