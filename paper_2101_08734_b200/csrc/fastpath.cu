@@ -649,11 +649,13 @@ __global__ void class_base_kernel(const uint64_t* __restrict__ cpre, uint64_t nb
 // class_list[cstart[wl*J + j-1] + pos] = sample, pos = position in the worker's class list.
 // One warp per (worker, epoch) segment, kBU blocks per iteration; the block record is spread
 // over lanes 0..Rp-1 and read through shuffles, the stream words are loaded up front.
+template <int NP>  // class bit-planes (0: runtime np)
 __global__ void __launch_bounds__(kThreads) class_write_kernel(
     Part part, uint32_t MB, const uint32_t* __restrict__ stream, const uint32_t* __restrict__ rec,
-    uint32_t np, uint32_t J, uint32_t Rp, const uint32_t* __restrict__ cbase,
+    uint32_t np_rt, uint32_t J, uint32_t Rp, const uint32_t* __restrict__ cbase,
     const uint64_t* __restrict__ cstart, uint32_t* __restrict__ class_list, uint64_t nblk) {
     const uint32_t lane = threadIdx.x & 31;
+    const uint32_t np = NP > 0 ? (uint32_t)NP : np_rt;
     const uint32_t E = part.E, nloc = part.wend - part.wbegin;
     const uint64_t nseg = (uint64_t)nloc * E;
     for (uint64_t seg = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; seg < nseg;
@@ -682,10 +684,15 @@ __global__ void __launch_bounds__(kThreads) class_write_kernel(
                 if (bi >= nb) break;
                 const uint64_t t = (uint64_t)bi * 32 + lane;
                 uint32_t cls = 0, cm = 0xffffffffu;
-                for (uint32_t p = 0; p < np; ++p)
+#pragma unroll
+                for (uint32_t p = 0; p < (NP > 0 ? (uint32_t)NP : 8u); ++p) {
+                    if (p >= np) break;
                     cls |= ((__shfl_sync(0xffffffffu, mine[u], p) >> lane) & 1u) << p;
+                }
                 if (t >= Le) cls = 0;
-                for (uint32_t p = 0; p < np; ++p) {
+#pragma unroll
+                for (uint32_t p = 0; p < (NP > 0 ? (uint32_t)NP : 8u); ++p) {
+                    if (p >= np) break;
                     const uint32_t pl = __shfl_sync(0xffffffffu, mine[u], p);
                     cm &= ((cls >> p) & 1u) ? pl : ~pl;
                 }
@@ -1089,8 +1096,13 @@ void launch_class_write(cudaStream_t s, const Part& part, uint32_t MB, const uin
                         const uint32_t* cbase, const uint64_t* cstart, uint32_t* class_list,
                         uint64_t nblk) {
     const uint64_t nseg = (uint64_t)(part.wend - part.wbegin) * part.E;
-    class_write_kernel<<<grid_for(nseg * 32, kThreads, 148u * 64u), kThreads, 0, s>>>(
-        part, MB, stream, rec, np, J, Rp, cbase, cstart, class_list, nblk);
+    const unsigned g = grid_for(nseg * 32, kThreads, 148u * 64u);
+    if (np == 1)
+        class_write_kernel<1><<<g, kThreads, 0, s>>>(part, MB, stream, rec, np, J, Rp, cbase, cstart, class_list, nblk);
+    else if (np == 2)
+        class_write_kernel<2><<<g, kThreads, 0, s>>>(part, MB, stream, rec, np, J, Rp, cbase, cstart, class_list, nblk);
+    else
+        class_write_kernel<0><<<g, kThreads, 0, s>>>(part, MB, stream, rec, np, J, Rp, cbase, cstart, class_list, nblk);
 }
 
 void launch_class_lens(cudaStream_t s, uint32_t nloc, uint32_t E, uint32_t MB, uint32_t J,
