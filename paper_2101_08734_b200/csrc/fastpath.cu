@@ -573,12 +573,15 @@ constexpr int kBU = 4;
 // One warp per (worker, epoch) segment, kBU blocks per iteration: no per-block division and
 // the dependent gathers (mask -> first-order index -> tier position -> class) of kBU blocks
 // overlap.
+template <int NJ>  // classes (0: runtime J); the bit-plane count follows
 __global__ void __launch_bounds__(kThreads) blk_codes_kernel(
     Part part, uint32_t MB, const uint32_t* __restrict__ blkmask,
     const uint32_t* __restrict__ blkbase, const uint32_t* __restrict__ dest,
-    const uint8_t* __restrict__ cls_sorted, uint32_t np, uint32_t J, uint32_t Rp,
+    const uint8_t* __restrict__ cls_sorted, uint32_t np_rt, uint32_t J_rt, uint32_t Rp,
     uint32_t* __restrict__ rec, uint32_t* __restrict__ ccount, uint64_t nblk) {
     const uint32_t lane = threadIdx.x & 31;
+    const uint32_t J = NJ > 0 ? (uint32_t)NJ : J_rt;
+    const uint32_t np = NJ > 0 ? (NJ >= 4 ? 3u : NJ >= 2 ? 2u : 1u) : np_rt;
     const uint32_t E = part.E, nloc = part.wend - part.wbegin;
     const uint64_t nseg = (uint64_t)nloc * E;
     for (uint64_t seg = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; seg < nseg;
@@ -609,11 +612,15 @@ __global__ void __launch_bounds__(kThreads) blk_codes_kernel(
                 if (bi >= MB) break;
                 const uint64_t blk = blk0 + bi;
                 uint32_t word = 0;  // lane p < np holds plane p, lane np + j holds count of class j+1
-                for (uint32_t p = 0; p < np; ++p) {
+#pragma unroll
+                for (uint32_t p = 0; p < (NJ > 0 ? 3u : 8u); ++p) {
+                    if (p >= np) break;
                     const uint32_t pl = __ballot_sync(0xffffffffu, (cls[u] >> p) & 1u);
                     if (lane == p) word = pl;
                 }
-                for (uint32_t j = 1; j <= J; ++j) {
+#pragma unroll
+                for (uint32_t j = 1; j <= (NJ > 0 ? (uint32_t)NJ : 16u); ++j) {
+                    if (j > J) break;
                     const uint32_t bj = __ballot_sync(0xffffffffu, cls[u] == j);
                     if (lane == j - 1) ccount[(uint64_t)(j - 1) * nblk + blk] = __popc(bj);
                 }
@@ -1078,8 +1085,15 @@ void launch_blk_codes(cudaStream_t s, const Part& part, uint32_t MB, const uint3
                       uint32_t np, uint32_t J, uint32_t Rp, uint32_t* rec, uint32_t* ccount,
                       uint64_t nblk) {
     const uint64_t nseg = (uint64_t)(part.wend - part.wbegin) * part.E;
-    blk_codes_kernel<<<grid_for(nseg * 32, kThreads, 148u * 64u), kThreads, 0, s>>>(
-        part, MB, blkmask, blkbase, dest, cls_sorted, np, J, Rp, rec, ccount, nblk);
+    const unsigned g = grid_for(nseg * 32, kThreads, 148u * 64u);
+    if (J == 1)
+        blk_codes_kernel<1><<<g, kThreads, 0, s>>>(part, MB, blkmask, blkbase, dest, cls_sorted, np, J, Rp, rec, ccount, nblk);
+    else if (J == 2)
+        blk_codes_kernel<2><<<g, kThreads, 0, s>>>(part, MB, blkmask, blkbase, dest, cls_sorted, np, J, Rp, rec, ccount, nblk);
+    else if (J == 3)
+        blk_codes_kernel<3><<<g, kThreads, 0, s>>>(part, MB, blkmask, blkbase, dest, cls_sorted, np, J, Rp, rec, ccount, nblk);
+    else
+        blk_codes_kernel<0><<<g, kThreads, 0, s>>>(part, MB, blkmask, blkbase, dest, cls_sorted, np, J, Rp, rec, ccount, nblk);
 }
 
 void launch_rec_fill(cudaStream_t s, const uint64_t* cpre, uint64_t nblk, uint32_t np, uint32_t J,
