@@ -981,7 +981,8 @@ __global__ void __launch_bounds__(kThreads) sample_tile_kernel(Part part, const 
             const uint32_t word = lane < W ? bm[lane] : 0u;
             const uint32_t c = __popc(word);
             uint32_t inc = c;
-            for (uint32_t d = 1; d < W; d <<= 1) {  // lanes >= W hold 0: log2(W) steps suffice
+#pragma unroll
+            for (uint32_t d = 1; d < 32; d <<= 1) {  // lanes >= W hold 0 (fixed 5 steps, no loop)
                 const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
                 if (lane >= d) inc += o;
             }
