@@ -612,17 +612,29 @@ __global__ void __launch_bounds__(kThreads) blk_codes_kernel(
                 if (bi >= MB) break;
                 const uint64_t blk = blk0 + bi;
                 uint32_t word = 0;  // lane p < np holds plane p, lane np + j holds count of class j+1
+                if constexpr (NJ > 0) {  // unrolled
 #pragma unroll
-                for (uint32_t p = 0; p < (NJ > 0 ? 3u : 8u); ++p) {
-                    if (p >= np) break;
-                    const uint32_t pl = __ballot_sync(0xffffffffu, (cls[u] >> p) & 1u);
-                    if (lane == p) word = pl;
-                }
+                    for (uint32_t p = 0; p < 3u; ++p) {
+                        if (p >= np) break;
+                        const uint32_t pl = __ballot_sync(0xffffffffu, (cls[u] >> p) & 1u);
+                        if (lane == p) word = pl;
+                    }
 #pragma unroll
-                for (uint32_t j = 1; j <= (NJ > 0 ? (uint32_t)NJ : 16u); ++j) {
-                    if (j > J) break;
-                    const uint32_t bj = __ballot_sync(0xffffffffu, cls[u] == j);
-                    if (lane == j - 1) ccount[(uint64_t)(j - 1) * nblk + blk] = __popc(bj);
+                    for (uint32_t j = 1; j <= (uint32_t)NJ; ++j) {
+                        const uint32_t bj = __ballot_sync(0xffffffffu, cls[u] == j);
+                        if (lane == j - 1) ccount[(uint64_t)(j - 1) * nblk + blk] = __popc(bj);
+                    }
+                } else {
+#pragma unroll 1
+                    for (uint32_t p = 0; p < np; ++p) {
+                        const uint32_t pl = __ballot_sync(0xffffffffu, (cls[u] >> p) & 1u);
+                        if (lane == p) word = pl;
+                    }
+#pragma unroll 1
+                    for (uint32_t j = 1; j <= J; ++j) {
+                        const uint32_t bj = __ballot_sync(0xffffffffu, cls[u] == j);
+                        if (lane == j - 1) ccount[(uint64_t)(j - 1) * nblk + blk] = __popc(bj);
+                    }
                 }
                 if (lane < np) rec[(rec0 + bi) * Rp + lane] = word;
             }
