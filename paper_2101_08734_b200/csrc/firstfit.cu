@@ -214,16 +214,20 @@ __global__ void ff_prefix_kernel(TileMap tm, const uint64_t* __restrict__ seg_le
     }
 }
 
+// warp per chunk: lane l composes elements [32 l, 32 l + 32) in order (contiguous loads, the
+// sectors re-read from L1), then one ordered warp reduction -- no block barriers per chunk
 __global__ void __launch_bounds__(kThreads) ff_agg_kernel(TileMap tm,
                                                            const uint64_t* __restrict__ seg_begin,
                                                            const uint64_t* __restrict__ seg_len,
                                                            const double* __restrict__ sz, double C,
                                                            FFChunks ch) {
-    __shared__ Mono wm[kThreads / 32];
-    for (uint64_t t = blockIdx.x; t < tm.max_tiles; t += gridDim.x) {
+    static_assert(kChunk == 32 * 32, "ff_agg: 32 elements per lane");
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t nwarp = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t t = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < tm.max_tiles; t += nwarp) {
         const uint32_t seg = tm.tile_seg[t];
         if (seg == kNone) break;
-        if (ch.segfit[seg]) continue;  // block-uniform: whole segment fits
+        if (ch.segfit[seg]) continue;  // warp-uniform: whole segment fits
         const uint64_t off = (t - tm.tile_base[seg]) * (uint64_t)tm.tile;
         const uint64_t L = seg_len[seg];
         const uint64_t n = L - off < tm.tile ? L - off : tm.tile;
@@ -235,29 +239,26 @@ __global__ void __launch_bounds__(kThreads) ff_agg_kernel(TileMap tm,
             const int k1 = binade(r1 - tol);
             if (binade(r0 + tol) == k1 && k1 > -1000 && ldexp(1.0, k1) >= ch.mx[t]) k = k1;
         }
-        if (k == kNoBinade) {  // uniform per block
-            if (threadIdx.x == 0) ch.k[t] = kNoBinade;
+        if (k == kNoBinade) {  // uniform per warp
+            if (lane == 0) ch.k[t] = kNoBinade;
             continue;
         }
-        const double* p = sz + seg_begin[seg] + off;
+        const double* p = sz + seg_begin[seg] + off + (uint64_t)lane * 32;
+        const uint32_t cnt = n > lane * 32u ? (n - lane * 32u < 32 ? (uint32_t)(n - lane * 32u) : 32u) : 0u;
         Mono m = mono_id();
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const uint64_t idx = (uint64_t)threadIdx.x * 4 + i;
-            if (idx < n) m = mono_compose(m, mono_elem(p[idx], k));
+        if (cnt == 32) {
+#pragma unroll 8
+            for (uint32_t i = 0; i < 32; ++i) m = mono_compose(m, mono_elem(p[i], k));
+        } else {
+            for (uint32_t i = 0; i < cnt; ++i) m = mono_compose(m, mono_elem(p[i], k));
         }
         m = warp_compose(m);
-        if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            Mono a = wm[0];
-            for (int i = 1; i < kThreads / 32; ++i) a = mono_compose(a, wm[i]);
+        if (lane == 0) {
             ch.k[t] = k;
-            ch.d0[t] = a.d0;
-            ch.d1[t] = a.d1;
-            ch.pbits[t] = (uint8_t)(a.p0 | (a.p1 << 1));
+            ch.d0[t] = m.d0;
+            ch.d1[t] = m.d1;
+            ch.pbits[t] = (uint8_t)(m.p0 | (m.p1 << 1));
         }
-        __syncthreads();
     }
 }
 
@@ -407,7 +408,7 @@ void first_fit_pass(cudaStream_t s, const uint64_t* seg_begin, const uint64_t* s
         ff_stats_kernel<false><<<g, kThreads, 0, s>>>(tm, seg_begin, seg_len, const_cast<double*>(sz),
                                                       nullptr, nullptr, ch);
     ff_prefix_kernel<<<grid_for((uint64_t)nseg * 32, kThreads), kThreads, 0, s>>>(tm, seg_len, C, ch);
-    ff_agg_kernel<<<g, kThreads, 0, s>>>(tm, seg_begin, seg_len, sz, C, ch);
+    ff_agg_kernel<<<grid_for(m * 32, kThreads, 148u * 64u), kThreads, 0, s>>>(tm, seg_begin, seg_len, sz, C, ch);
     ff_resolve_kernel<<<grid_for((uint64_t)nseg * 32, 128), 128, 0, s>>>(tm, seg_begin, seg_len,
                                                                          sz, C, ch, taken,
                                                                          taken_count);
