@@ -497,13 +497,18 @@ int first_fit_classes(clairplan_plan* p, const double* ssize, uint8_t* cls) {
     const double* seq_sz = ssize;
     const uint8_t* prev_taken = cls;  // class 1 writes its flags straight into cls (0/1)
     uint64_t remaining = D, prev_total = D;
+    p->h_known = false;
     for (uint32_t j = 1; j <= J; ++j) {
-        if (remaining == 0) break;
+        if (remaining == 0) {
+            p->h_known = true;  // classes < j took every candidate
+            break;
+        }
         if (j > 1 && class_takes_all(p, p->caps[j - 1])) {
             // every worker's whole candidate set fits class j: its first-fit chain over the
             // rejects of classes < j takes all of them (policies.cpp:40-55, any order)
             launch_fill_class(s, cls, D, (uint8_t)j);
             ++p->launches;
+            p->h_known = true;
             break;
         }
         uint8_t* taken = cls;
@@ -615,6 +620,15 @@ int assign_v2(clairplan_plan* p) {
         launch_class_lens(s, nloc, E, MB, J, cpre, nblk, clen);
         exclusive_scan(s, clen, (uint64_t)nloc * J, cstart, p->ws);
         launch_class_write(s, part, MB, stream_buf, rec, np, J, Rp, cbase, cstart, centries, nblk);
+        // build_export: when every candidate is cached (H = D, known here) the class lists are
+        // final and contiguous: copy them out behind the stream copy while the holders build
+        static const bool early_cl = ab_knob("CLAIRPLAN_EARLY_CL", 1) != 0;  // A/B
+        if (early_cl && p->x_class && p->h_known && D <= p->x_class_cap && p->xstream) {
+            CK(cudaEventRecord(p->xev, s));
+            CK(cudaStreamWaitEvent(p->xstream, p->xev, 0));
+            CK(cudaMemcpyAsync(p->x_class, centries, D * 4, cudaMemcpyDeviceToHost, p->xstream));
+            p->x_class_done = true;
+        }
         p->hp_path = hp_path_ok(p);
         if (p->hp_path) {
             uint32_t* hp = need<uint32_t>(p->hpos, (uint64_t)E * part.Fp, ok);
@@ -1161,9 +1175,14 @@ int clairplan_build_export(clairplan_t p, const double* host_sizes, uint32_t* st
     if (host_sizes)
         if (int rc = clairplan_set_sizes(p, host_sizes, 0)) return rc;
     p->x_streams = streams_out;
+    p->x_class = class_lists_out;
+    p->x_class_cap = class_lists_out ? cl_cap : 0;
+    p->x_class_done = false;
     int rc = clairplan_build(p);
     const bool copied = p->v2;  // the v2 build issued the stream copy on xstream
+    bool cl_copied = p->x_class_done;  // ... and the class lists
     p->x_streams = nullptr;
+    p->x_class = nullptr;
     if (rc) {
         cudaStreamSynchronize(p->xstream);
         return rc;
@@ -1186,11 +1205,16 @@ int clairplan_build_export(clairplan_t p, const double* host_sizes, uint32_t* st
     if (!copied)
         CK(cudaMemcpyAsync(streams_out, p->stream_buf.get<uint32_t>(), p->A * 4, cudaMemcpyDeviceToHost,
                            p->stream));
-    if (int rc2 = clairplan_export_class_lists_async(p, class_lists_out, cl_cap)) {
-        cudaStreamSynchronize(p->xstream);
-        cudaStreamSynchronize(p->stream);
-        return rc2;
+    if (cl_copied && p->H != p->D) {  // (not expected: every candidate was cached) exact copy
+        CK(cudaStreamSynchronize(p->xstream));
+        cl_copied = false;
     }
+    if (!cl_copied)
+        if (int rc2 = clairplan_export_class_lists_async(p, class_lists_out, cl_cap)) {
+            cudaStreamSynchronize(p->xstream);
+            cudaStreamSynchronize(p->stream);
+            return rc2;
+        }
     CK(cudaMemcpyAsync(offsets_out, p->holder_off_dev, ((uint64_t)p->part.F + 1) * 8,
                        cudaMemcpyDeviceToHost, p->stream));
     if (p->H) CK(cudaMemcpyAsync(holders_out, p->holders_dev, p->H * 12, cudaMemcpyDeviceToHost, p->stream));

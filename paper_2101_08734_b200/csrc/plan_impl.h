@@ -155,6 +155,10 @@ struct clairplan_plan {
     cudaStream_t xstream = nullptr;   // build_export: stream of the overlapped output copy
     cudaEvent_t xev = nullptr;
     uint32_t* x_streams = nullptr;     // build_export: host stream buffer of the running build
+    uint32_t* x_class = nullptr;       // build_export: host class-list buffer and its capacity
+    uint64_t x_class_cap = 0;
+    bool x_class_done = false;         // the class lists were copied during the build (xstream)
+    bool h_known = false;              // first fit: every candidate assigned (H = D) known on host
     // counts hook (multi-GPU holder-offset merge overlapped with the build's tail): once the
     // per-sample pair counts exist, they are copied to hook_counts, hook_stream waits for them
     // and hook_fn runs on the host (it enqueues the all-gather); valid if the build then took

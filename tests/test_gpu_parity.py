@@ -661,7 +661,9 @@ def test_build_export_matches_separate_exports(cp, ref):
     import ctypes as C
     F, N, B, E = 30_000, 12, 240, 9
     sizes = ref.generate_sizes(F, 0.1077, 0.2, None, 1)
-    for caps in ([1e6, 1e6], [20.0, 60.0]):
+    # all-fit path; tier path with rejects left over; tier path whose last class takes every
+    # reject (the class lists are then copied out during the build)
+    for caps in ([1e6, 1e6], [20.0, 60.0], [100.0, 1e6]):
         p = cp.Plan(5, F, cp.PartitionSpec(N, B, E, True), caps, sizes).build()
         st = p.stats()
         want_streams = np.concatenate([p.stream(w) for w in range(N)])
